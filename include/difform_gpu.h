@@ -1,0 +1,251 @@
+/*
+ * difform_gpu.h — C-ABI boundary of the B200-native dense diffeomorphic
+ * matching path (FireANTs direct-mode loop, reference "difform").
+ *
+ * Every entry point here replaces one function of the reference C++ API in
+ * /root/reference/proj/include/difform/ (cited per function).  The reference
+ * has no FFI of its own: its boundary is the header API, so the C-ABI keeps
+ * the same argument meaning with plain pointers and sizes:
+ *
+ *   - grids are described by dfm_grid (== difform::GridMeta, core.hpp:13-23);
+ *   - images are x-fastest arrays of voxel_count doubles (ScalarImage::data,
+ *     core.hpp:36-42); label maps int32 (LabelImage, core.hpp:44-50);
+ *   - vector fields are interleaved AoS doubles, ndim per voxel, voxel units
+ *     of their own grid (VectorField::data, core.hpp:54-64);
+ *   - every buffer argument is a HOST pointer; the library stages it through
+ *     pinned memory into device SoA planes of the context precision and
+ *     copies results back (no torch types, no device pointers in the
+ *     host-level calls).  The dfm_dev_* calls at the end take DEVICE pointers
+ *     for callers whose data already lives in HBM.
+ *
+ * Errors mirror the reference exception classes:
+ *   DFM_E_INVALID   <-> std::invalid_argument (validation, grid mismatch)
+ *   DFM_E_NUMERICAL <-> std::runtime_error    (non-finite loss/step, fold)
+ *   DFM_E_CUDA      <-> device failure (no reference counterpart)
+ * The message of the last failure on the calling host thread is returned by
+ * dfm_last_error().
+ *
+ * Threading: a dfm_ctx owns one CUDA stream, a workspace arena and a CUDA
+ * graph cache; it must be used by one host thread at a time.  Use one
+ * context per thread for the reference's concurrent sweep
+ * (pipeline.cpp:287-301).  Results never depend on the thread count.
+ */
+#ifndef DIFFORM_GPU_H
+#define DIFFORM_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DFM_ABI_VERSION 1
+
+typedef enum {
+    DFM_OK = 0,
+    DFM_E_INVALID = 1,
+    DFM_E_NUMERICAL = 2,
+    DFM_E_CUDA = 3
+} dfm_status;
+
+/* arithmetic/storage type of the device path */
+typedef enum { DFM_PREC_F32 = 0, DFM_PREC_F64 = 1 } dfm_precision;
+/* element type of host image/field buffers handed to dfm_register */
+typedef enum { DFM_HOST_F32 = 0, DFM_HOST_F64 = 1 } dfm_host_dtype;
+/* difform::LossKind (affine.hpp:9) */
+typedef enum { DFM_LOSS_SSD = 0, DFM_LOSS_LNCC = 1, DFM_LOSS_DICE = 2 } dfm_loss;
+/* difform::RegMode (pipeline.hpp:23) */
+typedef enum { DFM_MODE_DIRECT = 0, DFM_MODE_SVF = 1 } dfm_mode;
+/* difform::RegInit alternatives (pipeline.hpp:62) */
+typedef enum { DFM_INIT_NONE = 0, DFM_INIT_AFFINE = 1, DFM_INIT_FIELD = 2 } dfm_init_kind;
+
+/* difform::GridMeta (core.hpp:13-23).  ndim 2 uses dims[2] == 1. */
+typedef struct {
+    int32_t ndim;
+    int64_t dims[3];
+    double spacing[3];
+    double origin[3];
+} dfm_grid;
+
+/* difform::RegistrationConfig (pipeline.hpp:25-41) */
+typedef struct {
+    int32_t loss;        /* dfm_loss */
+    int32_t lncc_radius;
+    double eta;
+    double sigma_grad;
+    double sigma_warp;
+    int32_t use_jac;
+    int32_t mode;        /* dfm_mode; only DFM_MODE_DIRECT is on this path */
+    int32_t svf_M;
+    double beta1;
+    double beta2;
+    double eps_adam;
+    double step_cap;
+    int32_t conv_window;
+    double conv_tol;
+    uint64_t seed;
+} dfm_config;
+
+/* difform::IterationRecord (pipeline.hpp:45-53) */
+typedef struct {
+    int32_t scale_index;
+    double scale;
+    int32_t iter;
+    int64_t global_iter;
+    double loss;
+    double max_step;
+    double wall_ms;
+} dfm_iter_record;
+
+/* difform::RegInit (pipeline.hpp:62): none, AffineTransform (affine.hpp:12-16)
+ * or a displacement field on the full or the coarsest working grid. */
+typedef struct {
+    int32_t kind;        /* dfm_init_kind */
+    int32_t affine_ndim;
+    double A[9];         /* row-major, ndim x ndim used */
+    double t[3];
+    dfm_grid field_grid; /* DFM_INIT_FIELD: grid of `field` */
+    const double* field; /* DFM_INIT_FIELD: AoS doubles (host) */
+} dfm_init;
+
+/* Result summary of dfm_register: difform::RunLog (pipeline.hpp:55-60). */
+typedef struct {
+    int64_t n_records;   /* records written (<= capacity passed in)   */
+    int64_t n_total;     /* records produced (may exceed capacity)     */
+    double final_loss;
+    double final_singularity_fraction;
+    double total_ms;
+} dfm_runlog;
+
+typedef struct dfm_ctx dfm_ctx;
+
+/* ---- library / context ------------------------------------------------- */
+int dfm_abi_version(void);
+/* RegistrationConfig{} defaults (pipeline.hpp:25-41). */
+void dfm_config_defaults(dfm_config* cfg);
+/* Creates a context on `device` computing in `precision` (dfm_precision). */
+dfm_status dfm_ctx_create(int device, int precision, dfm_ctx** out);
+void dfm_ctx_destroy(dfm_ctx* ctx);
+int dfm_ctx_precision(const dfm_ctx* ctx);
+/* Copies the thread's last error message; returns its full length. */
+size_t dfm_last_error(char* buf, size_t cap);
+/* Kernel launches issued by this context since creation (evidence count). */
+int64_t dfm_ctx_launch_count(const dfm_ctx* ctx);
+
+/* ---- core.hpp ---------------------------------------------------------- */
+/* validate_meta (core.cpp:26-37) */
+dfm_status dfm_validate_grid(const dfm_grid* g);
+/* output grid of downsample_image (core.cpp:58-74) */
+dfm_status dfm_downsample_grid(const dfm_grid* g, const double factor[3], dfm_grid* out);
+/* downsample_image (core.hpp:86-87, core.cpp:58-96) */
+dfm_status dfm_downsample_image(dfm_ctx* ctx, const dfm_grid* g, const double* img,
+                                const double factor[3], dfm_grid* out_grid, double* out);
+
+/* ---- interp.hpp -------------------------------------------------------- */
+/* sample_linear + sample_linear_gradient (interp.hpp:11-17) at npts points
+ * (xyz triples); grads may be NULL. */
+dfm_status dfm_sample_linear_points(dfm_ctx* ctx, const dfm_grid* g, const double* img,
+                                    int64_t npts, const double* points, double* values,
+                                    double* grads);
+/* warp_image (interp.hpp:28) */
+dfm_status dfm_warp_image(dfm_ctx* ctx, const dfm_grid* g, const double* img,
+                          const double* phi, double* out);
+/* warp_labels (interp.hpp:31) */
+dfm_status dfm_warp_labels(dfm_ctx* ctx, const dfm_grid* g, const int32_t* labels,
+                           const double* phi, int32_t* out);
+/* compose (interp.hpp:35): out = u_psi + lerp(u_phi)(x + u_psi) */
+dfm_status dfm_compose(dfm_ctx* ctx, const dfm_grid* g, const double* phi,
+                       const double* psi, double* out);
+/* jacobian_det (interp.hpp:50) */
+dfm_status dfm_jacobian_det(dfm_ctx* ctx, const dfm_grid* g, const double* phi, double* out);
+/* gaussian_smooth / gaussian_smooth_field (interp.hpp:54-57) */
+dfm_status dfm_gaussian_smooth(dfm_ctx* ctx, const dfm_grid* g, const double* img,
+                               const double sigma[3], double* out);
+dfm_status dfm_gaussian_smooth_field(dfm_ctx* ctx, const dfm_grid* g, const double* f,
+                                     const double sigma[3], double* out);
+/* upsample_field (linear), resample_field_linear, resample_displacement
+ * (interp.hpp:65-75) */
+dfm_status dfm_upsample_field(dfm_ctx* ctx, const dfm_grid* g, const double* phi,
+                              const dfm_grid* new_grid, double* out);
+dfm_status dfm_resample_field_linear(dfm_ctx* ctx, const dfm_grid* g, const double* f,
+                                     const dfm_grid* new_grid, double* out);
+dfm_status dfm_resample_displacement(dfm_ctx* ctx, const dfm_grid* g, const double* phi,
+                                     const dfm_grid* new_grid, double* out);
+
+/* ---- similarity.hpp ---------------------------------------------------- */
+/* ssd_eval / lncc_eval (similarity.hpp:17-24).  The moving image may live on
+ * its own grid; phi must be on the fixed grid.  grad may be NULL. */
+dfm_status dfm_ssd_eval(dfm_ctx* ctx, const dfm_grid* fixed_grid, const double* fixed,
+                        const dfm_grid* moving_grid, const double* moving,
+                        const double* phi, double* value, double* grad);
+dfm_status dfm_lncc_eval(dfm_ctx* ctx, const dfm_grid* fixed_grid, const double* fixed,
+                         const dfm_grid* moving_grid, const double* moving,
+                         const double* phi, int window_radius, double* value, double* grad);
+/* dice_soft_eval (similarity.hpp:27-28): masks must lie in [0,1]. */
+dfm_status dfm_dice_eval(dfm_ctx* ctx, const dfm_grid* fixed_grid, const double* fixed,
+                         const dfm_grid* moving_grid, const double* moving,
+                         const double* phi, double* value, double* grad);
+
+/* ---- optim.hpp --------------------------------------------------------- */
+/* adam_step (optim.hpp:23): m, nu updated in place, *t advanced. */
+dfm_status dfm_adam_step(dfm_ctx* ctx, const dfm_grid* g, double* m, double* nu,
+                         int64_t* t, double beta1, double beta2, double eps,
+                         const double* v, double* dir);
+/* upsample_state (optim.hpp:31) */
+dfm_status dfm_upsample_state(dfm_ctx* ctx, const dfm_grid* g, const double* m,
+                              const double* nu, const dfm_grid* new_grid, double* m_out,
+                              double* nu_out);
+
+/* ---- diffeo.hpp -------------------------------------------------------- */
+/* eulerian_direction (diffeo.hpp:10-11) */
+dfm_status dfm_eulerian_direction(dfm_ctx* ctx, const dfm_grid* g, const double* grad,
+                                  const double* phi, int use_jac, double* out);
+/* apply_update (diffeo.hpp:16-17) */
+dfm_status dfm_apply_update(dfm_ctx* ctx, const dfm_grid* g, const double* phi,
+                            const double* v, double eta, double sigma_warp, double cap,
+                            double* out);
+
+/* ---- analysis.hpp ------------------------------------------------------ */
+/* singularity_fraction (analysis.hpp:40) */
+dfm_status dfm_singularity_fraction(dfm_ctx* ctx, const dfm_grid* g, const double* phi,
+                                    double* fraction);
+
+/* ---- pipeline.hpp ------------------------------------------------------ */
+/* register_images, direct mode (pipeline.hpp:70-73, pipeline.cpp:121-224).
+ * fixed/moving: host arrays of `image_dtype` (dfm_host_dtype) on grid g.
+ * out_field: host AoS array of `field_dtype` (voxel_count*ndim) or NULL.
+ * records: capacity `max_records`; log->n_total says how many were made. */
+dfm_status dfm_register(dfm_ctx* ctx, const dfm_grid* g, const void* fixed,
+                        const void* moving, int image_dtype, const dfm_config* cfg,
+                        const double* scales, const int32_t* iterations, int32_t nscales,
+                        const dfm_init* init, void* out_field, int field_dtype,
+                        dfm_iter_record* records, int64_t max_records, dfm_runlog* log);
+
+/* ---- device-resident entry points ------------------------------------- */
+/* Same as dfm_register but fixed/moving are DEVICE arrays of the context
+ * precision (float or double, voxel_count each) and the result field stays on
+ * the device as three SoA planes of the context precision (out_soa_field:
+ * 3*voxel_count elements, x-plane then y then z; may be NULL).  No host
+ * staging is done except the per-scale loss log readback. */
+dfm_status dfm_dev_register(dfm_ctx* ctx, const dfm_grid* g, const void* d_fixed,
+                            const void* d_moving, const dfm_config* cfg,
+                            const double* scales, const int32_t* iterations,
+                            int32_t nscales, void* d_out_soa_field,
+                            dfm_iter_record* records, int64_t max_records, dfm_runlog* log);
+
+/* Timing hook for benchmarks: per-kernel-class accumulated device time (ms)
+ * and launch counts over the last dfm_register/dfm_dev_register call when
+ * profiling is enabled with dfm_ctx_set_profiling(ctx, 1).  Class ids:
+ * 0 lncc/ssd forward, 1 lncc backward, 2 smooth+adam, 3 compose+smooth,
+ * 4 monitor, 5 pyramid (down/upsample), 6 epilogue. */
+#define DFM_NUM_KCLASS 7
+dfm_status dfm_ctx_set_profiling(dfm_ctx* ctx, int enable);
+dfm_status dfm_ctx_kernel_times(const dfm_ctx* ctx, double* ms, int64_t* launches,
+                                int64_t* voxels);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DIFFORM_GPU_H */
