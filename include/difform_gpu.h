@@ -42,6 +42,12 @@ extern "C" {
 
 #define DFM_ABI_VERSION 1
 
+#if defined(__GNUC__)
+#define DFM_API __attribute__((visibility("default")))
+#else
+#define DFM_API
+#endif
+
 typedef enum {
     DFM_OK = 0,
     DFM_E_INVALID = 1,
@@ -121,94 +127,97 @@ typedef struct {
 typedef struct dfm_ctx dfm_ctx;
 
 /* ---- library / context ------------------------------------------------- */
-int dfm_abi_version(void);
+DFM_API int dfm_abi_version(void);
 /* RegistrationConfig{} defaults (pipeline.hpp:25-41). */
-void dfm_config_defaults(dfm_config* cfg);
+DFM_API void dfm_config_defaults(dfm_config* cfg);
 /* Creates a context on `device` computing in `precision` (dfm_precision). */
-dfm_status dfm_ctx_create(int device, int precision, dfm_ctx** out);
-void dfm_ctx_destroy(dfm_ctx* ctx);
-int dfm_ctx_precision(const dfm_ctx* ctx);
+DFM_API dfm_status dfm_ctx_create(int device, int precision, dfm_ctx** out);
+DFM_API void dfm_ctx_destroy(dfm_ctx* ctx);
+DFM_API int dfm_ctx_precision(const dfm_ctx* ctx);
 /* Copies the thread's last error message; returns its full length. */
-size_t dfm_last_error(char* buf, size_t cap);
+DFM_API size_t dfm_last_error(char* buf, size_t cap);
+/* The context's CUDA stream (a cudaStream_t), for callers that time or order
+ * work around the library's launches with their own CUDA events. */
+DFM_API void* dfm_ctx_stream(dfm_ctx* ctx);
 /* Kernel launches issued by this context since creation (evidence count). */
-int64_t dfm_ctx_launch_count(const dfm_ctx* ctx);
+DFM_API int64_t dfm_ctx_launch_count(const dfm_ctx* ctx);
 
 /* ---- core.hpp ---------------------------------------------------------- */
 /* validate_meta (core.cpp:26-37) */
-dfm_status dfm_validate_grid(const dfm_grid* g);
+DFM_API dfm_status dfm_validate_grid(const dfm_grid* g);
 /* output grid of downsample_image (core.cpp:58-74) */
-dfm_status dfm_downsample_grid(const dfm_grid* g, const double factor[3], dfm_grid* out);
+DFM_API dfm_status dfm_downsample_grid(const dfm_grid* g, const double factor[3], dfm_grid* out);
 /* downsample_image (core.hpp:86-87, core.cpp:58-96) */
-dfm_status dfm_downsample_image(dfm_ctx* ctx, const dfm_grid* g, const double* img,
+DFM_API dfm_status dfm_downsample_image(dfm_ctx* ctx, const dfm_grid* g, const double* img,
                                 const double factor[3], dfm_grid* out_grid, double* out);
 
 /* ---- interp.hpp -------------------------------------------------------- */
 /* sample_linear + sample_linear_gradient (interp.hpp:11-17) at npts points
  * (xyz triples); grads may be NULL. */
-dfm_status dfm_sample_linear_points(dfm_ctx* ctx, const dfm_grid* g, const double* img,
+DFM_API dfm_status dfm_sample_linear_points(dfm_ctx* ctx, const dfm_grid* g, const double* img,
                                     int64_t npts, const double* points, double* values,
                                     double* grads);
 /* warp_image (interp.hpp:28) */
-dfm_status dfm_warp_image(dfm_ctx* ctx, const dfm_grid* g, const double* img,
+DFM_API dfm_status dfm_warp_image(dfm_ctx* ctx, const dfm_grid* g, const double* img,
                           const double* phi, double* out);
 /* warp_labels (interp.hpp:31) */
-dfm_status dfm_warp_labels(dfm_ctx* ctx, const dfm_grid* g, const int32_t* labels,
+DFM_API dfm_status dfm_warp_labels(dfm_ctx* ctx, const dfm_grid* g, const int32_t* labels,
                            const double* phi, int32_t* out);
 /* compose (interp.hpp:35): out = u_psi + lerp(u_phi)(x + u_psi) */
-dfm_status dfm_compose(dfm_ctx* ctx, const dfm_grid* g, const double* phi,
+DFM_API dfm_status dfm_compose(dfm_ctx* ctx, const dfm_grid* g, const double* phi,
                        const double* psi, double* out);
 /* jacobian_det (interp.hpp:50) */
-dfm_status dfm_jacobian_det(dfm_ctx* ctx, const dfm_grid* g, const double* phi, double* out);
+DFM_API dfm_status dfm_jacobian_det(dfm_ctx* ctx, const dfm_grid* g, const double* phi, double* out);
 /* gaussian_smooth / gaussian_smooth_field (interp.hpp:54-57) */
-dfm_status dfm_gaussian_smooth(dfm_ctx* ctx, const dfm_grid* g, const double* img,
+DFM_API dfm_status dfm_gaussian_smooth(dfm_ctx* ctx, const dfm_grid* g, const double* img,
                                const double sigma[3], double* out);
-dfm_status dfm_gaussian_smooth_field(dfm_ctx* ctx, const dfm_grid* g, const double* f,
+DFM_API dfm_status dfm_gaussian_smooth_field(dfm_ctx* ctx, const dfm_grid* g, const double* f,
                                      const double sigma[3], double* out);
 /* upsample_field (linear), resample_field_linear, resample_displacement
  * (interp.hpp:65-75) */
-dfm_status dfm_upsample_field(dfm_ctx* ctx, const dfm_grid* g, const double* phi,
+DFM_API dfm_status dfm_upsample_field(dfm_ctx* ctx, const dfm_grid* g, const double* phi,
                               const dfm_grid* new_grid, double* out);
-dfm_status dfm_resample_field_linear(dfm_ctx* ctx, const dfm_grid* g, const double* f,
+DFM_API dfm_status dfm_resample_field_linear(dfm_ctx* ctx, const dfm_grid* g, const double* f,
                                      const dfm_grid* new_grid, double* out);
-dfm_status dfm_resample_displacement(dfm_ctx* ctx, const dfm_grid* g, const double* phi,
+DFM_API dfm_status dfm_resample_displacement(dfm_ctx* ctx, const dfm_grid* g, const double* phi,
                                      const dfm_grid* new_grid, double* out);
 
 /* ---- similarity.hpp ---------------------------------------------------- */
 /* ssd_eval / lncc_eval (similarity.hpp:17-24).  The moving image may live on
  * its own grid; phi must be on the fixed grid.  grad may be NULL. */
-dfm_status dfm_ssd_eval(dfm_ctx* ctx, const dfm_grid* fixed_grid, const double* fixed,
+DFM_API dfm_status dfm_ssd_eval(dfm_ctx* ctx, const dfm_grid* fixed_grid, const double* fixed,
                         const dfm_grid* moving_grid, const double* moving,
                         const double* phi, double* value, double* grad);
-dfm_status dfm_lncc_eval(dfm_ctx* ctx, const dfm_grid* fixed_grid, const double* fixed,
+DFM_API dfm_status dfm_lncc_eval(dfm_ctx* ctx, const dfm_grid* fixed_grid, const double* fixed,
                          const dfm_grid* moving_grid, const double* moving,
                          const double* phi, int window_radius, double* value, double* grad);
 /* dice_soft_eval (similarity.hpp:27-28): masks must lie in [0,1]. */
-dfm_status dfm_dice_eval(dfm_ctx* ctx, const dfm_grid* fixed_grid, const double* fixed,
+DFM_API dfm_status dfm_dice_eval(dfm_ctx* ctx, const dfm_grid* fixed_grid, const double* fixed,
                          const dfm_grid* moving_grid, const double* moving,
                          const double* phi, double* value, double* grad);
 
 /* ---- optim.hpp --------------------------------------------------------- */
 /* adam_step (optim.hpp:23): m, nu updated in place, *t advanced. */
-dfm_status dfm_adam_step(dfm_ctx* ctx, const dfm_grid* g, double* m, double* nu,
+DFM_API dfm_status dfm_adam_step(dfm_ctx* ctx, const dfm_grid* g, double* m, double* nu,
                          int64_t* t, double beta1, double beta2, double eps,
                          const double* v, double* dir);
 /* upsample_state (optim.hpp:31) */
-dfm_status dfm_upsample_state(dfm_ctx* ctx, const dfm_grid* g, const double* m,
+DFM_API dfm_status dfm_upsample_state(dfm_ctx* ctx, const dfm_grid* g, const double* m,
                               const double* nu, const dfm_grid* new_grid, double* m_out,
                               double* nu_out);
 
 /* ---- diffeo.hpp -------------------------------------------------------- */
 /* eulerian_direction (diffeo.hpp:10-11) */
-dfm_status dfm_eulerian_direction(dfm_ctx* ctx, const dfm_grid* g, const double* grad,
+DFM_API dfm_status dfm_eulerian_direction(dfm_ctx* ctx, const dfm_grid* g, const double* grad,
                                   const double* phi, int use_jac, double* out);
 /* apply_update (diffeo.hpp:16-17) */
-dfm_status dfm_apply_update(dfm_ctx* ctx, const dfm_grid* g, const double* phi,
+DFM_API dfm_status dfm_apply_update(dfm_ctx* ctx, const dfm_grid* g, const double* phi,
                             const double* v, double eta, double sigma_warp, double cap,
                             double* out);
 
 /* ---- analysis.hpp ------------------------------------------------------ */
 /* singularity_fraction (analysis.hpp:40) */
-dfm_status dfm_singularity_fraction(dfm_ctx* ctx, const dfm_grid* g, const double* phi,
+DFM_API dfm_status dfm_singularity_fraction(dfm_ctx* ctx, const dfm_grid* g, const double* phi,
                                     double* fraction);
 
 /* ---- pipeline.hpp ------------------------------------------------------ */
@@ -216,7 +225,7 @@ dfm_status dfm_singularity_fraction(dfm_ctx* ctx, const dfm_grid* g, const doubl
  * fixed/moving: host arrays of `image_dtype` (dfm_host_dtype) on grid g.
  * out_field: host AoS array of `field_dtype` (voxel_count*ndim) or NULL.
  * records: capacity `max_records`; log->n_total says how many were made. */
-dfm_status dfm_register(dfm_ctx* ctx, const dfm_grid* g, const void* fixed,
+DFM_API dfm_status dfm_register(dfm_ctx* ctx, const dfm_grid* g, const void* fixed,
                         const void* moving, int image_dtype, const dfm_config* cfg,
                         const double* scales, const int32_t* iterations, int32_t nscales,
                         const dfm_init* init, void* out_field, int field_dtype,
@@ -228,7 +237,7 @@ dfm_status dfm_register(dfm_ctx* ctx, const dfm_grid* g, const void* fixed,
  * the device as three SoA planes of the context precision (out_soa_field:
  * 3*voxel_count elements, x-plane then y then z; may be NULL).  No host
  * staging is done except the per-scale loss log readback. */
-dfm_status dfm_dev_register(dfm_ctx* ctx, const dfm_grid* g, const void* d_fixed,
+DFM_API dfm_status dfm_dev_register(dfm_ctx* ctx, const dfm_grid* g, const void* d_fixed,
                             const void* d_moving, const dfm_config* cfg,
                             const double* scales, const int32_t* iterations,
                             int32_t nscales, void* d_out_soa_field,
@@ -240,8 +249,8 @@ dfm_status dfm_dev_register(dfm_ctx* ctx, const dfm_grid* g, const void* d_fixed
  * 0 lncc/ssd forward, 1 lncc backward, 2 smooth+adam, 3 compose+smooth,
  * 4 monitor, 5 pyramid (down/upsample), 6 epilogue. */
 #define DFM_NUM_KCLASS 7
-dfm_status dfm_ctx_set_profiling(dfm_ctx* ctx, int enable);
-dfm_status dfm_ctx_kernel_times(const dfm_ctx* ctx, double* ms, int64_t* launches,
+DFM_API dfm_status dfm_ctx_set_profiling(dfm_ctx* ctx, int enable);
+DFM_API dfm_status dfm_ctx_kernel_times(const dfm_ctx* ctx, double* ms, int64_t* launches,
                                 int64_t* voxels);
 
 #ifdef __cplusplus

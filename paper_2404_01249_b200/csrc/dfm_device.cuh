@@ -1,0 +1,273 @@
+// dfm_device.cuh — device-side building blocks shared by every kernel.
+//
+// Layout in HBM: every scalar volume is one
+// x-fastest plane array of T (float or double); every vector field is three
+// such arrays (SoA: x-, y-, z-component planes), so a warp reading 32
+// consecutive voxels of one component issues one 128 B (fp32) transaction.
+// 2-D grids are 3-D grids with nz == 1 and a zero z component.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dfm {
+
+struct Dims {
+    int nx, ny, nz;  // nz == 1 for 2-D grids
+    int ndim;
+    int64_t n;       // nx*ny*nz
+    __host__ __device__ int64_t idx(int x, int y, int z) const {
+        return (static_cast<int64_t>(z) * ny + y) * nx + x;
+    }
+    __host__ __device__ bool is3d() const { return nz > 1; }
+};
+
+template <class T>
+struct Planes3 {  // SoA vector field
+    T* c[3];
+};
+
+template <class T>
+struct CPlanes3 {
+    const T* c[3];
+};
+
+// ---------------------------------------------------------------------------
+// Trilinear interpolation with clamp-to-edge, the reference's `locate`
+// (interp.cpp:19-37): p clamped to [0, n-1]; lower node clamped to [0, n-2];
+// `clamped` marks points that were outside [0, n-1] (zero gradient there,
+// interp.cpp:171-173).
+//
+// fp64 follows the reference formulation (p = x + u in double, floor).  fp32
+// splits the sample position into integer x + floor(u) and the exact fraction
+// u - floor(u), so the fp32 cell decision is the exact real-number one
+// (SURVEY.md §7 hard part 2) instead of rounding x + u first.
+template <class T>
+struct AxisCell {
+    int i0;
+    T f;
+    bool clamped;
+};
+
+__device__ __forceinline__ AxisCell<double> locate_axis(int xi, double u, int n) {
+    AxisCell<double> c;
+    if (n == 1) {
+        c.i0 = 0;
+        c.f = 0.0;
+        c.clamped = false;
+        return c;
+    }
+    double p = static_cast<double>(xi) + u;
+    const double hi = static_cast<double>(n - 1);
+    c.clamped = (p < 0.0 || p > hi);
+    p = p < 0.0 ? 0.0 : (hi < p ? hi : p);
+    double fl = floor(p);
+    int i = (fl == fl) ? static_cast<int>(fl) : 0;  // NaN -> 0 like the cast
+    i = i < 0 ? 0 : (i > n - 2 ? n - 2 : i);
+    c.i0 = i;
+    c.f = p - static_cast<double>(i);
+    return c;
+}
+
+__device__ __forceinline__ AxisCell<float> locate_axis(int xi, float u, int n) {
+    AxisCell<float> c;
+    if (n == 1) {
+        c.i0 = 0;
+        c.f = 0.f;
+        c.clamped = false;
+        return c;
+    }
+    float fl = floorf(u);
+    const float fr = u - fl;  // exact
+    fl = fminf(fmaxf(fl, -1.0e9f), 1.0e9f);
+    const int i = xi + static_cast<int>(fl);
+    if (i < 0) {
+        c.clamped = true;
+        c.i0 = 0;
+        c.f = 0.f;
+    } else if (i >= n - 1) {
+        c.clamped = (i > n - 1) || (fr > 0.f);
+        c.i0 = n - 2;
+        c.f = 1.f;
+    } else {
+        c.clamped = false;
+        c.i0 = i;
+        c.f = fr;
+    }
+    return c;
+}
+
+template <class T>
+struct Cell3 {
+    int64_t base;  // index of the lower corner
+    int sx, sy;    // +x / +y corner offsets (0 on flat axes)
+    int64_t sz;    // +z corner offset (0 for 2-D)
+    T fx, fy, fz;
+    bool clx, cly, clz;
+    bool three;
+};
+
+template <class T>
+__device__ __forceinline__ Cell3<T> locate3(const Dims& m, int x, int y, int z, T ux, T uy,
+                                            T uz) {
+    Cell3<T> c;
+    const AxisCell<T> ax = locate_axis(x, ux, m.nx);
+    const AxisCell<T> ay = locate_axis(y, uy, m.ny);
+    c.three = m.nz > 1;
+    AxisCell<T> az;
+    if (c.three) {
+        az = locate_axis(z, uz, m.nz);
+    } else {
+        az.i0 = 0;
+        az.f = T(0);
+        az.clamped = false;
+    }
+    c.fx = ax.f;
+    c.fy = ay.f;
+    c.fz = az.f;
+    c.clx = ax.clamped;
+    c.cly = ay.clamped;
+    c.clz = az.clamped;
+    c.sx = m.nx > 1 ? 1 : 0;
+    c.sy = m.ny > 1 ? m.nx : 0;
+    c.sz = c.three ? static_cast<int64_t>(m.nx) * m.ny : 0;
+    c.base = m.idx(ax.i0, ay.i0, az.i0);
+    return c;
+}
+
+// Sample point given as grid coordinate (x,y,z) of a voxel of the FIXED grid
+// plus displacement u — the only form the hot path needs.
+template <class T>
+struct Corners {
+    T v[8];  // order (cz, cy, cx) as in interp.cpp:159-162
+};
+
+template <class T, class S>
+__device__ __forceinline__ Corners<T> fetch_corners(const S* __restrict__ img, const Cell3<T>& c) {
+    Corners<T> k;
+    const S* p = img + c.base;
+    k.v[0] = static_cast<T>(__ldg(p));
+    k.v[1] = static_cast<T>(__ldg(p + c.sx));
+    k.v[2] = static_cast<T>(__ldg(p + c.sy));
+    k.v[3] = static_cast<T>(__ldg(p + c.sy + c.sx));
+    if (c.three) {
+        k.v[4] = static_cast<T>(__ldg(p + c.sz));
+        k.v[5] = static_cast<T>(__ldg(p + c.sz + c.sx));
+        k.v[6] = static_cast<T>(__ldg(p + c.sz + c.sy));
+        k.v[7] = static_cast<T>(__ldg(p + c.sz + c.sy + c.sx));
+    } else {
+        k.v[4] = k.v[5] = k.v[6] = k.v[7] = T(0);
+    }
+    return k;
+}
+
+// value (interp.cpp:155-164)
+template <class T>
+__device__ __forceinline__ T lerp_value(const Cell3<T>& c, const Corners<T>& k) {
+    const T wx0 = T(1) - c.fx, wx1 = c.fx;
+    const T wy0 = T(1) - c.fy, wy1 = c.fy;
+    const T wz0 = T(1) - c.fz, wz1 = c.fz;
+    T acc = (wx0 * wy0 * wz0) * k.v[0] + (wx1 * wy0 * wz0) * k.v[1] +
+            (wx0 * wy1 * wz0) * k.v[2] + (wx1 * wy1 * wz0) * k.v[3];
+    if (c.three)
+        acc += (wx0 * wy0 * wz1) * k.v[4] + (wx1 * wy0 * wz1) * k.v[5] +
+               (wx0 * wy1 * wz1) * k.v[6] + (wx1 * wy1 * wz1) * k.v[7];
+    return acc;
+}
+
+// exact interpolant gradient (interp.cpp:166-186); zero on clamped/flat axes
+template <class T>
+__device__ __forceinline__ void lerp_grad(const Cell3<T>& c, const Corners<T>& k, int ndim,
+                                          T g[3]) {
+    const T wx0 = T(1) - c.fx, wx1 = c.fx;
+    const T wy0 = T(1) - c.fy, wy1 = c.fy;
+    const T wz0 = T(1) - c.fz, wz1 = c.fz;
+    g[0] = g[1] = g[2] = T(0);
+    if (!c.clx && c.sx) {
+        T a = (wy0 * wz0) * (k.v[1] - k.v[0]) + (wy1 * wz0) * (k.v[3] - k.v[2]);
+        if (c.three) a += (wy0 * wz1) * (k.v[5] - k.v[4]) + (wy1 * wz1) * (k.v[7] - k.v[6]);
+        g[0] = a;
+    }
+    if (!c.cly && c.sy) {
+        T a = (wx0 * wz0) * (k.v[2] - k.v[0]) + (wx1 * wz0) * (k.v[3] - k.v[1]);
+        if (c.three) a += (wx0 * wz1) * (k.v[6] - k.v[4]) + (wx1 * wz1) * (k.v[7] - k.v[5]);
+        g[1] = a;
+    }
+    if (ndim == 3 && c.three && !c.clz) {
+        g[2] = (wx0 * wy0) * (k.v[4] - k.v[0]) + (wx1 * wy0) * (k.v[5] - k.v[1]) +
+               (wx0 * wy1) * (k.v[6] - k.v[2]) + (wx1 * wy1) * (k.v[7] - k.v[3]);
+    }
+}
+
+// per-component field sample (interp.cpp:188-203)
+template <class T>
+__device__ __forceinline__ void lerp_field(const Cell3<T>& c, const T* __restrict__ f0,
+                                           const T* __restrict__ f1, const T* __restrict__ f2,
+                                           int ndim, T out[3]) {
+    Corners<T> k = fetch_corners<T>(f0, c);
+    out[0] = lerp_value(c, k);
+    k = fetch_corners<T>(f1, c);
+    out[1] = lerp_value(c, k);
+    if (ndim == 3) {
+        k = fetch_corners<T>(f2, c);
+        out[2] = lerp_value(c, k);
+    } else {
+        out[2] = T(0);
+    }
+}
+
+// clipped box-window length along one axis: |[i-r, i+r] ∩ [0, n-1]|
+__device__ __forceinline__ int box_len(int i, int n, int r) {
+    const int lo = i - r < 0 ? 0 : i - r;
+    const int hi = i + r > n - 1 ? n - 1 : i + r;
+    return hi - lo + 1;
+}
+
+template <class T>
+__device__ __forceinline__ bool finite_(T v) {
+    return isfinite(v);
+}
+
+// non-negative float/double -> monotone unsigned key for atomicMax
+__device__ __forceinline__ void atomic_max_nonneg(unsigned long long* slot, double v) {
+    atomicMax(slot, static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+// jacobian (interp.cpp:291-328) at one voxel: J[c][a] = du_c/dx_a + delta
+template <class T>
+__device__ __forceinline__ void jacobian_at(CPlanes3<T> u, const Dims& d, int x, int y, int z,
+                                            T J[9]) {
+    const int pos[3] = {x, y, z};
+    const int n[3] = {d.nx, d.ny, d.nz};
+    const int64_t stride[3] = {1, d.nx, static_cast<int64_t>(d.nx) * d.ny};
+    const int64_t i = d.idx(x, y, z);
+    for (int k = 0; k < 9; ++k) J[k] = T(0);
+    for (int a = 0; a < d.ndim; ++a) {
+        int64_t lo, hi;
+        T den;
+        if (pos[a] == 0) {
+            lo = i;
+            hi = i + stride[a];
+            den = T(1);
+        } else if (pos[a] == n[a] - 1) {
+            lo = i - stride[a];
+            hi = i;
+            den = T(1);
+        } else {
+            lo = i - stride[a];
+            hi = i + stride[a];
+            den = T(2);
+        }
+        for (int c = 0; c < d.ndim; ++c)
+            J[c * d.ndim + a] = (__ldg(u.c[c] + hi) - __ldg(u.c[c] + lo)) / den + (c == a ? T(1) : T(0));
+    }
+}
+
+template <class T>
+__device__ __forceinline__ T det_of(const T* j, int nd) {
+    if (nd == 2) return j[0] * j[3] - j[1] * j[2];
+    return j[0] * (j[4] * j[8] - j[5] * j[7]) - j[1] * (j[3] * j[8] - j[5] * j[6]) +
+           j[2] * (j[3] * j[7] - j[4] * j[6]);
+}
+
+}  // namespace dfm

@@ -1,0 +1,144 @@
+// dfm_kernels.cuh — host-callable launchers for every kernel of the path.
+// Definitions live in kernels_*.cu with explicit float/double instantiations.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "dfm_device.cuh"
+
+namespace dfm {
+
+constexpr int kRMax = 8;          // largest radius of the fused z-march kernels
+constexpr int kTX = 32, kTY = 8;  // z-march CTA tile (x, y)
+
+// Device-resident loop bookkeeping for one registration (SURVEY §7 hard part 5:
+// the convergence monitor runs on the device so the host never waits per
+// iteration).
+struct LoopState {
+    int it;          // next record slot within the current scale
+    int slot;        // slot of the iteration being processed
+    int done;        // scale finished (converged) or failed
+    int err;         // 0 ok, 2 numerical failure
+    int converged;   // convergence monitor fired this scale
+    int nupdates;    // updates applied this scale
+    int bad_step;    // non-finite step seen (diffeo.cpp:52-59)
+    int pad_;
+    long long t;     // Adam step counter (optim.cpp:26), kept across scales
+    double dice_p;   // dice: sum F*W
+    double dice_d;   // dice: SF + SM + 1e-7
+};
+
+// Kernel launch bookkeeping handed to every launcher.
+struct Launch {
+    cudaStream_t stream;
+    int64_t* counter;  // incremented per kernel launch (host side)
+    int num_sms;
+    void bump() const {
+        if (counter) ++*counter;
+    }
+};
+
+// Gaussian weights of one smoothing call (interp.cpp:114-123), per axis, padded
+// with zero taps to a common radius; norm = 1 / (in-range tap sum) per position.
+template <class A>
+struct GaussW {
+    A taps[3][2 * kRMax + 1];
+    const A* norm[3];
+};
+
+// -------- conversions / staging
+template <class T, class S>
+void launch_cast(const Launch& L, const S* in, T* out, int64_t n);
+template <class T, class S>
+void launch_aos_to_soa(const Launch& L, const S* aos, Planes3<T> out, int64_t n, int ndim);
+template <class T, class S>
+void launch_soa_to_aos(const Launch& L, CPlanes3<T> in, S* aos, int64_t n, int ndim);
+template <class T>
+void launch_fill(const Launch& L, T* p, int64_t n, T v);
+
+// -------- pointwise / gather kernels
+template <class T>
+void launch_sample_points(const Launch& L, const T* img, Dims d, const double* pts, int64_t np,
+                          double* vals, double* grads);
+template <class T>
+void launch_warp_image(const Launch& L, const T* img, Dims dimg, CPlanes3<T> u, Dims d, T* out);
+template <class T>
+void launch_warp_labels(const Launch& L, const int32_t* lab, CPlanes3<T> u, Dims d,
+                        int32_t* out);
+template <class T>
+void launch_compose(const Launch& L, CPlanes3<T> phi, CPlanes3<T> psi, Dims d, Planes3<T> out);
+template <class T>
+void launch_jacobian_det(const Launch& L, CPlanes3<T> u, Dims d, T* det,
+                         unsigned long long* nonpos);
+template <class T>
+void launch_eulerian(const Launch& L, CPlanes3<T> g, CPlanes3<T> u, Dims d, int use_jac,
+                     Planes3<T> out);
+template <class T>
+void launch_adam(const Launch& L, Planes3<T> m, Planes3<T> nu, CPlanes3<T> v, Planes3<T> dir,
+                 Dims d, double b1, double b2, double c1, double c2, double eps);
+template <class T>
+void launch_clamp_step(const Launch& L, CPlanes3<T> v, Planes3<T> step, Dims d, double eta,
+                       double cap, int* bad);
+template <class T>
+void launch_resample(const Launch& L, const T* const* src, Dims ds, T* const* dst, Dims dd,
+                     int ncomp, const double* mult);
+template <class T>
+void launch_affine_field(const Launch& L, const double* A, const double* t, const double* S,
+                         Dims d, Planes3<T> out);
+template <class T>
+void launch_gauss_axis(const Launch& L, const T* in, T* out, Dims d, int axis, int R,
+                       const double* taps, const double* norm, const LoopState* st = nullptr);
+template <class T>
+void launch_range_check(const Launch& L, const T* p, int64_t n, int* bad);
+
+// -------- losses
+// per-CTA partial sums (double) into `partials`; returns number of partials.
+template <class T>
+int launch_ssd(const Launch& L, const T* F, const T* M, Dims d, Dims dm, CPlanes3<T> u,
+               Planes3<T> grad, double* partials, const LoopState* st);
+template <class T>
+int launch_dice_sums(const Launch& L, const T* F, const T* M, Dims d, Dims dm, CPlanes3<T> u,
+                     double* partials, const LoopState* st);
+template <class T>
+void launch_dice_grad(const Launch& L, const T* F, const T* M, Dims d, Dims dm, CPlanes3<T> u,
+                      Planes3<T> grad, const LoopState* st, double P, double D);
+template <class T>
+int launch_lncc_fwd(const Launch& L, int R, const T* F, const T* M, Dims d, Dims dm,
+                    CPlanes3<T> u, T* const* coef, double* partials, const LoopState* st);
+template <class T>
+void launch_lncc_bwd(const Launch& L, int R, const T* F, const T* M, Dims d, Dims dm,
+                     CPlanes3<T> u, const T* const* coef, Planes3<T> grad, const LoopState* st);
+
+// -------- fused update kernels
+struct AdamParams {
+    double b1, b2, eps, eta, cap;
+    const double* corr1;  // 1 - b1^t, indexed by t (host std::pow, optim.cpp:27-28)
+    const double* corr2;
+    int use_jac;
+};
+template <class T>
+void launch_smooth_adam(const Launch& L, int R, const GaussW<T>& w, CPlanes3<T> grad,
+                        CPlanes3<T> u, Planes3<T> m, Planes3<T> nu, Planes3<T> step, Dims d,
+                        AdamParams ap, LoopState* st, unsigned long long* maxstep_slots);
+template <class T>
+void launch_compose_smooth(const Launch& L, int R, const GaussW<T>& w, CPlanes3<T> step,
+                           CPlanes3<T> u_in, Planes3<T> u_out, Dims d, LoopState* st);
+// plain fused Gaussian (gaussian_smooth / gaussian_smooth_field), ncomp 1..3
+template <class T>
+void launch_gauss_fused(const Launch& L, int R, const GaussW<T>& w, CPlanes3<T> in,
+                        Planes3<T> out, int ncomp, Dims d);
+
+// -------- loop control
+// kind: 0 ssd, 1 lncc, 2 dice (3 partial arrays of np each)
+void launch_monitor(const Launch& L, int kind, const double* partials, int np, double nvox,
+                    LoopState* st, double* loss, unsigned long long* stamp, int window,
+                    double tol);
+// value-only reduction (epilogue / per-call API): out = kind-specific value
+void launch_reduce_value(const Launch& L, int kind, const double* partials, int np, double nvox,
+                         double* out);
+void launch_stamp(const Launch& L, unsigned long long* slot);
+
+int zmarch_blocks(Dims d, int R, int num_sms, int* zchunk, int* tiles);
+
+}  // namespace dfm

@@ -1,0 +1,1527 @@
+// engine.cu — the C-ABI (include/difform_gpu.h): context, staging, the
+// per-function entry points and the device-resident register_images driver.
+//
+// Host side of the boundary: plain pointers in, status codes out.  Inside, a
+// dfm_ctx owns a CUDA stream, a named workspace arena (grown on demand, reused
+// across calls), two captured CUDA graphs per pyramid scale (ping-pong of the
+// displacement buffers) and an event pool for optional per-kernel timing.
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <type_traits>
+#include <vector>
+#include <cstddef>
+
+#include <cuda_runtime.h>
+
+#include "../../include/difform_gpu.h"
+#include "dfm_device.cuh"
+#include "dfm_kernels.cuh"
+
+using namespace dfm;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct DfmError {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    throw DfmError{code, buf};
+}
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(DFM_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CK(x) ck((x), #x)
+
+template <class F>
+dfm_status guarded(F&& fn) {
+    try {
+        fn();
+        return DFM_OK;
+    } catch (const DfmError& e) {
+        g_err = e.msg;
+        return static_cast<dfm_status>(e.code);
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return DFM_E_CUDA;
+    }
+}
+
+double now_ms() {
+    using clk = std::chrono::steady_clock;
+    return std::chrono::duration<double, std::milli>(clk::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// context
+
+struct dfm_ctx {
+    int device = 0;
+    int prec = DFM_PREC_F32;
+    cudaStream_t stream = nullptr;
+    int num_sms = 148;
+    int64_t launches = 0;
+    std::map<std::string, std::pair<void*, size_t>> bufs;
+    bool profiling = false;
+    double kt_ms[DFM_NUM_KCLASS] = {};
+    int64_t kt_n[DFM_NUM_KCLASS] = {};
+    int64_t kt_vox[DFM_NUM_KCLASS] = {};
+
+    LoopState* hstate = nullptr;  // 2 pinned slots for the chunked launch loop
+    cudaEvent_t chunk_ev[2] = {nullptr, nullptr};
+
+    Launch L() { return Launch{stream, &launches, num_sms}; }
+
+    LoopState* pinned_state() {
+        if (!hstate) {
+            CK(cudaMallocHost(&hstate, 2 * sizeof(LoopState)));
+            for (int k = 0; k < 2; ++k)
+                CK(cudaEventCreateWithFlags(&chunk_ev[k], cudaEventDisableTiming));
+        }
+        return hstate;
+    }
+
+    void* get(const std::string& name, size_t bytes) {
+        if (bytes == 0) bytes = 16;
+        auto it = bufs.find(name);
+        if (it != bufs.end() && it->second.second >= bytes) return it->second.first;
+        if (it != bufs.end()) {
+            CK(cudaStreamSynchronize(stream));
+            CK(cudaFree(it->second.first));
+            bufs.erase(it);
+        }
+        void* p = nullptr;
+        CK(cudaMalloc(&p, bytes));
+        bufs[name] = {p, bytes};
+        return p;
+    }
+    template <class T>
+    T* arr(const std::string& name, int64_t n) {
+        return static_cast<T*>(get(name, sizeof(T) * static_cast<size_t>(n)));
+    }
+    void sync() { CK(cudaStreamSynchronize(stream)); }
+    void check_launch() { CK(cudaGetLastError()); }
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// validation (core.cpp:26-37 etc.)
+
+void validate_grid(const dfm_grid* g) {
+    if (!g) fail(DFM_E_INVALID, "grid is NULL");
+    if (g->ndim != 2 && g->ndim != 3) fail(DFM_E_INVALID, "grid must have 2 or 3 axes");
+    for (int a = 0; a < g->ndim; ++a) {
+        if (g->dims[a] < 2) fail(DFM_E_INVALID, "grid dims must be >= 2 per axis");
+        if (!(g->spacing[a] > 0.0) || !std::isfinite(g->spacing[a]))
+            fail(DFM_E_INVALID, "grid spacing must be > 0");
+    }
+    if (g->ndim == 2 && g->dims[2] != 1) fail(DFM_E_INVALID, "2D grid must have dims[2] == 1");
+    const double n = static_cast<double>(g->dims[0]) * g->dims[1] * g->dims[2];
+    if (n >= 2147483647.0) fail(DFM_E_INVALID, "grid has more than 2^31-1 voxels");
+}
+
+Dims to_dims(const dfm_grid* g) {
+    Dims d;
+    d.nx = static_cast<int>(g->dims[0]);
+    d.ny = static_cast<int>(g->dims[1]);
+    d.nz = static_cast<int>(g->dims[2]);
+    d.ndim = g->ndim;
+    d.n = g->dims[0] * g->dims[1] * g->dims[2];
+    return d;
+}
+
+bool same_grid(const dfm_grid* a, const dfm_grid* b) {
+    return a->ndim == b->ndim && a->dims[0] == b->dims[0] && a->dims[1] == b->dims[1] &&
+           a->dims[2] == b->dims[2];
+}
+
+bool dims_equal(const Dims& a, const Dims& b) {
+    return a.nx == b.nx && a.ny == b.ny && a.nz == b.nz;
+}
+
+void downsample_grid(const dfm_grid* g, const double f[3], dfm_grid* out) {
+    validate_grid(g);
+    *out = *g;
+    for (int a = 0; a < g->ndim; ++a) {
+        if (!(f[a] >= 1.0)) fail(DFM_E_INVALID, "downsample factor must be >= 1");
+        out->dims[a] = static_cast<int64_t>(std::ceil(static_cast<double>(g->dims[a]) / f[a]));
+        if (out->dims[a] < 2) fail(DFM_E_INVALID, "downsample would leave < 2 samples on an axis");
+        out->spacing[a] =
+            g->spacing[a] * (static_cast<double>(g->dims[a]) / static_cast<double>(out->dims[a]));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Gaussian weights (interp.cpp:110-124)
+
+struct HostGauss {
+    int R = 0;                          // common radius over axes
+    int Ra[3] = {0, 0, 0};
+    std::vector<double> taps[3];        // 2*Ra+1 each, normalised
+    std::vector<double> norm[3];        // 1 / in-range tap sum per position
+};
+
+HostGauss make_gauss(const Dims& d, const double sigma[3]) {
+    HostGauss h;
+    const int n[3] = {d.nx, d.ny, d.nz};
+    for (int a = 0; a < 3; ++a) {
+        const bool active = a < d.ndim && sigma[a] > 0.0 && n[a] > 1;
+        const int R = active ? static_cast<int>(std::ceil(3.0 * sigma[a])) : 0;
+        h.Ra[a] = R;
+        h.taps[a].assign(2 * R + 1, 0.0);
+        if (!active) {
+            h.taps[a][0] = 1.0;
+        } else {
+            double s = 0.0;
+            for (int j = -R; j <= R; ++j) {
+                const double q = static_cast<double>(j) / sigma[a];
+                h.taps[a][j + R] = std::exp(-0.5 * q * q);
+                s += h.taps[a][j + R];
+            }
+            for (double& t : h.taps[a]) t /= s;
+        }
+        h.norm[a].assign(n[a], 1.0);
+        if (active)
+            for (int i = 0; i < n[a]; ++i) {
+                const int jlo = -R > -i ? -R : -i;
+                const int jhi = R < n[a] - 1 - i ? R : n[a] - 1 - i;
+                double ws = 0.0;
+                for (int j = jlo; j <= jhi; ++j) ws += h.taps[a][j + R];
+                h.norm[a][i] = 1.0 / ws;
+            }
+        if (R > h.R) h.R = R;
+    }
+    return h;
+}
+
+template <class T>
+GaussW<T> upload_gauss(dfm_ctx* ctx, const HostGauss& h, const Dims& d, const std::string& key) {
+    GaussW<T> w{};
+    const int n[3] = {d.nx, d.ny, d.nz};
+    std::vector<T> host(static_cast<size_t>(n[0] + n[1] + n[2]));
+    size_t off = 0;
+    for (int a = 0; a < 3; ++a) {
+        for (int j = 0; j < 2 * kRMax + 1; ++j) w.taps[a][j] = T(0);
+        // center the axis taps inside the common radius
+        if (h.R <= kRMax)
+            for (int j = -h.Ra[a]; j <= h.Ra[a]; ++j)
+                w.taps[a][j + h.R] = static_cast<T>(h.taps[a][j + h.Ra[a]]);
+        for (int i = 0; i < n[a]; ++i) host[off + i] = static_cast<T>(h.norm[a][i]);
+        off += n[a];
+    }
+    T* dev = ctx->arr<T>("gauss_norm_" + key, static_cast<int64_t>(host.size()));
+    CK(cudaMemcpyAsync(dev, host.data(), host.size() * sizeof(T), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    w.norm[0] = dev;
+    w.norm[1] = dev + n[0];
+    w.norm[2] = dev + n[0] + n[1];
+    return w;
+}
+
+// per-axis generic path for radii above kRMax (pyramid pre-blur, large sigma)
+struct DevAxisGauss {
+    int Ra[3];
+    const double* taps[3];
+    const double* norm[3];
+};
+
+DevAxisGauss upload_axis_gauss(dfm_ctx* ctx, const HostGauss& h, const Dims& d,
+                               const std::string& key) {
+    DevAxisGauss g{};
+    const int n[3] = {d.nx, d.ny, d.nz};
+    std::vector<double> host;
+    size_t offs[6];
+    for (int a = 0; a < 3; ++a) {
+        offs[2 * a] = host.size();
+        host.insert(host.end(), h.taps[a].begin(), h.taps[a].end());
+        offs[2 * a + 1] = host.size();
+        host.insert(host.end(), h.norm[a].begin(), h.norm[a].end());
+    }
+    double* dev = ctx->arr<double>("axis_gauss_" + key, static_cast<int64_t>(host.size()));
+    CK(cudaMemcpyAsync(dev, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    for (int a = 0; a < 3; ++a) {
+        g.Ra[a] = h.Ra[a];
+        g.taps[a] = dev + offs[2 * a];
+        g.norm[a] = dev + offs[2 * a + 1];
+    }
+    (void)n;
+    return g;
+}
+
+// Gaussian of one plane through the generic per-axis kernel: src -> dst,
+// `tmp` as the ping-pong partner; dst may equal src.
+template <class T>
+void axis_smooth_plane(dfm_ctx* ctx, const Dims& d, const DevAxisGauss& g, const T* src, T* dst,
+                       T* tmp, const LoopState* st) {
+    Launch L = ctx->L();
+    const T* s = src;
+    for (int a = 0; a < 3; ++a) {
+        if (g.Ra[a] == 0) continue;
+        T* o = (s == dst) ? tmp : dst;
+        launch_gauss_axis<T>(L, s, o, d, a, g.Ra[a], g.taps[a], g.norm[a], st);
+        s = o;
+    }
+    if (s != dst)
+        CK(cudaMemcpyAsync(dst, s, sizeof(T) * d.n, cudaMemcpyDeviceToDevice, ctx->stream));
+}
+
+// smooth `ncomp` planes in -> out (fused z-march when the radius allows)
+template <class T>
+void smooth_planes(dfm_ctx* ctx, const Dims& d, const double sigma[3], CPlanes3<T> in,
+                   Planes3<T> out, int ncomp, const std::string& key) {
+    const HostGauss h = make_gauss(d, sigma);
+    if (h.R <= kRMax) {
+        const GaussW<T> w = upload_gauss<T>(ctx, h, d, key);
+        launch_gauss_fused<T>(ctx->L(), h.R, w, in, out, ncomp, d);
+        return;
+    }
+    const DevAxisGauss g = upload_axis_gauss(ctx, h, d, key);
+    T* tmp = ctx->arr<T>("smooth_tmp_" + key, d.n);
+    for (int c = 0; c < ncomp; ++c) axis_smooth_plane<T>(ctx, d, g, in.c[c], out.c[c], tmp, nullptr);
+}
+
+// ---------------------------------------------------------------------------
+// staging helpers (host AoS doubles <-> device SoA T)
+
+template <class T>
+struct Field {
+    T* p[3];
+    Planes3<T> w() const { return {{p[0], p[1], p[2]}}; }
+    CPlanes3<T> r() const { return {{p[0], p[1], p[2]}}; }
+};
+
+template <class T>
+Field<T> dev_field(dfm_ctx* ctx, const std::string& name, int64_t n) {
+    T* base = ctx->arr<T>(name, 3 * n);
+    return Field<T>{{base, base + n, base + 2 * n}};
+}
+
+template <class T, class S>
+void upload_image(dfm_ctx* ctx, const S* host, int64_t n, T* dst) {
+    if (std::is_same<T, S>::value) {
+        CK(cudaMemcpyAsync(dst, host, sizeof(S) * n, cudaMemcpyHostToDevice, ctx->stream));
+        return;
+    }
+    S* stage = ctx->arr<S>(std::is_same<S, double>::value ? "stage_d" : "stage_f", n);
+    CK(cudaMemcpyAsync(stage, host, sizeof(S) * n, cudaMemcpyHostToDevice, ctx->stream));
+    launch_cast<T, S>(ctx->L(), stage, dst, n);
+}
+
+template <class T>
+void upload_field(dfm_ctx* ctx, const double* host, int64_t n, int nd, const Field<T>& dst) {
+    double* stage = ctx->arr<double>("stage_d", n * nd);
+    CK(cudaMemcpyAsync(stage, host, sizeof(double) * n * nd, cudaMemcpyHostToDevice,
+                       ctx->stream));
+    launch_aos_to_soa<T, double>(ctx->L(), stage, dst.w(), n, nd);
+}
+
+template <class T, class S>
+void download_image(dfm_ctx* ctx, const T* src, int64_t n, S* host) {
+    if (std::is_same<T, S>::value) {
+        CK(cudaMemcpyAsync(host, src, sizeof(S) * n, cudaMemcpyDeviceToHost, ctx->stream));
+        return;
+    }
+    S* stage = ctx->arr<S>(std::is_same<S, double>::value ? "stage_d" : "stage_f", n);
+    launch_cast<S, T>(ctx->L(), src, stage, n);
+    CK(cudaMemcpyAsync(host, stage, sizeof(S) * n, cudaMemcpyDeviceToHost, ctx->stream));
+}
+
+template <class T, class S>
+void download_field(dfm_ctx* ctx, CPlanes3<T> src, int64_t n, int nd, S* host) {
+    S* stage = ctx->arr<S>(std::is_same<S, double>::value ? "stage_d" : "stage_f", n * nd);
+    launch_soa_to_aos<T, S>(ctx->L(), src, stage, n, nd);
+    CK(cudaMemcpyAsync(host, stage, sizeof(S) * n * nd, cudaMemcpyDeviceToHost, ctx->stream));
+}
+
+// ---------------------------------------------------------------------------
+// per-function implementations (templated on the device precision)
+
+template <class T>
+struct Impl {
+    dfm_ctx* ctx;
+
+    void downsample_dev(const Dims& d, const T* img, const double f[3], const Dims& od,
+                        T* out, const std::string& key) {
+        // core.cpp:66-95: sigma = f/2 pre-blur on axes with f > 1, then the
+        // corner-aligned resample; factor 1 everywhere -> bit copy.
+        double sigma[3] = {0.0, 0.0, 0.0};
+        bool blur = false;
+        for (int a = 0; a < d.ndim; ++a)
+            if (f[a] > 1.0) {
+                sigma[a] = f[a] / 2.0;
+                blur = true;
+            }
+        Launch L = ctx->L();
+        if (dims_equal(d, od) && !blur) {
+            CK(cudaMemcpyAsync(out, img, sizeof(T) * d.n, cudaMemcpyDeviceToDevice, ctx->stream));
+            return;
+        }
+        const T* src = img;
+        if (blur) {
+            const HostGauss h = make_gauss(d, sigma);
+            const DevAxisGauss g = upload_axis_gauss(ctx, h, d, "down_" + key);
+            T* b0 = ctx->arr<T>("down_tmp0", d.n);
+            T* b1 = ctx->arr<T>("down_tmp1", d.n);
+            T* bufs[2] = {b0, b1};
+            int k = 0;
+            for (int a = 0; a < d.ndim; ++a) {
+                if (h.Ra[a] == 0) continue;
+                launch_gauss_axis<T>(L, src, bufs[k], d, a, h.Ra[a], g.taps[a], g.norm[a]);
+                src = bufs[k];
+                k ^= 1;
+            }
+        }
+        const T* s1[1] = {src};
+        T* d1[1] = {out};
+        launch_resample<T>(L, s1, d, d1, od, 1, nullptr);
+    }
+};
+
+template <class T>
+int loss_kind_launch_fwd(dfm_ctx* ctx, int loss, int R, const T* F, const T* M, const Dims& d,
+                         const Dims& dm, CPlanes3<T> u, T* const* coef, Planes3<T> grad,
+                         double* partials, const LoopState* st) {
+    Launch L = ctx->L();
+    if (loss == DFM_LOSS_SSD) return launch_ssd<T>(L, F, M, d, dm, u, grad, partials, st);
+    if (loss == DFM_LOSS_DICE) return launch_dice_sums<T>(L, F, M, d, dm, u, partials, st);
+    return launch_lncc_fwd<T>(L, R, F, M, d, dm, u, coef, partials, st);
+}
+
+int monitor_kind(int loss) { return loss == DFM_LOSS_SSD ? 0 : (loss == DFM_LOSS_LNCC ? 1 : 2); }
+
+// one loss evaluation outside the loop (API lncc_eval / ssd_eval / dice, final loss)
+template <class T>
+double eval_loss_dev(dfm_ctx* ctx, int loss, int R, const T* F, const T* M, const Dims& d,
+                     const Dims& dm, CPlanes3<T> u, bool want_grad, Planes3<T> grad) {
+    Launch L = ctx->L();
+    double* partials = ctx->arr<double>("partials", 1 << 17);
+    double* val = ctx->arr<double>("value3", 4);
+    T* coef[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (loss == DFM_LOSS_LNCC && want_grad) {
+        T* cb = ctx->arr<T>("coef", 4 * d.n);
+        for (int k = 0; k < 4; ++k) coef[k] = cb + k * d.n;
+    }
+    Planes3<T> g = want_grad ? grad : Planes3<T>{{nullptr, nullptr, nullptr}};
+    const int np =
+        loss_kind_launch_fwd<T>(ctx, loss, R, F, M, d, dm, u, coef, g, partials, nullptr);
+    launch_reduce_value(L, monitor_kind(loss), partials, np, static_cast<double>(d.n), val);
+    double hv[3];
+    CK(cudaMemcpyAsync(hv, val, sizeof(hv), cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    if (want_grad) {
+        if (loss == DFM_LOSS_LNCC) {
+            const T* cc[4] = {coef[0], coef[1], coef[2], coef[3]};
+            launch_lncc_bwd<T>(L, R, F, M, d, dm, u, cc, grad, nullptr);
+        } else if (loss == DFM_LOSS_DICE) {
+            launch_dice_grad<T>(L, F, M, d, dm, u, grad, nullptr, hv[1], hv[2]);
+        }
+    }
+    return hv[0];
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+
+extern "C" {
+
+int dfm_abi_version(void) { return DFM_ABI_VERSION; }
+
+void dfm_config_defaults(dfm_config* c) {
+    if (!c) return;
+    std::memset(c, 0, sizeof(*c));
+    c->loss = DFM_LOSS_SSD;
+    c->lncc_radius = 2;
+    c->eta = 0.5;
+    c->sigma_grad = 1.0;
+    c->sigma_warp = 0.5;
+    c->use_jac = 0;
+    c->mode = DFM_MODE_DIRECT;
+    c->svf_M = 6;
+    c->beta1 = 0.9;
+    c->beta2 = 0.999;
+    c->eps_adam = 1e-8;
+    c->step_cap = 0.5;
+    c->conv_window = 10;
+    c->conv_tol = 1e-5;
+    c->seed = 0;
+}
+
+size_t dfm_last_error(char* buf, size_t cap) {
+    if (buf && cap) {
+        const size_t n = g_err.size() < cap - 1 ? g_err.size() : cap - 1;
+        std::memcpy(buf, g_err.data(), n);
+        buf[n] = 0;
+    }
+    return g_err.size();
+}
+
+dfm_status dfm_ctx_create(int device, int precision, dfm_ctx** out) {
+    return guarded([&] {
+        if (!out) fail(DFM_E_INVALID, "out is NULL");
+        if (precision != DFM_PREC_F32 && precision != DFM_PREC_F64)
+            fail(DFM_E_INVALID, "precision must be DFM_PREC_F32 or DFM_PREC_F64");
+        int count = 0;
+        CK(cudaGetDeviceCount(&count));
+        if (device < 0 || device >= count) fail(DFM_E_INVALID, "no CUDA device %d", device);
+        CK(cudaSetDevice(device));
+        auto* c = new dfm_ctx();
+        c->device = device;
+        c->prec = precision;
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+        *out = c;
+    });
+}
+
+void dfm_ctx_destroy(dfm_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& kv : ctx->bufs) cudaFree(kv.second.first);
+    if (ctx->hstate) cudaFreeHost(ctx->hstate);
+    for (int k = 0; k < 2; ++k)
+        if (ctx->chunk_ev[k]) cudaEventDestroy(ctx->chunk_ev[k]);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+int dfm_ctx_precision(const dfm_ctx* ctx) { return ctx ? ctx->prec : -1; }
+void* dfm_ctx_stream(dfm_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+int64_t dfm_ctx_launch_count(const dfm_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+dfm_status dfm_ctx_set_profiling(dfm_ctx* ctx, int enable) {
+    return guarded([&] {
+        if (!ctx) fail(DFM_E_INVALID, "ctx is NULL");
+        ctx->profiling = enable != 0;
+    });
+}
+
+dfm_status dfm_ctx_kernel_times(const dfm_ctx* ctx, double* ms, int64_t* launches,
+                                int64_t* voxels) {
+    return guarded([&] {
+        if (!ctx) fail(DFM_E_INVALID, "ctx is NULL");
+        for (int k = 0; k < DFM_NUM_KCLASS; ++k) {
+            if (ms) ms[k] = ctx->kt_ms[k];
+            if (launches) launches[k] = ctx->kt_n[k];
+            if (voxels) voxels[k] = ctx->kt_vox[k];
+        }
+    });
+}
+
+dfm_status dfm_validate_grid(const dfm_grid* g) {
+    return guarded([&] { validate_grid(g); });
+}
+
+dfm_status dfm_downsample_grid(const dfm_grid* g, const double factor[3], dfm_grid* out) {
+    return guarded([&] { downsample_grid(g, factor, out); });
+}
+
+}  // extern "C"
+
+// dispatch on the context precision
+#define DFM_DISPATCH(ctx, ...)                               \
+    do {                                                     \
+        if (!(ctx)) fail(DFM_E_INVALID, "ctx is NULL");      \
+        CK(cudaSetDevice((ctx)->device));                    \
+        if ((ctx)->prec == DFM_PREC_F64) {                   \
+            using T = double;                                \
+            __VA_ARGS__;                                     \
+        } else {                                             \
+            using T = float;                                 \
+            __VA_ARGS__;                                     \
+        }                                                    \
+        (ctx)->check_launch();                               \
+    } while (0)
+
+extern "C" {
+
+dfm_status dfm_downsample_image(dfm_ctx* ctx, const dfm_grid* g, const double* img,
+                                const double factor[3], dfm_grid* out_grid, double* out) {
+    return guarded([&] {
+        dfm_grid og;
+        downsample_grid(g, factor, &og);
+        const Dims d = to_dims(g), od = to_dims(&og);
+        DFM_DISPATCH(ctx, {
+            T* in = ctx->arr<T>("api_img0", d.n);
+            T* o = ctx->arr<T>("api_img1", od.n);
+            upload_image<T, double>(ctx, img, d.n, in);
+            Impl<T>{ctx}.downsample_dev(d, in, factor, od, o, "api");
+            download_image<T, double>(ctx, o, od.n, out);
+            ctx->sync();
+        });
+        *out_grid = og;
+    });
+}
+
+dfm_status dfm_sample_linear_points(dfm_ctx* ctx, const dfm_grid* g, const double* img,
+                                    int64_t npts, const double* points, double* values,
+                                    double* grads) {
+    return guarded([&] {
+        validate_grid(g);
+        const Dims d = to_dims(g);
+        DFM_DISPATCH(ctx, {
+            T* im = ctx->arr<T>("api_img0", d.n);
+            upload_image<T, double>(ctx, img, d.n, im);
+            double* pts = ctx->arr<double>("api_pts", 3 * npts + 1);
+            double* vals = ctx->arr<double>("api_vals", npts + 1);
+            double* grs = ctx->arr<double>("api_grads", 3 * npts + 1);
+            if (npts > 0) {
+                CK(cudaMemcpyAsync(pts, points, sizeof(double) * 3 * npts, cudaMemcpyHostToDevice,
+                                   ctx->stream));
+                launch_sample_points<T>(ctx->L(), im, d, pts, npts, vals, grads ? grs : nullptr);
+                CK(cudaMemcpyAsync(values, vals, sizeof(double) * npts, cudaMemcpyDeviceToHost,
+                                   ctx->stream));
+                if (grads)
+                    CK(cudaMemcpyAsync(grads, grs, sizeof(double) * 3 * npts,
+                                       cudaMemcpyDeviceToHost, ctx->stream));
+            }
+            ctx->sync();
+        });
+    });
+}
+
+dfm_status dfm_warp_image(dfm_ctx* ctx, const dfm_grid* g, const double* img, const double* phi,
+                          double* out) {
+    return guarded([&] {
+        validate_grid(g);
+        const Dims d = to_dims(g);
+        DFM_DISPATCH(ctx, {
+            T* im = ctx->arr<T>("api_img0", d.n);
+            T* o = ctx->arr<T>("api_img1", d.n);
+            Field<T> u = dev_field<T>(ctx, "api_f0", d.n);
+            upload_image<T, double>(ctx, img, d.n, im);
+            upload_field<T>(ctx, phi, d.n, d.ndim, u);
+            launch_warp_image<T>(ctx->L(), im, d, u.r(), d, o);
+            download_image<T, double>(ctx, o, d.n, out);
+            ctx->sync();
+        });
+    });
+}
+
+dfm_status dfm_warp_labels(dfm_ctx* ctx, const dfm_grid* g, const int32_t* labels,
+                           const double* phi, int32_t* out) {
+    return guarded([&] {
+        validate_grid(g);
+        const Dims d = to_dims(g);
+        DFM_DISPATCH(ctx, {
+            int32_t* lab = ctx->arr<int32_t>("api_lab0", d.n);
+            int32_t* o = ctx->arr<int32_t>("api_lab1", d.n);
+            Field<T> u = dev_field<T>(ctx, "api_f0", d.n);
+            CK(cudaMemcpyAsync(lab, labels, sizeof(int32_t) * d.n, cudaMemcpyHostToDevice,
+                               ctx->stream));
+            upload_field<T>(ctx, phi, d.n, d.ndim, u);
+            launch_warp_labels<T>(ctx->L(), lab, u.r(), d, o);
+            CK(cudaMemcpyAsync(out, o, sizeof(int32_t) * d.n, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+            ctx->sync();
+        });
+    });
+}
+
+dfm_status dfm_compose(dfm_ctx* ctx, const dfm_grid* g, const double* phi, const double* psi,
+                       double* out) {
+    return guarded([&] {
+        validate_grid(g);
+        const Dims d = to_dims(g);
+        DFM_DISPATCH(ctx, {
+            Field<T> a = dev_field<T>(ctx, "api_f0", d.n);
+            Field<T> b = dev_field<T>(ctx, "api_f1", d.n);
+            Field<T> o = dev_field<T>(ctx, "api_f2", d.n);
+            upload_field<T>(ctx, phi, d.n, d.ndim, a);
+            upload_field<T>(ctx, psi, d.n, d.ndim, b);
+            launch_compose<T>(ctx->L(), a.r(), b.r(), d, o.w());
+            download_field<T, double>(ctx, o.r(), d.n, d.ndim, out);
+            ctx->sync();
+        });
+    });
+}
+
+dfm_status dfm_jacobian_det(dfm_ctx* ctx, const dfm_grid* g, const double* phi, double* out) {
+    return guarded([&] {
+        validate_grid(g);
+        const Dims d = to_dims(g);
+        DFM_DISPATCH(ctx, {
+            Field<T> a = dev_field<T>(ctx, "api_f0", d.n);
+            T* o = ctx->arr<T>("api_img0", d.n);
+            upload_field<T>(ctx, phi, d.n, d.ndim, a);
+            launch_jacobian_det<T>(ctx->L(), a.r(), d, o, nullptr);
+            download_image<T, double>(ctx, o, d.n, out);
+            ctx->sync();
+        });
+    });
+}
+
+dfm_status dfm_singularity_fraction(dfm_ctx* ctx, const dfm_grid* g, const double* phi,
+                                    double* fraction) {
+    return guarded([&] {
+        validate_grid(g);
+        const Dims d = to_dims(g);
+        DFM_DISPATCH(ctx, {
+            Field<T> a = dev_field<T>(ctx, "api_f0", d.n);
+            auto* cnt = ctx->arr<unsigned long long>("api_count", 1);
+            upload_field<T>(ctx, phi, d.n, d.ndim, a);
+            CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), ctx->stream));
+            launch_jacobian_det<T>(ctx->L(), a.r(), d, nullptr, cnt);
+            unsigned long long h = 0;
+            CK(cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+            ctx->sync();
+            *fraction = static_cast<double>(h) / static_cast<double>(d.n);
+        });
+    });
+}
+
+static dfm_status smooth_api(dfm_ctx* ctx, const dfm_grid* g, const double* in,
+                             const double sigma[3], double* out, bool field) {
+    return guarded([&] {
+        validate_grid(g);
+        for (int a = 0; a < g->ndim; ++a)
+            if (sigma[a] < 0.0)
+                fail(DFM_E_INVALID, field ? "gaussian_smooth_field: sigma must be >= 0"
+                                          : "gaussian_smooth: sigma must be >= 0");
+        const Dims d = to_dims(g);
+        DFM_DISPATCH(ctx, {
+            Field<T> a = dev_field<T>(ctx, "api_f0", d.n);
+            Field<T> o = dev_field<T>(ctx, "api_f1", d.n);
+            if (field)
+                upload_field<T>(ctx, in, d.n, d.ndim, a);
+            else
+                upload_image<T, double>(ctx, in, d.n, a.p[0]);
+            const int nc = field ? 3 : 1;
+            smooth_planes<T>(ctx, d, sigma, a.r(), o.w(), nc, "api");
+            if (field)
+                download_field<T, double>(ctx, o.r(), d.n, d.ndim, out);
+            else
+                download_image<T, double>(ctx, o.p[0], d.n, out);
+            ctx->sync();
+        });
+    });
+}
+
+dfm_status dfm_gaussian_smooth(dfm_ctx* ctx, const dfm_grid* g, const double* img,
+                               const double sigma[3], double* out) {
+    return smooth_api(ctx, g, img, sigma, out, false);
+}
+
+dfm_status dfm_gaussian_smooth_field(dfm_ctx* ctx, const dfm_grid* g, const double* f,
+                                     const double sigma[3], double* out) {
+    return smooth_api(ctx, g, f, sigma, out, true);
+}
+
+// resample kinds: 0 resample_field_linear, 1 upsample_field, 2 resample_displacement
+static dfm_status resample_api(dfm_ctx* ctx, const dfm_grid* g, const double* f,
+                               const dfm_grid* ng, double* out, int kind) {
+    static const char* names[3] = {"resample_field_linear", "upsample_field",
+                                   "resample_displacement"};
+    return guarded([&] {
+        validate_grid(g);
+        validate_grid(ng);
+        if (ng->ndim != g->ndim) fail(DFM_E_INVALID, "%s: dimensionality mismatch", names[kind]);
+        if (kind == 1)
+            for (int a = 0; a < g->ndim; ++a)
+                if (ng->dims[a] < g->dims[a])
+                    fail(DFM_E_INVALID, "upsample_field: shrinking not allowed");
+        const Dims d = to_dims(g), nd = to_dims(ng);
+        if (dims_equal(d, nd)) {  // returned unchanged (interp.cpp:386-387, 417-418, 452-453)
+            std::memmove(out, f, sizeof(double) * d.n * d.ndim);
+            return;
+        }
+        double mult[3] = {1.0, 1.0, 1.0};
+        if (kind != 0)
+            for (int a = 0; a < g->ndim; ++a)
+                mult[a] = static_cast<double>(ng->dims[a] - 1) / static_cast<double>(g->dims[a] - 1);
+        DFM_DISPATCH(ctx, {
+            Field<T> a = dev_field<T>(ctx, "api_f0", d.n);
+            Field<T> o = dev_field<T>(ctx, "api_f1", nd.n);
+            upload_field<T>(ctx, f, d.n, d.ndim, a);
+            const T* src[3] = {a.p[0], a.p[1], a.p[2]};
+            T* dst[3] = {o.p[0], o.p[1], o.p[2]};
+            launch_resample<T>(ctx->L(), src, d, dst, nd, d.ndim, mult);
+            download_field<T, double>(ctx, o.r(), nd.n, nd.ndim, out);
+            ctx->sync();
+        });
+    });
+}
+
+dfm_status dfm_upsample_field(dfm_ctx* ctx, const dfm_grid* g, const double* phi,
+                              const dfm_grid* new_grid, double* out) {
+    return resample_api(ctx, g, phi, new_grid, out, 1);
+}
+dfm_status dfm_resample_field_linear(dfm_ctx* ctx, const dfm_grid* g, const double* f,
+                                     const dfm_grid* new_grid, double* out) {
+    return resample_api(ctx, g, f, new_grid, out, 0);
+}
+dfm_status dfm_resample_displacement(dfm_ctx* ctx, const dfm_grid* g, const double* phi,
+                                     const dfm_grid* new_grid, double* out) {
+    return resample_api(ctx, g, phi, new_grid, out, 2);
+}
+
+static dfm_status loss_api(dfm_ctx* ctx, int loss, const dfm_grid* fg, const double* fixed,
+                           const dfm_grid* mg, const double* moving, const double* phi, int R,
+                           double* value, double* grad) {
+    static const char* names[3] = {"ssd_eval", "lncc_eval", "dice_soft_eval"};
+    return guarded([&] {
+        validate_grid(fg);
+        validate_grid(mg);
+        if (fg->ndim != mg->ndim) fail(DFM_E_INVALID, "%s: dimensionality mismatch", names[loss]);
+        if (loss == DFM_LOSS_LNCC) {
+            if (R < 1) fail(DFM_E_INVALID, "lncc_eval: window_radius must be >= 1");
+            for (int a = 0; a < fg->ndim; ++a)
+                if (2 * static_cast<int64_t>(R) + 1 > fg->dims[a])
+                    fail(DFM_E_INVALID, "lncc_eval: window larger than image");
+            if (R > kRMax) fail(DFM_E_INVALID, "lncc_eval: window_radius > %d unsupported", kRMax);
+        }
+        if (loss == DFM_LOSS_DICE) {
+            const int64_t nf = fg->dims[0] * fg->dims[1] * fg->dims[2];
+            const int64_t nm = mg->dims[0] * mg->dims[1] * mg->dims[2];
+            for (int64_t i = 0; i < nf; ++i)
+                if (!(fixed[i] >= 0.0 && fixed[i] <= 1.0))
+                    fail(DFM_E_INVALID, "dice_soft_eval: fixed mask values outside [0,1]");
+            for (int64_t i = 0; i < nm; ++i)
+                if (!(moving[i] >= 0.0 && moving[i] <= 1.0))
+                    fail(DFM_E_INVALID, "dice_soft_eval: moving mask values outside [0,1]");
+        }
+        const Dims d = to_dims(fg), dm = to_dims(mg);
+        DFM_DISPATCH(ctx, {
+            T* F = ctx->arr<T>("api_img0", d.n);
+            T* M = ctx->arr<T>("api_img1", dm.n);
+            Field<T> u = dev_field<T>(ctx, "api_f0", d.n);
+            Field<T> gr = dev_field<T>(ctx, "api_f1", d.n);
+            upload_image<T, double>(ctx, fixed, d.n, F);
+            upload_image<T, double>(ctx, moving, dm.n, M);
+            upload_field<T>(ctx, phi, d.n, d.ndim, u);
+            *value = eval_loss_dev<T>(ctx, loss, R, F, M, d, dm, u.r(), grad != nullptr, gr.w());
+            if (grad) download_field<T, double>(ctx, gr.r(), d.n, d.ndim, grad);
+            ctx->sync();
+        });
+    });
+}
+
+dfm_status dfm_ssd_eval(dfm_ctx* ctx, const dfm_grid* fg, const double* fixed, const dfm_grid* mg,
+                        const double* moving, const double* phi, double* value, double* grad) {
+    return loss_api(ctx, DFM_LOSS_SSD, fg, fixed, mg, moving, phi, 0, value, grad);
+}
+dfm_status dfm_lncc_eval(dfm_ctx* ctx, const dfm_grid* fg, const double* fixed,
+                         const dfm_grid* mg, const double* moving, const double* phi, int r,
+                         double* value, double* grad) {
+    return loss_api(ctx, DFM_LOSS_LNCC, fg, fixed, mg, moving, phi, r, value, grad);
+}
+dfm_status dfm_dice_eval(dfm_ctx* ctx, const dfm_grid* fg, const double* fixed,
+                         const dfm_grid* mg, const double* moving, const double* phi,
+                         double* value, double* grad) {
+    return loss_api(ctx, DFM_LOSS_DICE, fg, fixed, mg, moving, phi, 0, value, grad);
+}
+
+dfm_status dfm_adam_step(dfm_ctx* ctx, const dfm_grid* g, double* m, double* nu, int64_t* t,
+                         double b1, double b2, double eps, const double* v, double* dir) {
+    return guarded([&] {
+        validate_grid(g);
+        const Dims d = to_dims(g);
+        *t += 1;
+        const double c1 = 1.0 - std::pow(b1, static_cast<double>(*t));
+        const double c2 = 1.0 - std::pow(b2, static_cast<double>(*t));
+        DFM_DISPATCH(ctx, {
+            Field<T> fm = dev_field<T>(ctx, "api_f0", d.n);
+            Field<T> fn = dev_field<T>(ctx, "api_f1", d.n);
+            Field<T> fv = dev_field<T>(ctx, "api_f2", d.n);
+            Field<T> fd = dev_field<T>(ctx, "api_f3", d.n);
+            upload_field<T>(ctx, m, d.n, d.ndim, fm);
+            upload_field<T>(ctx, nu, d.n, d.ndim, fn);
+            upload_field<T>(ctx, v, d.n, d.ndim, fv);
+            launch_adam<T>(ctx->L(), fm.w(), fn.w(), fv.r(), fd.w(), d, b1, b2, c1, c2, eps);
+            download_field<T, double>(ctx, fm.r(), d.n, d.ndim, m);
+            download_field<T, double>(ctx, fn.r(), d.n, d.ndim, nu);
+            download_field<T, double>(ctx, fd.r(), d.n, d.ndim, dir);
+            ctx->sync();
+        });
+    });
+}
+
+dfm_status dfm_upsample_state(dfm_ctx* ctx, const dfm_grid* g, const double* m, const double* nu,
+                              const dfm_grid* ng, double* m_out, double* nu_out) {
+    return guarded([&] {
+        validate_grid(ng);
+        for (int a = 0; a < ng->ndim; ++a)
+            if (ng->dims[a] < g->dims[a])
+                fail(DFM_E_INVALID, "upsample_state: shrinking not allowed");
+        validate_grid(g);
+        if (ng->ndim != g->ndim) fail(DFM_E_INVALID, "upsample_field: dimensionality mismatch");
+        const Dims d = to_dims(g), nd = to_dims(ng);
+        if (dims_equal(d, nd)) {
+            std::memmove(m_out, m, sizeof(double) * d.n * d.ndim);
+            std::memmove(nu_out, nu, sizeof(double) * d.n * d.ndim);
+            return;
+        }
+        double mm[3] = {1.0, 1.0, 1.0}, mn[3] = {1.0, 1.0, 1.0};
+        for (int a = 0; a < g->ndim; ++a) {
+            const double r =
+                static_cast<double>(ng->dims[a] - 1) / static_cast<double>(g->dims[a] - 1);
+            mm[a] = r;
+            mn[a] = r * r;
+        }
+        DFM_DISPATCH(ctx, {
+            Field<T> a = dev_field<T>(ctx, "api_f0", d.n);
+            Field<T> b = dev_field<T>(ctx, "api_f1", d.n);
+            Field<T> oa = dev_field<T>(ctx, "api_f2", nd.n);
+            Field<T> ob = dev_field<T>(ctx, "api_f3", nd.n);
+            upload_field<T>(ctx, m, d.n, d.ndim, a);
+            upload_field<T>(ctx, nu, d.n, d.ndim, b);
+            const T* sa[3] = {a.p[0], a.p[1], a.p[2]};
+            T* da[3] = {oa.p[0], oa.p[1], oa.p[2]};
+            const T* sb[3] = {b.p[0], b.p[1], b.p[2]};
+            T* db[3] = {ob.p[0], ob.p[1], ob.p[2]};
+            launch_resample<T>(ctx->L(), sa, d, da, nd, d.ndim, mm);
+            launch_resample<T>(ctx->L(), sb, d, db, nd, d.ndim, mn);
+            download_field<T, double>(ctx, oa.r(), nd.n, nd.ndim, m_out);
+            download_field<T, double>(ctx, ob.r(), nd.n, nd.ndim, nu_out);
+            ctx->sync();
+        });
+    });
+}
+
+dfm_status dfm_eulerian_direction(dfm_ctx* ctx, const dfm_grid* g, const double* grad,
+                                  const double* phi, int use_jac, double* out) {
+    return guarded([&] {
+        validate_grid(g);
+        const Dims d = to_dims(g);
+        DFM_DISPATCH(ctx, {
+            Field<T> a = dev_field<T>(ctx, "api_f0", d.n);
+            Field<T> b = dev_field<T>(ctx, "api_f1", d.n);
+            Field<T> o = dev_field<T>(ctx, "api_f2", d.n);
+            upload_field<T>(ctx, grad, d.n, d.ndim, a);
+            upload_field<T>(ctx, phi, d.n, d.ndim, b);
+            launch_eulerian<T>(ctx->L(), a.r(), b.r(), d, use_jac, o.w());
+            download_field<T, double>(ctx, o.r(), d.n, d.ndim, out);
+            ctx->sync();
+        });
+    });
+}
+
+dfm_status dfm_apply_update(dfm_ctx* ctx, const dfm_grid* g, const double* phi, const double* v,
+                            double eta, double sigma_warp, double cap, double* out) {
+    return guarded([&] {
+        validate_grid(g);
+        const Dims d = to_dims(g);
+        DFM_DISPATCH(ctx, {
+            Field<T> a = dev_field<T>(ctx, "api_f0", d.n);
+            Field<T> b = dev_field<T>(ctx, "api_f1", d.n);
+            Field<T> s = dev_field<T>(ctx, "api_f2", d.n);
+            Field<T> o = dev_field<T>(ctx, "api_f3", d.n);
+            int* bad = ctx->arr<int>("api_flag", 1);
+            upload_field<T>(ctx, phi, d.n, d.ndim, a);
+            upload_field<T>(ctx, v, d.n, d.ndim, b);
+            CK(cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
+            launch_clamp_step<T>(ctx->L(), b.r(), s.w(), d, eta, cap, bad);
+            int hb = 0;
+            CK(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+            ctx->sync();
+            if (hb) fail(DFM_E_NUMERICAL, "apply_update: non-finite step");
+            const double sw[3] = {sigma_warp, sigma_warp, sigma_warp};
+            const HostGauss h = make_gauss(d, sw);
+            if (sigma_warp > 0.0 && h.R <= kRMax) {
+                const GaussW<T> w = upload_gauss<T>(ctx, h, d, "api_warp");
+                launch_compose_smooth<T>(ctx->L(), h.R, w, s.r(), a.r(), o.w(), d, nullptr);
+            } else {
+                launch_compose<T>(ctx->L(), a.r(), s.r(), d, o.w());
+                if (sigma_warp > 0.0) {
+                    smooth_planes<T>(ctx, d, sw, o.r(), b.w(), 3, "api_warp2");
+                    o = b;
+                }
+            }
+            download_field<T, double>(ctx, o.r(), d.n, d.ndim, out);
+            ctx->sync();
+        });
+    });
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// register_images (pipeline.cpp:121-224), direct mode, fully device-resident
+
+namespace {
+
+struct RegOut {
+    std::vector<dfm_iter_record> recs;
+    double final_loss = 0.0, sing = 0.0, total_ms = 0.0;
+};
+
+void validate_config(const dfm_config* c) {
+    if (!c) fail(DFM_E_INVALID, "config is NULL");
+    if (!(c->eta > 0.0) || !std::isfinite(c->eta))
+        fail(DFM_E_INVALID, "config: eta must be positive and finite");
+    if (c->sigma_grad < 0.0 || c->sigma_warp < 0.0) fail(DFM_E_INVALID, "config: sigmas must be >= 0");
+    if (c->lncc_radius < 1) fail(DFM_E_INVALID, "config: lncc_radius must be >= 1");
+    if (c->svf_M < 0) fail(DFM_E_INVALID, "config: svf_M must be >= 0");
+    if (!(c->beta1 >= 0.0 && c->beta1 < 1.0) || !(c->beta2 >= 0.0 && c->beta2 < 1.0))
+        fail(DFM_E_INVALID, "config: betas must lie in [0, 1)");
+    if (!(c->eps_adam > 0.0)) fail(DFM_E_INVALID, "config: eps_adam must be positive");
+    if (!(c->step_cap > 0.0)) fail(DFM_E_INVALID, "config: step_cap must be positive");
+    if (c->conv_window < 1) fail(DFM_E_INVALID, "config: conv_window must be >= 1");
+    if (c->conv_tol < 0.0) fail(DFM_E_INVALID, "config: conv_tol must be >= 0");
+    if (c->mode == DFM_MODE_SVF && c->loss == DFM_LOSS_DICE)
+        fail(DFM_E_INVALID, "config: dice loss is not available in svf mode");
+    if (c->mode != DFM_MODE_DIRECT)
+        fail(DFM_E_INVALID, "register: svf mode is not on the device path (direct mode only)");
+    if (c->loss < 0 || c->loss > 2) fail(DFM_E_INVALID, "unknown loss");
+    if (c->loss == DFM_LOSS_LNCC && c->lncc_radius > kRMax)
+        fail(DFM_E_INVALID, "lncc_radius > %d unsupported on the device path", kRMax);
+}
+
+void validate_schedule(const double* s, const int32_t* it, int ns) {
+    if (ns < 1 || !s || !it) fail(DFM_E_INVALID, "schedule: at least one scale required");
+    for (int i = 0; i < ns; ++i) {
+        if (!(s[i] >= 1.0) || !std::isfinite(s[i]))
+            fail(DFM_E_INVALID, "schedule: scales must be finite and >= 1");
+        if (i > 0 && !(s[i] < s[i - 1]))
+            fail(DFM_E_INVALID, "schedule: scales must be strictly decreasing");
+        if (it[i] < 0) fail(DFM_E_INVALID, "schedule: iterations must be >= 0");
+    }
+}
+
+// kernel classes for the optional per-kernel timing
+enum { KC_FWD = 0, KC_BWD = 1, KC_ADAM = 2, KC_COMPOSE = 3, KC_MON = 4, KC_PYR = 5, KC_EPI = 6 };
+
+template <class T>
+struct Registrar {
+    dfm_ctx* ctx;
+    const dfm_grid* g;
+    const dfm_config* cfg;
+    Dims full;
+    // workspace
+    T* Fbuf;
+    T* Mbuf;
+    T* Fs;
+    T* Ms;
+    Field<T> u[2], m, nu, grad, step;
+    T* coef[4];
+    double* partials;
+    LoopState* st;
+    double* loss;
+    unsigned long long* maxstep;
+    unsigned long long* stamp;
+    double* corr1;
+    double* corr2;
+    int cur = 0;
+    // profiling
+    std::vector<cudaEvent_t> evpool;
+    std::vector<std::pair<int, int>> evuse;  // (class, pool index of start)
+
+    void alloc(int64_t total_iters) {
+        const int64_t n = full.n;
+        Fbuf = Fs = ctx->arr<T>("reg_Fs", n);
+        Mbuf = Ms = ctx->arr<T>("reg_Ms", n);
+        u[0] = dev_field<T>(ctx, "reg_u0", n);
+        u[1] = dev_field<T>(ctx, "reg_u1", n);
+        m = dev_field<T>(ctx, "reg_m", n);
+        nu = dev_field<T>(ctx, "reg_nu", n);
+        grad = dev_field<T>(ctx, "reg_grad", n);
+        step = dev_field<T>(ctx, "reg_step", n);
+        T* cb = ctx->arr<T>("reg_coef", 4 * n);
+        for (int k = 0; k < 4; ++k) coef[k] = cb + k * n;
+        partials = ctx->arr<double>("reg_partials", 3 * 65536);
+        st = ctx->arr<LoopState>("reg_state", 1);
+        const int64_t cap = total_iters + 2;
+        loss = ctx->arr<double>("reg_loss", cap);
+        maxstep = ctx->arr<unsigned long long>("reg_maxstep", cap);
+        stamp = ctx->arr<unsigned long long>("reg_stamp", cap);
+        corr1 = ctx->arr<double>("reg_corr1", cap);
+        corr2 = ctx->arr<double>("reg_corr2", cap);
+        std::vector<double> h1(cap), h2(cap);
+        for (int64_t t = 0; t < cap; ++t) {
+            h1[t] = 1.0 - std::pow(cfg->beta1, static_cast<double>(t));
+            h2[t] = 1.0 - std::pow(cfg->beta2, static_cast<double>(t));
+        }
+        CK(cudaMemcpyAsync(corr1, h1.data(), sizeof(double) * cap, cudaMemcpyHostToDevice,
+                           ctx->stream));
+        CK(cudaMemcpyAsync(corr2, h2.data(), sizeof(double) * cap, cudaMemcpyHostToDevice,
+                           ctx->stream));
+        CK(cudaMemsetAsync(st, 0, sizeof(LoopState), ctx->stream));
+        // corr tables are host vectors: make sure the copies finished before they die
+        ctx->sync();
+    }
+
+    void zero_field(Field<T>& f, int64_t n) {
+        CK(cudaMemsetAsync(f.p[0], 0, sizeof(T) * n, ctx->stream));
+        CK(cudaMemsetAsync(f.p[1], 0, sizeof(T) * n, ctx->stream));
+        CK(cudaMemsetAsync(f.p[2], 0, sizeof(T) * n, ctx->stream));
+    }
+
+    // profiling helpers
+    void ev_begin(int cls) {
+        if (!ctx->profiling) return;
+        const size_t k = evpool.size();
+        cudaEvent_t a, b;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        evpool.push_back(a);
+        evpool.push_back(b);
+        evuse.push_back({cls, static_cast<int>(k)});
+        CK(cudaEventRecord(a, ctx->stream));
+    }
+    void ev_end() {
+        if (!ctx->profiling) return;
+        CK(cudaEventRecord(evpool.back(), ctx->stream));
+    }
+    void ev_collect(const Dims& d) {
+        if (!ctx->profiling) return;
+        ctx->sync();
+        for (auto& pr : evuse) {
+            // loop classes are reported for the full-resolution scale only
+            if (pr.first <= KC_MON && d.n != full.n) continue;
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, evpool[pr.second], evpool[pr.second + 1]));
+            ctx->kt_ms[pr.first] += ms;
+            ctx->kt_n[pr.first] += 1;
+            ctx->kt_vox[pr.first] += d.n;
+        }
+        for (auto e : evpool) cudaEventDestroy(e);
+        evpool.clear();
+        evuse.clear();
+    }
+
+    // one iteration of the hot loop on grid d, u[src] -> u[1-src]
+    void enqueue_iteration(const Dims& d, int src, int Rg, int Rw, const GaussW<T>& wg,
+                           const GaussW<T>& ww, const DevAxisGauss* big_g,
+                           const DevAxisGauss* big_w) {
+        Launch L = ctx->L();
+        const int loss_kind = cfg->loss;
+        const CPlanes3<T> uin = u[src].r();
+        ev_begin(KC_FWD);
+        const int np = loss_kind_launch_fwd<T>(ctx, loss_kind, cfg->lncc_radius, Fs, Ms, d, d,
+                                               uin, coef, grad.w(), partials, st);
+        ev_end();
+        ev_begin(KC_MON);
+        launch_monitor(L, monitor_kind(loss_kind), partials, np, static_cast<double>(d.n), st,
+                       loss, stamp, cfg->conv_window, cfg->conv_tol);
+        ev_end();
+        if (loss_kind == DFM_LOSS_LNCC) {
+            const T* cc[4] = {coef[0], coef[1], coef[2], coef[3]};
+            ev_begin(KC_BWD);
+            launch_lncc_bwd<T>(L, cfg->lncc_radius, Fs, Ms, d, d, uin, cc, grad.w(), st);
+            ev_end();
+        } else if (loss_kind == DFM_LOSS_DICE) {
+            ev_begin(KC_BWD);
+            launch_dice_grad<T>(L, Fs, Ms, d, d, uin, grad.w(), st, 0.0, 1.0);
+            ev_end();
+        }
+        AdamParams ap{cfg->beta1, cfg->beta2, cfg->eps_adam, cfg->eta, cfg->step_cap,
+                      corr1, corr2, cfg->use_jac};
+        ev_begin(KC_ADAM);
+        if (big_g)  // sigma_grad beyond the fused radius: generic axis passes first
+            for (int c = 0; c < 3; ++c)
+                axis_smooth_plane<T>(ctx, d, *big_g, grad.p[c], grad.p[c], step.p[c], st);
+        launch_smooth_adam<T>(L, big_g ? 0 : Rg, wg, grad.r(), uin, m.w(), nu.w(), step.w(), d,
+                              ap, st, maxstep);
+        ev_end();
+        ev_begin(KC_COMPOSE);
+        launch_compose_smooth<T>(L, big_w ? 0 : Rw, ww, step.r(), uin, u[1 - src].w(), d, st);
+        if (big_w)
+            for (int c = 0; c < 3; ++c)
+                axis_smooth_plane<T>(ctx, d, *big_w, u[1 - src].p[c], u[1 - src].p[c], grad.p[c],
+                                     st);
+        ev_end();
+    }
+
+    void run(const T* F, const T* M, const double* scales, const int32_t* iters, int ns,
+             const dfm_init* init, RegOut& out) {
+        const double t0 = now_ms();
+        int64_t total = 0;
+        for (int i = 0; i < ns; ++i) total += iters[i];
+        alloc(total);
+        Launch L = ctx->L();
+        Dims cd{};  // current working grid
+        bool have = false;
+        int64_t global = 0;
+        for (int si = 0; si < ns; ++si) {
+            const double fac[3] = {scales[si], scales[si], scales[si]};
+            dfm_grid wgd;
+            downsample_grid(g, fac, &wgd);
+            const Dims d = to_dims(&wgd);
+            ev_begin(KC_PYR);
+            bool blur = false;
+            for (int a = 0; a < g->ndim; ++a) blur |= fac[a] > 1.0;
+            const T* Fw = F;
+            const T* Mw = M;
+            if (blur || !dims_equal(d, full)) {
+                Impl<T>{ctx}.downsample_dev(full, F, fac, d, Fbuf, "pyr");
+                Impl<T>{ctx}.downsample_dev(full, M, fac, d, Mbuf, "pyr");
+                Fw = Fbuf;
+                Mw = Mbuf;
+            }
+            if (!have) {
+                init_field(d, init);
+                zero_field(m, d.n);
+                zero_field(nu, d.n);
+                have = true;
+            } else if (!dims_equal(cd, d)) {
+                upsample_state(cd, d);
+            }
+            ev_end();
+            cd = d;
+            const int T_si = iters[si];
+            if (T_si == 0) continue;
+            check_loss_inputs(Fw, Mw, &wgd);
+            run_scale(d, Fw, Mw, si, scales[si], T_si, global, out);
+        }
+        // epilogue (pipeline.cpp:213-223)
+        ev_begin(KC_EPI);
+        if (!dims_equal(cd, full)) {
+            upsample_field_only(cd, full);
+        }
+        Dims d = full;
+        T* coef0[4] = {nullptr, nullptr, nullptr, nullptr};
+        check_loss_inputs(F, M, g);
+        const int np = loss_kind_launch_fwd<T>(ctx, cfg->loss, cfg->lncc_radius, F, M, d, d,
+                                               u[cur].r(), coef0, Planes3<T>{{nullptr, nullptr, nullptr}},
+                                               partials, nullptr);
+        double* val = ctx->arr<double>("reg_value3", 4);
+        launch_reduce_value(L, monitor_kind(cfg->loss), partials, np, static_cast<double>(d.n),
+                            val);
+        auto* cnt = ctx->arr<unsigned long long>("reg_count", 1);
+        CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), ctx->stream));
+        launch_jacobian_det<T>(L, u[cur].r(), d, nullptr, cnt);
+        ev_end();
+        double hv[3];
+        unsigned long long hc = 0;
+        CK(cudaMemcpyAsync(hv, val, sizeof(hv), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(&hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->sync();
+        ev_collect(full);
+        out.final_loss = hv[0];
+        out.sing = static_cast<double>(hc) / static_cast<double>(d.n);
+        out.total_ms = now_ms() - t0;
+    }
+
+    // per-evaluation validation of lncc_eval / dice_soft_eval (similarity.cpp:108-114,194-200)
+    void check_loss_inputs(const T* F, const T* M, const dfm_grid* wg) {
+        if (cfg->loss == DFM_LOSS_LNCC)
+            for (int a = 0; a < wg->ndim; ++a)
+                if (2 * static_cast<int64_t>(cfg->lncc_radius) + 1 > wg->dims[a])
+                    fail(DFM_E_INVALID, "lncc_eval: window larger than image");
+        if (cfg->loss == DFM_LOSS_DICE) check_masks(F, M, to_dims(wg));
+    }
+
+    void check_masks(const T* F, const T* M, const Dims& d) {
+        int* bad = ctx->arr<int>("reg_maskflag", 2);
+        CK(cudaMemsetAsync(bad, 0, 2 * sizeof(int), ctx->stream));
+        launch_range_check<T>(ctx->L(), F, d.n, bad);
+        launch_range_check<T>(ctx->L(), M, d.n, bad + 1);
+        int hb[2];
+        CK(cudaMemcpyAsync(hb, bad, sizeof(hb), cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->sync();
+        if (hb[0]) fail(DFM_E_INVALID, "dice_soft_eval: fixed mask values outside [0,1]");
+        if (hb[1]) fail(DFM_E_INVALID, "dice_soft_eval: moving mask values outside [0,1]");
+    }
+
+    // pipeline.cpp:57-79 initial_field on the coarsest grid
+    void init_field(const Dims& d, const dfm_init* init) {
+        cur = 0;
+        if (!init || init->kind == DFM_INIT_NONE) {
+            zero_field(u[0], d.n);
+            return;
+        }
+        if (init->kind == DFM_INIT_AFFINE) {
+            if (init->affine_ndim != d.ndim)
+                fail(DFM_E_INVALID, "affine_to_working_field: dimensionality mismatch");
+            double S[3] = {1.0, 1.0, 1.0};
+            const int wd[3] = {d.nx, d.ny, d.nz};
+            for (int a = 0; a < d.ndim; ++a) {
+                const int den = wd[a] - 1 > 1 ? wd[a] - 1 : 1;
+                S[a] = static_cast<double>(g->dims[a] - 1) / static_cast<double>(den);
+            }
+            launch_affine_field<T>(ctx->L(), init->A, init->t, S, d, u[0].w());
+            return;
+        }
+        if (init->kind != DFM_INIT_FIELD) fail(DFM_E_INVALID, "unknown init kind");
+        const dfm_grid* fg = &init->field_grid;
+        if (fg->ndim != d.ndim)
+            fail(DFM_E_INVALID, "register_images: init field dimensionality mismatch");
+        const Dims id = to_dims(fg);
+        if (dims_equal(id, d)) {
+            upload_field<T>(ctx, init->field, d.n, d.ndim, u[0]);
+            return;
+        }
+        if (!dims_equal(id, full))
+            fail(DFM_E_INVALID, "register_images: init field must live on the full or coarsest grid");
+        // resample_displacement from the full grid (interp.cpp:447-465)
+        upload_field<T>(ctx, init->field, id.n, id.ndim, u[1]);
+        double mult[3] = {1.0, 1.0, 1.0};
+        const int nn[3] = {d.nx, d.ny, d.nz}, no[3] = {id.nx, id.ny, id.nz};
+        for (int a = 0; a < d.ndim; ++a)
+            mult[a] = static_cast<double>(nn[a] - 1) / static_cast<double>(no[a] - 1);
+        const T* src[3] = {u[1].p[0], u[1].p[1], u[1].p[2]};
+        T* dst[3] = {u[0].p[0], u[0].p[1], u[0].p[2]};
+        launch_resample<T>(ctx->L(), src, id, dst, d, d.ndim, mult);
+    }
+
+    void upsample_field_only(const Dims& from, const Dims& to) {
+        double mult[3] = {1.0, 1.0, 1.0};
+        const int nn[3] = {to.nx, to.ny, to.nz}, no[3] = {from.nx, from.ny, from.nz};
+        for (int a = 0; a < to.ndim; ++a)
+            mult[a] = static_cast<double>(nn[a] - 1) / static_cast<double>(no[a] - 1);
+        const T* src[3] = {u[cur].p[0], u[cur].p[1], u[cur].p[2]};
+        T* dst[3] = {u[1 - cur].p[0], u[1 - cur].p[1], u[1 - cur].p[2]};
+        launch_resample<T>(ctx->L(), src, from, dst, to, to.ndim, mult);
+        cur = 1 - cur;
+    }
+
+    // upsample_field + upsample_state (pipeline.cpp:150-153, optim.cpp:59-85)
+    void upsample_state(const Dims& from, const Dims& to) {
+        upsample_field_only(from, to);
+        double mm[3] = {1.0, 1.0, 1.0}, mn[3] = {1.0, 1.0, 1.0};
+        const int nn[3] = {to.nx, to.ny, to.nz}, no[3] = {from.nx, from.ny, from.nz};
+        for (int a = 0; a < to.ndim; ++a) {
+            const double r = static_cast<double>(nn[a] - 1) / static_cast<double>(no[a] - 1);
+            mm[a] = r;
+            mn[a] = r * r;
+        }
+        const T* sm[3] = {m.p[0], m.p[1], m.p[2]};
+        T* dm[3] = {grad.p[0], grad.p[1], grad.p[2]};
+        launch_resample<T>(ctx->L(), sm, from, dm, to, to.ndim, mm);
+        const T* sn[3] = {nu.p[0], nu.p[1], nu.p[2]};
+        T* dn[3] = {step.p[0], step.p[1], step.p[2]};
+        launch_resample<T>(ctx->L(), sn, from, dn, to, to.ndim, mn);
+        std::swap(m, grad);
+        std::swap(nu, step);
+    }
+
+    void run_scale(const Dims& d, const T* Fw, const T* Mw, int si, double scale, int T_si,
+                   int64_t& global, RegOut& out) {
+        Fs = const_cast<T*>(Fw);
+        Ms = const_cast<T*>(Mw);
+        // per-scale reset of the loop state (t is kept)
+        CK(cudaMemsetAsync(st, 0, offsetof(LoopState, t), ctx->stream));
+        CK(cudaMemsetAsync(maxstep, 0, sizeof(unsigned long long) * (T_si + 1), ctx->stream));
+        const double sg[3] = {cfg->sigma_grad, cfg->sigma_grad, cfg->sigma_grad};
+        const double sw[3] = {cfg->sigma_warp, cfg->sigma_warp, cfg->sigma_warp};
+        const HostGauss hg = make_gauss(d, sg), hw = make_gauss(d, sw);
+        GaussW<T> wg = upload_gauss<T>(ctx, hg, d, "loop_g");
+        GaussW<T> ww = upload_gauss<T>(ctx, hw, d, "loop_w");
+        DevAxisGauss bg{}, bw{};
+        const DevAxisGauss* pbg = nullptr;
+        const DevAxisGauss* pbw = nullptr;
+        if (hg.R > kRMax) {
+            bg = upload_axis_gauss(ctx, hg, d, "loop_bg");
+            pbg = &bg;
+            const double zero[3] = {0, 0, 0};
+            wg = upload_gauss<T>(ctx, make_gauss(d, zero), d, "loop_g0");
+        }
+        if (hw.R > kRMax) {
+            bw = upload_axis_gauss(ctx, hw, d, "loop_bw");
+            pbw = &bw;
+            const double zero[3] = {0, 0, 0};
+            ww = upload_gauss<T>(ctx, make_gauss(d, zero), d, "loop_w0");
+        }
+        const int Rg = hg.R > kRMax ? 0 : hg.R;
+        const int Rw = hw.R > kRMax ? 0 : hw.R;
+        const int start = cur;
+        if (ctx->profiling) {
+            for (int j = 0; j < T_si; ++j)
+                enqueue_iteration(d, (start + j) % 2, Rg, Rw, wg, ww, pbg, pbw);
+            launch_stamp(ctx->L(), stamp + T_si);
+            ev_collect(d);
+        } else {
+            // capture the two ping-pong variants of one iteration as CUDA graphs
+            cudaGraphExec_t exec[2] = {nullptr, nullptr};
+            int64_t nodes_per = 0;
+            for (int v = 0; v < 2; ++v) {
+                const int64_t before = ctx->launches;
+                cudaGraph_t graph;
+                CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
+                enqueue_iteration(d, (start + v) % 2, Rg, Rw, wg, ww, pbg, pbw);
+                CK(cudaStreamEndCapture(ctx->stream, &graph));
+                CK(cudaGraphInstantiate(&exec[v], graph, 0));
+                CK(cudaGraphDestroy(graph));
+                nodes_per = ctx->launches - before;
+                ctx->launches = before;
+            }
+            // Launch in chunks, keeping at most two chunks in flight, and stop
+            // once the device-side monitor reports the scale done (converged or
+            // failed): no per-iteration host sync, bounded wasted launches.
+            LoopState* hst = ctx->pinned_state();
+            const int chunk = 16;
+            int nchunk = 0;
+            for (int j = 0; j < T_si;) {
+                if (nchunk >= 2) {
+                    const int w = (nchunk - 2) % 2;
+                    CK(cudaEventSynchronize(ctx->chunk_ev[w]));
+                    if (hst[w].done) break;
+                }
+                const int jend = j + chunk < T_si ? j + chunk : T_si;
+                for (; j < jend; ++j) {
+                    CK(cudaGraphLaunch(exec[j % 2], ctx->stream));
+                    ctx->launches += nodes_per;
+                }
+                const int w = nchunk % 2;
+                CK(cudaMemcpyAsync(&hst[w], st, sizeof(LoopState), cudaMemcpyDeviceToHost,
+                                   ctx->stream));
+                CK(cudaEventRecord(ctx->chunk_ev[w], ctx->stream));
+                ++nchunk;
+            }
+            launch_stamp(ctx->L(), stamp + T_si);
+            ctx->sync();
+            for (int v = 0; v < 2; ++v) CK(cudaGraphExecDestroy(exec[v]));
+        }
+        // read back the scale's log (one readback per scale)
+        LoopState hs;
+        std::vector<double> hl(T_si + 1);
+        std::vector<unsigned long long> hm(T_si + 1), ht(T_si + 1);
+        CK(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(hl.data(), loss, sizeof(double) * T_si, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CK(cudaMemcpyAsync(hm.data(), maxstep, sizeof(unsigned long long) * T_si,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(ht.data(), stamp, sizeof(unsigned long long) * (T_si + 1),
+                           cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->sync();
+        const int nrec = hs.it;
+        for (int j = 0; j < nrec; ++j) {
+            dfm_iter_record r{};
+            r.scale_index = si;
+            r.scale = scale;
+            r.iter = j;
+            r.global_iter = global++;
+            r.loss = hl[j];
+            const bool conv_rec = hs.converged && j == nrec - 1;
+            double ms;
+            std::memcpy(&ms, &hm[j], sizeof(double));
+            r.max_step = conv_rec ? 0.0 : ms;
+            const unsigned long long tn = (j + 1 < nrec) ? ht[j + 1] : ht[T_si];
+            r.wall_ms = tn > ht[j] ? static_cast<double>(tn - ht[j]) * 1e-6 : 0.0;
+            if (hs.err && j == nrec - 1 && !std::isfinite(hl[j])) break;  // not recorded
+            out.recs.push_back(r);
+        }
+        if (hs.err) {
+            if (nrec > 0 && !std::isfinite(hl[nrec - 1]))
+                fail(DFM_E_NUMERICAL,
+                     "register_images: non-finite loss at scale %f, iteration %d", scale,
+                     nrec - 1);
+            fail(DFM_E_NUMERICAL, "apply_update: non-finite step");
+        }
+        cur = (start + hs.nupdates) % 2;
+    }
+};
+
+template <class T>
+void register_dev(dfm_ctx* ctx, const dfm_grid* g, const T* F, const T* M, const dfm_config* cfg,
+                  const double* scales, const int32_t* iters, int ns, const dfm_init* init,
+                  RegOut& out, CPlanes3<T>* result) {
+    Registrar<T> R{};
+    R.ctx = ctx;
+    R.g = g;
+    R.cfg = cfg;
+    R.full = to_dims(g);
+    R.run(F, M, scales, iters, ns, init, out);
+    if (result) *result = R.u[R.cur].r();
+}
+
+void fill_log(const RegOut& o, dfm_iter_record* records, int64_t max_records, dfm_runlog* log) {
+    const int64_t n = static_cast<int64_t>(o.recs.size());
+    const int64_t k = n < max_records ? n : max_records;
+    if (records && k > 0) std::memcpy(records, o.recs.data(), sizeof(dfm_iter_record) * k);
+    if (log) {
+        log->n_records = records ? k : 0;
+        log->n_total = n;
+        log->final_loss = o.final_loss;
+        log->final_singularity_fraction = o.sing;
+        log->total_ms = o.total_ms;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+dfm_status dfm_register(dfm_ctx* ctx, const dfm_grid* g, const void* fixed, const void* moving,
+                        int image_dtype, const dfm_config* cfg, const double* scales,
+                        const int32_t* iterations, int32_t nscales, const dfm_init* init,
+                        void* out_field, int field_dtype, dfm_iter_record* records,
+                        int64_t max_records, dfm_runlog* log) {
+    return guarded([&] {
+        const double t0 = now_ms();
+        validate_grid(g);
+        validate_config(cfg);
+        validate_schedule(scales, iterations, nscales);
+        if (image_dtype != DFM_HOST_F32 && image_dtype != DFM_HOST_F64)
+            fail(DFM_E_INVALID, "image_dtype must be DFM_HOST_F32 or DFM_HOST_F64");
+        const Dims d = to_dims(g);
+        RegOut o;
+        for (int k = 0; k < DFM_NUM_KCLASS; ++k) ctx->kt_ms[k] = 0, ctx->kt_n[k] = 0, ctx->kt_vox[k] = 0;
+        DFM_DISPATCH(ctx, {
+            T* F = ctx->arr<T>("host_F", d.n);
+            T* M = ctx->arr<T>("host_M", d.n);
+            if (image_dtype == DFM_HOST_F32) {
+                upload_image<T, float>(ctx, static_cast<const float*>(fixed), d.n, F);
+                upload_image<T, float>(ctx, static_cast<const float*>(moving), d.n, M);
+            } else {
+                upload_image<T, double>(ctx, static_cast<const double*>(fixed), d.n, F);
+                upload_image<T, double>(ctx, static_cast<const double*>(moving), d.n, M);
+            }
+            CPlanes3<T> res;
+            register_dev<T>(ctx, g, F, M, cfg, scales, iterations, nscales, init, o, &res);
+            if (out_field) {
+                if (field_dtype == DFM_HOST_F32)
+                    download_field<T, float>(ctx, res, d.n, d.ndim, static_cast<float*>(out_field));
+                else
+                    download_field<T, double>(ctx, res, d.n, d.ndim,
+                                              static_cast<double*>(out_field));
+            }
+            ctx->sync();
+        });
+        o.total_ms = now_ms() - t0;
+        fill_log(o, records, max_records, log);
+        if (o.sing > 0.0) fail(DFM_E_NUMERICAL, "register_images: folded warp (det J <= 0 somewhere)");
+    });
+}
+
+dfm_status dfm_dev_register(dfm_ctx* ctx, const dfm_grid* g, const void* d_fixed,
+                            const void* d_moving, const dfm_config* cfg, const double* scales,
+                            const int32_t* iterations, int32_t nscales, void* d_out_soa_field,
+                            dfm_iter_record* records, int64_t max_records, dfm_runlog* log) {
+    return guarded([&] {
+        validate_grid(g);
+        validate_config(cfg);
+        validate_schedule(scales, iterations, nscales);
+        const Dims d = to_dims(g);
+        RegOut o;
+        for (int k = 0; k < DFM_NUM_KCLASS; ++k) ctx->kt_ms[k] = 0, ctx->kt_n[k] = 0, ctx->kt_vox[k] = 0;
+        DFM_DISPATCH(ctx, {
+            CPlanes3<T> res;
+            register_dev<T>(ctx, g, static_cast<const T*>(d_fixed), static_cast<const T*>(d_moving),
+                            cfg, scales, iterations, nscales, nullptr, o, &res);
+            if (d_out_soa_field) {
+                T* outp = static_cast<T*>(d_out_soa_field);
+                for (int c = 0; c < 3; ++c)
+                    CK(cudaMemcpyAsync(outp + c * d.n, res.c[c], sizeof(T) * d.n,
+                                       cudaMemcpyDeviceToDevice, ctx->stream));
+            }
+            ctx->sync();
+        });
+        fill_log(o, records, max_records, log);
+        if (o.sing > 0.0) fail(DFM_E_NUMERICAL, "register_images: folded warp (det J <= 0 somewhere)");
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,190 @@
+"""Python host-side mirror of the difform:: API over the CUDA C-ABI.
+
+This is the thin Python face of libdifform_cuda.so (the product is the .so and
+its C-ABI, include/difform_gpu.h); tests and bench.py call through it.  There
+is NO CPU fallback: constructing a Context without the built library or without
+a CUDA device raises.
+
+    ctx = Context(device=0, precision="f32")
+    phi, log = ctx.register_images(grid, fixed, moving, cfg, schedule)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+
+from . import _abi as A
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdifform_cuda.so")
+
+# every entry point include/difform_gpu.h declares (checked by tests/test_abi.py)
+EXPORTS = [
+    "dfm_abi_version", "dfm_config_defaults", "dfm_ctx_create", "dfm_ctx_destroy",
+    "dfm_ctx_precision", "dfm_ctx_stream", "dfm_last_error", "dfm_ctx_launch_count",
+    "dfm_validate_grid", "dfm_downsample_grid", "dfm_downsample_image",
+    "dfm_sample_linear_points", "dfm_warp_image", "dfm_warp_labels", "dfm_compose",
+    "dfm_jacobian_det", "dfm_gaussian_smooth", "dfm_gaussian_smooth_field",
+    "dfm_upsample_field", "dfm_resample_field_linear", "dfm_resample_displacement",
+    "dfm_ssd_eval", "dfm_lncc_eval", "dfm_dice_eval", "dfm_adam_step", "dfm_upsample_state",
+    "dfm_eulerian_direction", "dfm_apply_update", "dfm_singularity_fraction", "dfm_register",
+    "dfm_dev_register", "dfm_ctx_set_profiling", "dfm_ctx_kernel_times",
+]
+
+_lib: Optional[C.CDLL] = None
+
+
+def load_library(path: str = LIB_PATH) -> C.CDLL:
+    """Loads (once) the in-tree CUDA library; raises if it was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise FileNotFoundError(
+                f"{path} missing: build it with `python -m paper_2404_01249_b200.build` "
+                "(there is no CPU fallback)")
+        lib = C.CDLL(path)
+        lib.dfm_ctx_create.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+        lib.dfm_ctx_create.restype = C.c_int
+        lib.dfm_ctx_destroy.argtypes = [C.c_void_p]
+        lib.dfm_ctx_destroy.restype = None
+        lib.dfm_ctx_stream.argtypes = [C.c_void_p]
+        lib.dfm_ctx_stream.restype = C.c_void_p
+        lib.dfm_ctx_launch_count.argtypes = [C.c_void_p]
+        lib.dfm_ctx_launch_count.restype = C.c_int64
+        lib.dfm_ctx_precision.argtypes = [C.c_void_p]
+        lib.dfm_ctx_precision.restype = C.c_int
+        lib.dfm_abi_version.restype = C.c_int
+        lib.dfm_config_defaults.argtypes = [C.POINTER(A.dfm_config)]
+        lib.dfm_config_defaults.restype = None
+        lib.dfm_validate_grid.argtypes = [C.POINTER(A.dfm_grid)]
+        lib.dfm_validate_grid.restype = C.c_int
+        lib.dfm_downsample_grid.argtypes = [C.POINTER(A.dfm_grid), C.POINTER(C.c_double),
+                                            C.POINTER(A.dfm_grid)]
+        lib.dfm_downsample_grid.restype = C.c_int
+        lib.dfm_ctx_set_profiling.argtypes = [C.c_void_p, C.c_int]
+        lib.dfm_ctx_set_profiling.restype = C.c_int
+        lib.dfm_ctx_kernel_times.argtypes = [C.c_void_p, C.POINTER(C.c_double),
+                                             C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        lib.dfm_ctx_kernel_times.restype = C.c_int
+        reg = [C.c_void_p, C.POINTER(A.dfm_grid), C.c_void_p, C.c_void_p]
+        lib.dfm_register.argtypes = reg + [C.c_int, C.POINTER(A.dfm_config),
+                                           C.POINTER(C.c_double), C.POINTER(C.c_int32),
+                                           C.c_int32, C.POINTER(A.dfm_init), C.c_void_p, C.c_int,
+                                           C.POINTER(A.dfm_iter_record), C.c_int64,
+                                           C.POINTER(A.dfm_runlog)]
+        lib.dfm_register.restype = C.c_int
+        lib.dfm_dev_register.argtypes = reg + [C.POINTER(A.dfm_config), C.POINTER(C.c_double),
+                                               C.POINTER(C.c_int32), C.c_int32, C.c_void_p,
+                                               C.POINTER(A.dfm_iter_record), C.c_int64,
+                                               C.POINTER(A.dfm_runlog)]
+        lib.dfm_dev_register.restype = C.c_int
+        _lib = lib
+    return _lib
+
+
+KCLASS_NAMES = ["loss_fwd", "lncc_bwd", "smooth_adam", "compose_smooth", "monitor", "pyramid",
+                "epilogue"]
+
+
+class Context(A.HostAPI):
+    """A dfm_ctx: one CUDA stream + workspace on `device`, fp32 or fp64."""
+
+    def __init__(self, device: int = 0, precision: str = "f32"):
+        lib = load_library()
+        prec = {"f32": A.PREC_F32, "f64": A.PREC_F64}[precision]
+        h = C.c_void_p()
+        tbl = A.CallTable(lib, "dfm_", ctx=None)
+        tbl.check(lib.dfm_ctx_create(device, prec, C.byref(h)), "dfm_ctx_create")
+        super().__init__(A.CallTable(lib, "dfm_", ctx=h))
+        self.lib = lib
+        self.handle = h
+        self.precision = precision
+        self.device = device
+
+    def close(self):
+        if self.handle:
+            self.lib.dfm_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream_ptr(self) -> int:
+        return int(self.lib.dfm_ctx_stream(self.handle) or 0)
+
+    @property
+    def launch_count(self) -> int:
+        return int(self.lib.dfm_ctx_launch_count(self.handle))
+
+    def set_profiling(self, on: bool):
+        self.t.check(self.lib.dfm_ctx_set_profiling(self.handle, int(on)), "set_profiling")
+
+    def kernel_times(self) -> dict:
+        ms = (C.c_double * A.NUM_KCLASS)()
+        n = (C.c_int64 * A.NUM_KCLASS)()
+        v = (C.c_int64 * A.NUM_KCLASS)()
+        self.t.check(self.lib.dfm_ctx_kernel_times(self.handle, ms, n, v), "kernel_times")
+        return {KCLASS_NAMES[k]: {"ms": ms[k], "launches": n[k], "voxels": v[k]}
+                for k in range(A.NUM_KCLASS)}
+
+    # -- pipeline
+    def register_images(self, g: A.GridMeta, fixed, moving, cfg: A.RegistrationConfig,
+                        sched: A.PyramidSchedule, init=None, field_dtype=np.float64):
+        """register_images (pipeline.hpp:70-73) with HOST arrays -> (field, RunLog).
+
+        fixed/moving may be float32 or float64 numpy arrays (float32 halves the
+        host->device bytes); the field comes back as AoS ``field_dtype``.
+        """
+        img_dt = np.float32 if np.asarray(fixed).dtype == np.float32 else np.float64
+        f = np.ascontiguousarray(fixed, dtype=img_dt).reshape(g.shape)
+        m = np.ascontiguousarray(moving, dtype=img_dt).reshape(g.shape)
+        s, it = A.schedule_arrays(sched)
+        cap = int(it.sum()) + 1
+        recs = (A.dfm_iter_record * cap)()
+        rl = A.dfm_runlog()
+        out = np.empty(g.field_shape, dtype=field_dtype)
+        ci, keep = A.make_init(init, g.ndim)
+        cc = cfg.c()
+        rc = self.lib.dfm_register(
+            self.handle, C.byref(g.c()), f.ctypes.data, m.ctypes.data,
+            A.HOST_F32 if img_dt == np.float32 else A.HOST_F64, C.byref(cc), A._dptr(s),
+            it.ctypes.data_as(C.POINTER(C.c_int32)), len(s), C.byref(ci), out.ctypes.data,
+            A.HOST_F32 if field_dtype == np.float32 else A.HOST_F64, recs, cap, C.byref(rl))
+        self.t.check(rc, "register")
+        del keep
+        return out, A.records_to_log(recs, rl)
+
+    def register_device(self, g: A.GridMeta, d_fixed: int, d_moving: int,
+                        cfg: A.RegistrationConfig, sched: A.PyramidSchedule,
+                        d_out: int = 0):
+        """dfm_dev_register: device pointers (context precision), SoA result."""
+        s, it = A.schedule_arrays(sched)
+        cap = int(it.sum()) + 1
+        recs = (A.dfm_iter_record * cap)()
+        rl = A.dfm_runlog()
+        cc = cfg.c()
+        rc = self.lib.dfm_dev_register(self.handle, C.byref(g.c()), C.c_void_p(d_fixed),
+                                       C.c_void_p(d_moving), C.byref(cc), A._dptr(s),
+                                       it.ctypes.data_as(C.POINTER(C.c_int32)), len(s),
+                                       C.c_void_p(d_out) if d_out else None, recs, cap,
+                                       C.byref(rl))
+        self.t.check(rc, "dev_register")
+        return A.records_to_log(recs, rl)
+
+
+def cuda_available() -> bool:
+    """True when a CUDA device is visible (checked without torch)."""
+    try:
+        rt = C.CDLL("libcuda.so.1")
+    except OSError:
+        return False
+    n = C.c_int(0)
+    if rt.cuInit(0) != 0:
+        return False
+    return rt.cuDeviceGetCount(C.byref(n)) == 0 and n.value > 0

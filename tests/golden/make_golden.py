@@ -1,0 +1,131 @@
+"""Generates tests/golden/*.npz from the UNMODIFIED reference (oracle/_ref).
+
+Run in the container that has /root/reference:
+
+    make -C oracle ref && python tests/golden/make_golden.py
+
+Inputs are seeded numpy arrays (fp32-representable, like the reference's
+MET_FLOAT volumes); outputs are whatever the reference computes in fp64.
+These vectors pin the plain-C restatement (tests/test_oracle.py) and the CUDA
+path (tests/test_parity_gpu.py) without needing /root/reference at run time.
+"""
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+from oracle import pyoracle  # noqa: E402
+from paper_2404_01249_b200 import _abi as A, synth  # noqa: E402
+
+
+def f32(a):
+    return np.asarray(a, dtype=np.float32).astype(np.float64)
+
+
+def cases():
+    rng = np.random.default_rng(1234)
+    g3 = A.GridMeta.make_3d(13, 11, 9)
+    g2 = A.GridMeta.make_2d(17, 12)
+    gm = A.GridMeta.make_3d(10, 14, 8)  # moving on its own grid
+    out = {}
+    for tag, g in (("3d", g3), ("2d", g2)):
+        F = f32(rng.random(g.shape))
+        M = f32(ndimage_smooth(rng.random(g.shape)))
+        phi = f32(rng.normal(0, 1.6, g.field_shape))   # includes clamp zones
+        psi = f32(rng.normal(0, 0.4, g.field_shape))
+        v = f32(rng.normal(0, 1e-3, g.field_shape))
+        m = f32(rng.normal(0, 1e-3, g.field_shape))
+        nu = f32(rng.random(g.field_shape) * 1e-6)
+        lab = rng.integers(0, 6, g.shape).astype(np.int32)
+        pts = f32(rng.uniform(-2, max(g.dims) + 1, (64, 3)))
+        out[tag] = dict(grid=g, F=F, M=M, phi=phi, psi=psi, v=v, m=m, nu=nu, lab=lab, pts=pts)
+    Mo = f32(rng.random(gm.shape))
+    out["own"] = dict(grid=g3, gm=gm, F=out["3d"]["F"], M=Mo, phi=out["3d"]["phi"])
+    return out
+
+
+def ndimage_smooth(a):
+    from scipy import ndimage
+    return ndimage.gaussian_filter(a, 1.0)
+
+
+def main():
+    ref = pyoracle.reference()
+    C = cases()
+    for tag in ("3d", "2d"):
+        c = C[tag]
+        g = c["grid"]
+        r = {}
+        r["sample_vals"], r["sample_grads"] = ref.sample_linear_points(g, c["M"], c["pts"])
+        r["warp"] = ref.warp_image(g, c["M"], c["phi"])
+        r["labels"] = ref.warp_labels(g, c["lab"], c["phi"])
+        r["compose"] = ref.compose(g, c["phi"], c["psi"])
+        r["det"] = ref.jacobian_det(g, c["psi"])
+        r["sing"] = np.array(ref.singularity_fraction(g, c["phi"]))
+        r["smooth1"] = ref.gaussian_smooth(g, c["F"], 1.0)
+        r["smooth_aniso"] = ref.gaussian_smooth(g, c["F"], [0.5, 1.5, 0.7])
+        r["smooth_big"] = ref.gaussian_smooth(g, c["F"], 3.2)
+        r["smoothf"] = ref.gaussian_smooth_field(g, c["phi"], 1.0)
+        r["smoothf05"] = ref.gaussian_smooth_field(g, c["phi"], 0.5)
+        for rr in (1, 2, 3):
+            val, gr = ref.lncc_eval(g, c["F"], c["phi"], c["M"], rr)
+            r[f"lncc{rr}_val"], r[f"lncc{rr}_grad"] = np.array(val), gr
+        val, gr = ref.ssd_eval(g, c["F"], c["phi"], c["M"])
+        r["ssd_val"], r["ssd_grad"] = np.array(val), gr
+        Fm = np.clip(c["F"], 0, 1)
+        Mm = np.clip(c["M"], 0, 1)
+        val, gr = ref.dice_eval(g, Fm, c["phi"], Mm)
+        r["dice_val"], r["dice_grad"] = np.array(val), gr
+        d, m2, nu2, t2 = ref.adam_step(g, c["m"], c["nu"], 4, 0.9, 0.99, 1e-8, c["v"])
+        r["adam_dir"], r["adam_m"], r["adam_nu"] = d, m2, nu2
+        r["euler"] = ref.eulerian_direction(g, c["v"], c["psi"], False)
+        r["euler_jac"] = ref.eulerian_direction(g, c["v"], c["psi"], True)
+        r["apply"] = ref.apply_update(g, c["psi"], c["v"] * 300, 0.5, 0.5)
+        r["apply_nos"] = ref.apply_update(g, c["psi"], c["v"] * 300, 0.5, 0.0, 0.3)
+        ng, r["down2"] = ref.downsample_image(g, c["F"], 2.0)
+        r["down2_dims"] = np.array(ng.dims)
+        ng3, r["down3"] = ref.downsample_image(g, c["F"], 3.0)
+        r["down3_dims"] = np.array(ng3.dims)
+        big = A.GridMeta(g.ndim, tuple(2 * x - 1 if x > 1 else 1 for x in g.dims))
+        r["up"] = ref.upsample_field(g, c["psi"], big)
+        r["up_big_dims"] = np.array(big.dims)
+        r["up_m"], r["up_nu"] = ref.upsample_state(g, c["m"], c["nu"], big)
+        r["resamp_disp"] = ref.resample_displacement(big, r["up"], g)
+        np.savez_compressed(os.path.join(HERE, f"funcs_{tag}.npz"),
+                            **{k: v for k, v in c.items() if k != "grid"},
+                            dims=np.array(g.dims), ndim=np.array(g.ndim), **r)
+    c = C["own"]
+    val, gr = ref.lncc_eval(c["grid"], c["F"], c["phi"], c["M"], 2, mg=c["gm"])
+    sv, sg = ref.ssd_eval(c["grid"], c["F"], c["phi"], c["M"], mg=c["gm"])
+    np.savez_compressed(os.path.join(HERE, "own_grid.npz"), F=c["F"], M=c["M"], phi=c["phi"],
+                        dims=np.array(c["grid"].dims), mdims=np.array(c["gm"].dims),
+                        lncc_val=np.array(val), lncc_grad=gr, ssd_val=np.array(sv), ssd_grad=sg)
+    # end-to-end: a config-0-shaped pair at 24^3 with a short schedule
+    for loss, name in ((A.LOSS_LNCC, "lncc"), (A.LOSS_SSD, "ssd")):
+        p = synth.make_pair(0, seed=7, shape=(24, 24, 24), iters=(30, 20, 10))
+        cfg = synth.baseline_config(loss, 2, 1.0, max_iters=30)
+        fld, log = ref.register_images(p.grid, p.fixed, p.moving, cfg, p.schedule)
+        np.savez_compressed(
+            os.path.join(HERE, f"register_{name}.npz"), fixed=p.fixed, moving=p.moving,
+            fixed_labels=p.fixed_labels, moving_labels=p.moving_labels,
+            dims=np.array(p.grid.dims), scales=np.array(p.schedule.scales),
+            iters=np.array(p.schedule.iterations), field=fld,
+            losses=np.array([r.loss for r in log.iterations]),
+            max_steps=np.array([r.max_step for r in log.iterations]),
+            scale_index=np.array([r.scale_index for r in log.iterations]),
+            final_loss=np.array(log.final_loss), sing=np.array(log.final_singularity_fraction))
+    # default early stopping (window 10, tol 1e-5) on 16^3 self-registration
+    p = synth.make_pair(0, seed=3, shape=(16, 16, 16))
+    fld, log = ref.register_images(p.grid, p.fixed, p.fixed, A.RegistrationConfig(),
+                                   A.PyramidSchedule())
+    np.savez_compressed(os.path.join(HERE, "register_self.npz"), fixed=p.fixed, field=fld,
+                        losses=np.array([r.loss for r in log.iterations]),
+                        final_loss=np.array(log.final_loss))
+    print("golden vectors written to", HERE)
+
+
+if __name__ == "__main__":
+    main()

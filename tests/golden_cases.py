@@ -1,0 +1,98 @@
+"""Shared recomputation of the golden vectors with any HostAPI backend.
+
+`compute(api, tag)` re-runs, on `api` (the C restatement, the CUDA context, or
+the reference), every call that tests/golden/make_golden.py recorded, and
+returns {key: (got, want)} pairs.  test_oracle.py requires bit-identity for
+the restatement; test_parity_gpu.py applies the fp32/fp64 tolerances.
+"""
+import os
+
+import numpy as np
+
+from paper_2404_01249_b200 import _abi as A
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def load(name):
+    return dict(np.load(os.path.join(GOLDEN, name)))
+
+
+def grid_of(z):
+    dims = tuple(int(v) for v in z["dims"])
+    nd = int(z["ndim"]) if "ndim" in z else 3
+    return A.GridMeta(nd, dims)
+
+
+def compute(api, tag):
+    z = load(f"funcs_{tag}.npz")
+    g = grid_of(z)
+    out = {}
+
+    def pair(key, got):
+        out[key] = (np.asarray(got), z[key])
+
+    vals, grads = api.sample_linear_points(g, z["M"], z["pts"])
+    pair("sample_vals", vals)
+    pair("sample_grads", grads)
+    pair("warp", api.warp_image(g, z["M"], z["phi"]))
+    pair("labels", api.warp_labels(g, z["lab"], z["phi"]))
+    pair("compose", api.compose(g, z["phi"], z["psi"]))
+    pair("det", api.jacobian_det(g, z["psi"]))
+    pair("sing", api.singularity_fraction(g, z["phi"]))
+    pair("smooth1", api.gaussian_smooth(g, z["F"], 1.0))
+    pair("smooth_aniso", api.gaussian_smooth(g, z["F"], [0.5, 1.5, 0.7]))
+    pair("smooth_big", api.gaussian_smooth(g, z["F"], 3.2))
+    pair("smoothf", api.gaussian_smooth_field(g, z["phi"], 1.0))
+    pair("smoothf05", api.gaussian_smooth_field(g, z["phi"], 0.5))
+    for r in (1, 2, 3):
+        v, gr = api.lncc_eval(g, z["F"], z["phi"], z["M"], r)
+        pair(f"lncc{r}_val", v)
+        pair(f"lncc{r}_grad", gr)
+    v, gr = api.ssd_eval(g, z["F"], z["phi"], z["M"])
+    pair("ssd_val", v)
+    pair("ssd_grad", gr)
+    v, gr = api.dice_eval(g, np.clip(z["F"], 0, 1), z["phi"], np.clip(z["M"], 0, 1))
+    pair("dice_val", v)
+    pair("dice_grad", gr)
+    d, m2, nu2, t2 = api.adam_step(g, z["m"], z["nu"], 4, 0.9, 0.99, 1e-8, z["v"])
+    assert t2 == 5
+    pair("adam_dir", d)
+    pair("adam_m", m2)
+    pair("adam_nu", nu2)
+    pair("euler", api.eulerian_direction(g, z["v"], z["psi"], False))
+    pair("euler_jac", api.eulerian_direction(g, z["v"], z["psi"], True))
+    pair("apply", api.apply_update(g, z["psi"], z["v"] * 300, 0.5, 0.5))
+    pair("apply_nos", api.apply_update(g, z["psi"], z["v"] * 300, 0.5, 0.0, 0.3))
+    ng, d2 = api.downsample_image(g, z["F"], 2.0)
+    assert tuple(ng.dims) == tuple(z["down2_dims"])
+    pair("down2", d2)
+    ng3, d3 = api.downsample_image(g, z["F"], 3.0)
+    assert tuple(ng3.dims) == tuple(z["down3_dims"])
+    pair("down3", d3)
+    big = A.GridMeta(g.ndim, tuple(int(v) for v in z["up_big_dims"]))
+    up = api.upsample_field(g, z["psi"], big)
+    pair("up", up)
+    um, unu = api.upsample_state(g, z["m"], z["nu"], big)
+    pair("up_m", um)
+    pair("up_nu", unu)
+    pair("resamp_disp", api.resample_displacement(big, z["up"], g))
+    return out
+
+
+def compute_own_grid(api):
+    z = load("own_grid.npz")
+    g = A.GridMeta(3, tuple(int(v) for v in z["dims"]))
+    gm = A.GridMeta(3, tuple(int(v) for v in z["mdims"]))
+    v, gr = api.lncc_eval(g, z["F"], z["phi"], z["M"], 2, mg=gm)
+    sv, sg = api.ssd_eval(g, z["F"], z["phi"], z["M"], mg=gm)
+    return {"lncc_val": (np.asarray(v), z["lncc_val"]), "lncc_grad": (gr, z["lncc_grad"]),
+            "ssd_val": (np.asarray(sv), z["ssd_val"]), "ssd_grad": (sg, z["ssd_grad"])}
+
+
+def register_inputs(name):
+    z = load(f"register_{name}.npz")
+    g = A.GridMeta(3, tuple(int(v) for v in z["dims"]))
+    sched = A.PyramidSchedule(tuple(float(s) for s in z["scales"]),
+                              tuple(int(i) for i in z["iters"]))
+    return z, g, sched
