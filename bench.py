@@ -29,14 +29,17 @@ sys.path.insert(0, ROOT)
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
 
-# algorithmic (compulsory) bytes per voxel per launch of each kernel class, fp32
-# element = 4 B (fp64: x2).  See DESIGN.md §4.
+# algorithmic (compulsory) bytes per voxel per launch of each kernel class of
+# the plane-streaming LNCC loop, in elements (fp32 4 B, fp64 8 B); DESIGN.md §4.
 ALG_ELEMS = {
-    "loss_fwd": 3 + 1 + 1 + 4,      # read u(3) F M, write 4 LNCC coefficients
-    "lncc_bwd": 4 + 3 + 1 + 1 + 3,  # read 4 coef, u(3), F, M; write grad(3)
+    "loss_fwd": 2 + 4,              # read F, W; write 4 window coefficients
+    "lncc_bwd": 4 + 1 + 1 + 3 + 3,  # read 4 coef, F, W, G(3); write grad(3)
     "smooth_adam": 3 + 3 + 3 + 3 + 3 + 3,  # read grad m nu; write m nu step
-    "compose_smooth": 3 + 3 + 3,    # read step u; write u'
+    "compose_smooth": 3 + 3 + 1 + 3 + 1 + 3,  # read step u M; write u' W G(3)
 }
+# the iteration's irreducible state traffic: read u m nu F M,
+# write u m nu = 20 elements (80 B fp32)
+ITER_MIN_ELEMS = 20
 
 
 def parse():
@@ -317,6 +320,12 @@ def main():
                 "traffic": None,
                 "per_kernel_frac": {k: v["gbs"] / peak for k, v in per.items()},
                 "per_kernel_ms": {k: v["avg_ms"] for k, v in per.items()}}
+        it_ms = sum(v["avg_ms"] for v in per.values()) + (
+            kt["monitor"]["ms"] / kt["monitor"]["launches"] if kt["monitor"]["launches"] else 0)
+        vox = per[dom]["alg_bytes"] / (ALG_ELEMS[dom] * esz)
+        roof["iteration"] = {"ms": it_ms, "min_bytes_per_voxel": ITER_MIN_ELEMS * esz,
+                             "achieved": vox * ITER_MIN_ELEMS * esz / (it_ms * 1e6),
+                             "frac": vox * ITER_MIN_ELEMS * esz / (it_ms * 1e6) / peak}
         tr = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tr):
             try:

@@ -129,6 +129,27 @@ template <class T>
 void launch_gauss_fused(const Launch& L, int R, const GaussW<T>& w, CPlanes3<T> in,
                         Planes3<T> out, int ncomp, Dims d);
 
+// -------- plane-streaming (TMA) kernels, kernels_tma.cu.  Fields are passed as
+// the base of their 3 (coef: 4) contiguous planes.  Launchers return < 0 when
+// the shape/radius is not supported (caller falls back to the kernels above).
+bool tma_supported(Dims d, int esz);
+template <class T>
+int launch_lncc_fwd_tma(const Launch& L, int R, const T* F, const T* W, Dims d, T* coef,
+                        double* partials, const LoopState* st);
+template <class T>
+int launch_lncc_bwd_tma(const Launch& L, int R, const T* coef, const T* F, const T* W,
+                        const T* G, Dims d, T* grad, const LoopState* st);
+template <class T>
+int launch_smooth_adam_tma(const Launch& L, int R, const GaussW<T>& w, const T* grad, T* m,
+                           T* nu, T* step, Dims d, AdamParams ap, LoopState* st,
+                           unsigned long long* maxstep);
+template <class T>
+int launch_compose_tma(const Launch& L, int R, double cap, const GaussW<T>& w, const T* step,
+                       const T* uin, T* uout, const T* M, Dims dm, Dims d, T* W, T* G,
+                       LoopState* st);
+template <class T>
+void launch_warpgrad(const Launch& L, const T* M, Dims dm, CPlanes3<T> u, Dims d, T* W, T* G);
+
 // -------- loop control
 // kind: 0 ssd, 1 lncc, 2 dice (3 partial arrays of np each)
 void launch_monitor(const Launch& L, int kind, const double* partials, int np, double nvox,

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <stdexcept>
@@ -81,6 +82,8 @@ struct dfm_ctx {
     int64_t launches = 0;
     std::map<std::string, std::pair<void*, size_t>> bufs;
     bool profiling = false;
+    bool force_legacy = getenv("DFM_FORCE_LEGACY") != nullptr;  // A/B the v1 kernels
+    int tma_mask = getenv("DFM_TMA_MASK") ? atoi(getenv("DFM_TMA_MASK")) : 15;
     double kt_ms[DFM_NUM_KCLASS] = {};
     int64_t kt_n[DFM_NUM_KCLASS] = {};
     int64_t kt_vox[DFM_NUM_KCLASS] = {};
@@ -416,6 +419,24 @@ double eval_loss_dev(dfm_ctx* ctx, int loss, int R, const T* F, const T* M, cons
     Launch L = ctx->L();
     double* partials = ctx->arr<double>("partials", 1 << 17);
     double* val = ctx->arr<double>("value3", 4);
+    if (loss == DFM_LOSS_LNCC && want_grad && R <= 5 && tma_supported(d, sizeof(T))) {
+        // plane-streaming path (the one the registration loop runs):
+        // W, G = M(x+u), grad M(x+u); TMA-fed box passes.  grad planes contiguous.
+        T* W = ctx->arr<T>("api_W", d.n);
+        T* G = ctx->arr<T>("api_G", 3 * d.n);
+        T* cb = ctx->arr<T>("coef", 4 * d.n);
+        launch_warpgrad<T>(L, M, dm, u, d, W, G);
+        const int np = launch_lncc_fwd_tma<T>(L, R, F, W, d, cb, partials, nullptr);
+        if (np > 0) {
+            launch_reduce_value(L, 1, partials, np, static_cast<double>(d.n), val);
+            if (launch_lncc_bwd_tma<T>(L, R, cb, F, W, G, d, grad.c[0], nullptr) < 0)
+                fail(DFM_E_CUDA, "lncc_bwd_tma launch failed");
+            double hv[3];
+            CK(cudaMemcpyAsync(hv, val, sizeof(hv), cudaMemcpyDeviceToHost, ctx->stream));
+            ctx->sync();
+            return hv[0];
+        }
+    }
     T* coef[4] = {nullptr, nullptr, nullptr, nullptr};
     if (loss == DFM_LOSS_LNCC && want_grad) {
         T* cb = ctx->arr<T>("coef", 4 * d.n);
@@ -939,7 +960,15 @@ dfm_status dfm_apply_update(dfm_ctx* ctx, const dfm_grid* g, const double* phi, 
             if (hb) fail(DFM_E_NUMERICAL, "apply_update: non-finite step");
             const double sw[3] = {sigma_warp, sigma_warp, sigma_warp};
             const HostGauss h = make_gauss(d, sw);
-            if (sigma_warp > 0.0 && h.R <= kRMax) {
+            int done_tma = -1;
+            if (h.R <= 4 && tma_supported(d, sizeof(T))) {
+                const GaussW<T> w = upload_gauss<T>(ctx, h, d, "api_warp");
+                done_tma = launch_compose_tma<T>(ctx->L(), h.R, cap, w, s.p[0], a.p[0], o.p[0],
+                                                 nullptr, d, d, nullptr, nullptr, nullptr);
+            }
+            if (done_tma >= 0) {
+                // plane-streaming compose + sigma_warp smoothing (the loop's kernel)
+            } else if (sigma_warp > 0.0 && h.R <= kRMax) {
                 const GaussW<T> w = upload_gauss<T>(ctx, h, d, "api_warp");
                 launch_compose_smooth<T>(ctx->L(), h.R, w, s.r(), a.r(), o.w(), d, nullptr);
             } else {
@@ -1024,6 +1053,9 @@ struct Registrar {
     double* corr1;
     double* corr2;
     int cur = 0;
+    T* Wb = nullptr;  // W = M(x+u) for the current u (TMA path)
+    T* Gb = nullptr;  // grad M(x+u), 3 planes
+    bool use_tma = false;
     // profiling
     std::vector<cudaEvent_t> evpool;
     std::vector<std::pair<int, int>> evuse;  // (class, pool index of start)
@@ -1040,6 +1072,8 @@ struct Registrar {
         step = dev_field<T>(ctx, "reg_step", n);
         T* cb = ctx->arr<T>("reg_coef", 4 * n);
         for (int k = 0; k < 4; ++k) coef[k] = cb + k * n;
+        Wb = ctx->arr<T>("reg_W", n);
+        Gb = ctx->arr<T>("reg_G", 3 * n);
         partials = ctx->arr<double>("reg_partials", 3 * 65536);
         st = ctx->arr<LoopState>("reg_state", 1);
         const int64_t cap = total_iters + 2;
@@ -1101,10 +1135,79 @@ struct Registrar {
         evuse.clear();
     }
 
+    // can this scale run the plane-streaming (TMA) kernels?
+    bool tma_eligible(const Dims& d, int Rg, int Rw, bool big) const {
+        return !big && !cfg->use_jac && cfg->step_cap <= 1.5 && Rg <= 6 && Rw <= 4 &&
+               (cfg->loss != DFM_LOSS_LNCC || cfg->lncc_radius <= 5) &&
+               tma_supported(d, sizeof(T));
+    }
+
+    // one iteration with the plane-streaming kernels: u[src] -> u[1-src]; W, G
+    // (warped moving image and its interpolant gradient at u[src]) are kept
+    // current by the compose of the previous iteration / warpgrad at scale start.
+    void enqueue_iteration_tma(const Dims& d, int src, int Rg, int Rw, const GaussW<T>& wg,
+                               const GaussW<T>& ww) {
+        Launch L = ctx->L();
+        const int loss_kind = cfg->loss;
+        const CPlanes3<T> uin = u[src].r();
+        const bool lncc = loss_kind == DFM_LOSS_LNCC;
+        const int mask = ctx->tma_mask;  // A/B switch per kernel (DFM_TMA_MASK)
+        int np;
+        ev_begin(KC_FWD);
+        if (lncc && (mask & 1))
+            np = launch_lncc_fwd_tma<T>(L, cfg->lncc_radius, Fs, Wb, d, coef[0], partials, st);
+        else
+            np = loss_kind_launch_fwd<T>(ctx, loss_kind, cfg->lncc_radius, Fs, Ms, d, d, uin,
+                                         coef, grad.w(), partials, st);
+        ev_end();
+        ev_begin(KC_MON);
+        launch_monitor(L, monitor_kind(loss_kind), partials, np, static_cast<double>(d.n), st,
+                       loss, stamp, cfg->conv_window, cfg->conv_tol);
+        ev_end();
+        if (lncc) {
+            ev_begin(KC_BWD);
+            if (mask & 2) {
+                launch_lncc_bwd_tma<T>(L, cfg->lncc_radius, coef[0], Fs, Wb, Gb, d, grad.p[0], st);
+            } else {
+                const T* cc[4] = {coef[0], coef[1], coef[2], coef[3]};
+                launch_lncc_bwd<T>(L, cfg->lncc_radius, Fs, Ms, d, d, uin, cc, grad.w(), st);
+            }
+            ev_end();
+        } else if (loss_kind == DFM_LOSS_DICE) {
+            ev_begin(KC_BWD);
+            launch_dice_grad<T>(L, Fs, Ms, d, d, uin, grad.w(), st, 0.0, 1.0);
+            ev_end();
+        }
+        AdamParams ap{cfg->beta1, cfg->beta2, cfg->eps_adam, cfg->eta, cfg->step_cap,
+                      corr1, corr2, cfg->use_jac};
+        ev_begin(KC_ADAM);
+        if (mask & 4)
+            launch_smooth_adam_tma<T>(L, Rg, wg, grad.p[0], m.p[0], nu.p[0], step.p[0], d, ap, st,
+                                      maxstep);
+        else
+            launch_smooth_adam<T>(L, Rg, wg, grad.r(), uin, m.w(), nu.w(), step.w(), d, ap, st,
+                                  maxstep);
+        ev_end();
+        ev_begin(KC_COMPOSE);
+        if (mask & 8) {
+            launch_compose_tma<T>(L, Rw, cfg->step_cap, ww, step.p[0], u[src].p[0],
+                                  u[1 - src].p[0], Ms, d, d, lncc ? Wb : nullptr,
+                                  lncc ? Gb : nullptr, st);
+        } else {
+            launch_compose_smooth<T>(L, Rw, ww, step.r(), uin, u[1 - src].w(), d, st);
+            if (lncc) launch_warpgrad<T>(L, Ms, d, u[1 - src].r(), d, Wb, Gb);
+        }
+        ev_end();
+    }
+
     // one iteration of the hot loop on grid d, u[src] -> u[1-src]
     void enqueue_iteration(const Dims& d, int src, int Rg, int Rw, const GaussW<T>& wg,
                            const GaussW<T>& ww, const DevAxisGauss* big_g,
                            const DevAxisGauss* big_w) {
+        if (use_tma) {
+            enqueue_iteration_tma(d, src, Rg, Rw, wg, ww);
+            return;
+        }
         Launch L = ctx->L();
         const int loss_kind = cfg->loss;
         const CPlanes3<T> uin = u[src].r();
@@ -1171,12 +1274,14 @@ struct Registrar {
                 Mw = Mbuf;
             }
             if (!have) {
+                layout_all(d.n);
                 init_field(d, init);
                 zero_field(m, d.n);
                 zero_field(nu, d.n);
                 have = true;
             } else if (!dims_equal(cd, d)) {
                 upsample_state(cd, d);
+                layout_all(d.n);
             }
             ev_end();
             cd = d;
@@ -1266,6 +1371,7 @@ struct Registrar {
         if (!dims_equal(id, full))
             fail(DFM_E_INVALID, "register_images: init field must live on the full or coarsest grid");
         // resample_displacement from the full grid (interp.cpp:447-465)
+        relayout(u[1], id.n);
         upload_field<T>(ctx, init->field, id.n, id.ndim, u[1]);
         double mult[3] = {1.0, 1.0, 1.0};
         const int nn[3] = {d.nx, d.ny, d.nz}, no[3] = {id.nx, id.ny, id.nz};
@@ -1274,9 +1380,28 @@ struct Registrar {
         const T* src[3] = {u[1].p[0], u[1].p[1], u[1].p[2]};
         T* dst[3] = {u[0].p[0], u[0].p[1], u[0].p[2]};
         launch_resample<T>(ctx->L(), src, id, dst, d, d.ndim, mult);
+        relayout(u[1], d.n);
+    }
+
+    // Field planes are packed at the current scale's voxel count (the TMA maps
+    // and the fused kernels address component k at base + k*n).
+    static void relayout(Field<T>& f, int64_t n) {
+        f.p[1] = f.p[0] + n;
+        f.p[2] = f.p[0] + 2 * n;
+    }
+    // re-pack the buffers that carry no state across the scale change
+    void layout_all(int64_t n) {
+        relayout(u[1 - cur], n);
+        relayout(grad, n);
+        relayout(step, n);
+        if (cur == 0 && u[0].p[1] != u[0].p[0] + n) relayout(u[0], n);
+        if (m.p[1] != m.p[0] + n) relayout(m, n);
+        if (nu.p[1] != nu.p[0] + n) relayout(nu, n);
+        for (int k = 1; k < 4; ++k) coef[k] = coef[0] + k * n;
     }
 
     void upsample_field_only(const Dims& from, const Dims& to) {
+        relayout(u[1 - cur], to.n);
         double mult[3] = {1.0, 1.0, 1.0};
         const int nn[3] = {to.nx, to.ny, to.nz}, no[3] = {from.nx, from.ny, from.nz};
         for (int a = 0; a < to.ndim; ++a)
@@ -1297,6 +1422,8 @@ struct Registrar {
             mm[a] = r;
             mn[a] = r * r;
         }
+        relayout(grad, to.n);
+        relayout(step, to.n);
         const T* sm[3] = {m.p[0], m.p[1], m.p[2]};
         T* dm[3] = {grad.p[0], grad.p[1], grad.p[2]};
         launch_resample<T>(ctx->L(), sm, from, dm, to, to.ndim, mm);
@@ -1337,6 +1464,9 @@ struct Registrar {
         const int Rg = hg.R > kRMax ? 0 : hg.R;
         const int Rw = hw.R > kRMax ? 0 : hw.R;
         const int start = cur;
+        use_tma = !ctx->force_legacy && tma_eligible(d, Rg, Rw, pbg || pbw);
+        if (use_tma && cfg->loss == DFM_LOSS_LNCC)
+            launch_warpgrad<T>(ctx->L(), Ms, d, u[cur].r(), d, Wb, Gb);
         if (ctx->profiling) {
             for (int j = 0; j < T_si; ++j)
                 enqueue_iteration(d, (start + j) % 2, Rg, Rw, wg, ww, pbg, pbw);

@@ -1,0 +1,797 @@
+// kernels_tma.cu — plane-streaming stencil kernels of the hot loop (v2).
+//
+// Same 2.5-D z-march as kernels_stencil.cu (haloed xy tile per plane, x/y
+// filters in shared memory, z filter in a register ring), but every input
+// plane tile is fetched by TMA (cp.async.bulk.tensor, zero fill outside the
+// volume) into an S-stage shared-memory ring guarded by mbarriers, one
+// elected thread running S-1 planes ahead of the compute.  Memory latency is
+// therefore off the critical path and the compute reads only shared memory.
+//
+// Data flow of one LNCC iteration with these kernels:
+//   compose (previous iteration / warpgrad at scale start) -> u, W=M(x+u), G=grad M(x+u)
+//   lncc_fwd   F, W (halo r)          -> 4 window coefficients + cc^2 partials
+//   lncc_bwd   coefficients (halo r)  -> grad = dW * G            (center F, W, G)
+//   smooth_adam grad (halo 3 sigma_g) -> m, nu, capped step       (center m, nu)
+//   compose    step (halo 3 sigma_w), u (halo 3 sigma_w + cap)  -> u', W', G'
+// The compose gathers u(x+step) from the shared-memory u tiles: with
+// |step| <= cap <= 1.5 the 8 interpolation corners lie within 2 voxels.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+#include <type_traits>
+
+#include "dfm_device.cuh"
+#include "dfm_kernels.cuh"
+#include "tma_util.cuh"
+
+namespace dfm {
+
+namespace {
+
+constexpr int TX = kTX, TY = kTY, NT = TX * TY;
+
+template <class T>
+constexpr int round_bx(int w) {
+    return (w + (16 / int(sizeof(T))) - 1) / (16 / int(sizeof(T))) * (16 / int(sizeof(T)));
+}
+constexpr int align128(int b) { return (b + 127) / 128 * 128; }
+
+struct Red2 {
+    double sum;
+    double mx;
+};
+
+struct ZG2 {
+    Dims d;
+    int zchunk;
+    int tiles_x;
+};
+
+template <int NTH>
+__device__ double bsum(double v, double* sh) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    v = 0.0;
+    if (w == 0) {
+        v = l < NTH / 32 ? sh[l] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    }
+    __syncthreads();
+    return v;
+}
+
+template <int NTH>
+__device__ double bmax(double v, double* sh) {
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    v = 0.0;
+    if (w == 0) {
+        v = l < NTH / 32 ? sh[l] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
+    }
+    __syncthreads();
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// the streaming z-march driver
+template <class Op>
+__global__ void __launch_bounds__(NT) k_zm2(const __grid_constant__ Op op, const ZG2 g) {
+    using Acc = typename Op::Acc;
+    constexpr int R = Op::R, C = Op::C, S = Op::S, K = 2 * R + 1;
+    constexpr int HI = TY + 2 * R, WI = TX + 2 * R;
+    constexpr int SB = Op::kStageBytes;
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned char* stages = smem;
+    Acc* s_in = reinterpret_cast<Acc*>(smem + S * SB);
+    Acc* s_x = s_in + (Op::kStaged ? C * HI * WI : 0);  // two buffers of C*HI*TX
+    __shared__ __align__(8) uint64_t bars[S];
+    __shared__ double s_red[32];
+
+    if (op.skip()) return;
+    const Dims& d = g.d;
+    const int tid = threadIdx.x;
+    const int tx = tid % TX, ty = tid / TX;
+    const int x0 = (blockIdx.x % g.tiles_x) * TX;
+    const int y0 = (blockIdx.x / g.tiles_x) * TY;
+    const int z0 = blockIdx.y * g.zchunk;
+    const int z1 = min(z0 + g.zchunk, d.nz);
+    const int x = x0 + tx, y = y0 + ty;
+    const bool own = x < d.nx && y < d.ny;
+    const int q0 = z0 - R - Op::BACK;
+    const int qend = z1 + R + Op::AHEAD;
+
+    if (tid == 0) {
+        op.prefetch_maps();
+#pragma unroll
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int q = q0; q < qend && q < q0 + S; ++q)
+            op.issue(stages + ((q - q0) % S) * SB, &bars[(q - q0) % S], x0, y0, q);
+
+    Acc ring[C][K];
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+#pragma unroll
+        for (int k = 0; k < K; ++k) ring[c][k] = Acc(0);
+    double rsum = 0.0, rmax = 0.0;
+    int waited = q0 - 1;
+    int buf = 0;
+
+    for (int zi = z0 - R; zi < z1 + R; ++zi) {
+        const int zo = zi - R;
+        const bool em = (zo >= z0) && own;
+        typename Op::Center cen;
+        if (em) op.load_center(x, y, zo, cen);
+        while (waited < zi + Op::AHEAD) {
+            ++waited;
+            const int k = waited - q0;
+            mbar_wait(&bars[k % S], (k / S) & 1);
+        }
+        Acc* sx = s_x + buf * (C * HI * TX);
+        if constexpr (Op::kStaged) {
+            for (int e = tid; e < HI * WI; e += NT) {
+                const int row = e / WI, col = e - row * WI;
+                Acc v[C];
+                op.stage(stages, q0, x0, y0, zi, row, col, v);
+#pragma unroll
+                for (int c = 0; c < C; ++c) s_in[(c * HI + row) * WI + col] = v[c];
+            }
+            __syncthreads();
+            for (int row = ty; row < HI; row += TY) {
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    const Acc* src = s_in + (c * HI + row) * WI + tx;
+                    Acc a = Acc(0);
+#pragma unroll
+                    for (int j = 0; j < K; ++j) a += op.wgt(0, j) * src[j];
+                    sx[(c * HI + row) * TX + tx] = a * op.nrm(0, x);
+                }
+            }
+        } else {
+            const unsigned char* st = stages + ((zi - q0) % S) * SB;
+            for (int row = ty; row < HI; row += TY) {
+                Acc v[C];
+                op.xpass(st, row, tx, x, v);
+#pragma unroll
+                for (int c = 0; c < C; ++c) sx[(c * HI + row) * TX + tx] = v[c];
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            const int qf = zi - Op::BACK + S;
+            if (qf < qend) {
+                const int k = qf - q0;
+                op.issue(stages + (k % S) * SB, &bars[k % S], x0, y0, qf);
+            }
+        }
+        // y pass + z ring
+        const Acc ny = own ? op.nrm(1, y) : Acc(0);
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            const Acc* src = sx + (c * HI + ty) * TX + tx;
+            Acc a = Acc(0);
+#pragma unroll
+            for (int j = 0; j < K; ++j) a += op.wgt(1, j) * src[j * TX];
+#pragma unroll
+            for (int k = 0; k < K - 1; ++k) ring[c][k] = ring[c][k + 1];
+            ring[c][K - 1] = a * ny;
+        }
+        if (em) {
+            const Acc nz = op.nrm(2, zo);
+            Acc s[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                Acc a = Acc(0);
+#pragma unroll
+                for (int k = 0; k < K; ++k) a += op.wgt(2, k) * ring[c][k];
+                s[c] = a * nz;
+            }
+            const Red2 r = op.emit(x, y, zo, s, cen);
+            rsum += r.sum;
+            rmax = fmax(rmax, r.mx);
+        }
+        buf ^= 1;
+    }
+    if constexpr (Op::kSum || Op::kMax) {
+        const int blk = blockIdx.y * gridDim.x + blockIdx.x;
+        const double bs = Op::kSum ? bsum<NT>(rsum, s_red) : 0.0;
+        const double bm = Op::kMax ? bmax<NT>(rmax, s_red) : 0.0;
+        if (tid == 0) op.finish(blk, bs, bm);
+    } else {
+        if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0) op.finish(0, 0.0, 0.0);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// ops
+
+struct NoCenter {};
+
+// similarity.cpp:122-168 — box moments of F and W = M(x+u), window coefficients
+template <class T, int R_>
+struct LnccFwd2 {
+    using Acc = double;
+    static constexpr int R = R_, C = 5, BACK = 0, AHEAD = 0, S = 4;
+    static constexpr bool kStaged = false, kSum = true, kMax = false;
+    static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TY + 2 * R;
+    static constexpr int kBytes = BX * BY * int(sizeof(T));
+    static constexpr int kBox = align128(kBytes);  // TMA smem destinations 128 B aligned
+    static constexpr int kStageBytes = 2 * kBox;
+    CUtensorMap mF, mW;
+    T* coef;  // 4 planes, coef[k*n + i]; nullptr -> value only
+    double* partials;
+    const LoopState* st;
+    Dims d;
+    using Center = NoCenter;
+
+    __device__ bool skip() const { return st && st->done; }
+    __device__ void prefetch_maps() const {
+        prefetch_tmap(&mF);
+        prefetch_tmap(&mW);
+    }
+    __device__ void issue(unsigned char* dst, uint64_t* bar, int x0, int y0, int q) const {
+        mbar_expect_tx(bar, 2 * kBytes);
+        tma_load_4d(dst, &mF, bar, x0 - XA, y0 - R, q, 0);
+        tma_load_4d(dst + kBox, &mW, bar, x0 - XA, y0 - R, q, 0);
+    }
+    __device__ Acc wgt(int, int) const { return 1.0; }
+    __device__ Acc nrm(int, int) const { return 1.0; }
+    __device__ void xpass(const unsigned char* st_, int row, int col, int, Acc v[5]) const {
+        const T* F = reinterpret_cast<const T*>(st_) + row * BX + col + (XA - R);
+        const T* W = F + kBox / int(sizeof(T));
+        double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
+#pragma unroll
+        for (int j = 0; j < 2 * R + 1; ++j) {
+            const double f = static_cast<double>(F[j]), w = static_cast<double>(W[j]);
+            a0 += f;
+            a1 += w;
+            a2 += f * f;
+            a3 += w * w;
+            a4 += f * w;
+        }
+        v[0] = a0;
+        v[1] = a1;
+        v[2] = a2;
+        v[3] = a3;
+        v[4] = a4;
+    }
+    __device__ void load_center(int, int, int, Center&) const {}
+    __device__ Red2 emit(int x, int y, int z, const double s[5], const Center&) const {
+        const double n = static_cast<double>(box_len(x, d.nx, R) * box_len(y, d.ny, R) *
+                                             (d.nz > 1 ? box_len(z, d.nz, R) : 1));
+        const double muF = s[0] / n;
+        const double muW = s[1] / n;
+        double vF = s[2] / n - muF * muF;
+        double vW = s[3] / n - muW * muW;
+        vF = vF < 0.0 ? 0.0 : vF;
+        vW = vW < 0.0 ? 0.0 : vW;
+        const double cv = s[4] / n - muF * muW;
+        double cc2 = 0.0, an = 0.0, amu = 0.0, bn = 0.0, bmu = 0.0;
+        if (!(vF < 1e-5 || vW < 1e-5)) {
+            const double cc = cv / sqrt(vF * vW);
+            cc2 = cc * cc;
+            const double alpha = cv / (vF * vW);
+            const double beta = cv * cv / (vF * vW * vW);
+            an = alpha / n;
+            amu = alpha * muF / n;
+            bn = beta / n;
+            bmu = beta * muW / n;
+        }
+        if (coef) {
+            const int64_t i = d.idx(x, y, z);
+            coef[i] = static_cast<T>(an);
+            coef[d.n + i] = static_cast<T>(amu);
+            coef[2 * d.n + i] = static_cast<T>(bn);
+            coef[3 * d.n + i] = static_cast<T>(bmu);
+        }
+        return {cc2, 0.0};
+    }
+    __device__ void finish(int blk, double s, double) const { partials[blk] = s; }
+};
+
+// similarity.cpp:170-189 — box sums of the coefficients, dW, grad = dW * G
+template <class T, int R_>
+struct LnccBwd2 {
+    using Acc = double;
+    static constexpr int R = R_, C = 4, BACK = 0, AHEAD = 0, S = 4;
+    static constexpr bool kStaged = false, kSum = false, kMax = false;
+    static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TY + 2 * R;
+    static constexpr int kBytes = BX * BY * int(sizeof(T));
+    static constexpr int kBox = align128(kBytes);
+    static constexpr int kStageBytes = 4 * kBox;
+    CUtensorMap mC;
+    const T* F;
+    const T* W;
+    const T* G;  // 3 planes
+    T* grad;     // 3 planes
+    const LoopState* st;
+    Dims d;
+    struct Center {
+        T f, w, g0, g1, g2;
+    };
+
+    __device__ bool skip() const { return st && st->done; }
+    __device__ void prefetch_maps() const { prefetch_tmap(&mC); }
+    __device__ void issue(unsigned char* dst, uint64_t* bar, int x0, int y0, int q) const {
+        mbar_expect_tx(bar, 4 * kBytes);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) tma_load_4d(dst + k * kBox, &mC, bar, x0 - XA, y0 - R, q, k);
+    }
+    __device__ Acc wgt(int, int) const { return 1.0; }
+    __device__ Acc nrm(int, int) const { return 1.0; }
+    __device__ void xpass(const unsigned char* st_, int row, int col, int, Acc v[4]) const {
+        const T* p = reinterpret_cast<const T*>(st_) + row * BX + col + (XA - R);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            double a = 0.0;
+#pragma unroll
+            for (int j = 0; j < 2 * R + 1; ++j)
+                a += static_cast<double>(p[c * (kBox / int(sizeof(T))) + j]);
+            v[c] = a;
+        }
+    }
+    __device__ void load_center(int x, int y, int z, Center& c) const {
+        const int64_t i = d.idx(x, y, z);
+        c.f = __ldg(F + i);
+        c.w = __ldg(W + i);
+        c.g0 = __ldg(G + i);
+        c.g1 = __ldg(G + d.n + i);
+        c.g2 = d.ndim == 3 ? __ldg(G + 2 * d.n + i) : T(0);
+    }
+    __device__ Red2 emit(int x, int y, int z, const double s[4], const Center& c) const {
+        const int64_t i = d.idx(x, y, z);
+        const double f = static_cast<double>(c.f), w = static_cast<double>(c.w);
+        const double dW = -2.0 / static_cast<double>(d.n) * (f * s[0] - s[1] - w * s[2] + s[3]);
+        grad[i] = static_cast<T>(dW * static_cast<double>(c.g0));
+        grad[d.n + i] = static_cast<T>(dW * static_cast<double>(c.g1));
+        grad[2 * d.n + i] = static_cast<T>(dW * static_cast<double>(c.g2));
+        return {0.0, 0.0};
+    }
+    __device__ void finish(int, double, double) const {}
+};
+
+// pipeline.cpp:182-186 + optim.cpp:22-42 + diffeo.cpp:47-57
+template <class T, int R_>
+struct SmoothAdam2 {
+    using Acc = T;
+    static constexpr int R = R_, C = 3, BACK = 0, AHEAD = 0, S = 4;
+    static constexpr bool kStaged = false, kSum = false, kMax = true;
+    static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TY + 2 * R;
+    static constexpr int kBytes = BX * BY * int(sizeof(T));
+    static constexpr int kBox = align128(kBytes);
+    static constexpr int kStageBytes = 3 * kBox;
+    CUtensorMap mG;
+    GaussW<T> w;
+    T* m;   // 3 planes
+    T* nu;  // 3 planes
+    T* step;
+    T b1, omb1, b2, omb2, eps, eta, cap;
+    const double* corr1;
+    const double* corr2;
+    LoopState* st;
+    unsigned long long* maxstep;
+    Dims d;
+    struct Center {
+        T m[3], nu[3];
+    };
+
+    __device__ bool skip() const { return st && st->done; }
+    __device__ void prefetch_maps() const { prefetch_tmap(&mG); }
+    __device__ void issue(unsigned char* dst, uint64_t* bar, int x0, int y0, int q) const {
+        mbar_expect_tx(bar, 3 * kBytes);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) tma_load_4d(dst + k * kBox, &mG, bar, x0 - XA, y0 - R, q, k);
+    }
+    __device__ Acc wgt(int a, int j) const { return w.taps[a][j]; }
+    __device__ Acc nrm(int a, int i) const { return __ldg(w.norm[a] + i); }
+    __device__ void xpass(const unsigned char* st_, int row, int col, int x, Acc v[3]) const {
+        const T* p = reinterpret_cast<const T*>(st_) + row * BX + col + (XA - R);
+        const T nx = x < d.nx ? __ldg(w.norm[0] + x) : T(0);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            T a = T(0);
+#pragma unroll
+            for (int j = 0; j < 2 * R + 1; ++j) a += w.taps[0][j] * p[c * (kBox / int(sizeof(T))) + j];
+            v[c] = a * nx;
+        }
+    }
+    __device__ void load_center(int x, int y, int z, Center& c) const {
+        const int64_t i = d.idx(x, y, z);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            c.m[k] = k < d.ndim ? m[k * d.n + i] : T(0);
+            c.nu[k] = k < d.ndim ? nu[k * d.n + i] : T(0);
+        }
+    }
+    __device__ Red2 emit(int x, int y, int z, const T s[3], const Center& c) const {
+        const int64_t i = d.idx(x, y, z);
+        const long long t = st ? st->t : 1;
+        const T c1 = static_cast<T>(corr1[t]);
+        const T c2 = static_cast<T>(corr2[t]);
+        double mx = 0.0;
+        bool bad = false;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            if (k >= d.ndim) {
+                step[k * d.n + i] = T(0);
+                continue;
+            }
+            const T v = -s[k];
+            const T mm = b1 * c.m[k] + omb1 * v;
+            const T nn = b2 * c.nu[k] + omb2 * v * v;
+            m[k * d.n + i] = mm;
+            nu[k * d.n + i] = nn;
+            const T dir = (mm / c1) / (sqrt(nn / c2) + eps);
+            const T sv = eta * dir;
+            bad |= !isfinite(sv);
+            const T cl = sv < -cap ? -cap : (cap < sv ? cap : sv);
+            step[k * d.n + i] = cl;
+            mx = fmax(mx, static_cast<double>(fabs(cl)));
+        }
+        if (bad && st) st->bad_step = 1;
+        return {0.0, mx};
+    }
+    __device__ void finish(int, double, double mx) const {
+        if (maxstep) atomic_max_nonneg(maxstep + (st ? st->slot : 0), mx);
+    }
+};
+
+// diffeo.cpp:60-62 + interp.cpp:269-289 — u' = step + u(x+step), sigma_warp
+// Gaussian, then W = M(x+u') and G = grad M(x+u') for the next loss pass.
+template <class T, int R_, int CAPH>
+struct Compose2 {
+    using Acc = T;
+    static constexpr int R = R_, C = 3, BACK = CAPH, AHEAD = CAPH, S = 2 * CAPH + 3;
+    static constexpr bool kStaged = true, kSum = false, kMax = false;
+    static constexpr int HU = R + CAPH;  // u halo: Gaussian radius + gather reach
+    static constexpr int XAS = round_bx<T>(R), BXS = round_bx<T>(TX + XAS + R), BYS = TY + 2 * R;
+    static constexpr int XAU = round_bx<T>(HU), BXU = round_bx<T>(TX + XAU + HU), BYU = TY + 2 * HU;
+    static constexpr int kBytesS = BXS * BYS * int(sizeof(T));
+    static constexpr int kBytesU = BXU * BYU * int(sizeof(T));
+    static constexpr int kBoxS = align128(kBytesS), kBoxU = align128(kBytesU);
+    static constexpr int kStageBytes = 3 * kBoxS + 3 * kBoxU;
+    static constexpr int PS = kBoxS / int(sizeof(T)), PU = kBoxU / int(sizeof(T));
+    CUtensorMap mS, mU;
+    GaussW<T> w;
+    T* uout;  // 3 planes
+    const T* M;
+    Dims dm;
+    T* W;     // nullptr: do not produce W/G
+    T* G;     // 3 planes
+    LoopState* st;
+    Dims d;
+    using Center = NoCenter;
+
+    __device__ bool skip() const {
+        if (!st) return false;
+        if (st->done) return true;
+        if (st->bad_step) {  // diffeo.cpp:52-53: throw before composing
+            if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+                st->err = 2;
+                st->done = 1;
+            }
+            return true;
+        }
+        return false;
+    }
+    __device__ void prefetch_maps() const {
+        prefetch_tmap(&mS);
+        prefetch_tmap(&mU);
+    }
+    __device__ void issue(unsigned char* dst, uint64_t* bar, int x0, int y0, int q) const {
+        mbar_expect_tx(bar, 3 * kBytesS + 3 * kBytesU);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) tma_load_4d(dst + k * kBoxS, &mS, bar, x0 - XAS, y0 - R, q, k);
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            tma_load_4d(dst + 3 * kBoxS + k * kBoxU, &mU, bar, x0 - XAU, y0 - HU, q, k);
+    }
+    __device__ Acc wgt(int a, int j) const { return w.taps[a][j]; }
+    __device__ Acc nrm(int a, int i) const { return i < (a == 0 ? d.nx : (a == 1 ? d.ny : d.nz))
+                                                       ? __ldg(w.norm[a] + i) : T(0); }
+    __device__ void stage(const unsigned char* stages, int q0, int x0, int y0, int zi, int row,
+                          int col, T v[3]) const {
+        const int gx = x0 - R + col, gy = y0 - R + row;
+        if (gx < 0 || gx >= d.nx || gy < 0 || gy >= d.ny || zi < 0 || zi >= d.nz) {
+            v[0] = v[1] = v[2] = T(0);
+            return;
+        }
+        const T* sp = reinterpret_cast<const T*>(stages + ((zi - q0) % S) * kStageBytes);
+        const int so = row * BXS + col + (XAS - R);
+        const T s0 = sp[so], s1 = sp[PS + so];
+        const T s2 = d.ndim == 3 ? sp[2 * PS + so] : T(0);
+        const AxisCell<T> ax = locate_axis(gx, s0, d.nx);
+        const AxisCell<T> ay = locate_axis(gy, s1, d.ny);
+        const bool three = d.nz > 1;
+        AxisCell<T> az;
+        if (three) {
+            az = locate_axis(zi, s2, d.nz);
+        } else {
+            az.i0 = 0;
+            az.f = T(0);
+        }
+        const int lx = ax.i0 - (x0 - XAU), ly = ay.i0 - (y0 - HU);
+        const int o = ly * BXU + lx;
+        const int ox = d.nx > 1 ? 1 : 0;
+        const T wx0 = T(1) - ax.f, wx1 = ax.f, wy0 = T(1) - ay.f, wy1 = ay.f;
+        const T wz0 = T(1) - az.f, wz1 = az.f;
+        const T* u0 = reinterpret_cast<const T*>(stages + ((az.i0 - q0) % S) * kStageBytes +
+                                                 3 * kBoxS);
+        const T* u1 = three ? reinterpret_cast<const T*>(stages +
+                                                         ((az.i0 + 1 - q0) % S) * kStageBytes +
+                                                         3 * kBoxS)
+                            : u0;
+        const T s[3] = {s0, s1, s2};
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            if (k >= d.ndim) {
+                v[k] = T(0);
+                continue;
+            }
+            const T* a = u0 + k * PU + o;
+            T acc = (wx0 * wy0 * wz0) * a[0] + (wx1 * wy0 * wz0) * a[ox] +
+                    (wx0 * wy1 * wz0) * a[BXU] + (wx1 * wy1 * wz0) * a[BXU + ox];
+            if (three) {
+                const T* b = u1 + k * PU + o;
+                acc += (wx0 * wy0 * wz1) * b[0] + (wx1 * wy0 * wz1) * b[ox] +
+                       (wx0 * wy1 * wz1) * b[BXU] + (wx1 * wy1 * wz1) * b[BXU + ox];
+            }
+            v[k] = s[k] + acc;
+        }
+    }
+    __device__ void xpass(const unsigned char*, int, int, int, Acc*) const {}
+    __device__ void load_center(int, int, int, Center&) const {}
+    __device__ Red2 emit(int x, int y, int z, const T u[3], const Center&) const {
+        const int64_t i = d.idx(x, y, z);
+        uout[i] = u[0];
+        uout[d.n + i] = u[1];
+        uout[2 * d.n + i] = d.ndim == 3 ? u[2] : T(0);
+        if (W) {  // similarity.cpp:25-45 for the next loss evaluation
+            const Cell3<T> c = locate3<T>(dm, x, y, z, u[0], u[1], d.ndim == 3 ? u[2] : T(0));
+            const Corners<T> k = fetch_corners<T>(M, c);
+            W[i] = lerp_value(c, k);
+            T gr[3];
+            lerp_grad(c, k, d.ndim, gr);
+            G[i] = gr[0];
+            G[d.n + i] = gr[1];
+            G[2 * d.n + i] = gr[2];
+        }
+        return {0.0, 0.0};
+    }
+    __device__ void finish(int, double, double) const {
+        if (st) st->nupdates += 1;
+    }
+};
+
+// W = M(x+u), G = grad M(x+u) (similarity.cpp:25-45) at scale start / epilogue
+template <class T>
+__global__ void k_warpgrad(const T* __restrict__ M, Dims dm, CPlanes3<T> u, Dims d,
+                           T* __restrict__ W, T* __restrict__ G) {
+    const int64_t i = blockIdx.x * 256ll + threadIdx.x;
+    if (i >= d.n) return;
+    const int x = static_cast<int>(i % d.nx);
+    const int64_t r = i / d.nx;
+    const int y = static_cast<int>(r % d.ny), z = static_cast<int>(r / d.ny);
+    const Cell3<T> c = locate3<T>(dm, x, y, z, __ldg(u.c[0] + i), __ldg(u.c[1] + i),
+                                  d.ndim == 3 ? __ldg(u.c[2] + i) : T(0));
+    const Corners<T> k = fetch_corners<T>(M, c);
+    W[i] = lerp_value(c, k);
+    if (G) {
+        T gr[3];
+        lerp_grad(c, k, d.ndim, gr);
+        G[i] = gr[0];
+        G[d.n + i] = gr[1];
+        G[2 * d.n + i] = gr[2];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side: tensor maps and launches
+
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return nullptr;
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+template <class T>
+bool make_map(CUtensorMap* m, const T* base, const Dims& d, int ncomp, int bx, int by) {
+    auto enc = encoder();
+    if (!enc) return false;
+    const cuuint64_t esz = sizeof(T);
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(d.nx), static_cast<cuuint64_t>(d.ny),
+                          static_cast<cuuint64_t>(d.nz), static_cast<cuuint64_t>(ncomp)};
+    cuuint64_t strides[3] = {d.nx * esz, static_cast<cuuint64_t>(d.nx) * d.ny * esz,
+                             static_cast<cuuint64_t>(d.n) * esz};
+    cuuint32_t box[4] = {static_cast<cuuint32_t>(bx), static_cast<cuuint32_t>(by), 1, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    const CUresult r = enc(m, sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                             : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                           4, const_cast<T*>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <class Op>
+size_t zm2_smem() {
+    using Acc = typename Op::Acc;
+    constexpr int HI = TY + 2 * Op::R, WI = TX + 2 * Op::R;
+    return static_cast<size_t>(Op::S) * Op::kStageBytes +
+           (Op::kStaged ? sizeof(Acc) * Op::C * HI * WI : 0) +
+           2 * sizeof(Acc) * Op::C * HI * TX;
+}
+
+template <class Op>
+int run_zm2(const Launch& L, const Op& op, Dims d) {
+    ZG2 g;
+    g.d = d;
+    int tiles = 0;
+    const int nchunks = zmarch_blocks(d, Op::R, L.num_sms, &g.zchunk, &tiles);
+    g.tiles_x = (d.nx + TX - 1) / TX;
+    const size_t smem = zm2_smem<Op>();
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_zm2<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        configured = true;
+    }
+    k_zm2<Op><<<dim3(tiles, nchunks), NT, smem, L.stream>>>(op, g);
+    L.bump();
+    return tiles * nchunks;
+}
+
+template <int RLO, int RHI, class F>
+int with_r(int R, F&& f) {
+    switch (R) {
+#define DFM_R2(r)                                                                   \
+    case r:                                                                         \
+        if constexpr (r >= RLO && r <= RHI) return f(std::integral_constant<int, r>{}); \
+        break;
+        DFM_R2(0) DFM_R2(1) DFM_R2(2) DFM_R2(3) DFM_R2(4) DFM_R2(5) DFM_R2(6) DFM_R2(7) DFM_R2(8)
+#undef DFM_R2
+    }
+    return -2;
+}
+
+}  // namespace
+
+bool tma_supported(Dims d, int esz) {
+    return encoder() != nullptr && (static_cast<int64_t>(d.nx) * esz) % 16 == 0;
+}
+
+template <class T>
+int launch_lncc_fwd_tma(const Launch& L, int R, const T* F, const T* W, Dims d, T* coef,
+                        double* partials, const LoopState* st) {
+    return with_r<1, 5>(R, [&](auto rc) {
+        constexpr int RR = decltype(rc)::value;
+        using Op = LnccFwd2<T, RR>;
+        Op op;
+        if (!make_map<T>(&op.mF, F, d, 1, Op::BX, Op::BY) ||
+            !make_map<T>(&op.mW, W, d, 1, Op::BX, Op::BY))
+            return -1;
+        op.coef = coef;
+        op.partials = partials;
+        op.st = st;
+        op.d = d;
+        return run_zm2(L, op, d);
+    });
+}
+
+template <class T>
+int launch_lncc_bwd_tma(const Launch& L, int R, const T* coef, const T* F, const T* W,
+                        const T* G, Dims d, T* grad, const LoopState* st) {
+    return with_r<1, 5>(R, [&](auto rc) {
+        constexpr int RR = decltype(rc)::value;
+        using Op = LnccBwd2<T, RR>;
+        Op op;
+        if (!make_map<T>(&op.mC, coef, d, 4, Op::BX, Op::BY)) return -1;
+        op.F = F;
+        op.W = W;
+        op.G = G;
+        op.grad = grad;
+        op.st = st;
+        op.d = d;
+        return run_zm2(L, op, d);
+    });
+}
+
+template <class T>
+int launch_smooth_adam_tma(const Launch& L, int R, const GaussW<T>& w, const T* grad, T* m,
+                           T* nu, T* step, Dims d, AdamParams ap, LoopState* st,
+                           unsigned long long* maxstep) {
+    return with_r<0, 6>(R, [&](auto rc) {
+        constexpr int RR = decltype(rc)::value;
+        using Op = SmoothAdam2<T, RR>;
+        Op op;
+        if (!make_map<T>(&op.mG, grad, d, 3, Op::BX, Op::BY)) return -1;
+        op.w = w;
+        op.m = m;
+        op.nu = nu;
+        op.step = step;
+        op.b1 = T(ap.b1);
+        op.omb1 = T(1.0 - ap.b1);
+        op.b2 = T(ap.b2);
+        op.omb2 = T(1.0 - ap.b2);
+        op.eps = T(ap.eps);
+        op.eta = T(ap.eta);
+        op.cap = T(ap.cap);
+        op.corr1 = ap.corr1;
+        op.corr2 = ap.corr2;
+        op.st = st;
+        op.maxstep = maxstep;
+        op.d = d;
+        return run_zm2(L, op, d);
+    });
+}
+
+template <class T>
+int launch_compose_tma(const Launch& L, int R, double cap, const GaussW<T>& w, const T* step,
+                       const T* uin, T* uout, const T* M, Dims dm, Dims d, T* W, T* G,
+                       LoopState* st) {
+    const int caph = cap <= 0.5 ? 1 : (cap <= 1.5 ? 2 : 0);
+    if (caph == 0) return -2;
+    return with_r<0, 4>(R, [&](auto rc) {
+        constexpr int RR = decltype(rc)::value;
+        auto go = [&](auto ch) {
+            constexpr int CH = decltype(ch)::value;
+            using Op = Compose2<T, RR, CH>;
+            Op op;
+            if (!make_map<T>(&op.mS, step, d, 3, Op::BXS, Op::BYS) ||
+                !make_map<T>(&op.mU, uin, d, 3, Op::BXU, Op::BYU))
+                return -1;
+            op.w = w;
+            op.uout = uout;
+            op.M = M;
+            op.dm = dm;
+            op.W = W;
+            op.G = G;
+            op.st = st;
+            op.d = d;
+            return run_zm2(L, op, d);
+        };
+        return caph == 1 ? go(std::integral_constant<int, 1>{})
+                         : go(std::integral_constant<int, 2>{});
+    });
+}
+
+template <class T>
+void launch_warpgrad(const Launch& L, const T* M, Dims dm, CPlanes3<T> u, Dims d, T* W, T* G) {
+    k_warpgrad<T><<<static_cast<unsigned>((d.n + 255) / 256), 256, 0, L.stream>>>(M, dm, u, d, W, G);
+    L.bump();
+}
+
+#define DFM_INST_TMA(T)                                                                        \
+    template int launch_lncc_fwd_tma<T>(const Launch&, int, const T*, const T*, Dims, T*,      \
+                                        double*, const LoopState*);                            \
+    template int launch_lncc_bwd_tma<T>(const Launch&, int, const T*, const T*, const T*,      \
+                                        const T*, Dims, T*, const LoopState*);                 \
+    template int launch_smooth_adam_tma<T>(const Launch&, int, const GaussW<T>&, const T*, T*, \
+                                           T*, T*, Dims, AdamParams, LoopState*,               \
+                                           unsigned long long*);                               \
+    template int launch_compose_tma<T>(const Launch&, int, double, const GaussW<T>&, const T*, \
+                                       const T*, T*, const T*, Dims, Dims, T*, T*,             \
+                                       LoopState*);                                            \
+    template void launch_warpgrad<T>(const Launch&, const T*, Dims, CPlanes3<T>, Dims, T*, T*);
+
+DFM_INST_TMA(float)
+DFM_INST_TMA(double)
+
+}  // namespace dfm

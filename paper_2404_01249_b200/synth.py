@@ -9,10 +9,11 @@ Every volume is returned as float32 (the reference reads MET_FLOAT volumes,
 io.cpp:245-269) in numpy (z, y, x) order, i.e. x-fastest memory.
 
 Moving images follow the shared recipe: velocity v = N(0,1) noise per
-component, Gaussian-smoothed with sigma 8, scaled so that max |v| over all
-voxels and components equals the stated maximum displacement (BASELINE's "max
-N-voxel displacement" is applied to the velocity — documented ambiguity), then
-integrated by 6 scaling-and-squaring steps; moving = fixed o exp(v).
+component, Gaussian-smoothed with sigma 8 (periodic boundary, so the field is
+stationary and its maximum is not an edge artefact), scaled so that max |v| over
+all voxels and components equals the stated maximum displacement (BASELINE's
+"max N-voxel displacement" is applied to the velocity — documented ambiguity),
+then integrated by 6 scaling-and-squaring steps; moving = fixed o exp(v).
 """
 from __future__ import annotations
 
@@ -45,7 +46,7 @@ def exp_velocity(v: np.ndarray, steps: int = 6) -> np.ndarray:
 
 def random_velocity(shape, max_disp: float, rng: np.random.Generator,
                     sigma: float = 8.0) -> np.ndarray:
-    v = np.stack([ndimage.gaussian_filter(rng.standard_normal(shape), sigma, mode="nearest")
+    v = np.stack([ndimage.gaussian_filter(rng.standard_normal(shape), sigma, mode="wrap")
                   for _ in range(3)], axis=-1)
     return v * (max_disp / np.abs(v).max())
 
