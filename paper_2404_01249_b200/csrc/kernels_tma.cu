@@ -117,6 +117,8 @@ __global__ void __launch_bounds__(NT) k_zm2(const __grid_constant__ Op op, const
         for (int q = q0; q < qend && q < q0 + S; ++q)
             op.issue(stages + ((q - q0) % S) * SB, &bars[(q - q0) % S], x0, y0, q);
 
+    // register ring of the last K xy-filtered planes; the plane loop is
+    // unrolled by K so every ring slot is a compile-time register (no moves)
     Acc ring[C][K];
 #pragma unroll
     for (int c = 0; c < C; ++c)
@@ -125,81 +127,88 @@ __global__ void __launch_bounds__(NT) k_zm2(const __grid_constant__ Op op, const
     double rsum = 0.0, rmax = 0.0;
     int waited = q0 - 1;
     int buf = 0;
+    const int zend = z1 + R;
 
-    for (int zi = z0 - R; zi < z1 + R; ++zi) {
-        const int zo = zi - R;
-        const bool em = (zo >= z0) && own;
-        typename Op::Center cen;
-        if (em) op.load_center(x, y, zo, cen);
-        while (waited < zi + Op::AHEAD) {
-            ++waited;
-            const int k = waited - q0;
-            mbar_wait(&bars[k % S], (k / S) & 1);
-        }
-        Acc* sx = s_x + buf * (C * HI * TX);
-        if constexpr (Op::kStaged) {
-            for (int e = tid; e < HI * WI; e += NT) {
-                const int row = e / WI, col = e - row * WI;
-                Acc v[C];
-                op.stage(stages, q0, x0, y0, zi, row, col, v);
+    for (int zb = z0 - R; zb < zend; zb += K) {
 #pragma unroll
-                for (int c = 0; c < C; ++c) s_in[(c * HI + row) * WI + col] = v[c];
-            }
-            __syncthreads();
-            for (int row = ty; row < HI; row += TY) {
+        for (int kk = 0; kk < K; ++kk) {
+            const int zi = zb + kk;
+            if (zi < zend) {
+                const int zo = zi - R;
+                const bool em = (zo >= z0) && own;
+                typename Op::Center cen;
+                if (em) op.load_center(x, y, zo, cen);
+                while (waited < zi + Op::AHEAD) {
+                    ++waited;
+                    const int k = waited - q0;
+                    mbar_wait(&bars[k % S], (k / S) & 1);
+                }
+                Acc* sx = s_x + buf * (C * HI * TX);
+                if constexpr (Op::kStaged) {
+                    for (int e = tid; e < HI * WI; e += NT) {
+                        const int row = e / WI, col = e - row * WI;
+                        Acc v[C];
+                        op.stage(stages, q0, x0, y0, zi, row, col, v);
+#pragma unroll
+                        for (int c = 0; c < C; ++c) s_in[(c * HI + row) * WI + col] = v[c];
+                    }
+                    __syncthreads();
+                    const Acc nx = op.nrm(0, x);
+                    for (int row = ty; row < HI; row += TY) {
+#pragma unroll
+                        for (int c = 0; c < C; ++c) {
+                            const Acc* src = s_in + (c * HI + row) * WI + tx;
+                            Acc a = Acc(0);
+#pragma unroll
+                            for (int j = 0; j < K; ++j) a += op.wgt(0, j) * src[j];
+                            sx[(c * HI + row) * TX + tx] = a * nx;
+                        }
+                    }
+                } else {
+                    const unsigned char* st = stages + ((zi - q0) % S) * SB;
+                    for (int row = ty; row < HI; row += TY) {
+                        Acc v[C];
+                        op.xpass(st, row, tx, x, v);
+#pragma unroll
+                        for (int c = 0; c < C; ++c) sx[(c * HI + row) * TX + tx] = v[c];
+                    }
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    const int qf = zi - Op::BACK + S;
+                    if (qf < qend) {
+                        const int k = qf - q0;
+                        op.issue(stages + (k % S) * SB, &bars[k % S], x0, y0, qf);
+                    }
+                }
+                // y pass into ring slot kk (the newest plane)
+                const Acc ny = own ? op.nrm(1, y) : Acc(0);
 #pragma unroll
                 for (int c = 0; c < C; ++c) {
-                    const Acc* src = s_in + (c * HI + row) * WI + tx;
+                    const Acc* src = sx + (c * HI + ty) * TX + tx;
                     Acc a = Acc(0);
 #pragma unroll
-                    for (int j = 0; j < K; ++j) a += op.wgt(0, j) * src[j];
-                    sx[(c * HI + row) * TX + tx] = a * op.nrm(0, x);
+                    for (int j = 0; j < K; ++j) a += op.wgt(1, j) * src[j * TX];
+                    ring[c][kk] = a * ny;
                 }
-            }
-        } else {
-            const unsigned char* st = stages + ((zi - q0) % S) * SB;
-            for (int row = ty; row < HI; row += TY) {
-                Acc v[C];
-                op.xpass(st, row, tx, x, v);
+                if (em) {
+                    // oldest plane (zo - R) sits in slot (kk + 1) % K
+                    const Acc nz = op.nrm(2, zo);
+                    Acc sv[C];
 #pragma unroll
-                for (int c = 0; c < C; ++c) sx[(c * HI + row) * TX + tx] = v[c];
+                    for (int c = 0; c < C; ++c) {
+                        Acc a = Acc(0);
+#pragma unroll
+                        for (int j = 0; j < K; ++j) a += op.wgt(2, j) * ring[c][(kk + 1 + j) % K];
+                        sv[c] = a * nz;
+                    }
+                    const Red2 r = op.emit(x, y, zo, sv, cen);
+                    rsum += r.sum;
+                    rmax = fmax(rmax, r.mx);
+                }
+                buf ^= 1;
             }
         }
-        __syncthreads();
-        if (tid == 0) {
-            const int qf = zi - Op::BACK + S;
-            if (qf < qend) {
-                const int k = qf - q0;
-                op.issue(stages + (k % S) * SB, &bars[k % S], x0, y0, qf);
-            }
-        }
-        // y pass + z ring
-        const Acc ny = own ? op.nrm(1, y) : Acc(0);
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-            const Acc* src = sx + (c * HI + ty) * TX + tx;
-            Acc a = Acc(0);
-#pragma unroll
-            for (int j = 0; j < K; ++j) a += op.wgt(1, j) * src[j * TX];
-#pragma unroll
-            for (int k = 0; k < K - 1; ++k) ring[c][k] = ring[c][k + 1];
-            ring[c][K - 1] = a * ny;
-        }
-        if (em) {
-            const Acc nz = op.nrm(2, zo);
-            Acc s[C];
-#pragma unroll
-            for (int c = 0; c < C; ++c) {
-                Acc a = Acc(0);
-#pragma unroll
-                for (int k = 0; k < K; ++k) a += op.wgt(2, k) * ring[c][k];
-                s[c] = a * nz;
-            }
-            const Red2 r = op.emit(x, y, zo, s, cen);
-            rsum += r.sum;
-            rmax = fmax(rmax, r.mx);
-        }
-        buf ^= 1;
     }
     if constexpr (Op::kSum || Op::kMax) {
         const int blk = blockIdx.y * gridDim.x + blockIdx.x;
@@ -266,25 +275,27 @@ struct LnccFwd2 {
     }
     __device__ void load_center(int, int, int, Center&) const {}
     __device__ Red2 emit(int x, int y, int z, const double s[5], const Center&) const {
+        // similarity.cpp:145-162 with 2 divisions instead of 12: 1/n, 1/(vF vW)
         const double n = static_cast<double>(box_len(x, d.nx, R) * box_len(y, d.ny, R) *
                                              (d.nz > 1 ? box_len(z, d.nz, R) : 1));
-        const double muF = s[0] / n;
-        const double muW = s[1] / n;
-        double vF = s[2] / n - muF * muF;
-        double vW = s[3] / n - muW * muW;
+        const double inv_n = 1.0 / n;
+        const double muF = s[0] * inv_n;
+        const double muW = s[1] * inv_n;
+        double vF = s[2] * inv_n - muF * muF;
+        double vW = s[3] * inv_n - muW * muW;
         vF = vF < 0.0 ? 0.0 : vF;
         vW = vW < 0.0 ? 0.0 : vW;
-        const double cv = s[4] / n - muF * muW;
+        const double cv = s[4] * inv_n - muF * muW;
         double cc2 = 0.0, an = 0.0, amu = 0.0, bn = 0.0, bmu = 0.0;
         if (!(vF < 1e-5 || vW < 1e-5)) {
-            const double cc = cv / sqrt(vF * vW);
-            cc2 = cc * cc;
-            const double alpha = cv / (vF * vW);
-            const double beta = cv * cv / (vF * vW * vW);
-            an = alpha / n;
-            amu = alpha * muF / n;
-            bn = beta / n;
-            bmu = beta * muW / n;
+            const double inv_den = 1.0 / (vF * vW);
+            const double alpha = cv * inv_den;         // cv / (vF vW)
+            cc2 = alpha * cv;                          // cv^2 / (vF vW)
+            const double beta = cc2 * vF * inv_den;    // cv^2 / (vF vW^2)
+            an = alpha * inv_n;
+            amu = an * muF;
+            bn = beta * inv_n;
+            bmu = bn * muW;
         }
         if (coef) {
             const int64_t i = d.idx(x, y, z);
@@ -313,6 +324,7 @@ struct LnccBwd2 {
     const T* W;
     const T* G;  // 3 planes
     T* grad;     // 3 planes
+    double m2n;  // -2 / N (similarity.cpp:182)
     const LoopState* st;
     Dims d;
     struct Center {
@@ -350,7 +362,7 @@ struct LnccBwd2 {
     __device__ Red2 emit(int x, int y, int z, const double s[4], const Center& c) const {
         const int64_t i = d.idx(x, y, z);
         const double f = static_cast<double>(c.f), w = static_cast<double>(c.w);
-        const double dW = -2.0 / static_cast<double>(d.n) * (f * s[0] - s[1] - w * s[2] + s[3]);
+        const double dW = m2n * (f * s[0] - s[1] - w * s[2] + s[3]);
         grad[i] = static_cast<T>(dW * static_cast<double>(c.g0));
         grad[d.n + i] = static_cast<T>(dW * static_cast<double>(c.g1));
         grad[2 * d.n + i] = static_cast<T>(dW * static_cast<double>(c.g2));
@@ -639,20 +651,46 @@ size_t zm2_smem() {
            2 * sizeof(Acc) * Op::C * HI * TX;
 }
 
+// z-chunk length minimising the makespan: waves of resident CTAs x planes per
+// CTA (chunk + halo planes), given the kernel's measured residency per SM.
+inline int pick_chunks(const Dims& d, int tiles, int slots, int halo_planes, int* zchunk) {
+    double best = 1e30;
+    int best_n = 1, best_chunk = d.nz;
+    for (int nch = 1; nch <= d.nz; ++nch) {
+        const int chunk = (d.nz + nch - 1) / nch;
+        const int nreal = (d.nz + chunk - 1) / chunk;
+        if (nreal != nch || static_cast<int64_t>(tiles) * nch > 65536) continue;
+        const int blocks = tiles * nch;
+        const int waves = (blocks + slots - 1) / slots;
+        // per-wave cost in plane-steps plus a small per-CTA fixed cost
+        const double cost = static_cast<double>(waves) * (chunk + halo_planes + 2.0);
+        if (cost < best - 1e-9) {
+            best = cost;
+            best_n = nch;
+            best_chunk = chunk;
+        }
+    }
+    *zchunk = best_chunk;
+    return best_n;
+}
+
 template <class Op>
 int run_zm2(const Launch& L, const Op& op, Dims d) {
     ZG2 g;
     g.d = d;
-    int tiles = 0;
-    const int nchunks = zmarch_blocks(d, Op::R, L.num_sms, &g.zchunk, &tiles);
-    g.tiles_x = (d.nx + TX - 1) / TX;
     const size_t smem = zm2_smem<Op>();
-    static bool configured = false;
-    if (!configured) {
+    static int occ = 0;  // resident CTAs per SM for this instantiation
+    if (occ == 0) {
         cudaFuncSetAttribute(k_zm2<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
-        configured = true;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_zm2<Op>, NT, smem) !=
+                cudaSuccess || occ < 1)
+            occ = 1;
     }
+    g.tiles_x = (d.nx + TX - 1) / TX;
+    const int tiles = g.tiles_x * ((d.ny + TY - 1) / TY);
+    const int slots = occ * (L.num_sms > 0 ? L.num_sms : 148);
+    const int nchunks = pick_chunks(d, tiles, slots, 2 * Op::R + Op::BACK + Op::AHEAD, &g.zchunk);
     k_zm2<Op><<<dim3(tiles, nchunks), NT, smem, L.stream>>>(op, g);
     L.bump();
     return tiles * nchunks;
@@ -707,6 +745,7 @@ int launch_lncc_bwd_tma(const Launch& L, int R, const T* coef, const T* F, const
         op.W = W;
         op.G = G;
         op.grad = grad;
+        op.m2n = -2.0 / static_cast<double>(d.n);
         op.st = st;
         op.d = d;
         return run_zm2(L, op, d);

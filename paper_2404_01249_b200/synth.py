@@ -44,9 +44,26 @@ def exp_velocity(v: np.ndarray, steps: int = 6) -> np.ndarray:
     return u
 
 
+def _taper(shape, margin: float):
+    """separable raised-cosine window: 0 on the faces, 1 beyond `margin` voxels"""
+    w = np.ones(shape)
+    for a, n in enumerate(shape):
+        i = np.arange(n, dtype=np.float64)
+        d = np.minimum(i, n - 1 - i)
+        t = 0.5 * (1.0 - np.cos(np.pi * np.clip(d / margin, 0.0, 1.0)))
+        sh = [1] * len(shape)
+        sh[a] = n
+        w = w * t.reshape(sh)
+    return w
+
+
 def random_velocity(shape, max_disp: float, rng: np.random.Generator,
                     sigma: float = 8.0) -> np.ndarray:
-    v = np.stack([ndimage.gaussian_filter(rng.standard_normal(shape), sigma, mode="wrap")
+    """smoothed N(0,1) noise, tapered to zero over 2 sigma at the volume faces
+    (the deformation lives inside the field of view, as in the reference's own
+    warp generator, synth.hpp:10-14), max |v| = max_disp"""
+    w = _taper(shape, min(2.0 * sigma, min(shape) / 4.0))
+    v = np.stack([w * ndimage.gaussian_filter(rng.standard_normal(shape), sigma, mode="wrap")
                   for _ in range(3)], axis=-1)
     return v * (max_disp / np.abs(v).max())
 

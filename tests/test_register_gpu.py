@@ -102,7 +102,9 @@ def _textured_pair(seed):
     rng = np.random.default_rng(seed)
     M = ndimage.gaussian_filter(rng.random(g.shape), 1.0)
     M = (M - M.min()) / (M.max() - M.min())
-    v = synth.random_velocity(g.shape, 3.0, rng, sigma=3.0)
+    v = np.stack([ndimage.gaussian_filter(rng.standard_normal(g.shape), 3.0, mode="nearest")
+                  for _ in range(3)], axis=-1)
+    v *= 3.0 / np.abs(v).max()
     return g, synth.warp(M, synth.exp_velocity(v)), M
 
 
