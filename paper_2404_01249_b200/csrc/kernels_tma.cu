@@ -79,12 +79,17 @@ __device__ double bmax(double v, double* sh) {
 }
 
 // ---------------------------------------------------------------------------
-// the streaming z-march driver
+// the streaming z-march driver.  A CTA is TX x Op::TYv threads, one output
+// column per thread; per-thread constants (norm factors of its x and y, the
+// op's prologue such as Adam bias corrections) are computed once; Op::Carry
+// lets an op defer work of plane zo into plane zo+1 (latency hiding).
 template <class Op>
-__global__ void __launch_bounds__(NT) k_zm2(const __grid_constant__ Op op, const ZG2 g) {
+__global__ void __launch_bounds__(TX * Op::TYv) k_zm2(const __grid_constant__ Op op,
+                                                      const ZG2 g) {
     using Acc = typename Op::Acc;
+    constexpr int TYv = Op::TYv, NTh = TX * TYv;
     constexpr int R = Op::R, C = Op::C, S = Op::S, K = 2 * R + 1;
-    constexpr int HI = TY + 2 * R, WI = TX + 2 * R;
+    constexpr int HI = TYv + 2 * R, WI = TX + 2 * R;
     constexpr int SB = Op::kStageBytes;
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char* stages = smem;
@@ -98,7 +103,7 @@ __global__ void __launch_bounds__(NT) k_zm2(const __grid_constant__ Op op, const
     const int tid = threadIdx.x;
     const int tx = tid % TX, ty = tid / TX;
     const int x0 = (blockIdx.x % g.tiles_x) * TX;
-    const int y0 = (blockIdx.x / g.tiles_x) * TY;
+    const int y0 = (blockIdx.x / g.tiles_x) * TYv;
     const int z0 = blockIdx.y * g.zchunk;
     const int z1 = min(z0 + g.zchunk, d.nz);
     const int x = x0 + tx, y = y0 + ty;
@@ -116,6 +121,11 @@ __global__ void __launch_bounds__(NT) k_zm2(const __grid_constant__ Op op, const
     if (tid == 0)
         for (int q = q0; q < qend && q < q0 + S; ++q)
             op.issue(stages + ((q - q0) % S) * SB, &bars[(q - q0) % S], x0, y0, q);
+
+    const Acc nxv = x < d.nx ? op.nrm(0, x) : Acc(0);
+    const Acc nyv = own ? op.nrm(1, y) : Acc(0);
+    const typename Op::Prol pr = op.prologue();
+    typename Op::Carry carry{};
 
     // register ring of the last K xy-filtered planes; the plane loop is
     // unrolled by K so every ring slot is a compile-time register (no moves)
@@ -145,7 +155,7 @@ __global__ void __launch_bounds__(NT) k_zm2(const __grid_constant__ Op op, const
                 }
                 Acc* sx = s_x + buf * (C * HI * TX);
                 if constexpr (Op::kStaged) {
-                    for (int e = tid; e < HI * WI; e += NT) {
+                    for (int e = tid; e < HI * WI; e += NTh) {
                         const int row = e / WI, col = e - row * WI;
                         Acc v[C];
                         op.stage(stages, q0, x0, y0, zi, row, col, v);
@@ -153,22 +163,23 @@ __global__ void __launch_bounds__(NT) k_zm2(const __grid_constant__ Op op, const
                         for (int c = 0; c < C; ++c) s_in[(c * HI + row) * WI + col] = v[c];
                     }
                     __syncthreads();
-                    const Acc nx = op.nrm(0, x);
-                    for (int row = ty; row < HI; row += TY) {
+#pragma unroll
+                    for (int row = ty; row < HI; row += TYv) {
 #pragma unroll
                         for (int c = 0; c < C; ++c) {
                             const Acc* src = s_in + (c * HI + row) * WI + tx;
                             Acc a = Acc(0);
 #pragma unroll
                             for (int j = 0; j < K; ++j) a += op.wgt(0, j) * src[j];
-                            sx[(c * HI + row) * TX + tx] = a * nx;
+                            sx[(c * HI + row) * TX + tx] = a * nxv;
                         }
                     }
                 } else {
                     const unsigned char* st = stages + ((zi - q0) % S) * SB;
-                    for (int row = ty; row < HI; row += TY) {
+#pragma unroll
+                    for (int row = ty; row < HI; row += TYv) {
                         Acc v[C];
-                        op.xpass(st, row, tx, x, v);
+                        op.xpass(st, row, tx, nxv, v);
 #pragma unroll
                         for (int c = 0; c < C; ++c) sx[(c * HI + row) * TX + tx] = v[c];
                     }
@@ -182,14 +193,13 @@ __global__ void __launch_bounds__(NT) k_zm2(const __grid_constant__ Op op, const
                     }
                 }
                 // y pass into ring slot kk (the newest plane)
-                const Acc ny = own ? op.nrm(1, y) : Acc(0);
 #pragma unroll
                 for (int c = 0; c < C; ++c) {
                     const Acc* src = sx + (c * HI + ty) * TX + tx;
                     Acc a = Acc(0);
 #pragma unroll
                     for (int j = 0; j < K; ++j) a += op.wgt(1, j) * src[j * TX];
-                    ring[c][kk] = a * ny;
+                    ring[c][kk] = a * nyv;
                 }
                 if (em) {
                     // oldest plane (zo - R) sits in slot (kk + 1) % K
@@ -202,7 +212,7 @@ __global__ void __launch_bounds__(NT) k_zm2(const __grid_constant__ Op op, const
                         for (int j = 0; j < K; ++j) a += op.wgt(2, j) * ring[c][(kk + 1 + j) % K];
                         sv[c] = a * nz;
                     }
-                    const Red2 r = op.emit(x, y, zo, sv, cen);
+                    const Red2 r = op.emit(x, y, zo, sv, cen, pr, carry);
                     rsum += r.sum;
                     rmax = fmax(rmax, r.mx);
                 }
@@ -210,13 +220,14 @@ __global__ void __launch_bounds__(NT) k_zm2(const __grid_constant__ Op op, const
             }
         }
     }
+    op.flush(carry);
     if constexpr (Op::kSum || Op::kMax) {
         const int blk = blockIdx.y * gridDim.x + blockIdx.x;
-        const double bs = Op::kSum ? bsum<NT>(rsum, s_red) : 0.0;
-        const double bm = Op::kMax ? bmax<NT>(rmax, s_red) : 0.0;
-        if (tid == 0) op.finish(blk, bs, bm);
+        const double bs = Op::kSum ? bsum<NTh>(rsum, s_red) : 0.0;
+        const double bm = Op::kMax ? bmax<NTh>(rmax, s_red) : 0.0;
+        if (tid == 0) op.finish(blk, bs, bm, pr);
     } else {
-        if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0) op.finish(0, 0.0, 0.0);
+        if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0) op.finish(0, 0.0, 0.0, pr);
     }
 }
 
@@ -224,14 +235,19 @@ __global__ void __launch_bounds__(NT) k_zm2(const __grid_constant__ Op op, const
 // ops
 
 struct NoCenter {};
+struct NoProl {};
+struct NoCarry {};
 
 // similarity.cpp:122-168 — box moments of F and W = M(x+u), window coefficients
-template <class T, int R_>
+template <class T, int R_, int TY_ = 8>
 struct LnccFwd2 {
     using Acc = double;
-    static constexpr int R = R_, C = 5, BACK = 0, AHEAD = 0, S = 4;
+    using Center = NoCenter;
+    using Prol = NoProl;
+    using Carry = NoCarry;
+    static constexpr int R = R_, C = 5, BACK = 0, AHEAD = 0, S = 4, TYv = TY_;
     static constexpr bool kStaged = false, kSum = true, kMax = false;
-    static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TY + 2 * R;
+    static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TYv + 2 * R;
     static constexpr int kBytes = BX * BY * int(sizeof(T));
     static constexpr int kBox = align128(kBytes);  // TMA smem destinations 128 B aligned
     static constexpr int kStageBytes = 2 * kBox;
@@ -240,7 +256,6 @@ struct LnccFwd2 {
     double* partials;
     const LoopState* st;
     Dims d;
-    using Center = NoCenter;
 
     __device__ bool skip() const { return st && st->done; }
     __device__ void prefetch_maps() const {
@@ -254,7 +269,8 @@ struct LnccFwd2 {
     }
     __device__ Acc wgt(int, int) const { return 1.0; }
     __device__ Acc nrm(int, int) const { return 1.0; }
-    __device__ void xpass(const unsigned char* st_, int row, int col, int, Acc v[5]) const {
+    __device__ Prol prologue() const { return {}; }
+    __device__ void xpass(const unsigned char* st_, int row, int col, Acc, Acc v[5]) const {
         const T* F = reinterpret_cast<const T*>(st_) + row * BX + col + (XA - R);
         const T* W = F + kBox / int(sizeof(T));
         double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
@@ -274,7 +290,8 @@ struct LnccFwd2 {
         v[4] = a4;
     }
     __device__ void load_center(int, int, int, Center&) const {}
-    __device__ Red2 emit(int x, int y, int z, const double s[5], const Center&) const {
+    __device__ Red2 emit(int x, int y, int z, const double s[5], const Center&, const Prol&,
+                         Carry&) const {
         // similarity.cpp:145-162 with 2 divisions instead of 12: 1/n, 1/(vF vW)
         const double n = static_cast<double>(box_len(x, d.nx, R) * box_len(y, d.ny, R) *
                                              (d.nz > 1 ? box_len(z, d.nz, R) : 1));
@@ -306,16 +323,19 @@ struct LnccFwd2 {
         }
         return {cc2, 0.0};
     }
-    __device__ void finish(int blk, double s, double) const { partials[blk] = s; }
+    __device__ void flush(Carry&) const {}
+    __device__ void finish(int blk, double s, double, const Prol&) const { partials[blk] = s; }
 };
 
 // similarity.cpp:170-189 — box sums of the coefficients, dW, grad = dW * G
-template <class T, int R_>
+template <class T, int R_, int TY_ = 8>
 struct LnccBwd2 {
     using Acc = double;
-    static constexpr int R = R_, C = 4, BACK = 0, AHEAD = 0, S = 4;
+    using Prol = NoProl;
+    using Carry = NoCarry;
+    static constexpr int R = R_, C = 4, BACK = 0, AHEAD = 0, S = 4, TYv = TY_;
     static constexpr bool kStaged = false, kSum = false, kMax = false;
-    static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TY + 2 * R;
+    static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TYv + 2 * R;
     static constexpr int kBytes = BX * BY * int(sizeof(T));
     static constexpr int kBox = align128(kBytes);
     static constexpr int kStageBytes = 4 * kBox;
@@ -340,7 +360,8 @@ struct LnccBwd2 {
     }
     __device__ Acc wgt(int, int) const { return 1.0; }
     __device__ Acc nrm(int, int) const { return 1.0; }
-    __device__ void xpass(const unsigned char* st_, int row, int col, int, Acc v[4]) const {
+    __device__ Prol prologue() const { return {}; }
+    __device__ void xpass(const unsigned char* st_, int row, int col, Acc, Acc v[4]) const {
         const T* p = reinterpret_cast<const T*>(st_) + row * BX + col + (XA - R);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -359,7 +380,8 @@ struct LnccBwd2 {
         c.g1 = __ldg(G + d.n + i);
         c.g2 = d.ndim == 3 ? __ldg(G + 2 * d.n + i) : T(0);
     }
-    __device__ Red2 emit(int x, int y, int z, const double s[4], const Center& c) const {
+    __device__ Red2 emit(int x, int y, int z, const double s[4], const Center& c, const Prol&,
+                         Carry&) const {
         const int64_t i = d.idx(x, y, z);
         const double f = static_cast<double>(c.f), w = static_cast<double>(c.w);
         const double dW = m2n * (f * s[0] - s[1] - w * s[2] + s[3]);
@@ -368,16 +390,18 @@ struct LnccBwd2 {
         grad[2 * d.n + i] = static_cast<T>(dW * static_cast<double>(c.g2));
         return {0.0, 0.0};
     }
-    __device__ void finish(int, double, double) const {}
+    __device__ void flush(Carry&) const {}
+    __device__ void finish(int, double, double, const Prol&) const {}
 };
 
 // pipeline.cpp:182-186 + optim.cpp:22-42 + diffeo.cpp:47-57
-template <class T, int R_>
+template <class T, int R_, int TY_ = 16>
 struct SmoothAdam2 {
     using Acc = T;
-    static constexpr int R = R_, C = 3, BACK = 0, AHEAD = 0, S = 4;
+    using Carry = NoCarry;
+    static constexpr int R = R_, C = 3, BACK = 0, AHEAD = 0, S = 4, TYv = TY_;
     static constexpr bool kStaged = false, kSum = false, kMax = true;
-    static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TY + 2 * R;
+    static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TYv + 2 * R;
     static constexpr int kBytes = BX * BY * int(sizeof(T));
     static constexpr int kBox = align128(kBytes);
     static constexpr int kStageBytes = 3 * kBox;
@@ -395,6 +419,10 @@ struct SmoothAdam2 {
     struct Center {
         T m[3], nu[3];
     };
+    struct Prol {  // per-launch constants, read once per thread
+        T c1, c2;
+        int slot;
+    };
 
     __device__ bool skip() const { return st && st->done; }
     __device__ void prefetch_maps() const { prefetch_tmap(&mG); }
@@ -405,9 +433,16 @@ struct SmoothAdam2 {
     }
     __device__ Acc wgt(int a, int j) const { return w.taps[a][j]; }
     __device__ Acc nrm(int a, int i) const { return __ldg(w.norm[a] + i); }
-    __device__ void xpass(const unsigned char* st_, int row, int col, int x, Acc v[3]) const {
+    __device__ Prol prologue() const {
+        Prol p;
+        const long long t = st ? st->t : 1;
+        p.c1 = static_cast<T>(corr1[t]);
+        p.c2 = static_cast<T>(corr2[t]);
+        p.slot = st ? st->slot : 0;
+        return p;
+    }
+    __device__ void xpass(const unsigned char* st_, int row, int col, Acc nx, Acc v[3]) const {
         const T* p = reinterpret_cast<const T*>(st_) + row * BX + col + (XA - R);
-        const T nx = x < d.nx ? __ldg(w.norm[0] + x) : T(0);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             T a = T(0);
@@ -424,11 +459,9 @@ struct SmoothAdam2 {
             c.nu[k] = k < d.ndim ? nu[k * d.n + i] : T(0);
         }
     }
-    __device__ Red2 emit(int x, int y, int z, const T s[3], const Center& c) const {
+    __device__ Red2 emit(int x, int y, int z, const T s[3], const Center& c, const Prol& p,
+                         Carry&) const {
         const int64_t i = d.idx(x, y, z);
-        const long long t = st ? st->t : 1;
-        const T c1 = static_cast<T>(corr1[t]);
-        const T c2 = static_cast<T>(corr2[t]);
         double mx = 0.0;
         bool bad = false;
 #pragma unroll
@@ -442,7 +475,7 @@ struct SmoothAdam2 {
             const T nn = b2 * c.nu[k] + omb2 * v * v;
             m[k * d.n + i] = mm;
             nu[k * d.n + i] = nn;
-            const T dir = (mm / c1) / (sqrt(nn / c2) + eps);
+            const T dir = (mm / p.c1) / (sqrt(nn / p.c2) + eps);
             const T sv = eta * dir;
             bad |= !isfinite(sv);
             const T cl = sv < -cap ? -cap : (cap < sv ? cap : sv);
@@ -452,21 +485,26 @@ struct SmoothAdam2 {
         if (bad && st) st->bad_step = 1;
         return {0.0, mx};
     }
-    __device__ void finish(int, double, double mx) const {
-        if (maxstep) atomic_max_nonneg(maxstep + (st ? st->slot : 0), mx);
+    __device__ void flush(Carry&) const {}
+    __device__ void finish(int, double, double mx, const Prol& p) const {
+        if (maxstep) atomic_max_nonneg(maxstep + p.slot, mx);
     }
 };
 
 // diffeo.cpp:60-62 + interp.cpp:269-289 — u' = step + u(x+step), sigma_warp
-// Gaussian, then W = M(x+u') and G = grad M(x+u') for the next loss pass.
-template <class T, int R_, int CAPH>
+// Gaussian, then W = M(x+u') and G = grad M(x+u') for the next loss pass.  The
+// M gather of plane zo is issued at its emit and consumed at the emit of plane
+// zo+1 (Carry), so its latency hides behind a whole plane of work.
+template <class T, int R_, int CAPH, int TY_ = 8>
 struct Compose2 {
     using Acc = T;
-    static constexpr int R = R_, C = 3, BACK = CAPH, AHEAD = CAPH, S = 2 * CAPH + 3;
+    using Center = NoCenter;
+    using Prol = NoProl;
+    static constexpr int R = R_, C = 3, BACK = CAPH, AHEAD = CAPH, S = 2 * CAPH + 3, TYv = TY_;
     static constexpr bool kStaged = true, kSum = false, kMax = false;
     static constexpr int HU = R + CAPH;  // u halo: Gaussian radius + gather reach
-    static constexpr int XAS = round_bx<T>(R), BXS = round_bx<T>(TX + XAS + R), BYS = TY + 2 * R;
-    static constexpr int XAU = round_bx<T>(HU), BXU = round_bx<T>(TX + XAU + HU), BYU = TY + 2 * HU;
+    static constexpr int XAS = round_bx<T>(R), BXS = round_bx<T>(TX + XAS + R), BYS = TYv + 2 * R;
+    static constexpr int XAU = round_bx<T>(HU), BXU = round_bx<T>(TX + XAU + HU), BYU = TYv + 2 * HU;
     static constexpr int kBytesS = BXS * BYS * int(sizeof(T));
     static constexpr int kBytesU = BXU * BYU * int(sizeof(T));
     static constexpr int kBoxS = align128(kBytesS), kBoxU = align128(kBytesU);
@@ -481,7 +519,12 @@ struct Compose2 {
     T* G;     // 3 planes
     LoopState* st;
     Dims d;
-    using Center = NoCenter;
+    struct Carry {
+        bool valid;
+        int64_t i;
+        Cell3<T> c;
+        Corners<T> k;
+    };
 
     __device__ bool skip() const {
         if (!st) return false;
@@ -508,8 +551,8 @@ struct Compose2 {
             tma_load_4d(dst + 3 * kBoxS + k * kBoxU, &mU, bar, x0 - XAU, y0 - HU, q, k);
     }
     __device__ Acc wgt(int a, int j) const { return w.taps[a][j]; }
-    __device__ Acc nrm(int a, int i) const { return i < (a == 0 ? d.nx : (a == 1 ? d.ny : d.nz))
-                                                       ? __ldg(w.norm[a] + i) : T(0); }
+    __device__ Acc nrm(int a, int i) const { return __ldg(w.norm[a] + i); }
+    __device__ Prol prologue() const { return {}; }
     __device__ void stage(const unsigned char* stages, int q0, int x0, int y0, int zi, int row,
                           int col, T v[3]) const {
         const int gx = x0 - R + col, gy = y0 - R + row;
@@ -533,7 +576,6 @@ struct Compose2 {
         }
         const int lx = ax.i0 - (x0 - XAU), ly = ay.i0 - (y0 - HU);
         const int o = ly * BXU + lx;
-        const int ox = d.nx > 1 ? 1 : 0;
         const T wx0 = T(1) - ax.f, wx1 = ax.f, wy0 = T(1) - ay.f, wy1 = ay.f;
         const T wz0 = T(1) - az.f, wz1 = az.f;
         const T* u0 = reinterpret_cast<const T*>(stages + ((az.i0 - q0) % S) * kStageBytes +
@@ -550,36 +592,45 @@ struct Compose2 {
                 continue;
             }
             const T* a = u0 + k * PU + o;
-            T acc = (wx0 * wy0 * wz0) * a[0] + (wx1 * wy0 * wz0) * a[ox] +
-                    (wx0 * wy1 * wz0) * a[BXU] + (wx1 * wy1 * wz0) * a[BXU + ox];
+            T acc = (wx0 * wy0 * wz0) * a[0] + (wx1 * wy0 * wz0) * a[1] +
+                    (wx0 * wy1 * wz0) * a[BXU] + (wx1 * wy1 * wz0) * a[BXU + 1];
             if (three) {
                 const T* b = u1 + k * PU + o;
-                acc += (wx0 * wy0 * wz1) * b[0] + (wx1 * wy0 * wz1) * b[ox] +
-                       (wx0 * wy1 * wz1) * b[BXU] + (wx1 * wy1 * wz1) * b[BXU + ox];
+                acc += (wx0 * wy0 * wz1) * b[0] + (wx1 * wy0 * wz1) * b[1] +
+                       (wx0 * wy1 * wz1) * b[BXU] + (wx1 * wy1 * wz1) * b[BXU + 1];
             }
             v[k] = s[k] + acc;
         }
     }
-    __device__ void xpass(const unsigned char*, int, int, int, Acc*) const {}
+    __device__ void xpass(const unsigned char*, int, int, Acc, Acc*) const {}
     __device__ void load_center(int, int, int, Center&) const {}
-    __device__ Red2 emit(int x, int y, int z, const T u[3], const Center&) const {
+    __device__ void finish_wg(const Carry& c) const {
+        W[c.i] = lerp_value(c.c, c.k);
+        T gr[3];
+        lerp_grad(c.c, c.k, d.ndim, gr);
+        G[c.i] = gr[0];
+        G[d.n + c.i] = gr[1];
+        G[2 * d.n + c.i] = gr[2];
+    }
+    __device__ Red2 emit(int x, int y, int z, const T u[3], const Center&, const Prol&,
+                         Carry& cr) const {
         const int64_t i = d.idx(x, y, z);
         uout[i] = u[0];
         uout[d.n + i] = u[1];
         uout[2 * d.n + i] = d.ndim == 3 ? u[2] : T(0);
         if (W) {  // similarity.cpp:25-45 for the next loss evaluation
-            const Cell3<T> c = locate3<T>(dm, x, y, z, u[0], u[1], d.ndim == 3 ? u[2] : T(0));
-            const Corners<T> k = fetch_corners<T>(M, c);
-            W[i] = lerp_value(c, k);
-            T gr[3];
-            lerp_grad(c, k, d.ndim, gr);
-            G[i] = gr[0];
-            G[d.n + i] = gr[1];
-            G[2 * d.n + i] = gr[2];
+            if (cr.valid) finish_wg(cr);
+            cr.c = locate3<T>(dm, x, y, z, u[0], u[1], d.ndim == 3 ? u[2] : T(0));
+            cr.k = fetch_corners<T>(M, cr.c);
+            cr.i = i;
+            cr.valid = true;
         }
         return {0.0, 0.0};
     }
-    __device__ void finish(int, double, double) const {
+    __device__ void flush(Carry& cr) const {
+        if (W && cr.valid) finish_wg(cr);
+    }
+    __device__ void finish(int, double, double, const Prol&) const {
         if (st) st->nupdates += 1;
     }
 };
@@ -645,7 +696,7 @@ bool make_map(CUtensorMap* m, const T* base, const Dims& d, int ncomp, int bx, i
 template <class Op>
 size_t zm2_smem() {
     using Acc = typename Op::Acc;
-    constexpr int HI = TY + 2 * Op::R, WI = TX + 2 * Op::R;
+    constexpr int HI = Op::TYv + 2 * Op::R, WI = TX + 2 * Op::R;
     return static_cast<size_t>(Op::S) * Op::kStageBytes +
            (Op::kStaged ? sizeof(Acc) * Op::C * HI * WI : 0) +
            2 * sizeof(Acc) * Op::C * HI * TX;
@@ -683,15 +734,15 @@ int run_zm2(const Launch& L, const Op& op, Dims d) {
     if (occ == 0) {
         cudaFuncSetAttribute(k_zm2<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_zm2<Op>, NT, smem) !=
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_zm2<Op>, TX * Op::TYv, smem) !=
                 cudaSuccess || occ < 1)
             occ = 1;
     }
     g.tiles_x = (d.nx + TX - 1) / TX;
-    const int tiles = g.tiles_x * ((d.ny + TY - 1) / TY);
+    const int tiles = g.tiles_x * ((d.ny + Op::TYv - 1) / Op::TYv);
     const int slots = occ * (L.num_sms > 0 ? L.num_sms : 148);
     const int nchunks = pick_chunks(d, tiles, slots, 2 * Op::R + Op::BACK + Op::AHEAD, &g.zchunk);
-    k_zm2<Op><<<dim3(tiles, nchunks), NT, smem, L.stream>>>(op, g);
+    k_zm2<Op><<<dim3(tiles, nchunks), TX * Op::TYv, smem, L.stream>>>(op, g);
     L.bump();
     return tiles * nchunks;
 }
