@@ -23,11 +23,50 @@ struct LoopState {
     int converged;   // convergence monitor fired this scale
     int nupdates;    // updates applied this scale
     int bad_step;    // non-finite step seen (diffeo.cpp:52-59)
-    int pad_;
+    unsigned int arrive;  // CTAs done in a fused loss+monitor launch (reset by the last)
     long long t;     // Adam step counter (optim.cpp:26), kept across scales
     double dice_p;   // dice: sum F*W
     double dice_d;   // dice: SF + SM + 1e-7
 };
+
+__device__ __forceinline__ unsigned long long dfm_global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Thread-0 part of the convergence monitor (pipeline.cpp:157-179): records the
+// loss of the current iteration; non-finite -> error; converged -> the record
+// is kept and the scale ends before the update; else the Adam step advances.
+__device__ __forceinline__ void monitor_commit(LoopState* st, double v, double P, double D,
+                                               double* loss, unsigned long long* stamp,
+                                               int window, double tol) {
+    const int slot = st->it;
+    loss[slot] = v;
+    stamp[slot] = dfm_global_ns();
+    st->slot = slot;
+    st->it = slot + 1;
+    st->dice_p = P;
+    st->dice_d = D;
+    if (!isfinite(v)) {
+        st->err = 2;
+        st->done = 1;
+        return;
+    }
+    const int n = slot + 1;
+    if (n >= window + 1) {
+        const double prev = loss[n - 1 - window];
+        const double cur = loss[n - 1];
+        const double den = fabs(prev) > 1e-30 ? fabs(prev) : 1e-30;
+        const double rel = ((prev - cur) / static_cast<double>(window)) / den;
+        if (rel < tol) {
+            st->converged = 1;
+            st->done = 1;
+            return;
+        }
+    }
+    st->t += 1;
+}
 
 // Kernel launch bookkeeping handed to every launcher.
 struct Launch {
@@ -133,9 +172,19 @@ void launch_gauss_fused(const Launch& L, int R, const GaussW<T>& w, CPlanes3<T> 
 // the base of their 3 (coef: 4) contiguous planes.  Launchers return < 0 when
 // the shape/radius is not supported (caller falls back to the kernels above).
 bool tma_supported(Dims d, int esz);
+// With `mon` set, the last CTA to finish also reduces the partials (fixed
+// order) and runs the convergence monitor: one launch instead of two.
+struct MonitorArgs {
+    LoopState* st;
+    double* loss;
+    unsigned long long* stamp;
+    int window;
+    double tol;
+};
 template <class T>
 int launch_lncc_fwd_tma(const Launch& L, int R, const T* F, const T* W, Dims d, T* coef,
-                        double* partials, const LoopState* st);
+                        double* partials, const LoopState* st,
+                        const MonitorArgs* mon = nullptr);
 template <class T>
 int launch_lncc_bwd_tma(const Launch& L, int R, const T* coef, const T* F, const T* W,
                         const T* G, Dims d, T* grad, const LoopState* st);

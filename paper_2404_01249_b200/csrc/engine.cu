@@ -1154,16 +1154,22 @@ struct Registrar {
         const int mask = ctx->tma_mask;  // A/B switch per kernel (DFM_TMA_MASK)
         int np;
         ev_begin(KC_FWD);
-        if (lncc && (mask & 1))
-            np = launch_lncc_fwd_tma<T>(L, cfg->lncc_radius, Fs, Wb, d, coef[0], partials, st);
-        else
+        const bool fused = lncc && (mask & 1);
+        if (fused) {  // LNCC moments + window coefficients + loss + monitor, one launch
+            const MonitorArgs mon{st, loss, stamp, cfg->conv_window, cfg->conv_tol};
+            np = launch_lncc_fwd_tma<T>(L, cfg->lncc_radius, Fs, Wb, d, coef[0], partials, st,
+                                        &mon);
+        } else {
             np = loss_kind_launch_fwd<T>(ctx, loss_kind, cfg->lncc_radius, Fs, Ms, d, d, uin,
                                          coef, grad.w(), partials, st);
+        }
         ev_end();
-        ev_begin(KC_MON);
-        launch_monitor(L, monitor_kind(loss_kind), partials, np, static_cast<double>(d.n), st,
-                       loss, stamp, cfg->conv_window, cfg->conv_tol);
-        ev_end();
+        if (!fused) {
+            ev_begin(KC_MON);
+            launch_monitor(L, monitor_kind(loss_kind), partials, np, static_cast<double>(d.n),
+                           st, loss, stamp, cfg->conv_window, cfg->conv_tol);
+            ev_end();
+        }
         if (lncc) {
             ev_begin(KC_BWD);
             if (mask & 2) {

@@ -569,11 +569,6 @@ __device__ double loss_value(int kind, const double* partials, int np, double nv
     return kind == 1 ? -s / nvox : s / nvox;
 }
 
-__device__ __forceinline__ unsigned long long global_ns() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
 
 // Finishes the loss of the current iteration and runs the convergence monitor
 // (pipeline.cpp:157-179): non-finite -> error; converged -> record kept, the
@@ -587,31 +582,7 @@ __global__ void __launch_bounds__(1024) k_monitor(int kind, const double* partia
     double P = 0.0, D = 0.0;
     const double v = loss_value(kind, partials, np, nvox, sh, &P, &D);
     if (threadIdx.x != 0) return;
-    const int slot = st->it;
-    loss[slot] = v;
-    stamp[slot] = global_ns();
-    st->slot = slot;
-    st->it = slot + 1;
-    st->dice_p = P;
-    st->dice_d = D;
-    if (!isfinite(v)) {
-        st->err = 2;
-        st->done = 1;
-        return;
-    }
-    const int n = slot + 1;
-    if (n >= window + 1) {
-        const double prev = loss[n - 1 - window];
-        const double cur = loss[n - 1];
-        const double den = fabs(prev) > 1e-30 ? fabs(prev) : 1e-30;
-        const double rel = ((prev - cur) / static_cast<double>(window)) / den;
-        if (rel < tol) {
-            st->converged = 1;
-            st->done = 1;
-            return;
-        }
-    }
-    st->t += 1;
+    monitor_commit(st, v, P, D, loss, stamp, window, tol);
 }
 
 void launch_monitor(const Launch& L, int kind, const double* partials, int np, double nvox,
@@ -639,7 +610,7 @@ void launch_reduce_value(const Launch& L, int kind, const double* partials, int 
     L.bump();
 }
 
-__global__ void k_stamp(unsigned long long* slot) { *slot = global_ns(); }
+__global__ void k_stamp(unsigned long long* slot) { *slot = dfm_global_ns(); }
 
 void launch_stamp(const Launch& L, unsigned long long* slot) {
     k_stamp<<<1, 1, 0, L.stream>>>(slot);

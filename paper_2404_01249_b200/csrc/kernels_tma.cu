@@ -226,6 +226,29 @@ __global__ void __launch_bounds__(TX * Op::TYv) k_zm2(const __grid_constant__ Op
         const double bs = Op::kSum ? bsum<NTh>(rsum, s_red) : 0.0;
         const double bm = Op::kMax ? bmax<NTh>(rmax, s_red) : 0.0;
         if (tid == 0) op.finish(blk, bs, bm, pr);
+        if constexpr (Op::kSum) {
+            if (op.mon.st) {  // fused convergence monitor: the last CTA reduces
+                __shared__ int s_last;
+                if (tid == 0) {
+                    __threadfence();
+                    const int nb = gridDim.x * gridDim.y;
+                    s_last = atomicAdd(&op.mon.st->arrive, 1u) == static_cast<unsigned>(nb - 1);
+                }
+                __syncthreads();
+                if (s_last) {
+                    __threadfence();
+                    const int nb = gridDim.x * gridDim.y;
+                    double acc = 0.0;
+                    for (int k = tid; k < nb; k += NTh) acc += __ldcg(op.partials + k);
+                    const double tot = bsum<NTh>(acc, s_red);
+                    if (tid == 0) {
+                        op.mon.st->arrive = 0;
+                        monitor_commit(op.mon.st, -tot / static_cast<double>(d.n), 0.0, 0.0,
+                                       op.mon.loss, op.mon.stamp, op.mon.window, op.mon.tol);
+                    }
+                }
+            }
+        }
     } else {
         if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0) op.finish(0, 0.0, 0.0, pr);
     }
@@ -233,6 +256,17 @@ __global__ void __launch_bounds__(TX * Op::TYv) k_zm2(const __grid_constant__ Op
 
 // ---------------------------------------------------------------------------
 // ops
+
+// Adam division / square root: fp32 uses the MUFU approximations (<= 2 ulp;
+// the fp32 path is held to 1e-5 relative), fp64 the IEEE operations.
+__device__ __forceinline__ float adam_div(float a, float b) { return __fdividef(a, b); }
+__device__ __forceinline__ double adam_div(double a, double b) { return a / b; }
+__device__ __forceinline__ float adam_sqrt(float a) {
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(a));
+    return r;
+}
+__device__ __forceinline__ double adam_sqrt(double a) { return sqrt(a); }
 
 struct NoCenter {};
 struct NoProl {};
@@ -255,6 +289,7 @@ struct LnccFwd2 {
     T* coef;  // 4 planes, coef[k*n + i]; nullptr -> value only
     double* partials;
     const LoopState* st;
+    MonitorArgs mon;  // mon.st == nullptr: no fused monitor
     Dims d;
 
     __device__ bool skip() const { return st && st->done; }
@@ -420,7 +455,7 @@ struct SmoothAdam2 {
         T m[3], nu[3];
     };
     struct Prol {  // per-launch constants, read once per thread
-        T c1, c2;
+        T ic1, ic2;  // 1 / (1 - beta^t), optim.cpp:27-30
         int slot;
     };
 
@@ -436,8 +471,8 @@ struct SmoothAdam2 {
     __device__ Prol prologue() const {
         Prol p;
         const long long t = st ? st->t : 1;
-        p.c1 = static_cast<T>(corr1[t]);
-        p.c2 = static_cast<T>(corr2[t]);
+        p.ic1 = static_cast<T>(1.0 / corr1[t]);
+        p.ic2 = static_cast<T>(1.0 / corr2[t]);
         p.slot = st ? st->slot : 0;
         return p;
     }
@@ -445,14 +480,17 @@ struct SmoothAdam2 {
         const T* p = reinterpret_cast<const T*>(st_) + row * BX + col + (XA - R);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            T a = T(0);
+            const T* q = p + c * (kBox / int(sizeof(T)));
+            T a0 = T(0), a1 = T(0);  // two chains: halves the FMA dependency depth
 #pragma unroll
-            for (int j = 0; j < 2 * R + 1; ++j) a += w.taps[0][j] * p[c * (kBox / int(sizeof(T))) + j];
-            v[c] = a * nx;
+            for (int j = 0; j < 2 * R + 1; j += 2) a0 += w.taps[0][j] * q[j];
+#pragma unroll
+            for (int j = 1; j < 2 * R + 1; j += 2) a1 += w.taps[0][j] * q[j];
+            v[c] = (a0 + a1) * nx;
         }
     }
     __device__ void load_center(int x, int y, int z, Center& c) const {
-        const int64_t i = d.idx(x, y, z);
+        const int64_t i = static_cast<int64_t>((z * d.ny + y) * d.nx + x);
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             c.m[k] = k < d.ndim ? m[k * d.n + i] : T(0);
@@ -461,8 +499,8 @@ struct SmoothAdam2 {
     }
     __device__ Red2 emit(int x, int y, int z, const T s[3], const Center& c, const Prol& p,
                          Carry&) const {
-        const int64_t i = d.idx(x, y, z);
-        double mx = 0.0;
+        const int64_t i = static_cast<int64_t>((z * d.ny + y) * d.nx + x);
+        T mx = T(0);
         bool bad = false;
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
@@ -475,15 +513,16 @@ struct SmoothAdam2 {
             const T nn = b2 * c.nu[k] + omb2 * v * v;
             m[k * d.n + i] = mm;
             nu[k * d.n + i] = nn;
-            const T dir = (mm / p.c1) / (sqrt(nn / p.c2) + eps);
+            // dir = (m/c1) / (sqrt(nu/c2) + eps)
+            const T dir = adam_div(mm * p.ic1, adam_sqrt(nn * p.ic2) + eps);
             const T sv = eta * dir;
             bad |= !isfinite(sv);
-            const T cl = sv < -cap ? -cap : (cap < sv ? cap : sv);
+            const T cl = fmin(fmax(sv, -cap), cap);
             step[k * d.n + i] = cl;
-            mx = fmax(mx, static_cast<double>(fabs(cl)));
+            mx = fmax(mx, fabs(cl));
         }
         if (bad && st) st->bad_step = 1;
-        return {0.0, mx};
+        return {0.0, static_cast<double>(mx)};
     }
     __device__ void flush(Carry&) const {}
     __device__ void finish(int, double, double mx, const Prol& p) const {
@@ -768,7 +807,7 @@ bool tma_supported(Dims d, int esz) {
 
 template <class T>
 int launch_lncc_fwd_tma(const Launch& L, int R, const T* F, const T* W, Dims d, T* coef,
-                        double* partials, const LoopState* st) {
+                        double* partials, const LoopState* st, const MonitorArgs* mon) {
     return with_r<1, 5>(R, [&](auto rc) {
         constexpr int RR = decltype(rc)::value;
         using Op = LnccFwd2<T, RR>;
@@ -779,6 +818,7 @@ int launch_lncc_fwd_tma(const Launch& L, int R, const T* F, const T* W, Dims d, 
         op.coef = coef;
         op.partials = partials;
         op.st = st;
+        op.mon = mon ? *mon : MonitorArgs{nullptr, nullptr, nullptr, 0, 0.0};
         op.d = d;
         return run_zm2(L, op, d);
     });
@@ -870,7 +910,7 @@ void launch_warpgrad(const Launch& L, const T* M, Dims dm, CPlanes3<T> u, Dims d
 
 #define DFM_INST_TMA(T)                                                                        \
     template int launch_lncc_fwd_tma<T>(const Launch&, int, const T*, const T*, Dims, T*,      \
-                                        double*, const LoopState*);                            \
+                                        double*, const LoopState*, const MonitorArgs*);        \
     template int launch_lncc_bwd_tma<T>(const Launch&, int, const T*, const T*, const T*,      \
                                         const T*, Dims, T*, const LoopState*);                 \
     template int launch_smooth_adam_tma<T>(const Launch&, int, const GaussW<T>&, const T*, T*, \
