@@ -155,10 +155,12 @@ __global__ void __launch_bounds__(TX * Op::TYv) k_zm2(const __grid_constant__ Op
                 }
                 Acc* sx = s_x + buf * (C * HI * TX);
                 if constexpr (Op::kStaged) {
+                    const typename Op::PlaneCtx pc = op.plane_ctx(stages, q0, zi);
+#pragma unroll 2
                     for (int e = tid; e < HI * WI; e += NTh) {
                         const int row = e / WI, col = e - row * WI;
                         Acc v[C];
-                        op.stage(stages, q0, x0, y0, zi, row, col, v);
+                        op.stage(pc, x0, y0, zi, row, col, v);
 #pragma unroll
                         for (int c = 0; c < C; ++c) s_in[(c * HI + row) * WI + col] = v[c];
                     }
@@ -539,7 +541,7 @@ struct Compose2 {
     using Acc = T;
     using Center = NoCenter;
     using Prol = NoProl;
-    static constexpr int R = R_, C = 3, BACK = CAPH, AHEAD = CAPH, S = 2 * CAPH + 3, TYv = TY_;
+    static constexpr int R = R_, C = 3, BACK = CAPH, AHEAD = CAPH, S = 2 * CAPH + 2, TYv = TY_;
     static constexpr bool kStaged = true, kSum = false, kMax = false;
     static constexpr int HU = R + CAPH;  // u halo: Gaussian radius + gather reach
     static constexpr int XAS = round_bx<T>(R), BXS = round_bx<T>(TX + XAS + R), BYS = TYv + 2 * R;
@@ -592,53 +594,66 @@ struct Compose2 {
     __device__ Acc wgt(int a, int j) const { return w.taps[a][j]; }
     __device__ Acc nrm(int a, int i) const { return __ldg(w.norm[a] + i); }
     __device__ Prol prologue() const { return {}; }
-    __device__ void stage(const unsigned char* stages, int q0, int x0, int y0, int zi, int row,
-                          int col, T v[3]) const {
+    // stage pointers of the planes one composed plane needs (zi-CAPH .. zi+CAPH)
+    struct PlaneCtx {
+        const T* step;               // step box of plane zi
+        const T* u[2 * CAPH + 1];    // u boxes of planes zi-CAPH .. zi+CAPH
+    };
+    __device__ PlaneCtx plane_ctx(const unsigned char* stages, int q0, int zi) const {
+        PlaneCtx pc;
+        pc.step = reinterpret_cast<const T*>(stages + ((zi - q0) % S) * kStageBytes);
+#pragma unroll
+        for (int k = 0; k < 2 * CAPH + 1; ++k) {
+            const int q = zi - CAPH + k;
+            pc.u[k] = reinterpret_cast<const T*>(stages + ((q - q0) % S) * kStageBytes + 3 * kBoxS);
+        }
+        return pc;
+    }
+    // composed value step + u(x + step) at halo element (row, col) of plane zi
+    __device__ void stage(const PlaneCtx& pc, int x0, int y0, int zi, int row, int col,
+                          T v[3]) const {
         const int gx = x0 - R + col, gy = y0 - R + row;
         if (gx < 0 || gx >= d.nx || gy < 0 || gy >= d.ny || zi < 0 || zi >= d.nz) {
             v[0] = v[1] = v[2] = T(0);
             return;
         }
-        const T* sp = reinterpret_cast<const T*>(stages + ((zi - q0) % S) * kStageBytes);
         const int so = row * BXS + col + (XAS - R);
-        const T s0 = sp[so], s1 = sp[PS + so];
-        const T s2 = d.ndim == 3 ? sp[2 * PS + so] : T(0);
+        const T s0 = pc.step[so], s1 = pc.step[PS + so];
+        const bool three = d.ndim == 3;
+        const T s2 = three ? pc.step[2 * PS + so] : T(0);
         const AxisCell<T> ax = locate_axis(gx, s0, d.nx);
         const AxisCell<T> ay = locate_axis(gy, s1, d.ny);
-        const bool three = d.nz > 1;
-        AxisCell<T> az;
+        int dz = 0;  // lower z corner relative to zi, in [-CAPH, CAPH-1]
+        T fz = T(0);
         if (three) {
-            az = locate_axis(zi, s2, d.nz);
-        } else {
-            az.i0 = 0;
-            az.f = T(0);
+            const AxisCell<T> az = locate_axis(zi, s2, d.nz);
+            dz = az.i0 - zi;
+            fz = az.f;
         }
-        const int lx = ax.i0 - (x0 - XAU), ly = ay.i0 - (y0 - HU);
-        const int o = ly * BXU + lx;
+        const int o = (ay.i0 - (y0 - HU)) * BXU + (ax.i0 - (x0 - XAU));
+        // 8 corner weights, computed once for the 3 components
         const T wx0 = T(1) - ax.f, wx1 = ax.f, wy0 = T(1) - ay.f, wy1 = ay.f;
-        const T wz0 = T(1) - az.f, wz1 = az.f;
-        const T* u0 = reinterpret_cast<const T*>(stages + ((az.i0 - q0) % S) * kStageBytes +
-                                                 3 * kBoxS);
-        const T* u1 = three ? reinterpret_cast<const T*>(stages +
-                                                         ((az.i0 + 1 - q0) % S) * kStageBytes +
-                                                         3 * kBoxS)
-                            : u0;
+        const T w00 = wx0 * wy0, w10 = wx1 * wy0, w01 = wx0 * wy1, w11 = wx1 * wy1;
+        const T wz0 = T(1) - fz, wz1 = fz;
+        const T* u0 = pc.u[CAPH];
+        const T* u1 = pc.u[CAPH];
+#pragma unroll
+        for (int k = 0; k < 2 * CAPH; ++k)
+            if (dz == k - CAPH) {
+                u0 = pc.u[k];
+                u1 = pc.u[k + 1];
+            }
         const T s[3] = {s0, s1, s2};
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-            if (k >= d.ndim) {
-                v[k] = T(0);
-                continue;
-            }
             const T* a = u0 + k * PU + o;
-            T acc = (wx0 * wy0 * wz0) * a[0] + (wx1 * wy0 * wz0) * a[1] +
-                    (wx0 * wy1 * wz0) * a[BXU] + (wx1 * wy1 * wz0) * a[BXU + 1];
+            T acc = w00 * a[0] + w10 * a[1] + w01 * a[BXU] + w11 * a[BXU + 1];
             if (three) {
                 const T* b = u1 + k * PU + o;
-                acc += (wx0 * wy0 * wz1) * b[0] + (wx1 * wy0 * wz1) * b[1] +
-                       (wx0 * wy1 * wz1) * b[BXU] + (wx1 * wy1 * wz1) * b[BXU + 1];
+                const T up = w00 * b[0] + w10 * b[1] + w01 * b[BXU] + w11 * b[BXU + 1];
+                acc = wz0 * acc + wz1 * up;
             }
-            v[k] = s[k] + acc;
+            v[k] = (k < d.ndim) ? s[k] + acc : T(0);
         }
     }
     __device__ void xpass(const unsigned char*, int, int, Acc, Acc*) const {}
