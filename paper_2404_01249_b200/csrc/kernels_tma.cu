@@ -139,11 +139,13 @@ __global__ void __launch_bounds__(TX * Op::TYv) k_zm2(const __grid_constant__ Op
     int buf = 0;
     const int zend = z1 + R;
 
-    for (int zb = z0 - R; zb < zend; zb += K) {
-#pragma unroll
-        for (int kk = 0; kk < K; ++kk) {
-            const int zi = zb + kk;
-            if (zi < zend) {
+    // the ring shifts by register moves (C*(K-1) MOVs per plane) rather than
+    // unrolling the plane loop by K: the unrolled body overflowed the
+    // instruction cache (26% no_instruction stalls at the coarse scales)
+    {
+        {
+            for (int zi = z0 - R; zi < zend; ++zi) {
+                constexpr int kk = K - 1;
                 const int zo = zi - R;
                 const bool em = (zo >= z0) && own;
                 typename Op::Center cen;
@@ -201,10 +203,12 @@ __global__ void __launch_bounds__(TX * Op::TYv) k_zm2(const __grid_constant__ Op
                     Acc a = Acc(0);
 #pragma unroll
                     for (int j = 0; j < K; ++j) a += op.wgt(1, j) * src[j * TX];
+#pragma unroll
+                    for (int k = 0; k < K - 1; ++k) ring[c][k] = ring[c][k + 1];
                     ring[c][kk] = a * nyv;
                 }
                 if (em) {
-                    // oldest plane (zo - R) sits in slot (kk + 1) % K
+                    // oldest plane (zo - R) sits in slot 0 (slot (kk + 1) % K)
                     const Acc nz = op.nrm(2, zo);
                     Acc sv[C];
 #pragma unroll
