@@ -19,6 +19,8 @@ struct Dims {
     __host__ __device__ int64_t idx(int x, int y, int z) const {
         return (static_cast<int64_t>(z) * ny + y) * nx + x;
     }
+    // 32-bit index math (volumes are validated to < 2^31 voxels)
+    __host__ __device__ int idx32(int x, int y, int z) const { return (z * ny + y) * nx + x; }
     __host__ __device__ bool is3d() const { return nz > 1; }
 };
 

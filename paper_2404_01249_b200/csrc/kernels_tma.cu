@@ -158,13 +158,22 @@ __global__ void __launch_bounds__(TX * Op::TYv) k_zm2(const __grid_constant__ Op
                 Acc* sx = s_x + buf * (C * HI * TX);
                 if constexpr (Op::kStaged) {
                     const typename Op::PlaneCtx pc = op.plane_ctx(stages, q0, zi);
-#pragma unroll 2
-                    for (int e = tid; e < HI * WI; e += NTh) {
-                        const int row = e / WI, col = e - row * WI;
-                        Acc v[C];
-                        op.stage(pc, x0, y0, zi, row, col, v);
+                    if (op.interior(x0, y0, zi)) {  // CTA-uniform: no clamping, no bounds
+                        for (int e = tid; e < HI * WI; e += NTh) {
+                            const int row = e / WI, col = e - row * WI;
+                            Acc v[C];
+                            op.stage_fast(pc, x0, y0, zi, row, col, v);
 #pragma unroll
-                        for (int c = 0; c < C; ++c) s_in[(c * HI + row) * WI + col] = v[c];
+                            for (int c = 0; c < C; ++c) s_in[(c * HI + row) * WI + col] = v[c];
+                        }
+                    } else {
+                        for (int e = tid; e < HI * WI; e += NTh) {
+                            const int row = e / WI, col = e - row * WI;
+                            Acc v[C];
+                            op.stage(pc, x0, y0, zi, row, col, v);
+#pragma unroll
+                            for (int c = 0; c < C; ++c) s_in[(c * HI + row) * WI + col] = v[c];
+                        }
                     }
                     __syncthreads();
 #pragma unroll
@@ -356,7 +365,7 @@ struct LnccFwd2 {
             bmu = bn * muW;
         }
         if (coef) {
-            const int64_t i = d.idx(x, y, z);
+            const int64_t i = d.idx32(x, y, z);
             coef[i] = static_cast<T>(an);
             coef[d.n + i] = static_cast<T>(amu);
             coef[2 * d.n + i] = static_cast<T>(bn);
@@ -414,7 +423,7 @@ struct LnccBwd2 {
         }
     }
     __device__ void load_center(int x, int y, int z, Center& c) const {
-        const int64_t i = d.idx(x, y, z);
+        const int64_t i = d.idx32(x, y, z);
         c.f = __ldg(F + i);
         c.w = __ldg(W + i);
         c.g0 = __ldg(G + i);
@@ -423,7 +432,7 @@ struct LnccBwd2 {
     }
     __device__ Red2 emit(int x, int y, int z, const double s[4], const Center& c, const Prol&,
                          Carry&) const {
-        const int64_t i = d.idx(x, y, z);
+        const int64_t i = d.idx32(x, y, z);
         const double f = static_cast<double>(c.f), w = static_cast<double>(c.w);
         const double dW = m2n * (f * s[0] - s[1] - w * s[2] + s[3]);
         grad[i] = static_cast<T>(dW * static_cast<double>(c.g0));
@@ -613,6 +622,55 @@ struct Compose2 {
         }
         return pc;
     }
+    // every composed element of this CTA-plane (tile + Gaussian halo) has its
+    // interpolation cell strictly inside the volume: no clamping is possible
+    __device__ bool interior(int x0, int y0, int zi) const {
+        return d.ndim == 3 && x0 - R - CAPH >= 0 && x0 + TX + R - 1 + CAPH <= d.nx - 1 &&
+               y0 - R - CAPH >= 0 && y0 + TYv + R - 1 + CAPH <= d.ny - 1 && zi - CAPH >= 0 &&
+               zi + CAPH <= d.nz - 1;
+    }
+    __device__ __forceinline__ static void cell_fast(int g, float s, int& i0, float& f) {
+        const float fl = floorf(s);
+        f = s - fl;
+        i0 = g + static_cast<int>(fl);
+    }
+    __device__ __forceinline__ static void cell_fast(int g, double s, int& i0, double& f) {
+        const double p = static_cast<double>(g) + s;  // the reference's formulation
+        const double fl = floor(p);
+        f = p - fl;
+        i0 = static_cast<int>(fl);
+    }
+    __device__ void stage_fast(const PlaneCtx& pc, int x0, int y0, int zi, int row, int col,
+                               T v[3]) const {
+        const int so = row * BXS + col + (XAS - R);
+        const T s0 = pc.step[so], s1 = pc.step[PS + so], s2 = pc.step[2 * PS + so];
+        int ix, iy, iz;
+        T fx, fy, fz;
+        cell_fast(x0 - R + col, s0, ix, fx);
+        cell_fast(y0 - R + row, s1, iy, fy);
+        cell_fast(zi, s2, iz, fz);
+        const int o = (iy - (y0 - HU)) * BXU + (ix - (x0 - XAU));
+        const T wx0 = T(1) - fx, wy0 = T(1) - fy, wz0 = T(1) - fz;
+        const T w00 = wx0 * wy0, w10 = fx * wy0, w01 = wx0 * fy, w11 = fx * fy;
+        const int dz = iz - zi;
+        const T* u0 = pc.u[CAPH];
+        const T* u1 = pc.u[CAPH];
+#pragma unroll
+        for (int k = 0; k < 2 * CAPH; ++k)
+            if (dz == k - CAPH) {
+                u0 = pc.u[k];
+                u1 = pc.u[k + 1];
+            }
+        const T s[3] = {s0, s1, s2};
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const T* a = u0 + k * PU + o;
+            const T* b = u1 + k * PU + o;
+            const T lo = w00 * a[0] + w10 * a[1] + w01 * a[BXU] + w11 * a[BXU + 1];
+            const T hi = w00 * b[0] + w10 * b[1] + w01 * b[BXU] + w11 * b[BXU + 1];
+            v[k] = s[k] + (wz0 * lo + fz * hi);
+        }
+    }
     // composed value step + u(x + step) at halo element (row, col) of plane zi
     __device__ void stage(const PlaneCtx& pc, int x0, int y0, int zi, int row, int col,
                           T v[3]) const {
@@ -672,7 +730,7 @@ struct Compose2 {
     }
     __device__ Red2 emit(int x, int y, int z, const T u[3], const Center&, const Prol&,
                          Carry& cr) const {
-        const int64_t i = d.idx(x, y, z);
+        const int64_t i = d.idx32(x, y, z);
         uout[i] = u[0];
         uout[d.n + i] = u[1];
         uout[2 * d.n + i] = d.ndim == 3 ? u[2] : T(0);
