@@ -243,6 +243,34 @@ DFM_API dfm_status dfm_dev_register(dfm_ctx* ctx, const dfm_grid* g, const void*
                             int32_t nscales, void* d_out_soa_field,
                             dfm_iter_record* records, int64_t max_records, dfm_runlog* log);
 
+/* ---- z-slab decomposition (BASELINE config 4) ------------ */
+/* Owned planes [zlo, zhi) and halo depths (hlo, hhi) of slab `part` of
+ * `nparts` over nz planes with halo H: out = {zlo, zhi, hlo, hhi}. */
+DFM_API dfm_status dfm_slab_bounds(int64_t nz, int part, int nparts, int halo, int64_t out[4]);
+/* Halo depth (planes) the iteration needs for this config on grid g. */
+DFM_API int dfm_slab_halo(const dfm_config* cfg, const dfm_grid* g);
+/* 128-byte NCCL unique id for a slab group (rank 0 creates, all ranks use). */
+DFM_API dfm_status dfm_slab_unique_id(unsigned char id[128]);
+/* register_images (direct mode, LNCC) on a z-slab decomposition: the z
+ * planes are split into `world` slabs; this process owns slab `rank` on the
+ * context's device and exchanges halo planes with its neighbours over NCCL
+ * (nccl_id from dfm_slab_unique_id) inside the captured iteration graphs; the
+ * loss is all-reduced every iteration so the convergence monitor is global.
+ * With world == 1, `emulate` > 1 splits the volume into that many slabs on
+ * this one device and exchanges halos by device copies (same kernels, same
+ * exchange plan).  d_fixed / d_moving: the FULL volumes (context precision)
+ * on this device.  d_out_soa_field: 3 component planes of this process's
+ * owned full-resolution planes (emulation: the whole volume); out_zlo/zhi
+ * return them. */
+DFM_API dfm_status dfm_dev_register_slab(dfm_ctx* ctx, const dfm_grid* g, const void* d_fixed,
+                                         const void* d_moving, const dfm_config* cfg,
+                                         const double* scales, const int32_t* iterations,
+                                         int32_t nscales, int rank, int world,
+                                         const unsigned char* nccl_id, int emulate,
+                                         void* d_out_soa_field, int64_t* out_zlo,
+                                         int64_t* out_zhi, dfm_iter_record* records,
+                                         int64_t max_records, dfm_runlog* log);
+
 /* Timing hook for benchmarks: per-kernel-class accumulated device time (ms)
  * and launch counts over the last dfm_register/dfm_dev_register call when
  * profiling is enabled with dfm_ctx_set_profiling(ctx, 1).  Class ids:

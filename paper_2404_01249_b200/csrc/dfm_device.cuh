@@ -16,6 +16,12 @@ struct Dims {
     int nx, ny, nz;  // nz == 1 for 2-D grids
     int ndim;
     int64_t n;       // nx*ny*nz
+    // z-slab view (all 0 for a whole volume): local plane 0 is global plane
+    // zoff of a volume with gnz planes; kernels produce local planes [zb, ze).
+    int zoff = 0, gnz = 0, zb = 0, ze = 0;
+    __host__ __device__ int gz() const { return gnz ? gnz : nz; }
+    __host__ __device__ int out_begin() const { return zb; }
+    __host__ __device__ int out_end() const { return ze ? ze : nz; }
     __host__ __device__ int64_t idx(int x, int y, int z) const {
         return (static_cast<int64_t>(z) * ny + y) * nx + x;
     }
@@ -239,8 +245,9 @@ __device__ __forceinline__ void atomic_max_nonneg(unsigned long long* slot, doub
 template <class T>
 __device__ __forceinline__ void jacobian_at(CPlanes3<T> u, const Dims& d, int x, int y, int z,
                                             T J[9]) {
-    const int pos[3] = {x, y, z};
-    const int n[3] = {d.nx, d.ny, d.nz};
+    // boundary decisions in global coordinates (z-slab views carry halos)
+    const int pos[3] = {x, y, z + d.zoff};
+    const int n[3] = {d.nx, d.ny, d.gz()};
     const int64_t stride[3] = {1, d.nx, static_cast<int64_t>(d.nx) * d.ny};
     const int64_t i = d.idx(x, y, z);
     for (int k = 0; k < 9; ++k) J[k] = T(0);

@@ -195,7 +195,7 @@ int launch_smooth_adam_tma(const Launch& L, int R, const GaussW<T>& w, const T* 
 template <class T>
 int launch_compose_tma(const Launch& L, int R, double cap, const GaussW<T>& w, const T* step,
                        const T* uin, T* uout, const T* M, Dims dm, Dims d, T* W, T* G,
-                       LoopState* st);
+                       LoopState* st, bool count_update = true);
 template <class T>
 void launch_warpgrad(const Launch& L, const T* M, Dims dm, CPlanes3<T> u, Dims d, T* W, T* G);
 

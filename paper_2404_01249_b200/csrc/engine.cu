@@ -1661,3 +1661,599 @@ dfm_status dfm_dev_register(dfm_ctx* ctx, const dfm_grid* g, const void* d_fixed
 }
 
 }  // extern "C"
+
+// ===========================================================================
+// z-slab decomposition of register_images: each slab owns a
+// contiguous range of z planes at every scale plus H halo planes on each
+// side; the plane-streaming kernels run on slab views (Dims::zoff/gnz/zb/ze)
+// and halo planes are exchanged after each producing stage — by device copies
+// between emulated slabs on one GPU, or by NCCL send/recv between processes.
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+namespace {
+
+// NCCL resolved at run time from the libnccl.so.2 already in the process (torch
+// bundles one) or the system one; the library does not link NCCL.
+struct NcclApi {
+    void* h = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+
+    void load() {
+        if (h) return;
+        for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+            h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+            if (h) break;
+        }
+        if (!h) fail(DFM_E_CUDA, "NCCL: cannot dlopen libnccl.so.2");
+        auto sym = [&](const char* n) {
+            void* p = dlsym(h, n);
+            if (!p) fail(DFM_E_CUDA, "NCCL: missing symbol %s", n);
+            return p;
+        };
+        GetUniqueId = reinterpret_cast<decltype(GetUniqueId)>(sym("ncclGetUniqueId"));
+        CommInitRank = reinterpret_cast<decltype(CommInitRank)>(sym("ncclCommInitRank"));
+        CommDestroy = reinterpret_cast<decltype(CommDestroy)>(sym("ncclCommDestroy"));
+        Send = reinterpret_cast<decltype(Send)>(sym("ncclSend"));
+        Recv = reinterpret_cast<decltype(Recv)>(sym("ncclRecv"));
+        AllReduce = reinterpret_cast<decltype(AllReduce)>(sym("ncclAllReduce"));
+        Broadcast = reinterpret_cast<decltype(Broadcast)>(sym("ncclBroadcast"));
+        GroupStart = reinterpret_cast<decltype(GroupStart)>(sym("ncclGroupStart"));
+        GroupEnd = reinterpret_cast<decltype(GroupEnd)>(sym("ncclGroupEnd"));
+        GetErrorString = reinterpret_cast<decltype(GetErrorString)>(sym("ncclGetErrorString"));
+    }
+    void ck(ncclResult_t r, const char* what) const {
+        if (r != ncclSuccess) fail(DFM_E_CUDA, "NCCL %s: %s", what, GetErrorString(r));
+    }
+};
+
+NcclApi& nccl_api() {
+    static NcclApi api;
+    return api;
+}
+
+struct SlabBounds {
+    int zlo, zhi, hlo, hhi;
+    int owned() const { return zhi - zlo; }
+    int z0g() const { return zlo - hlo; }
+    int nzl() const { return hlo + owned() + hhi; }
+};
+
+SlabBounds slab_bounds(int nz, int part, int nparts, int H) {
+    SlabBounds b;
+    b.zlo = static_cast<int>(static_cast<int64_t>(part) * nz / nparts);
+    b.zhi = static_cast<int>(static_cast<int64_t>(part + 1) * nz / nparts);
+    b.hlo = std::min(H, b.zlo);
+    b.hhi = std::min(H, nz - b.zhi);
+    return b;
+}
+
+// halo depth: LNCC window r, sigma_grad radius, sigma_warp radius + gather
+// reach of the capped compose (the u halo the compose kernel reads)
+int slab_halo(const dfm_config* c) {
+    const int rg = c->sigma_grad > 0 ? static_cast<int>(std::ceil(3.0 * c->sigma_grad)) : 0;
+    const int rw = c->sigma_warp > 0 ? static_cast<int>(std::ceil(3.0 * c->sigma_warp)) : 0;
+    const int caph = c->step_cap <= 0.5 ? 1 : 2;
+    return std::max(std::max(c->lncc_radius, rg), rw + caph);
+}
+
+template <class T>
+struct SlabRun {
+    dfm_ctx* ctx;
+    const dfm_grid* g;
+    const dfm_config* cfg;
+    Dims full;
+    int rank = 0, world = 1, E = 1;  // E local slabs (emulation) or 1 (NCCL)
+    ncclComm_t comm = nullptr;
+    int H = 0;
+
+    struct Part {
+        SlabBounds b;
+        Dims dl;  // slab view at the current scale
+        T* base[10];  // W G coef grad step u0 u1 m nu (F is a view of the pyramid)
+        T* W() const { return base[0]; }
+        T* G() const { return base[1]; }
+        T* coef() const { return base[2]; }
+        T* grad() const { return base[3]; }
+        T* step() const { return base[4]; }
+        T* u(int k) const { return base[5 + k]; }
+        T* m() const { return base[7]; }
+        T* nu() const { return base[8]; }
+    };
+    std::vector<Part> parts;
+    T* Fs = nullptr;
+    T* Ms = nullptr;
+    T* gath[3] = {nullptr, nullptr, nullptr};  // u, m, nu gathered at the previous scale
+    LoopState* st = nullptr;
+    double *loss = nullptr, *corr1 = nullptr, *corr2 = nullptr, *partials = nullptr,
+           *red = nullptr;
+    unsigned long long *maxstep = nullptr, *stamp = nullptr;
+    int cur = 0;
+    const NcclApi* nc = nullptr;
+
+    int nparts() const { return world > 1 ? world : E; }
+    int part_id(int j) const { return world > 1 ? rank : j; }
+    bool is_nccl() const { return world > 1; }
+    int64_t plane() const { return static_cast<int64_t>(full.nx) * full.ny; }
+
+    void alloc(int64_t total_iters) {
+        const int64_t pl = plane();
+        // local capacity: the largest owned range at full resolution + 2H
+        int maxn = 0;
+        for (int j = 0; j < E; ++j) {
+            const SlabBounds b = slab_bounds(full.nz, part_id(j), nparts(), H);
+            maxn = std::max(maxn, b.nzl());
+        }
+        const int64_t cap = pl * maxn;
+        parts.resize(E);
+        const int comps[9] = {1, 3, 4, 3, 3, 3, 3, 3, 3};
+        for (int j = 0; j < E; ++j)
+            for (int k = 0; k < 9; ++k)
+                parts[j].base[k] = ctx->arr<T>("slab" + std::to_string(j) + "_" + std::to_string(k),
+                                               comps[k] * cap);
+        Fs = ctx->arr<T>("slab_Fs", full.n);
+        Ms = ctx->arr<T>("slab_Ms", full.n);
+        for (int k = 0; k < 3; ++k) gath[k] = ctx->arr<T>("slab_gath" + std::to_string(k), 3 * full.n);
+        st = ctx->arr<LoopState>("slab_state", 1);
+        const int64_t ni = total_iters + 2;
+        loss = ctx->arr<double>("slab_loss", ni);
+        maxstep = ctx->arr<unsigned long long>("slab_maxstep", ni);
+        stamp = ctx->arr<unsigned long long>("slab_stamp", ni);
+        corr1 = ctx->arr<double>("slab_corr1", ni);
+        corr2 = ctx->arr<double>("slab_corr2", ni);
+        partials = ctx->arr<double>("slab_partials", 3 * 65536);
+        red = ctx->arr<double>("slab_red", 4);
+        std::vector<double> h1(ni), h2(ni);
+        for (int64_t t = 0; t < ni; ++t) {
+            h1[t] = 1.0 - std::pow(cfg->beta1, static_cast<double>(t));
+            h2[t] = 1.0 - std::pow(cfg->beta2, static_cast<double>(t));
+        }
+        CK(cudaMemcpyAsync(corr1, h1.data(), sizeof(double) * ni, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(corr2, h2.data(), sizeof(double) * ni, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemsetAsync(st, 0, sizeof(LoopState), ctx->stream));
+        ctx->sync();
+    }
+
+    // slab views of every part at scale grid ds
+    void layout(const Dims& ds) {
+        for (int j = 0; j < E; ++j) {
+            Part& p = parts[j];
+            p.b = slab_bounds(ds.nz, part_id(j), nparts(), H);
+            if (p.b.owned() < H && nparts() > 1)
+                fail(DFM_E_INVALID, "slab: %d slabs leave fewer than %d planes per slab at nz=%d",
+                     nparts(), H, ds.nz);
+            Dims& d = p.dl;
+            d = ds;
+            d.nz = p.b.nzl();
+            d.n = static_cast<int64_t>(ds.nx) * ds.ny * d.nz;
+            d.zoff = p.b.z0g();
+            d.gnz = ds.nz;
+            d.zb = p.b.hlo;
+            d.ze = p.b.hlo + p.b.owned();
+        }
+    }
+
+    // copy the owned planes of component buffers into halos of the neighbours
+    void exchange(int which, int ncomp) {
+        const int64_t pl = plane();
+        if (!is_nccl()) {
+            for (int j = 0; j < E; ++j) {
+                const Part& p = parts[j];
+                if (j > 0 && p.b.hlo > 0) {  // lower halo <- part j-1's top owned planes
+                    const Part& q = parts[j - 1];
+                    const int src_local = p.b.zlo - p.b.hlo - q.b.z0g();
+                    for (int c = 0; c < ncomp; ++c)
+                        CK(cudaMemcpyAsync(p.base[which] + c * p.dl.n,
+                                           q.base[which] + c * q.dl.n + src_local * pl,
+                                           sizeof(T) * pl * p.b.hlo, cudaMemcpyDeviceToDevice,
+                                           ctx->stream));
+                }
+                if (j + 1 < E && p.b.hhi > 0) {  // upper halo <- part j+1's bottom owned planes
+                    const Part& q = parts[j + 1];
+                    const int src_local = p.b.zhi - q.b.z0g();
+                    const int dst_local = p.b.hlo + p.b.owned();
+                    for (int c = 0; c < ncomp; ++c)
+                        CK(cudaMemcpyAsync(p.base[which] + c * p.dl.n + dst_local * pl,
+                                           q.base[which] + c * q.dl.n + src_local * pl,
+                                           sizeof(T) * pl * p.b.hhi, cudaMemcpyDeviceToDevice,
+                                           ctx->stream));
+                }
+            }
+            return;
+        }
+        const Part& p = parts[0];
+        const ncclDataType_t dt = sizeof(T) == 4 ? ncclFloat32 : ncclFloat64;
+        nc->ck(nc->GroupStart(), "group");
+        for (int c = 0; c < ncomp; ++c) {
+            T* buf = p.base[which] + c * p.dl.n;
+            if (rank > 0) {  // exchange with the lower neighbour: H planes each way
+                nc->ck(nc->Send(buf + p.b.hlo * pl, pl * p.b.hlo, dt, rank - 1, comm, ctx->stream), "send");
+                nc->ck(nc->Recv(buf, pl * p.b.hlo, dt, rank - 1, comm, ctx->stream), "recv");
+            }
+            if (rank + 1 < world) {
+                const int top = p.b.hlo + p.b.owned();
+                nc->ck(nc->Send(buf + (top - p.b.hhi) * pl, pl * p.b.hhi, dt, rank + 1, comm,
+                                ctx->stream), "send");
+                nc->ck(nc->Recv(buf + top * pl, pl * p.b.hhi, dt, rank + 1, comm, ctx->stream), "recv");
+            }
+        }
+        nc->ck(nc->GroupEnd(), "group");
+    }
+
+    // owned planes of (u[cur], m, nu) of every slab -> full volumes at grid ds
+    void gather(const Dims& ds) {
+        const int64_t pl = plane();
+        T* srcs[3];
+        for (int j = 0; j < E; ++j) {
+            const Part& p = parts[j];
+            srcs[0] = p.u(cur);
+            srcs[1] = p.m();
+            srcs[2] = p.nu();
+            for (int f = 0; f < 3; ++f)
+                for (int c = 0; c < 3; ++c) {
+                    if (!is_nccl())
+                        CK(cudaMemcpyAsync(gath[f] + c * ds.n + static_cast<int64_t>(p.b.zlo) * pl,
+                                           srcs[f] + c * p.dl.n + p.b.hlo * pl,
+                                           sizeof(T) * pl * p.b.owned(), cudaMemcpyDeviceToDevice,
+                                           ctx->stream));
+                }
+        }
+        if (is_nccl()) {  // every rank broadcasts its owned block to all
+            const Part& p = parts[0];
+            srcs[0] = p.u(cur);
+            srcs[1] = p.m();
+            srcs[2] = p.nu();
+            const ncclDataType_t dt = sizeof(T) == 4 ? ncclFloat32 : ncclFloat64;
+            nc->ck(nc->GroupStart(), "group");
+            for (int r = 0; r < world; ++r) {
+                const SlabBounds b = slab_bounds(ds.nz, r, world, H);
+                for (int f = 0; f < 3; ++f)
+                    for (int c = 0; c < 3; ++c)
+                        nc->ck(nc->Broadcast(srcs[f] + c * p.dl.n + p.b.hlo * pl,
+                                             gath[f] + c * ds.n + static_cast<int64_t>(b.zlo) * pl,
+                                             pl * b.owned(), dt, r, comm, ctx->stream),
+                               "broadcast");
+            }
+            nc->ck(nc->GroupEnd(), "group");
+        }
+    }
+
+    // full volumes at grid from -> every slab's local planes at grid to
+    void scatter_resample(const Dims& from, const Dims& to, bool with_state) {
+        double mult[3] = {1, 1, 1}, sq[3] = {1, 1, 1};
+        const int nn[3] = {to.nx, to.ny, to.nz}, no[3] = {from.nx, from.ny, from.nz};
+        for (int a = 0; a < to.ndim; ++a) {
+            mult[a] = static_cast<double>(nn[a] - 1) / static_cast<double>(no[a] - 1);
+            sq[a] = mult[a] * mult[a];
+        }
+        for (int j = 0; j < E; ++j) {
+            Part& p = parts[j];
+            Dims dall = p.dl;  // every local plane, halos included
+            dall.zb = 0;
+            dall.ze = 0;
+            const int tgt = 1 - cur;
+            const T* su[3] = {gath[0], gath[0] + from.n, gath[0] + 2 * from.n};
+            T* du[3] = {p.u(tgt), p.u(tgt) + p.dl.n, p.u(tgt) + 2 * p.dl.n};
+            launch_resample<T>(ctx->L(), su, from, du, dall, to.ndim, mult);
+            if (with_state) {
+                const T* sm[3] = {gath[1], gath[1] + from.n, gath[1] + 2 * from.n};
+                T* dm[3] = {p.m(), p.m() + p.dl.n, p.m() + 2 * p.dl.n};
+                launch_resample<T>(ctx->L(), sm, from, dm, dall, to.ndim, mult);
+                const T* sn[3] = {gath[2], gath[2] + from.n, gath[2] + 2 * from.n};
+                T* dn[3] = {p.nu(), p.nu() + p.dl.n, p.nu() + 2 * p.dl.n};
+                launch_resample<T>(ctx->L(), sn, from, dn, dall, to.ndim, sq);
+            }
+        }
+        cur = 1 - cur;
+    }
+
+    double global_sum(const double* part_sums, int np) {
+        // fixed-order device reduction, then (NCCL) a sum over ranks
+        launch_reduce_value(ctx->L(), 0, part_sums, np, 1.0, red);
+        if (is_nccl())
+            nc->ck(nc->AllReduce(red, red, 1, ncclFloat64, ncclSum, comm, ctx->stream), "allreduce");
+        double h[3];
+        CK(cudaMemcpyAsync(h, red, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->sync();
+        return h[0];
+    }
+
+    void enqueue_iteration(const Dims& ds, int src, int Rg, int Rw, const GaussW<T>& wg,
+                           const GaussW<T>& ww) {
+        Launch L = ctx->L();
+        const int64_t pl = plane();
+        const double N = static_cast<double>(ds.n);
+        int off = 0;
+        for (int j = 0; j < E; ++j) {
+            Part& p = parts[j];
+            const int np = launch_lncc_fwd_tma<T>(L, cfg->lncc_radius, Fs + p.b.z0g() * pl, p.W(),
+                                                  p.dl, p.coef(), partials + off, st);
+            if (np < 0) fail(DFM_E_CUDA, "slab: lncc forward launch failed");
+            off += np;
+        }
+        if (is_nccl()) {
+            launch_reduce_value(L, 0, partials, off, 1.0, red);
+            nc->ck(nc->AllReduce(red, red, 1, ncclFloat64, ncclSum, comm, ctx->stream), "allreduce");
+            launch_monitor(L, 1, red, 1, N, st, loss, stamp, cfg->conv_window, cfg->conv_tol);
+        } else {
+            launch_monitor(L, 1, partials, off, N, st, loss, stamp, cfg->conv_window, cfg->conv_tol);
+        }
+        exchange(2, 4);  // coefficients
+        for (Part& p : parts)
+            launch_lncc_bwd_tma<T>(L, cfg->lncc_radius, p.coef(), Fs + p.b.z0g() * pl, p.W(), p.G(),
+                                   p.dl, p.grad(), st);
+        exchange(3, 3);  // gradient
+        AdamParams ap{cfg->beta1, cfg->beta2, cfg->eps_adam, cfg->eta, cfg->step_cap,
+                      corr1, corr2, cfg->use_jac};
+        for (Part& p : parts)
+            launch_smooth_adam_tma<T>(L, Rg, wg, p.grad(), p.m(), p.nu(), p.step(), p.dl, ap, st,
+                                      maxstep);
+        if (is_nccl())  // a non-finite step anywhere aborts everywhere
+            nc->ck(nc->AllReduce(&st->bad_step, &st->bad_step, 1, ncclInt32, ncclMax, comm,
+                                 ctx->stream), "allreduce");
+        exchange(4, 3);  // step
+        for (int j = 0; j < E; ++j) {
+            Part& p = parts[j];
+            launch_compose_tma<T>(L, Rw, cfg->step_cap, ww, p.step(), p.u(src), p.u(1 - src), Ms,
+                                  ds, p.dl, p.W(), p.G(), st, j == 0);
+        }
+        exchange(6 - src, 3);  // u (the buffer just written)
+        exchange(0, 1);        // W
+    }
+
+    void run(const T* F, const T* M, const double* scales, const int32_t* iters, int ns,
+             RegOut& out, T* d_out, int64_t* ozlo, int64_t* ozhi) {
+        const double t0 = now_ms();
+        if (cfg->loss != DFM_LOSS_LNCC || cfg->use_jac)
+            fail(DFM_E_INVALID, "slab decomposition: LNCC loss, use_jac off only");
+        if (!tma_supported(full, sizeof(T)))
+            fail(DFM_E_INVALID, "slab decomposition: x extent must be a multiple of 16 bytes");
+        H = slab_halo(cfg);
+        int64_t total = 0;
+        for (int i = 0; i < ns; ++i) total += iters[i];
+        alloc(total);
+        Dims prev{};
+        bool have = false;
+        int64_t global = 0;
+        const int64_t pl = plane();
+        for (int si = 0; si < ns; ++si) {
+            const double fac[3] = {scales[si], scales[si], scales[si]};
+            dfm_grid wgd;
+            downsample_grid(g, fac, &wgd);
+            const Dims ds = to_dims(&wgd);
+            if (2 * static_cast<int64_t>(cfg->lncc_radius) + 1 > ds.nx ||
+                2 * static_cast<int64_t>(cfg->lncc_radius) + 1 > ds.ny ||
+                2 * static_cast<int64_t>(cfg->lncc_radius) + 1 > ds.nz)
+                fail(DFM_E_INVALID, "lncc_eval: window larger than image");
+            Impl<T>{ctx}.downsample_dev(full, F, fac, ds, Fs, "spyr");
+            Impl<T>{ctx}.downsample_dev(full, M, fac, ds, Ms, "spyr");
+            if (!have) {
+                layout(ds);
+                for (Part& p : parts)
+                    for (int k : {5, 6, 7, 8})
+                        CK(cudaMemsetAsync(p.base[k], 0, sizeof(T) * 3 * p.dl.n, ctx->stream));
+                cur = 0;
+                have = true;
+            } else if (!dims_equal(prev, ds)) {
+                gather(prev);
+                layout(ds);
+                scatter_resample(prev, ds, true);
+            }
+            prev = ds;
+            const int T_si = iters[si];
+            if (T_si == 0) continue;
+            for (Part& p : parts)
+                launch_warpgrad<T>(ctx->L(), Ms, ds, CPlanes3<T>{{p.u(cur), p.u(cur) + p.dl.n,
+                                                                  p.u(cur) + 2 * p.dl.n}},
+                                   [&] { Dims a = p.dl; a.zb = a.ze = 0; return a; }(), p.W(), p.G());
+            CK(cudaMemsetAsync(st, 0, offsetof(LoopState, t), ctx->stream));
+            CK(cudaMemsetAsync(maxstep, 0, sizeof(unsigned long long) * (T_si + 1), ctx->stream));
+            const double sg[3] = {cfg->sigma_grad, cfg->sigma_grad, cfg->sigma_grad};
+            const double sw[3] = {cfg->sigma_warp, cfg->sigma_warp, cfg->sigma_warp};
+            const HostGauss hg = make_gauss(ds, sg), hw = make_gauss(ds, sw);
+            if (hg.R > 6 || hw.R > 4)
+                fail(DFM_E_INVALID, "slab decomposition: sigma_grad <= 2, sigma_warp <= 1.33 only");
+            const GaussW<T> wg = upload_gauss<T>(ctx, hg, ds, "slab_g");
+            const GaussW<T> ww = upload_gauss<T>(ctx, hw, ds, "slab_w");
+            const int start = cur;
+            cudaGraphExec_t exec[2] = {nullptr, nullptr};
+            for (int v = 0; v < 2; ++v) {
+                cudaGraph_t graph;
+                CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
+                enqueue_iteration(ds, (start + v) % 2, hg.R, hw.R, wg, ww);
+                CK(cudaStreamEndCapture(ctx->stream, &graph));
+                CK(cudaGraphInstantiate(&exec[v], graph, 0));
+                CK(cudaGraphDestroy(graph));
+            }
+            // every rank launches the same number of graphs (global decisions)
+            LoopState* hst = ctx->pinned_state();
+            int nchunk = 0;
+            for (int j = 0; j < T_si;) {
+                if (nchunk >= 2) {
+                    const int w = (nchunk - 2) % 2;
+                    CK(cudaEventSynchronize(ctx->chunk_ev[w]));
+                    if (hst[w].done) break;
+                }
+                const int jend = std::min(j + 16, T_si);
+                for (; j < jend; ++j) CK(cudaGraphLaunch(exec[j % 2], ctx->stream));
+                const int w = nchunk % 2;
+                CK(cudaMemcpyAsync(&hst[w], st, sizeof(LoopState), cudaMemcpyDeviceToHost, ctx->stream));
+                CK(cudaEventRecord(ctx->chunk_ev[w], ctx->stream));
+                ++nchunk;
+            }
+            launch_stamp(ctx->L(), stamp + T_si);
+            if (is_nccl())  // max |step| of the log over ranks
+                nc->ck(nc->AllReduce(maxstep, maxstep, T_si, ncclUint64, ncclMax, comm, ctx->stream),
+                       "allreduce");
+            ctx->sync();
+            for (int v = 0; v < 2; ++v) CK(cudaGraphExecDestroy(exec[v]));
+            LoopState hs;
+            std::vector<double> hl(T_si + 1);
+            std::vector<unsigned long long> hm(T_si + 1), ht(T_si + 1);
+            CK(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaMemcpyAsync(hl.data(), loss, sizeof(double) * T_si, cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaMemcpyAsync(hm.data(), maxstep, sizeof(unsigned long long) * T_si,
+                               cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaMemcpyAsync(ht.data(), stamp, sizeof(unsigned long long) * (T_si + 1),
+                               cudaMemcpyDeviceToHost, ctx->stream));
+            ctx->sync();
+            const int nrec = hs.it;
+            for (int j = 0; j < nrec; ++j) {
+                dfm_iter_record r{};
+                r.scale_index = si;
+                r.scale = scales[si];
+                r.iter = j;
+                r.global_iter = global++;
+                r.loss = hl[j];
+                double ms;
+                std::memcpy(&ms, &hm[j], sizeof(double));
+                r.max_step = (hs.converged && j == nrec - 1) ? 0.0 : ms;
+                const unsigned long long tn = (j + 1 < nrec) ? ht[j + 1] : ht[T_si];
+                r.wall_ms = tn > ht[j] ? static_cast<double>(tn - ht[j]) * 1e-6 : 0.0;
+                if (hs.err && j == nrec - 1 && !std::isfinite(hl[j])) break;
+                out.recs.push_back(r);
+            }
+            if (hs.err) {
+                if (nrec > 0 && !std::isfinite(hl[nrec - 1]))
+                    fail(DFM_E_NUMERICAL, "register_images: non-finite loss at scale %f, iteration %d",
+                         scales[si], nrec - 1);
+                fail(DFM_E_NUMERICAL, "apply_update: non-finite step");
+            }
+            cur = (start + hs.nupdates) % 2;
+        }
+        // epilogue at full resolution (pipeline.cpp:213-223)
+        if (!dims_equal(prev, full)) {
+            gather(prev);
+            layout(full);
+            scatter_resample(prev, full, false);
+        }
+        int off = 0;
+        for (Part& p : parts) {
+            Dims dall = p.dl;
+            dall.zb = dall.ze = 0;
+            launch_warpgrad<T>(ctx->L(), M, full,
+                               CPlanes3<T>{{p.u(cur), p.u(cur) + p.dl.n, p.u(cur) + 2 * p.dl.n}},
+                               dall, p.W(), nullptr);
+            const int np = launch_lncc_fwd_tma<T>(ctx->L(), cfg->lncc_radius, F + p.b.z0g() * pl, p.W(),
+                                                  p.dl, nullptr, partials + off, nullptr);
+            off += np;
+        }
+        const double S = global_sum(partials, off);
+        out.final_loss = -S / static_cast<double>(full.n);
+        auto* cnt = ctx->arr<unsigned long long>("slab_count", 1);
+        CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), ctx->stream));
+        for (Part& p : parts)
+            launch_jacobian_det<T>(ctx->L(), CPlanes3<T>{{p.u(cur), p.u(cur) + p.dl.n,
+                                                          p.u(cur) + 2 * p.dl.n}},
+                                   p.dl, nullptr, cnt);
+        if (is_nccl())
+            nc->ck(nc->AllReduce(cnt, cnt, 1, ncclUint64, ncclSum, comm, ctx->stream), "allreduce");
+        unsigned long long hc = 0;
+        CK(cudaMemcpyAsync(&hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream));
+        // result planes
+        int64_t zlo = parts.front().b.zlo, zhi = parts.back().b.zhi;
+        const int64_t nout = (zhi - zlo) * pl;
+        if (d_out)
+            for (Part& p : parts)
+                for (int c = 0; c < 3; ++c)
+                    CK(cudaMemcpyAsync(d_out + c * nout + (p.b.zlo - zlo) * pl,
+                                       p.u(cur) + c * p.dl.n + p.b.hlo * pl,
+                                       sizeof(T) * pl * p.b.owned(), cudaMemcpyDeviceToDevice,
+                                       ctx->stream));
+        ctx->sync();
+        out.sing = static_cast<double>(hc) / static_cast<double>(full.n);
+        out.total_ms = now_ms() - t0;
+        if (ozlo) *ozlo = zlo;
+        if (ozhi) *ozhi = zhi;
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+dfm_status dfm_slab_bounds(int64_t nz, int part, int nparts, int halo, int64_t out[4]) {
+    return guarded([&] {
+        if (nz < 1 || nparts < 1 || part < 0 || part >= nparts || halo < 0)
+            fail(DFM_E_INVALID, "slab_bounds: bad arguments");
+        const SlabBounds b = slab_bounds(static_cast<int>(nz), part, nparts, halo);
+        out[0] = b.zlo;
+        out[1] = b.zhi;
+        out[2] = b.hlo;
+        out[3] = b.hhi;
+    });
+}
+
+int dfm_slab_halo(const dfm_config* cfg, const dfm_grid*) { return cfg ? slab_halo(cfg) : -1; }
+
+dfm_status dfm_slab_unique_id(unsigned char id[128]) {
+    return guarded([&] {
+        NcclApi& api = nccl_api();
+        api.load();
+        ncclUniqueId u;
+        api.ck(api.GetUniqueId(&u), "get unique id");
+        std::memcpy(id, u.internal, 128);
+    });
+}
+
+dfm_status dfm_dev_register_slab(dfm_ctx* ctx, const dfm_grid* g, const void* d_fixed,
+                                 const void* d_moving, const dfm_config* cfg,
+                                 const double* scales, const int32_t* iterations,
+                                 int32_t nscales, int rank, int world,
+                                 const unsigned char* nccl_id, int emulate,
+                                 void* d_out_soa_field, int64_t* out_zlo, int64_t* out_zhi,
+                                 dfm_iter_record* records, int64_t max_records, dfm_runlog* log) {
+    return guarded([&] {
+        validate_grid(g);
+        validate_config(cfg);
+        validate_schedule(scales, iterations, nscales);
+        if (g->ndim != 3) fail(DFM_E_INVALID, "slab decomposition needs a 3-D grid");
+        if (world < 1 || rank < 0 || rank >= world) fail(DFM_E_INVALID, "slab: bad rank/world");
+        if (world > 1 && emulate > 1) fail(DFM_E_INVALID, "slab: emulate needs world == 1");
+        RegOut o;
+        DFM_DISPATCH(ctx, {
+            SlabRun<T> R;
+            R.ctx = ctx;
+            R.g = g;
+            R.cfg = cfg;
+            R.full = to_dims(g);
+            R.rank = rank;
+            R.world = world;
+            R.E = world > 1 ? 1 : std::max(1, emulate);
+            if (world > 1) {
+                if (!nccl_id) fail(DFM_E_INVALID, "slab: nccl_id required when world > 1");
+                NcclApi& api = nccl_api();
+                api.load();
+                ncclUniqueId u;
+                std::memcpy(u.internal, nccl_id, 128);
+                api.ck(api.CommInitRank(&R.comm, world, u, rank), "comm init");
+                R.nc = &api;
+            }
+            try {
+                R.run(static_cast<const T*>(d_fixed), static_cast<const T*>(d_moving), scales,
+                      iterations, nscales, o, static_cast<T*>(d_out_soa_field), out_zlo, out_zhi);
+            } catch (...) {
+                if (R.comm) R.nc->CommDestroy(R.comm);
+                throw;
+            }
+            if (R.comm) R.nc->CommDestroy(R.comm);
+        });
+        fill_log(o, records, max_records, log);
+        if (o.sing > 0.0)
+            fail(DFM_E_NUMERICAL, "register_images: folded warp (det J <= 0 somewhere)");
+    });
+}
+
+}  // extern "C"

@@ -191,9 +191,11 @@ void launch_compose(const Launch& L, CPlanes3<T> phi, CPlanes3<T> psi, Dims d, P
 // jacobian_det (interp.cpp:330-349) + singularity count (analysis.cpp:160-167)
 template <class T>
 __global__ void k_jacobian_det(CPlanes3<T> u, Dims d, T* det, unsigned long long* nonpos) {
-    const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
+    // only the produced planes [zb, ze) of a slab view are evaluated
+    const int64_t plane = static_cast<int64_t>(d.nx) * d.ny;
+    const int64_t i = d.out_begin() * plane + blockIdx.x * (int64_t)kNT + threadIdx.x;
     int bad = 0;
-    if (i < d.n) {
+    if (i < d.out_end() * plane) {
         int x, y, z;
         voxel_xyz(d, i, x, y, z);
         T J[9];
@@ -326,7 +328,7 @@ __global__ void k_resample(ResampleArgs<T> a, Dims ds, Dims dd, int ncomp) {
     double fx, fy, fz;
     locate_point(x * a.step[0], ds.nx, ix, fx);
     locate_point(y * a.step[1], ds.ny, iy, fy);
-    locate_point(z * a.step[2], ds.nz, iz, fz);
+    locate_point((z + dd.zoff) * a.step[2], ds.nz, iz, fz);  // dd may be a z-slab view
     Cell3<T> c;
     c.base = ds.idx(ix, iy, iz);
     c.sx = ds.nx > 1 ? 1 : 0;
@@ -347,7 +349,7 @@ template <class T>
 void launch_resample(const Launch& L, const T* const* src, Dims ds, T* const* dst, Dims dd,
                      int ncomp, const double* mult) {
     ResampleArgs<T> a;
-    const int ns[3] = {ds.nx, ds.ny, ds.nz}, nd[3] = {dd.nx, dd.ny, dd.nz};
+    const int ns[3] = {ds.nx, ds.ny, ds.nz}, nd[3] = {dd.nx, dd.ny, dd.gz()};
     for (int k = 0; k < 3; ++k) {
         a.src[k] = k < ncomp ? src[k] : nullptr;
         a.dst[k] = k < ncomp ? dst[k] : nullptr;

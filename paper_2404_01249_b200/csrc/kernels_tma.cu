@@ -104,8 +104,8 @@ __global__ void __launch_bounds__(TX * Op::TYv) k_zm2(const __grid_constant__ Op
     const int tx = tid % TX, ty = tid / TX;
     const int x0 = (blockIdx.x % g.tiles_x) * TX;
     const int y0 = (blockIdx.x / g.tiles_x) * TYv;
-    const int z0 = blockIdx.y * g.zchunk;
-    const int z1 = min(z0 + g.zchunk, d.nz);
+    const int z0 = d.out_begin() + blockIdx.y * g.zchunk;
+    const int z1 = min(z0 + g.zchunk, d.out_end());
     const int x = x0 + tx, y = y0 + ty;
     const bool own = x < d.nx && y < d.ny;
     const int q0 = z0 - R - Op::BACK;
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(TX * Op::TYv) k_zm2(const __grid_constant__ Op
                 }
                 if (em) {
                     // oldest plane (zo - R) sits in slot 0 (slot (kk + 1) % K)
-                    const Acc nz = op.nrm(2, zo);
+                    const Acc nz = op.nrm(2, zo + d.zoff);
                     Acc sv[C];
 #pragma unroll
                     for (int c = 0; c < C; ++c) {
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(TX * Op::TYv) k_zm2(const __grid_constant__ Op
                     const double tot = bsum<NTh>(acc, s_red);
                     if (tid == 0) {
                         op.mon.st->arrive = 0;
-                        monitor_commit(op.mon.st, -tot / static_cast<double>(d.n), 0.0, 0.0,
+                        monitor_commit(op.mon.st, -tot / (static_cast<double>(d.nx) * d.ny * d.gz()), 0.0, 0.0,
                                        op.mon.loss, op.mon.stamp, op.mon.window, op.mon.tol);
                     }
                 }
@@ -344,7 +344,7 @@ struct LnccFwd2 {
                          Carry&) const {
         // similarity.cpp:145-162 with 2 divisions instead of 12: 1/n, 1/(vF vW)
         const double n = static_cast<double>(box_len(x, d.nx, R) * box_len(y, d.ny, R) *
-                                             (d.nz > 1 ? box_len(z, d.nz, R) : 1));
+                                             (d.gz() > 1 ? box_len(z + d.zoff, d.gz(), R) : 1));
         const double inv_n = 1.0 / n;
         const double muF = s[0] * inv_n;
         const double muW = s[1] * inv_n;
@@ -572,6 +572,7 @@ struct Compose2 {
     T* W;     // nullptr: do not produce W/G
     T* G;     // 3 planes
     LoopState* st;
+    int count_update;  // 0 for all but one slab of an emulated decomposition
     Dims d;
     struct Carry {
         bool valid;
@@ -625,9 +626,10 @@ struct Compose2 {
     // every composed element of this CTA-plane (tile + Gaussian halo) has its
     // interpolation cell strictly inside the volume: no clamping is possible
     __device__ bool interior(int x0, int y0, int zi) const {
+        const int zg = zi + d.zoff;
         return d.ndim == 3 && x0 - R - CAPH >= 0 && x0 + TX + R - 1 + CAPH <= d.nx - 1 &&
-               y0 - R - CAPH >= 0 && y0 + TYv + R - 1 + CAPH <= d.ny - 1 && zi - CAPH >= 0 &&
-               zi + CAPH <= d.nz - 1;
+               y0 - R - CAPH >= 0 && y0 + TYv + R - 1 + CAPH <= d.ny - 1 && zg - CAPH >= 0 &&
+               zg + CAPH <= d.gz() - 1;
     }
     __device__ __forceinline__ static void cell_fast(int g, float s, int& i0, float& f) {
         const float fl = floorf(s);
@@ -648,7 +650,8 @@ struct Compose2 {
         T fx, fy, fz;
         cell_fast(x0 - R + col, s0, ix, fx);
         cell_fast(y0 - R + row, s1, iy, fy);
-        cell_fast(zi, s2, iz, fz);
+        cell_fast(zi + d.zoff, s2, iz, fz);
+        iz -= d.zoff;
         const int o = (iy - (y0 - HU)) * BXU + (ix - (x0 - XAU));
         const T wx0 = T(1) - fx, wy0 = T(1) - fy, wz0 = T(1) - fz;
         const T w00 = wx0 * wy0, w10 = fx * wy0, w01 = wx0 * fy, w11 = fx * fy;
@@ -674,8 +677,8 @@ struct Compose2 {
     // composed value step + u(x + step) at halo element (row, col) of plane zi
     __device__ void stage(const PlaneCtx& pc, int x0, int y0, int zi, int row, int col,
                           T v[3]) const {
-        const int gx = x0 - R + col, gy = y0 - R + row;
-        if (gx < 0 || gx >= d.nx || gy < 0 || gy >= d.ny || zi < 0 || zi >= d.nz) {
+        const int gx = x0 - R + col, gy = y0 - R + row, zg = zi + d.zoff;
+        if (gx < 0 || gx >= d.nx || gy < 0 || gy >= d.ny || zg < 0 || zg >= d.gz()) {
             v[0] = v[1] = v[2] = T(0);
             return;
         }
@@ -688,8 +691,8 @@ struct Compose2 {
         int dz = 0;  // lower z corner relative to zi, in [-CAPH, CAPH-1]
         T fz = T(0);
         if (three) {
-            const AxisCell<T> az = locate_axis(zi, s2, d.nz);
-            dz = az.i0 - zi;
+            const AxisCell<T> az = locate_axis(zg, s2, d.gz());
+            dz = az.i0 - zg;
             fz = az.f;
         }
         const int o = (ay.i0 - (y0 - HU)) * BXU + (ax.i0 - (x0 - XAU));
@@ -736,7 +739,7 @@ struct Compose2 {
         uout[2 * d.n + i] = d.ndim == 3 ? u[2] : T(0);
         if (W) {  // similarity.cpp:25-45 for the next loss evaluation
             if (cr.valid) finish_wg(cr);
-            cr.c = locate3<T>(dm, x, y, z, u[0], u[1], d.ndim == 3 ? u[2] : T(0));
+            cr.c = locate3<T>(dm, x, y, z + d.zoff, u[0], u[1], d.ndim == 3 ? u[2] : T(0));
             cr.k = fetch_corners<T>(M, cr.c);
             cr.i = i;
             cr.valid = true;
@@ -747,7 +750,7 @@ struct Compose2 {
         if (W && cr.valid) finish_wg(cr);
     }
     __device__ void finish(int, double, double, const Prol&) const {
-        if (st) st->nupdates += 1;
+        if (st && count_update) st->nupdates += 1;
     }
 };
 
@@ -760,7 +763,7 @@ __global__ void k_warpgrad(const T* __restrict__ M, Dims dm, CPlanes3<T> u, Dims
     const int x = static_cast<int>(i % d.nx);
     const int64_t r = i / d.nx;
     const int y = static_cast<int>(r % d.ny), z = static_cast<int>(r / d.ny);
-    const Cell3<T> c = locate3<T>(dm, x, y, z, __ldg(u.c[0] + i), __ldg(u.c[1] + i),
+    const Cell3<T> c = locate3<T>(dm, x, y, z + d.zoff, __ldg(u.c[0] + i), __ldg(u.c[1] + i),
                                   d.ndim == 3 ? __ldg(u.c[2] + i) : T(0));
     const Corners<T> k = fetch_corners<T>(M, c);
     W[i] = lerp_value(c, k);
@@ -857,7 +860,9 @@ int run_zm2(const Launch& L, const Op& op, Dims d) {
     g.tiles_x = (d.nx + TX - 1) / TX;
     const int tiles = g.tiles_x * ((d.ny + Op::TYv - 1) / Op::TYv);
     const int slots = occ * (L.num_sms > 0 ? L.num_sms : 148);
-    const int nchunks = pick_chunks(d, tiles, slots, 2 * Op::R + Op::BACK + Op::AHEAD, &g.zchunk);
+    Dims dr = d;  // chunk the produced plane range only
+    dr.nz = d.out_end() - d.out_begin();
+    const int nchunks = pick_chunks(dr, tiles, slots, 2 * Op::R + Op::BACK + Op::AHEAD, &g.zchunk);
     k_zm2<Op><<<dim3(tiles, nchunks), TX * Op::TYv, smem, L.stream>>>(op, g);
     L.bump();
     return tiles * nchunks;
@@ -913,7 +918,7 @@ int launch_lncc_bwd_tma(const Launch& L, int R, const T* coef, const T* F, const
         op.W = W;
         op.G = G;
         op.grad = grad;
-        op.m2n = -2.0 / static_cast<double>(d.n);
+        op.m2n = -2.0 / (static_cast<double>(d.nx) * d.ny * d.gz());  // global N
         op.st = st;
         op.d = d;
         return run_zm2(L, op, d);
@@ -952,7 +957,7 @@ int launch_smooth_adam_tma(const Launch& L, int R, const GaussW<T>& w, const T* 
 template <class T>
 int launch_compose_tma(const Launch& L, int R, double cap, const GaussW<T>& w, const T* step,
                        const T* uin, T* uout, const T* M, Dims dm, Dims d, T* W, T* G,
-                       LoopState* st) {
+                       LoopState* st, bool count_update) {
     const int caph = cap <= 0.5 ? 1 : (cap <= 1.5 ? 2 : 0);
     if (caph == 0) return -2;
     return with_r<0, 4>(R, [&](auto rc) {
@@ -971,6 +976,7 @@ int launch_compose_tma(const Launch& L, int R, double cap, const GaussW<T>& w, c
             op.W = W;
             op.G = G;
             op.st = st;
+            op.count_update = count_update ? 1 : 0;
             op.d = d;
             return run_zm2(L, op, d);
         };
@@ -995,7 +1001,7 @@ void launch_warpgrad(const Launch& L, const T* M, Dims dm, CPlanes3<T> u, Dims d
                                            unsigned long long*);                               \
     template int launch_compose_tma<T>(const Launch&, int, double, const GaussW<T>&, const T*, \
                                        const T*, T*, const T*, Dims, Dims, T*, T*,             \
-                                       LoopState*);                                            \
+                                       LoopState*, bool);                                      \
     template void launch_warpgrad<T>(const Launch&, const T*, Dims, CPlanes3<T>, Dims, T*, T*);
 
 DFM_INST_TMA(float)

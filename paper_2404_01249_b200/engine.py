@@ -31,6 +31,7 @@ EXPORTS = [
     "dfm_ssd_eval", "dfm_lncc_eval", "dfm_dice_eval", "dfm_adam_step", "dfm_upsample_state",
     "dfm_eulerian_direction", "dfm_apply_update", "dfm_singularity_fraction", "dfm_register",
     "dfm_dev_register", "dfm_ctx_set_profiling", "dfm_ctx_kernel_times",
+    "dfm_slab_bounds", "dfm_slab_halo", "dfm_slab_unique_id", "dfm_dev_register_slab",
 ]
 
 _lib: Optional[C.CDLL] = None
@@ -80,6 +81,19 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                                C.POINTER(A.dfm_iter_record), C.c_int64,
                                                C.POINTER(A.dfm_runlog)]
         lib.dfm_dev_register.restype = C.c_int
+        lib.dfm_slab_bounds.argtypes = [C.c_int64, C.c_int, C.c_int, C.c_int,
+                                        C.POINTER(C.c_int64)]
+        lib.dfm_slab_bounds.restype = C.c_int
+        lib.dfm_slab_halo.argtypes = [C.POINTER(A.dfm_config), C.POINTER(A.dfm_grid)]
+        lib.dfm_slab_halo.restype = C.c_int
+        lib.dfm_slab_unique_id.argtypes = [C.c_char_p]
+        lib.dfm_slab_unique_id.restype = C.c_int
+        lib.dfm_dev_register_slab.argtypes = reg + [
+            C.POINTER(A.dfm_config), C.POINTER(C.c_double), C.POINTER(C.c_int32), C.c_int32,
+            C.c_int, C.c_int, C.c_char_p, C.c_int, C.c_void_p, C.POINTER(C.c_int64),
+            C.POINTER(C.c_int64), C.POINTER(A.dfm_iter_record), C.c_int64,
+            C.POINTER(A.dfm_runlog)]
+        lib.dfm_dev_register_slab.restype = C.c_int
         _lib = lib
     return _lib
 
@@ -176,6 +190,50 @@ class Context(A.HostAPI):
                                        C.byref(rl))
         self.t.check(rc, "dev_register")
         return A.records_to_log(recs, rl)
+
+
+def slab_bounds(nz: int, part: int, nparts: int, halo: int):
+    """(zlo, zhi, hlo, hhi) of slab `part` — the plan every rank computes."""
+    lib = load_library()
+    out = (C.c_int64 * 4)()
+    rc = lib.dfm_slab_bounds(int(nz), int(part), int(nparts), int(halo), out)
+    if rc != A.DFM_OK:
+        raise A.InvalidArgument("slab_bounds: bad arguments")
+    return tuple(int(v) for v in out)
+
+
+def slab_halo(cfg: A.RegistrationConfig) -> int:
+    lib = load_library()
+    cc = cfg.c()
+    return int(lib.dfm_slab_halo(C.byref(cc), None))
+
+
+def slab_unique_id() -> bytes:
+    lib = load_library()
+    buf = C.create_string_buffer(128)
+    rc = lib.dfm_slab_unique_id(buf)
+    if rc != A.DFM_OK:
+        raise A.DeviceError("dfm_slab_unique_id failed")
+    return buf.raw
+
+
+def register_slab(ctx: "Context", g: A.GridMeta, d_fixed: int, d_moving: int,
+                  cfg: A.RegistrationConfig, sched: A.PyramidSchedule, rank: int = 0,
+                  world: int = 1, nccl_id: bytes = None, emulate: int = 1, d_out: int = 0):
+    """dfm_dev_register_slab: z-slab decomposed registration -> (zlo, zhi, RunLog)."""
+    s, it = A.schedule_arrays(sched)
+    cap = int(it.sum()) + 1
+    recs = (A.dfm_iter_record * cap)()
+    rl = A.dfm_runlog()
+    cc = cfg.c()
+    zlo, zhi = C.c_int64(), C.c_int64()
+    rc = ctx.lib.dfm_dev_register_slab(
+        ctx.handle, C.byref(g.c()), C.c_void_p(d_fixed), C.c_void_p(d_moving), C.byref(cc),
+        A._dptr(s), it.ctypes.data_as(C.POINTER(C.c_int32)), len(s), rank, world, nccl_id,
+        emulate, C.c_void_p(d_out) if d_out else None, C.byref(zlo), C.byref(zhi), recs, cap,
+        C.byref(rl))
+    ctx.t.check(rc, "register_slab")
+    return zlo.value, zhi.value, A.records_to_log(recs, rl)
 
 
 def cuda_available() -> bool:
