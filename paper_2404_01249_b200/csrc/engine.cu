@@ -1786,10 +1786,12 @@ struct SlabRun {
     int nparts() const { return world > 1 ? world : E; }
     int part_id(int j) const { return world > 1 ? rank : j; }
     bool is_nccl() const { return world > 1; }
-    int64_t plane() const { return static_cast<int64_t>(full.nx) * full.ny; }
+    // plane size of the current slab views (the scale being processed)
+    int64_t plane() const { return static_cast<int64_t>(parts.empty() ? full.nx * full.ny
+                                                                       : parts[0].dl.nx * parts[0].dl.ny); }
 
     void alloc(int64_t total_iters) {
-        const int64_t pl = plane();
+        const int64_t pl = static_cast<int64_t>(full.nx) * full.ny;
         // local capacity: the largest owned range at full resolution + 2H
         int maxn = 0;
         for (int j = 0; j < E; ++j) {
@@ -1894,7 +1896,7 @@ struct SlabRun {
 
     // owned planes of (u[cur], m, nu) of every slab -> full volumes at grid ds
     void gather(const Dims& ds) {
-        const int64_t pl = plane();
+        const int64_t pl = static_cast<int64_t>(ds.nx) * ds.ny;
         T* srcs[3];
         for (int j = 0; j < E; ++j) {
             const Part& p = parts[j];
@@ -1973,7 +1975,7 @@ struct SlabRun {
     void enqueue_iteration(const Dims& ds, int src, int Rg, int Rw, const GaussW<T>& wg,
                            const GaussW<T>& ww) {
         Launch L = ctx->L();
-        const int64_t pl = plane();
+        const int64_t pl = static_cast<int64_t>(ds.nx) * ds.ny;
         const double N = static_cast<double>(ds.n);
         int off = 0;
         for (int j = 0; j < E; ++j) {
@@ -2027,7 +2029,7 @@ struct SlabRun {
         Dims prev{};
         bool have = false;
         int64_t global = 0;
-        const int64_t pl = plane();
+        const int64_t pl = static_cast<int64_t>(full.nx) * full.ny;  // epilogue (full grid)
         for (int si = 0; si < ns; ++si) {
             const double fac[3] = {scales[si], scales[si], scales[si]};
             dfm_grid wgd;
