@@ -281,6 +281,20 @@ DFM_API dfm_status dfm_ctx_set_profiling(dfm_ctx* ctx, int enable);
 DFM_API dfm_status dfm_ctx_kernel_times(const dfm_ctx* ctx, double* ms, int64_t* launches,
                                 int64_t* voxels);
 
+/* Kernel-family tuning of a context (no reference counterpart; defaults are
+ * the tuned ones).  DFM_OPT_BRICK_MAX: pyramid levels with at most this many
+ * voxels run the brick kernels, larger ones the plane-streaming kernels
+ * (default 200000; 0 = never brick).  DFM_OPT_FORCE_LEGACY: 1 = run the v1
+ * z-march kernels everywhere (A/B reference).  Environment variables
+ * DFM_BRICK_MAX / DFM_FORCE_LEGACY set the same at context creation. */
+#define DFM_OPT_BRICK_MAX 1
+#define DFM_OPT_FORCE_LEGACY 2
+/* DFM_OPT_PERSIST: 1 = brick levels of an LNCC registration run as
+ * one persistent cooperative launch per level; 0 = one CUDA graph per
+ * iteration (default 0: measured faster).  Env DFM_PERSIST. */
+#define DFM_OPT_PERSIST 3
+DFM_API dfm_status dfm_ctx_set_option(dfm_ctx* ctx, int key, int64_t value);
+
 #ifdef __cplusplus
 }
 #endif

@@ -150,19 +150,27 @@ struct Corners {
     T v[8];  // order (cz, cy, cx) as in interp.cpp:159-162
 };
 
-template <class T, class S>
+// NC = true reads through the non-coherent (read-only) path: only for data
+// that no thread writes during the kernel.
+template <class S, bool NC>
+__device__ __forceinline__ S ld_(const S* p) {
+    if constexpr (NC) return __ldg(p);
+    else return *p;
+}
+
+template <class T, class S, bool NC = true>
 __device__ __forceinline__ Corners<T> fetch_corners(const S* __restrict__ img, const Cell3<T>& c) {
     Corners<T> k;
     const S* p = img + c.base;
-    k.v[0] = static_cast<T>(__ldg(p));
-    k.v[1] = static_cast<T>(__ldg(p + c.sx));
-    k.v[2] = static_cast<T>(__ldg(p + c.sy));
-    k.v[3] = static_cast<T>(__ldg(p + c.sy + c.sx));
+    k.v[0] = static_cast<T>(ld_<S, NC>(p));
+    k.v[1] = static_cast<T>(ld_<S, NC>(p + c.sx));
+    k.v[2] = static_cast<T>(ld_<S, NC>(p + c.sy));
+    k.v[3] = static_cast<T>(ld_<S, NC>(p + c.sy + c.sx));
     if (c.three) {
-        k.v[4] = static_cast<T>(__ldg(p + c.sz));
-        k.v[5] = static_cast<T>(__ldg(p + c.sz + c.sx));
-        k.v[6] = static_cast<T>(__ldg(p + c.sz + c.sy));
-        k.v[7] = static_cast<T>(__ldg(p + c.sz + c.sy + c.sx));
+        k.v[4] = static_cast<T>(ld_<S, NC>(p + c.sz));
+        k.v[5] = static_cast<T>(ld_<S, NC>(p + c.sz + c.sx));
+        k.v[6] = static_cast<T>(ld_<S, NC>(p + c.sz + c.sy));
+        k.v[7] = static_cast<T>(ld_<S, NC>(p + c.sz + c.sy + c.sx));
     } else {
         k.v[4] = k.v[5] = k.v[6] = k.v[7] = T(0);
     }
@@ -208,16 +216,16 @@ __device__ __forceinline__ void lerp_grad(const Cell3<T>& c, const Corners<T>& k
 }
 
 // per-component field sample (interp.cpp:188-203)
-template <class T>
+template <class T, bool NC = true>
 __device__ __forceinline__ void lerp_field(const Cell3<T>& c, const T* __restrict__ f0,
                                            const T* __restrict__ f1, const T* __restrict__ f2,
                                            int ndim, T out[3]) {
-    Corners<T> k = fetch_corners<T>(f0, c);
+    Corners<T> k = fetch_corners<T, T, NC>(f0, c);
     out[0] = lerp_value(c, k);
-    k = fetch_corners<T>(f1, c);
+    k = fetch_corners<T, T, NC>(f1, c);
     out[1] = lerp_value(c, k);
     if (ndim == 3) {
-        k = fetch_corners<T>(f2, c);
+        k = fetch_corners<T, T, NC>(f2, c);
         out[2] = lerp_value(c, k);
     } else {
         out[2] = T(0);

@@ -199,6 +199,62 @@ int launch_compose_tma(const Launch& L, int R, double cap, const GaussW<T>& w, c
 template <class T>
 void launch_warpgrad(const Launch& L, const T* M, Dims dm, CPlanes3<T> u, Dims d, T* W, T* G);
 
+// -------- brick kernels (kernels_brick.cu): 8x8x8 bricks, every pass in
+// parallel; used on the small pyramid levels where the z-march is
+// latency-bound.  Same contracts as the plane-streaming launchers; return < 0
+// when the radius / precision combination is not instantiated.
+constexpr int kBrickLnccRMax = 3, kBrickGaussRMax = 6, kBrickComposeRMax = 4;
+bool brick_supported(Dims d, int esz, int lncc_r, int rg, int rw);
+template <class T>
+int launch_lncc_fwd_brick(const Launch& L, int R, const T* F, const T* W, Dims d, T* coef,
+                          double* partials, const LoopState* st,
+                          const MonitorArgs* mon = nullptr);
+template <class T>
+int launch_lncc_bwd_brick(const Launch& L, int R, const T* coef, const T* F, const T* W,
+                          const T* G, Dims d, T* grad, const LoopState* st);
+template <class T>
+int launch_smooth_adam_brick(const Launch& L, int R, const GaussW<T>& w, const T* grad, T* m,
+                             T* nu, T* step, Dims d, AdamParams ap, LoopState* st,
+                             unsigned long long* maxstep);
+template <class T>
+int launch_compose_brick(const Launch& L, int R, const GaussW<T>& w, const T* step,
+                         const T* uin, T* uout, const T* M, Dims dm, Dims d, T* W, T* G,
+                         LoopState* st, bool count_update = true);
+
+// Persistent scale solver (kernels_brick.cu): every iteration of one small
+// LNCC pyramid level in ONE cooperative launch, grid barriers between the
+// brick phases, device-side monitor.  u0 -> u1 on even iterations (ping-pong);
+// on return LoopState holds it / t / nupdates / err like the graph path.
+// Returns < 0 if the radius triple is not instantiated or co-residency fails.
+template <class T>
+struct PersistScale {
+    Dims d;
+    int lncc_r, rg, rw;
+    const T* F;
+    const T* M;
+    T* W;
+    T* G;
+    T* coef;
+    T* grad;
+    T* m;
+    T* nu;
+    T* step;
+    T* u0;
+    T* u1;
+    GaussW<T> wg, ww;
+    AdamParams ap;
+    LoopState* st;
+    double* partials;
+    double* loss;
+    unsigned long long* stamp;
+    unsigned long long* maxstep;
+    int window;
+    double tol;
+    int iters;
+};
+template <class T>
+int launch_persist_scale(const Launch& L, const PersistScale<T>& p);
+
 // -------- loop control
 // kind: 0 ssd, 1 lncc, 2 dice (3 partial arrays of np each)
 void launch_monitor(const Launch& L, int kind, const double* partials, int np, double nvox,

@@ -84,6 +84,10 @@ struct dfm_ctx {
     bool profiling = false;
     bool force_legacy = getenv("DFM_FORCE_LEGACY") != nullptr;  // A/B the v1 kernels
     int tma_mask = getenv("DFM_TMA_MASK") ? atoi(getenv("DFM_TMA_MASK")) : 15;
+    // pyramid levels up to this many voxels run the brick kernels
+    int64_t brick_max = getenv("DFM_BRICK_MAX") ? atoll(getenv("DFM_BRICK_MAX")) : 200000;
+    // brick levels of an LNCC registration run as one persistent launch per level
+    bool persist = getenv("DFM_PERSIST") ? atoi(getenv("DFM_PERSIST")) != 0 : false;
     double kt_ms[DFM_NUM_KCLASS] = {};
     int64_t kt_n[DFM_NUM_KCLASS] = {};
     int64_t kt_vox[DFM_NUM_KCLASS] = {};
@@ -536,6 +540,22 @@ dfm_status dfm_ctx_set_profiling(dfm_ctx* ctx, int enable) {
     return guarded([&] {
         if (!ctx) fail(DFM_E_INVALID, "ctx is NULL");
         ctx->profiling = enable != 0;
+    });
+}
+
+dfm_status dfm_ctx_set_option(dfm_ctx* ctx, int key, int64_t value) {
+    return guarded([&] {
+        if (!ctx) fail(DFM_E_INVALID, "ctx is NULL");
+        if (key == DFM_OPT_BRICK_MAX) {
+            if (value < 0) fail(DFM_E_INVALID, "brick_max must be >= 0");
+            ctx->brick_max = value;
+        } else if (key == DFM_OPT_FORCE_LEGACY) {
+            ctx->force_legacy = value != 0;
+        } else if (key == DFM_OPT_PERSIST) {
+            ctx->persist = value != 0;
+        } else {
+            fail(DFM_E_INVALID, "unknown context option %d", key);
+        }
     });
 }
 
@@ -1055,7 +1075,8 @@ struct Registrar {
     int cur = 0;
     T* Wb = nullptr;  // W = M(x+u) for the current u (TMA path)
     T* Gb = nullptr;  // grad M(x+u), 3 planes
-    bool use_tma = false;
+    bool use_tma = false;    // fused W/G-carrying loop (plane-streaming and/or brick kernels)
+    bool use_brick = false;  // this scale runs the brick kernels
     // profiling
     std::vector<cudaEvent_t> evpool;
     std::vector<std::pair<int, int>> evuse;  // (class, pool index of start)
@@ -1157,8 +1178,10 @@ struct Registrar {
         const bool fused = lncc && (mask & 1);
         if (fused) {  // LNCC moments + window coefficients + loss + monitor, one launch
             const MonitorArgs mon{st, loss, stamp, cfg->conv_window, cfg->conv_tol};
-            np = launch_lncc_fwd_tma<T>(L, cfg->lncc_radius, Fs, Wb, d, coef[0], partials, st,
-                                        &mon);
+            np = use_brick ? launch_lncc_fwd_brick<T>(L, cfg->lncc_radius, Fs, Wb, d, coef[0],
+                                                      partials, st, &mon)
+                           : launch_lncc_fwd_tma<T>(L, cfg->lncc_radius, Fs, Wb, d, coef[0],
+                                                    partials, st, &mon);
         } else {
             np = loss_kind_launch_fwd<T>(ctx, loss_kind, cfg->lncc_radius, Fs, Ms, d, d, uin,
                                          coef, grad.w(), partials, st);
@@ -1172,7 +1195,10 @@ struct Registrar {
         }
         if (lncc) {
             ev_begin(KC_BWD);
-            if (mask & 2) {
+            if (use_brick) {
+                launch_lncc_bwd_brick<T>(L, cfg->lncc_radius, coef[0], Fs, Wb, Gb, d, grad.p[0],
+                                         st);
+            } else if (mask & 2) {
                 launch_lncc_bwd_tma<T>(L, cfg->lncc_radius, coef[0], Fs, Wb, Gb, d, grad.p[0], st);
             } else {
                 const T* cc[4] = {coef[0], coef[1], coef[2], coef[3]};
@@ -1187,7 +1213,10 @@ struct Registrar {
         AdamParams ap{cfg->beta1, cfg->beta2, cfg->eps_adam, cfg->eta, cfg->step_cap,
                       corr1, corr2, cfg->use_jac};
         ev_begin(KC_ADAM);
-        if (mask & 4)
+        if (use_brick)
+            launch_smooth_adam_brick<T>(L, Rg, wg, grad.p[0], m.p[0], nu.p[0], step.p[0], d, ap,
+                                        st, maxstep);
+        else if (mask & 4)
             launch_smooth_adam_tma<T>(L, Rg, wg, grad.p[0], m.p[0], nu.p[0], step.p[0], d, ap, st,
                                       maxstep);
         else
@@ -1195,7 +1224,10 @@ struct Registrar {
                                   maxstep);
         ev_end();
         ev_begin(KC_COMPOSE);
-        if (mask & 8) {
+        if (use_brick) {
+            launch_compose_brick<T>(L, Rw, ww, step.p[0], u[src].p[0], u[1 - src].p[0], Ms, d, d,
+                                    lncc ? Wb : nullptr, lncc ? Gb : nullptr, st);
+        } else if (mask & 8) {
             launch_compose_tma<T>(L, Rw, cfg->step_cap, ww, step.p[0], u[src].p[0],
                                   u[1 - src].p[0], Ms, d, d, lncc ? Wb : nullptr,
                                   lncc ? Gb : nullptr, st);
@@ -1470,10 +1502,51 @@ struct Registrar {
         const int Rg = hg.R > kRMax ? 0 : hg.R;
         const int Rw = hw.R > kRMax ? 0 : hw.R;
         const int start = cur;
-        use_tma = !ctx->force_legacy && tma_eligible(d, Rg, Rw, pbg || pbw);
+        const bool big = pbg || pbw;
+        use_brick = !ctx->force_legacy && !big && !cfg->use_jac && d.n <= ctx->brick_max &&
+                    brick_supported(d, static_cast<int>(sizeof(T)),
+                                    cfg->loss == DFM_LOSS_LNCC ? cfg->lncc_radius : 1, Rg, Rw);
+        use_tma = use_brick || (!ctx->force_legacy && tma_eligible(d, Rg, Rw, big));
         if (use_tma && cfg->loss == DFM_LOSS_LNCC)
             launch_warpgrad<T>(ctx->L(), Ms, d, u[cur].r(), d, Wb, Gb);
-        if (ctx->profiling) {
+        bool persisted = false;
+        if (!ctx->profiling && ctx->persist && use_brick && cfg->loss == DFM_LOSS_LNCC) {
+            PersistScale<T> ps{};
+            ps.d = d;
+            ps.lncc_r = cfg->lncc_radius;
+            ps.rg = Rg;
+            ps.rw = Rw;
+            ps.F = Fs;
+            ps.M = Ms;
+            ps.W = Wb;
+            ps.G = Gb;
+            ps.coef = coef[0];
+            ps.grad = grad.p[0];
+            ps.m = m.p[0];
+            ps.nu = nu.p[0];
+            ps.step = step.p[0];
+            ps.u0 = u[start].p[0];
+            ps.u1 = u[1 - start].p[0];
+            ps.wg = wg;
+            ps.ww = ww;
+            ps.ap = AdamParams{cfg->beta1, cfg->beta2, cfg->eps_adam, cfg->eta, cfg->step_cap,
+                               corr1, corr2, cfg->use_jac};
+            ps.st = st;
+            ps.partials = partials;
+            ps.loss = loss;
+            ps.stamp = stamp;
+            ps.maxstep = maxstep;
+            ps.window = cfg->conv_window;
+            ps.tol = cfg->conv_tol;
+            ps.iters = T_si;
+            persisted = launch_persist_scale<T>(ctx->L(), ps) >= 0;
+            if (persisted) {
+                launch_stamp(ctx->L(), stamp + T_si);
+                ctx->sync();
+            }
+        }
+        if (persisted) {
+        } else if (ctx->profiling) {
             for (int j = 0; j < T_si; ++j)
                 enqueue_iteration(d, (start + j) % 2, Rg, Rw, wg, ww, pbg, pbw);
             launch_stamp(ctx->L(), stamp + T_si);

@@ -1,0 +1,780 @@
+// kernels_brick.cu — brick-tiled stencil kernels of the hot loop for the
+// small pyramid levels.
+//
+// The plane-streaming kernels (kernels_tma.cu) march each CTA through a long
+// z-chunk, which is the right shape for a 160x192x224 volume but latency-bound
+// on the 40x48x56 and 80x96x112 levels: there a CTA walks only a few planes,
+// each a serial chain of TMA wait -> x pass -> barrier -> y pass -> z ring.
+// Here a CTA owns an 8x8x8 brick instead and does every pass for the whole
+// brick in parallel:
+//   1. stage the haloed brick (8+2R)^3 of the op's raw channels into shared
+//      memory (all loads independent: one L2 round trip; zero outside the
+//      volume, which together with the per-position renormalisation factors
+//      reproduces the reference's clipped windows / truncated Gaussians);
+//   2. x pass over (8+2R)^2 rows x 8 columns -> shared;
+//   3. y pass over (8+2R) planes x 8 x 8 -> shared (reuses the staging buffer);
+//   4. z pass + the op's per-voxel epilogue for the 512 voxels of the brick.
+// Three barriers per launch, no serial plane loop.  The per-voxel arithmetic
+// is loop_ops.cuh, shared with the plane-streaming kernels.
+//
+// Buffers the loop rewrites (W, G, coefficients, grad, step, u) are read with
+// plain coherent loads, never ld.global.nc: the persistent solver below reads
+// them after grid barriers within one launch.
+//
+// Ops (same roles as in kernels_tma.cu):
+//   LnccFwdB    F, W          -> 4 window coefficients, cc^2 partials (+ monitor)
+//   LnccBwdB    coefficients  -> grad = dW * G
+//   SmoothAdamB grad          -> m, nu, capped step, max |step|
+//   ComposeB    step, u       -> u' = smooth(step + u(x+step)), W, G
+#include <cstdint>
+#include <mutex>
+
+#include <cooperative_groups.h>
+
+#include "dfm_device.cuh"
+#include "dfm_kernels.cuh"
+#include "loop_ops.cuh"
+
+namespace dfm {
+
+namespace {
+
+constexpr int NTB = 512;
+constexpr int BX = 8, BY = 8, BZ = 8;
+constexpr size_t kBrickSmemMax = 227 * 1024;
+
+struct BG {
+    Dims d;
+    int nbx, nby;
+};
+
+template <class Op>
+struct BrickLayout {
+    using A = typename Op::Acc;
+    using S = typename Op::Raw;
+    static constexpr int R = Op::R, C = Op::C, NR = Op::NR;
+    static constexpr int HX = BX + 2 * R, HY = BY + 2 * R, HZ = BZ + 2 * R;
+    static constexpr int nS = HX * HY * HZ;  // per staged channel
+    static constexpr int nX = HZ * HY * BX;  // per channel, x-pass output
+    static constexpr int nY = HZ * BY * BX;  // per channel, y-pass output
+    static constexpr size_t bX = (static_cast<size_t>(C) * nX * sizeof(A) + 15) / 16 * 16;
+    static constexpr size_t bS = static_cast<size_t>(NR) * nS * sizeof(S);
+    static constexpr size_t bY = static_cast<size_t>(C) * nY * sizeof(A);
+    static constexpr size_t bytes = bX + (bS > bY ? bS : bY);
+};
+
+// One brick of one op: stage, x, y, z passes, per-voxel epilogue and the
+// CTA reduction; op.finish(b, ...) records brick b's partial.  Ends with the
+// CTA's threads synchronised (smem reusable).
+template <class Op>
+__device__ __forceinline__ void brick_body(const Op& op, const BG& g, int b, unsigned char* smem,
+                                           double* s_red) {
+    using Lay = BrickLayout<Op>;
+    using A = typename Op::Acc;
+    using S = typename Op::Raw;
+    constexpr int R = Op::R, C = Op::C, NR = Op::NR, K = 2 * R + 1;
+    constexpr int HX = Lay::HX, HY = Lay::HY;
+    constexpr int nS = Lay::nS, nX = Lay::nX, nY = Lay::nY;
+    A* sX = reinterpret_cast<A*>(smem);
+    S* sS = reinterpret_cast<S*>(smem + Lay::bX);
+    A* sY = reinterpret_cast<A*>(smem + Lay::bX);  // aliases sS after the x pass
+
+    const Dims& d = g.d;
+    const int tid = threadIdx.x;
+    const int bid = b;
+    const int x0 = (b % g.nbx) * BX;
+    b /= g.nbx;
+    const int y0 = (b % g.nby) * BY;
+    const int z0 = (b / g.nby) * BZ;
+
+    // 1. stage: the loads of a batch of elements are all issued before any is
+    // stored (one L2 round trip per batch instead of one per element)
+    const bool inner = x0 - R >= 0 && x0 + BX + R <= d.nx && y0 - R >= 0 &&
+                       y0 + BY + R <= d.ny && z0 - R >= 0 && z0 + BZ + R <= d.nz;
+    constexpr int IS = (nS + NTB - 1) / NTB, SB = Op::kStageBatch;
+    for (int b0 = 0; b0 < IS; b0 += SB) {
+        S v[SB][NR];
+#pragma unroll
+        for (int k = 0; k < SB; ++k) {
+            const int e = tid + (b0 + k) * NTB;
+            const int xl = e % HX, t = e / HX, yl = t % HY, zl = t / HY;
+            const int gx = x0 - R + xl, gy = y0 - R + yl, gz = z0 - R + zl;
+            if (b0 + k < IS && e < nS &&
+                (inner || (gx >= 0 && gx < d.nx && gy >= 0 && gy < d.ny && gz >= 0 &&
+                           gz < d.nz))) {
+                op.stage(gx, gy, gz, v[k]);
+            } else {
+#pragma unroll
+                for (int c = 0; c < NR; ++c) v[k][c] = S(0);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < SB; ++k) {
+            const int e = tid + (b0 + k) * NTB;
+            if (b0 + k < IS && e < nS) {
+#pragma unroll
+                for (int c = 0; c < NR; ++c) sS[c * nS + e] = v[k][c];
+            }
+        }
+    }
+    __syncthreads();
+    // 2. x pass
+    constexpr int IX = (nX + NTB - 1) / NTB;
+#pragma unroll
+    for (int k = 0; k < IX; ++k) {
+        const int e = tid + k * NTB;
+        if (e < nX) {
+            const int xl = e % BX, t = e / BX;  // t = zl*HY + yl
+            const int gx = x0 + xl;
+            A v[C];
+            op.xpass(sS + t * HX + xl, nS, v);
+            const A nxv = gx < d.nx ? op.nrm(0, gx) : A(0);
+#pragma unroll
+            for (int c = 0; c < C; ++c) sX[c * nX + e] = v[c] * nxv;
+        }
+    }
+    __syncthreads();
+    // 3. y pass (into the dead staging buffer)
+    constexpr int IY = (nY + NTB - 1) / NTB;
+#pragma unroll
+    for (int k = 0; k < IY; ++k) {
+        const int e = tid + k * NTB;
+        if (e < nY) {
+            const int xl = e % BX, t = e / BX, yl = t % BY, zl = t / BY;
+            const int gy = y0 + yl;
+            const A nyv = gy < d.ny ? op.nrm(1, gy) : A(0);
+            const A* src = sX + (zl * HY + yl) * BX + xl;
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                A a = A(0);
+#pragma unroll
+                for (int j = 0; j < K; ++j) a += op.wgt(1, j) * src[c * nX + j * BX];
+                sY[c * nY + e] = a * nyv;
+            }
+        }
+    }
+    __syncthreads();
+    // 4. z pass + per-voxel epilogue (both voxels of a thread in flight together)
+    const typename Op::Prol pr = op.prologue();
+    double rsum = 0.0, rmax = 0.0;
+    constexpr int IZ = BZ * BY * BX / NTB;
+    static_assert(IZ * NTB == BZ * BY * BX, "brick must be a multiple of the CTA size");
+#pragma unroll
+    for (int k = 0; k < IZ; ++k) {
+        const int e = tid + k * NTB;
+        const int xl = e % BX, t = e / BX, yl = t % BY, zl = t / BY;
+        const int gx = x0 + xl, gy = y0 + yl, gz = z0 + zl;
+        if (gx < d.nx && gy < d.ny && gz < d.nz) {
+            const A nzv = op.nrm(2, gz);
+            const A* src = sY + e;
+            A sv[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                A a = A(0);
+#pragma unroll
+                for (int j = 0; j < K; ++j) a += op.wgt(2, j) * src[c * nY + j * (BY * BX)];
+                sv[c] = a * nzv;
+            }
+            const Red2 r = op.emit(gx, gy, gz, sv, pr);
+            rsum += r.sum;
+            rmax = fmax(rmax, r.mx);
+        }
+    }
+    if constexpr (Op::kSum || Op::kMax) {
+        const double bs = Op::kSum ? bsum<NTB>(rsum, s_red) : 0.0;
+        const double bm = Op::kMax ? bmax<NTB>(rmax, s_red) : 0.0;
+        if (tid == 0) op.finish(bid, bs, bm, pr);
+    } else {
+        if (tid == 0 && bid == 0) op.finish(0, 0.0, 0.0, pr);
+        __syncthreads();
+    }
+}
+
+template <class Op>
+__global__ void __launch_bounds__(NTB, 2) k_brick(const __grid_constant__ Op op, const BG g) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ double s_red[32];
+    if (op.skip()) return;
+    brick_body(op, g, blockIdx.x, smem, s_red);
+    if constexpr (Op::kSum) {
+        if (op.mon.st)
+            monitor_tail<NTB>(op.mon, op.partials, gridDim.x,
+                              static_cast<double>(g.d.nx) * g.d.ny * g.d.nz, s_red);
+    }
+}
+
+struct NoProl {};
+
+// similarity.cpp:122-168 — five box moments of F and W = M(x+u) (fp64), the
+// window coefficients and cc^2
+template <class T, int R_>
+struct LnccFwdB {
+    using Acc = double;
+    using Raw = double;
+    using Prol = NoProl;
+    static constexpr int R = R_, C = 5, NR = 2, kStageBatch = 8;
+    static constexpr bool kSum = true, kMax = false;
+    const T* F;
+    const T* W;
+    T* coef;  // 4 planes; nullptr -> value only
+    double* partials;
+    const LoopState* st;
+    MonitorArgs mon;
+    Dims d;
+
+    __device__ bool skip() const { return st && st->done; }
+    __device__ void stage(int x, int y, int z, double v[2]) const {
+        const int i = d.idx32(x, y, z);
+        v[0] = static_cast<double>(__ldg(F + i));
+        v[1] = static_cast<double>(W[i]);
+    }
+    __device__ void xpass(const double* p, int cs, double v[5]) const {
+        double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
+#pragma unroll
+        for (int j = 0; j < 2 * R + 1; ++j) {
+            const double f = p[j], w = p[cs + j];
+            a0 += f;
+            a1 += w;
+            a2 += f * f;
+            a3 += w * w;
+            a4 += f * w;
+        }
+        v[0] = a0;
+        v[1] = a1;
+        v[2] = a2;
+        v[3] = a3;
+        v[4] = a4;
+    }
+    __device__ double wgt(int, int) const { return 1.0; }
+    __device__ double nrm(int, int) const { return 1.0; }
+    __device__ Prol prologue() const { return {}; }
+    __device__ Red2 emit(int x, int y, int z, const double s[5], const Prol&) const {
+        const double n = static_cast<double>(box_len(x, d.nx, R) * box_len(y, d.ny, R) *
+                                             box_len(z, d.nz, R));
+        const LnccCoef k = lncc_coef(s, n);
+        if (coef) {
+            const int i = d.idx32(x, y, z);
+            coef[i] = static_cast<T>(k.an);
+            coef[d.n + i] = static_cast<T>(k.amu);
+            coef[2 * d.n + i] = static_cast<T>(k.bn);
+            coef[3 * d.n + i] = static_cast<T>(k.bmu);
+        }
+        return {k.cc2, 0.0};
+    }
+    __device__ void finish(int blk, double s, double, const Prol&) const { partials[blk] = s; }
+};
+
+// similarity.cpp:170-189 — box sums of the 4 coefficients, dW, grad = dW * G
+template <class T, int R_>
+struct LnccBwdB {
+    using Acc = double;
+    using Raw = double;
+    using Prol = NoProl;
+    static constexpr int R = R_, C = 4, NR = 4, kStageBatch = 8;
+    static constexpr bool kSum = false, kMax = false;
+    const T* coef;  // 4 planes
+    const T* F;
+    const T* W;
+    const T* G;  // 3 planes
+    T* grad;     // 3 planes
+    double m2n;  // -2 / N
+    const LoopState* st;
+    Dims d;
+
+    __device__ bool skip() const { return st && st->done; }
+    __device__ void stage(int x, int y, int z, double v[4]) const {
+        const int i = d.idx32(x, y, z);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = static_cast<double>(coef[k * d.n + i]);
+    }
+    __device__ void xpass(const double* p, int cs, double v[4]) const {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            double a = 0.0;
+#pragma unroll
+            for (int j = 0; j < 2 * R + 1; ++j) a += p[c * cs + j];
+            v[c] = a;
+        }
+    }
+    __device__ double wgt(int, int) const { return 1.0; }
+    __device__ double nrm(int, int) const { return 1.0; }
+    __device__ Prol prologue() const { return {}; }
+    __device__ Red2 emit(int x, int y, int z, const double s[4], const Prol&) const {
+        const int i = d.idx32(x, y, z);
+        const double f = static_cast<double>(__ldg(F + i)), w = static_cast<double>(W[i]);
+        const double dW = lncc_dw(m2n, f, w, s);
+        grad[i] = static_cast<T>(dW * static_cast<double>(G[i]));
+        grad[d.n + i] = static_cast<T>(dW * static_cast<double>(G[d.n + i]));
+        grad[2 * d.n + i] = static_cast<T>(dW * static_cast<double>(G[2 * d.n + i]));
+        return {0.0, 0.0};
+    }
+    __device__ void finish(int, double, double, const Prol&) const {}
+};
+
+// Gaussian x pass shared by the smoothing ops (interp.cpp:110-151)
+template <class T, int R>
+__device__ __forceinline__ void gauss_xpass(const GaussW<T>& w, const T* p, int cs, T v[3]) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const T* q = p + c * cs;
+        T a0 = T(0), a1 = T(0);
+#pragma unroll
+        for (int j = 0; j < 2 * R + 1; j += 2) a0 += w.taps[0][j] * q[j];
+#pragma unroll
+        for (int j = 1; j < 2 * R + 1; j += 2) a1 += w.taps[0][j] * q[j];
+        v[c] = a0 + a1;
+    }
+}
+
+// pipeline.cpp:182-186 + optim.cpp:22-42 + diffeo.cpp:47-57: sigma_grad
+// smoothing, v = -g, Adam, capped step, max |step|
+template <class T, int R_>
+struct SmoothAdamB {
+    using Acc = T;
+    using Raw = T;
+    static constexpr int R = R_, C = 3, NR = 3, kStageBatch = 8;
+    static constexpr bool kSum = false, kMax = true;
+    const T* grad;  // 3 planes
+    GaussW<T> w;
+    T* m;
+    T* nu;
+    T* step;
+    AdamK<T> ak;
+    const double* corr1;
+    const double* corr2;
+    LoopState* st;
+    unsigned long long* maxstep;
+    Dims d;
+    struct Prol {
+        T ic1, ic2;
+        int slot;
+    };
+
+    __device__ bool skip() const { return st && st->done; }
+    __device__ void stage(int x, int y, int z, T v[3]) const {
+        const int i = d.idx32(x, y, z);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) v[k] = grad[k * d.n + i];
+    }
+    __device__ void xpass(const T* p, int cs, T v[3]) const { gauss_xpass<T, R>(w, p, cs, v); }
+    __device__ T wgt(int a, int j) const { return w.taps[a][j]; }
+    __device__ T nrm(int a, int i) const { return __ldg(w.norm[a] + i); }
+    __device__ Prol prologue() const {
+        Prol p;
+        const long long t = st ? st->t : 1;
+        p.ic1 = static_cast<T>(1.0 / corr1[t]);
+        p.ic2 = static_cast<T>(1.0 / corr2[t]);
+        p.slot = st ? st->slot : 0;
+        return p;
+    }
+    __device__ Red2 emit(int x, int y, int z, const T s[3], const Prol& p) const {
+        const int i = d.idx32(x, y, z);
+        T mx = T(0);
+        bool bad = false;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            T mm = m[k * d.n + i], nn = nu[k * d.n + i];
+            const T cl = adam_component(ak, s[k], mm, nn, p.ic1, p.ic2, bad);
+            m[k * d.n + i] = mm;
+            nu[k * d.n + i] = nn;
+            step[k * d.n + i] = cl;
+            mx = fmax(mx, fabs(cl));
+        }
+        if (bad && st) st->bad_step = 1;
+        return {0.0, static_cast<double>(mx)};
+    }
+    __device__ void finish(int, double, double mx, const Prol& p) const {
+        if (maxstep) atomic_max_nonneg(maxstep + p.slot, mx);
+    }
+};
+
+// diffeo.cpp:60-62 + interp.cpp:269-289: u' = step + u(x+step) (clamp-to-edge
+// trilinear), sigma_warp smoothing, then W = M(x+u'), G = grad M(x+u')
+// (similarity.cpp:25-45) for the next loss evaluation.  The u gather reads
+// global memory (L1/L2), so any step cap is supported.
+template <class T, int R_>
+struct ComposeB {
+    using Acc = T;
+    using Raw = T;
+    using Prol = NoProl;
+    static constexpr int R = R_, C = 3, NR = 3, kStageBatch = 4;
+    static constexpr bool kSum = false, kMax = false;
+    const T* step;  // 3 planes
+    const T* u;     // 3 planes
+    GaussW<T> w;
+    T* uout;
+    const T* M;
+    Dims dm;
+    T* W;  // nullptr: no W / G
+    T* G;
+    LoopState* st;
+    int count_update;
+    Dims d;
+
+    __device__ bool skip() const {
+        if (!st) return false;
+        if (st->done) return true;
+        if (st->bad_step) {  // diffeo.cpp:52-53: throw before composing
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                st->err = 2;
+                st->done = 1;
+            }
+            return true;
+        }
+        return false;
+    }
+    __device__ void stage(int x, int y, int z, T v[3]) const {
+        const int i = d.idx32(x, y, z);
+        const T s0 = step[i], s1 = step[d.n + i], s2 = step[2 * d.n + i];
+        const Cell3<T> c = locate3<T>(d, x, y, z, s0, s1, s2);
+        T o[3];
+        lerp_field<T, false>(c, u, u + d.n, u + 2 * d.n, 3, o);
+        v[0] = s0 + o[0];
+        v[1] = s1 + o[1];
+        v[2] = s2 + o[2];
+    }
+    __device__ void xpass(const T* p, int cs, T v[3]) const { gauss_xpass<T, R>(w, p, cs, v); }
+    __device__ T wgt(int a, int j) const { return w.taps[a][j]; }
+    __device__ T nrm(int a, int i) const { return __ldg(w.norm[a] + i); }
+    __device__ Prol prologue() const { return {}; }
+    __device__ Red2 emit(int x, int y, int z, const T s[3], const Prol&) const {
+        const int i = d.idx32(x, y, z);
+        uout[i] = s[0];
+        uout[d.n + i] = s[1];
+        uout[2 * d.n + i] = s[2];
+        if (W) {
+            const Cell3<T> c = locate3<T>(dm, x, y, z, s[0], s[1], s[2]);
+            const Corners<T> k = fetch_corners<T>(M, c);
+            W[i] = lerp_value(c, k);
+            T gr[3];
+            lerp_grad(c, k, 3, gr);
+            G[i] = gr[0];
+            G[d.n + i] = gr[1];
+            G[2 * d.n + i] = gr[2];
+        }
+        return {0.0, 0.0};
+    }
+    __device__ void finish(int, double, double, const Prol&) const {
+        if (st && count_update) st->nupdates += 1;
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Persistent scale solver: one cooperative launch runs every iteration of a
+// (small) pyramid level.  Phases are the four brick ops over all bricks
+// (grid-stride), separated by grid-wide barriers; the convergence monitor is
+// evaluated redundantly by every CTA from the per-brick partials (same values,
+// same order -> the same decision everywhere), CTA 0 keeps the device log.
+// Replaces 4 kernel launches + 4 kernel boundaries per iteration by 4 grid
+// barriers.  pipeline.cpp:157-205 semantics: loss -> converged? -> smooth ->
+// Adam -> non-finite step check -> compose.
+template <class T, int R, int RG, int RW>
+struct PersistArgs {
+    LnccFwdB<T, R> fwd;
+    LnccBwdB<T, R> bwd;
+    SmoothAdamB<T, RG> sa;
+    ComposeB<T, RW> co;  // u -> uout in even iterations, swapped in odd ones
+    int iters;
+    LoopState* st;
+    double* loss;
+    unsigned long long* stamp;
+    int window;
+    double tol;
+};
+
+template <class T, int R, int RG, int RW>
+__global__ void __launch_bounds__(NTB, 1)
+    k_persist(const __grid_constant__ PersistArgs<T, R, RG, RW> a, const BG g, int nb) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ double s_red[32];
+    LoopState* st = a.st;
+    const double nvox = static_cast<double>(g.d.nx) * g.d.ny * g.d.nz;
+    int nupd = 0;
+    for (int it = 0; it < a.iters; ++it) {
+        // loss: fused LNCC forward over every brick
+        for (int b = blockIdx.x; b < nb; b += gridDim.x) brick_body(a.fwd, g, b, smem, s_red);
+        grid.sync();
+        double acc = 0.0;
+        for (int k = threadIdx.x; k < nb; k += NTB) acc += __ldcg(a.fwd.partials + k);
+        const double v = -bsum<NTB>(acc, s_red) / nvox;
+        // the monitor's decision (monitor_commit), taken identically by all CTAs
+        const int slot = it;
+        bool stop = !isfinite(v);
+        if (!stop && slot + 1 >= a.window + 1) {
+            const double prev = __ldcg(a.loss + slot - a.window);
+            const double den = fabs(prev) > 1e-30 ? fabs(prev) : 1e-30;
+            stop = ((prev - v) / static_cast<double>(a.window)) / den < a.tol;
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0)
+            monitor_commit(st, v, 0.0, 0.0, a.loss, a.stamp, a.window, a.tol);
+        if (stop) break;
+        for (int b = blockIdx.x; b < nb; b += gridDim.x) brick_body(a.bwd, g, b, smem, s_red);
+        grid.sync();  // also publishes CTA 0's st->t / st->slot to the Adam prologue
+        for (int b = blockIdx.x; b < nb; b += gridDim.x) brick_body(a.sa, g, b, smem, s_red);
+        grid.sync();
+        if (*reinterpret_cast<volatile int*>(&st->bad_step)) {  // diffeo.cpp:52-53
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                st->err = 2;
+                st->done = 1;
+            }
+            break;
+        }
+        ComposeB<T, RW> co = a.co;
+        if (it & 1) {
+            co.u = a.co.uout;
+            co.uout = const_cast<T*>(a.co.u);
+        }
+        for (int b = blockIdx.x; b < nb; b += gridDim.x) brick_body(co, g, b, smem, s_red);
+        ++nupd;
+        grid.sync();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->nupdates += nupd;
+}
+
+template <class T, int R, int RG, int RW>
+int run_persist(const Launch& L, const PersistArgs<T, R, RG, RW>& a, const Dims& d) {
+    using A = PersistArgs<T, R, RG, RW>;
+    constexpr size_t b1 = BrickLayout<decltype(A::fwd)>::bytes;
+    constexpr size_t b2 = BrickLayout<decltype(A::bwd)>::bytes;
+    constexpr size_t b3 = BrickLayout<decltype(A::sa)>::bytes;
+    constexpr size_t b4 = BrickLayout<decltype(A::co)>::bytes;
+    constexpr size_t m12 = b1 > b2 ? b1 : b2, m34 = b3 > b4 ? b3 : b4;
+    constexpr size_t bytes = m12 > m34 ? m12 : m34;
+    if constexpr (bytes > kBrickSmemMax) {
+        return -2;
+    } else {
+        static std::once_flag once;
+        static int per_sm = 0;
+        std::call_once(once, [] {
+            cudaFuncSetAttribute(k_persist<T, R, RG, RW>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(bytes));
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_persist<T, R, RG, RW>,
+                                                              NTB, bytes) != cudaSuccess)
+                per_sm = 0;
+        });
+        if (per_sm < 1) return -3;
+        BG g;
+        g.d = d;
+        g.nbx = (d.nx + BX - 1) / BX;
+        g.nby = (d.ny + BY - 1) / BY;
+        int nb = g.nbx * g.nby * ((d.nz + BZ - 1) / BZ);
+        const int cap = per_sm * (L.num_sms > 0 ? L.num_sms : 148);
+        const int grid = nb < cap ? nb : cap;
+        void* args[] = {const_cast<A*>(&a), &g, &nb};
+        const cudaError_t e = cudaLaunchCooperativeKernel(
+            reinterpret_cast<const void*>(k_persist<T, R, RG, RW>), dim3(grid), dim3(NTB), args,
+            bytes, L.stream);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return -4;
+        }
+        L.bump();
+        return grid;
+    }
+}
+
+template <class Op>
+int run_brick(const Launch& L, const Op& op, const Dims& d) {
+    using Lay = BrickLayout<Op>;
+    if constexpr (Lay::bytes > kBrickSmemMax) {
+        return -2;  // e.g. fp64 with a large Gaussian radius: caller falls back
+    } else {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaFuncSetAttribute(k_brick<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(Lay::bytes));
+    });
+    BG g;
+    g.d = d;
+    g.nbx = (d.nx + BX - 1) / BX;
+    g.nby = (d.ny + BY - 1) / BY;
+    const int nb = g.nbx * g.nby * ((d.nz + BZ - 1) / BZ);
+    k_brick<Op><<<nb, NTB, Lay::bytes, L.stream>>>(op, g);
+    L.bump();
+    return nb;
+    }
+}
+
+template <int RLO, int RHI, class F>
+int with_rb(int R, F&& f) {
+    switch (R) {
+#define DFM_RB(r)                                                                   \
+    case r:                                                                         \
+        if constexpr (r >= RLO && r <= RHI) return f(std::integral_constant<int, r>{}); \
+        break;
+        DFM_RB(0) DFM_RB(1) DFM_RB(2) DFM_RB(3) DFM_RB(4) DFM_RB(5) DFM_RB(6)
+#undef DFM_RB
+    }
+    return -2;
+}
+
+}  // namespace
+
+bool brick_supported(Dims d, int esz, int lncc_r, int rg, int rw) {
+    // fp64 smoothing at radius 6 would need > 227 KB of shared memory
+    const int rg_max = esz == 8 ? kBrickGaussRMax - 1 : kBrickGaussRMax;
+    return d.ndim == 3 && d.nz > 1 && d.zoff == 0 && d.gnz == 0 && d.zb == 0 && d.ze == 0 &&
+           lncc_r >= 1 && lncc_r <= kBrickLnccRMax && rg >= 0 && rg <= rg_max &&
+           rw >= 0 && rw <= kBrickComposeRMax && d.n < (int64_t(1) << 31);
+}
+
+template <class T>
+int launch_lncc_fwd_brick(const Launch& L, int R, const T* F, const T* W, Dims d, T* coef,
+                          double* partials, const LoopState* st, const MonitorArgs* mon) {
+    return with_rb<1, kBrickLnccRMax>(R, [&](auto rc) {
+        using Op = LnccFwdB<T, decltype(rc)::value>;
+        Op op;
+        op.F = F;
+        op.W = W;
+        op.coef = coef;
+        op.partials = partials;
+        op.st = st;
+        op.mon = mon ? *mon : MonitorArgs{nullptr, nullptr, nullptr, 0, 0.0};
+        op.d = d;
+        return run_brick(L, op, d);
+    });
+}
+
+template <class T>
+int launch_lncc_bwd_brick(const Launch& L, int R, const T* coef, const T* F, const T* W,
+                          const T* G, Dims d, T* grad, const LoopState* st) {
+    return with_rb<1, kBrickLnccRMax>(R, [&](auto rc) {
+        using Op = LnccBwdB<T, decltype(rc)::value>;
+        Op op;
+        op.coef = coef;
+        op.F = F;
+        op.W = W;
+        op.G = G;
+        op.grad = grad;
+        op.m2n = -2.0 / static_cast<double>(d.n);
+        op.st = st;
+        op.d = d;
+        return run_brick(L, op, d);
+    });
+}
+
+template <class T>
+int launch_smooth_adam_brick(const Launch& L, int R, const GaussW<T>& w, const T* grad, T* m,
+                             T* nu, T* step, Dims d, AdamParams ap, LoopState* st,
+                             unsigned long long* maxstep) {
+    return with_rb<0, kBrickGaussRMax>(R, [&](auto rc) {
+        using Op = SmoothAdamB<T, decltype(rc)::value>;
+        Op op;
+        op.grad = grad;
+        op.w = w;
+        op.m = m;
+        op.nu = nu;
+        op.step = step;
+        op.ak = adam_k<T>(ap);
+        op.corr1 = ap.corr1;
+        op.corr2 = ap.corr2;
+        op.st = st;
+        op.maxstep = maxstep;
+        op.d = d;
+        return run_brick(L, op, d);
+    });
+}
+
+template <class T>
+int launch_compose_brick(const Launch& L, int R, const GaussW<T>& w, const T* step,
+                         const T* uin, T* uout, const T* M, Dims dm, Dims d, T* W, T* G,
+                         LoopState* st, bool count_update) {
+    return with_rb<0, kBrickComposeRMax>(R, [&](auto rc) {
+        using Op = ComposeB<T, decltype(rc)::value>;
+        Op op;
+        op.step = step;
+        op.u = uin;
+        op.w = w;
+        op.uout = uout;
+        op.M = M;
+        op.dm = dm;
+        op.W = W;
+        op.G = G;
+        op.st = st;
+        op.count_update = count_update ? 1 : 0;
+        op.d = d;
+        return run_brick(L, op, d);
+    });
+}
+
+// instantiated radius triples of the persistent solver (LNCC r, sigma_grad
+// radius, sigma_warp radius): BASELINE's kernel 5 / 7 with sigma 1.0 / 0.5
+template <class T>
+int launch_persist_scale(const Launch& L, const PersistScale<T>& p) {
+    auto go = [&](auto rr) -> int {
+        constexpr int R = decltype(rr)::value;
+        PersistArgs<T, R, 3, 2> a;
+        a.fwd.F = p.F;
+        a.fwd.W = p.W;
+        a.fwd.coef = p.coef;
+        a.fwd.partials = p.partials;
+        a.fwd.st = p.st;
+        a.fwd.mon = MonitorArgs{nullptr, nullptr, nullptr, 0, 0.0};
+        a.fwd.d = p.d;
+        a.bwd.coef = p.coef;
+        a.bwd.F = p.F;
+        a.bwd.W = p.W;
+        a.bwd.G = p.G;
+        a.bwd.grad = p.grad;
+        a.bwd.m2n = -2.0 / static_cast<double>(p.d.n);
+        a.bwd.st = p.st;
+        a.bwd.d = p.d;
+        a.sa.grad = p.grad;
+        a.sa.w = p.wg;
+        a.sa.m = p.m;
+        a.sa.nu = p.nu;
+        a.sa.step = p.step;
+        a.sa.ak = adam_k<T>(p.ap);
+        a.sa.corr1 = p.ap.corr1;
+        a.sa.corr2 = p.ap.corr2;
+        a.sa.st = p.st;
+        a.sa.maxstep = p.maxstep;
+        a.sa.d = p.d;
+        a.co.step = p.step;
+        a.co.u = p.u0;
+        a.co.w = p.ww;
+        a.co.uout = p.u1;
+        a.co.M = p.M;
+        a.co.dm = p.d;
+        a.co.W = p.W;
+        a.co.G = p.G;
+        a.co.st = p.st;
+        a.co.count_update = 0;
+        a.co.d = p.d;
+        a.iters = p.iters;
+        a.st = p.st;
+        a.loss = p.loss;
+        a.stamp = p.stamp;
+        a.window = p.window;
+        a.tol = p.tol;
+        return run_persist(L, a, p.d);
+    };
+    if (p.rg != 3 || p.rw != 2) return -2;
+    switch (p.lncc_r) {
+        case 1: return go(std::integral_constant<int, 1>{});
+        case 2: return go(std::integral_constant<int, 2>{});
+        case 3: return go(std::integral_constant<int, 3>{});
+    }
+    return -2;
+}
+
+#define DFM_INST_BRICK(T)                                                                      \
+    template int launch_lncc_fwd_brick<T>(const Launch&, int, const T*, const T*, Dims, T*,    \
+                                          double*, const LoopState*, const MonitorArgs*);      \
+    template int launch_lncc_bwd_brick<T>(const Launch&, int, const T*, const T*, const T*,    \
+                                          const T*, Dims, T*, const LoopState*);               \
+    template int launch_smooth_adam_brick<T>(const Launch&, int, const GaussW<T>&, const T*,   \
+                                             T*, T*, T*, Dims, AdamParams, LoopState*,         \
+                                             unsigned long long*);                             \
+    template int launch_compose_brick<T>(const Launch&, int, const GaussW<T>&, const T*,       \
+                                         const T*, T*, const T*, Dims, Dims, T*, T*,           \
+                                         LoopState*, bool);                                    \
+    template int launch_persist_scale<T>(const Launch&, const PersistScale<T>&);
+
+DFM_INST_BRICK(float)
+DFM_INST_BRICK(double)
+
+}  // namespace dfm

@@ -23,6 +23,7 @@
 
 #include "dfm_device.cuh"
 #include "dfm_kernels.cuh"
+#include "loop_ops.cuh"
 #include "tma_util.cuh"
 
 namespace dfm {
@@ -31,52 +32,31 @@ namespace {
 
 constexpr int TX = kTX, TY = kTY, NT = TX * TY;
 
+// TMA ring depths (planes in flight per CTA); overridable for tuning builds
+#ifndef DFM_S_FWD
+#define DFM_S_FWD 4
+#endif
+#ifndef DFM_S_BWD
+#define DFM_S_BWD 4
+#endif
+#ifndef DFM_S_SA
+#define DFM_S_SA 4
+#endif
+#ifndef DFM_S_CO_EXTRA
+#define DFM_S_CO_EXTRA 0
+#endif
+
 template <class T>
 constexpr int round_bx(int w) {
     return (w + (16 / int(sizeof(T))) - 1) / (16 / int(sizeof(T))) * (16 / int(sizeof(T)));
 }
 constexpr int align128(int b) { return (b + 127) / 128 * 128; }
 
-struct Red2 {
-    double sum;
-    double mx;
-};
-
 struct ZG2 {
     Dims d;
     int zchunk;
     int tiles_x;
 };
-
-template <int NTH>
-__device__ double bsum(double v, double* sh) {
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    if (l == 0) sh[w] = v;
-    __syncthreads();
-    v = 0.0;
-    if (w == 0) {
-        v = l < NTH / 32 ? sh[l] : 0.0;
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    }
-    __syncthreads();
-    return v;
-}
-
-template <int NTH>
-__device__ double bmax(double v, double* sh) {
-    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    if (l == 0) sh[w] = v;
-    __syncthreads();
-    v = 0.0;
-    if (w == 0) {
-        v = l < NTH / 32 ? sh[l] : 0.0;
-        for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
-    }
-    __syncthreads();
-    return v;
-}
 
 // ---------------------------------------------------------------------------
 // the streaming z-march driver.  A CTA is TX x Op::TYv threads, one output
@@ -242,27 +222,9 @@ __global__ void __launch_bounds__(TX * Op::TYv) k_zm2(const __grid_constant__ Op
         const double bm = Op::kMax ? bmax<NTh>(rmax, s_red) : 0.0;
         if (tid == 0) op.finish(blk, bs, bm, pr);
         if constexpr (Op::kSum) {
-            if (op.mon.st) {  // fused convergence monitor: the last CTA reduces
-                __shared__ int s_last;
-                if (tid == 0) {
-                    __threadfence();
-                    const int nb = gridDim.x * gridDim.y;
-                    s_last = atomicAdd(&op.mon.st->arrive, 1u) == static_cast<unsigned>(nb - 1);
-                }
-                __syncthreads();
-                if (s_last) {
-                    __threadfence();
-                    const int nb = gridDim.x * gridDim.y;
-                    double acc = 0.0;
-                    for (int k = tid; k < nb; k += NTh) acc += __ldcg(op.partials + k);
-                    const double tot = bsum<NTh>(acc, s_red);
-                    if (tid == 0) {
-                        op.mon.st->arrive = 0;
-                        monitor_commit(op.mon.st, -tot / (static_cast<double>(d.nx) * d.ny * d.gz()), 0.0, 0.0,
-                                       op.mon.loss, op.mon.stamp, op.mon.window, op.mon.tol);
-                    }
-                }
-            }
+            if (op.mon.st)  // fused convergence monitor: the last CTA reduces
+                monitor_tail<NTh>(op.mon, op.partials, gridDim.x * gridDim.y,
+                                  static_cast<double>(d.nx) * d.ny * d.gz(), s_red);
         }
     } else {
         if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0) op.finish(0, 0.0, 0.0, pr);
@@ -271,17 +233,6 @@ __global__ void __launch_bounds__(TX * Op::TYv) k_zm2(const __grid_constant__ Op
 
 // ---------------------------------------------------------------------------
 // ops
-
-// Adam division / square root: fp32 uses the MUFU approximations (<= 2 ulp;
-// the fp32 path is held to 1e-5 relative), fp64 the IEEE operations.
-__device__ __forceinline__ float adam_div(float a, float b) { return __fdividef(a, b); }
-__device__ __forceinline__ double adam_div(double a, double b) { return a / b; }
-__device__ __forceinline__ float adam_sqrt(float a) {
-    float r;
-    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(a));
-    return r;
-}
-__device__ __forceinline__ double adam_sqrt(double a) { return sqrt(a); }
 
 struct NoCenter {};
 struct NoProl {};
@@ -294,7 +245,7 @@ struct LnccFwd2 {
     using Center = NoCenter;
     using Prol = NoProl;
     using Carry = NoCarry;
-    static constexpr int R = R_, C = 5, BACK = 0, AHEAD = 0, S = 4, TYv = TY_;
+    static constexpr int R = R_, C = 5, BACK = 0, AHEAD = 0, S = DFM_S_FWD, TYv = TY_;
     static constexpr bool kStaged = false, kSum = true, kMax = false;
     static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TYv + 2 * R;
     static constexpr int kBytes = BX * BY * int(sizeof(T));
@@ -342,36 +293,18 @@ struct LnccFwd2 {
     __device__ void load_center(int, int, int, Center&) const {}
     __device__ Red2 emit(int x, int y, int z, const double s[5], const Center&, const Prol&,
                          Carry&) const {
-        // similarity.cpp:145-162 with 2 divisions instead of 12: 1/n, 1/(vF vW)
+        // similarity.cpp:145-162 (loop_ops.cuh)
         const double n = static_cast<double>(box_len(x, d.nx, R) * box_len(y, d.ny, R) *
                                              (d.gz() > 1 ? box_len(z + d.zoff, d.gz(), R) : 1));
-        const double inv_n = 1.0 / n;
-        const double muF = s[0] * inv_n;
-        const double muW = s[1] * inv_n;
-        double vF = s[2] * inv_n - muF * muF;
-        double vW = s[3] * inv_n - muW * muW;
-        vF = vF < 0.0 ? 0.0 : vF;
-        vW = vW < 0.0 ? 0.0 : vW;
-        const double cv = s[4] * inv_n - muF * muW;
-        double cc2 = 0.0, an = 0.0, amu = 0.0, bn = 0.0, bmu = 0.0;
-        if (!(vF < 1e-5 || vW < 1e-5)) {
-            const double inv_den = 1.0 / (vF * vW);
-            const double alpha = cv * inv_den;         // cv / (vF vW)
-            cc2 = alpha * cv;                          // cv^2 / (vF vW)
-            const double beta = cc2 * vF * inv_den;    // cv^2 / (vF vW^2)
-            an = alpha * inv_n;
-            amu = an * muF;
-            bn = beta * inv_n;
-            bmu = bn * muW;
-        }
+        const LnccCoef k = lncc_coef(s, n);
         if (coef) {
             const int64_t i = d.idx32(x, y, z);
-            coef[i] = static_cast<T>(an);
-            coef[d.n + i] = static_cast<T>(amu);
-            coef[2 * d.n + i] = static_cast<T>(bn);
-            coef[3 * d.n + i] = static_cast<T>(bmu);
+            coef[i] = static_cast<T>(k.an);
+            coef[d.n + i] = static_cast<T>(k.amu);
+            coef[2 * d.n + i] = static_cast<T>(k.bn);
+            coef[3 * d.n + i] = static_cast<T>(k.bmu);
         }
-        return {cc2, 0.0};
+        return {k.cc2, 0.0};
     }
     __device__ void flush(Carry&) const {}
     __device__ void finish(int blk, double s, double, const Prol&) const { partials[blk] = s; }
@@ -383,7 +316,7 @@ struct LnccBwd2 {
     using Acc = double;
     using Prol = NoProl;
     using Carry = NoCarry;
-    static constexpr int R = R_, C = 4, BACK = 0, AHEAD = 0, S = 4, TYv = TY_;
+    static constexpr int R = R_, C = 4, BACK = 0, AHEAD = 0, S = DFM_S_BWD, TYv = TY_;
     static constexpr bool kStaged = false, kSum = false, kMax = false;
     static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TYv + 2 * R;
     static constexpr int kBytes = BX * BY * int(sizeof(T));
@@ -434,7 +367,7 @@ struct LnccBwd2 {
                          Carry&) const {
         const int64_t i = d.idx32(x, y, z);
         const double f = static_cast<double>(c.f), w = static_cast<double>(c.w);
-        const double dW = m2n * (f * s[0] - s[1] - w * s[2] + s[3]);
+        const double dW = lncc_dw(m2n, f, w, s);
         grad[i] = static_cast<T>(dW * static_cast<double>(c.g0));
         grad[d.n + i] = static_cast<T>(dW * static_cast<double>(c.g1));
         grad[2 * d.n + i] = static_cast<T>(dW * static_cast<double>(c.g2));
@@ -449,7 +382,7 @@ template <class T, int R_, int TY_ = 16>
 struct SmoothAdam2 {
     using Acc = T;
     using Carry = NoCarry;
-    static constexpr int R = R_, C = 3, BACK = 0, AHEAD = 0, S = 4, TYv = TY_;
+    static constexpr int R = R_, C = 3, BACK = 0, AHEAD = 0, S = DFM_S_SA, TYv = TY_;
     static constexpr bool kStaged = false, kSum = false, kMax = true;
     static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TYv + 2 * R;
     static constexpr int kBytes = BX * BY * int(sizeof(T));
@@ -460,7 +393,7 @@ struct SmoothAdam2 {
     T* m;   // 3 planes
     T* nu;  // 3 planes
     T* step;
-    T b1, omb1, b2, omb2, eps, eta, cap;
+    AdamK<T> ak;
     const double* corr1;
     const double* corr2;
     LoopState* st;
@@ -523,16 +456,10 @@ struct SmoothAdam2 {
                 step[k * d.n + i] = T(0);
                 continue;
             }
-            const T v = -s[k];
-            const T mm = b1 * c.m[k] + omb1 * v;
-            const T nn = b2 * c.nu[k] + omb2 * v * v;
+            T mm = c.m[k], nn = c.nu[k];
+            const T cl = adam_component(ak, s[k], mm, nn, p.ic1, p.ic2, bad);
             m[k * d.n + i] = mm;
             nu[k * d.n + i] = nn;
-            // dir = (m/c1) / (sqrt(nu/c2) + eps)
-            const T dir = adam_div(mm * p.ic1, adam_sqrt(nn * p.ic2) + eps);
-            const T sv = eta * dir;
-            bad |= !isfinite(sv);
-            const T cl = fmin(fmax(sv, -cap), cap);
             step[k * d.n + i] = cl;
             mx = fmax(mx, fabs(cl));
         }
@@ -554,7 +481,8 @@ struct Compose2 {
     using Acc = T;
     using Center = NoCenter;
     using Prol = NoProl;
-    static constexpr int R = R_, C = 3, BACK = CAPH, AHEAD = CAPH, S = 2 * CAPH + 2, TYv = TY_;
+    static constexpr int R = R_, C = 3, BACK = CAPH, AHEAD = CAPH,
+                         S = 2 * CAPH + 2 + DFM_S_CO_EXTRA, TYv = TY_;
     static constexpr bool kStaged = true, kSum = false, kMax = false;
     static constexpr int HU = R + CAPH;  // u halo: Gaussian radius + gather reach
     static constexpr int XAS = round_bx<T>(R), BXS = round_bx<T>(TX + XAS + R), BYS = TYv + 2 * R;
@@ -938,13 +866,7 @@ int launch_smooth_adam_tma(const Launch& L, int R, const GaussW<T>& w, const T* 
         op.m = m;
         op.nu = nu;
         op.step = step;
-        op.b1 = T(ap.b1);
-        op.omb1 = T(1.0 - ap.b1);
-        op.b2 = T(ap.b2);
-        op.omb2 = T(1.0 - ap.b2);
-        op.eps = T(ap.eps);
-        op.eta = T(ap.eta);
-        op.cap = T(ap.cap);
+        op.ak = adam_k<T>(ap);
         op.corr1 = ap.corr1;
         op.corr2 = ap.corr2;
         op.st = st;

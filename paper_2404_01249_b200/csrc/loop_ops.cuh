@@ -1,0 +1,150 @@
+// loop_ops.cuh — per-voxel math of the hot loop shared by the plane-streaming
+// (kernels_tma.cu) and brick (kernels_brick.cu) kernel families, plus the
+// CTA reductions and the fused convergence-monitor tail.  Keeping one copy of
+// the arithmetic means both tilings compute identical values per voxel.
+#pragma once
+
+#include <cstdint>
+
+#include "dfm_device.cuh"
+#include "dfm_kernels.cuh"
+
+namespace dfm {
+
+struct Red2 {
+    double sum;
+    double mx;
+};
+
+// ---------------------------------------------------------------------------
+// CTA reductions (fixed order: warp shuffles, then warp 0 over the warp sums)
+template <int NTH>
+__device__ double bsum(double v, double* sh) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    v = 0.0;
+    if (w == 0) {
+        v = l < NTH / 32 ? sh[l] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    }
+    __syncthreads();
+    return v;
+}
+
+template <int NTH>
+__device__ double bmax(double v, double* sh) {
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    v = 0.0;
+    if (w == 0) {
+        v = l < NTH / 32 ? sh[l] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
+    }
+    __syncthreads();
+    return v;
+}
+
+// Fused loss + convergence monitor tail: every CTA has written its partial;
+// the last CTA to arrive sums all partials in fixed order (deterministic) and
+// runs monitor_commit (pipeline.cpp:157-179).  nvox = global voxel count.
+template <int NTH>
+__device__ void monitor_tail(const MonitorArgs& mon, const double* partials, int nb, double nvox,
+                             double* s_red) {
+    __shared__ int s_last;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&mon.st->arrive, 1u) == static_cast<unsigned>(nb - 1);
+    }
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        double acc = 0.0;
+        for (int k = threadIdx.x; k < nb; k += NTH) acc += __ldcg(partials + k);
+        const double tot = bsum<NTH>(acc, s_red);
+        if (threadIdx.x == 0) {
+            mon.st->arrive = 0;
+            monitor_commit(mon.st, -tot / nvox, 0.0, 0.0, mon.loss, mon.stamp, mon.window,
+                           mon.tol);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// LNCC window coefficients from the five box moments s = (ΣF, ΣW, ΣF², ΣW², ΣFW)
+// over a clipped window of n voxels (similarity.cpp:145-162), with 2 divisions
+// instead of 12: 1/n and 1/(vF vW).  Returns cc² (the loss term).
+struct LnccCoef {
+    double cc2, an, amu, bn, bmu;
+};
+
+__device__ __forceinline__ LnccCoef lncc_coef(const double s[5], double n) {
+    LnccCoef r{0.0, 0.0, 0.0, 0.0, 0.0};
+    const double inv_n = 1.0 / n;
+    const double muF = s[0] * inv_n;
+    const double muW = s[1] * inv_n;
+    double vF = s[2] * inv_n - muF * muF;
+    double vW = s[3] * inv_n - muW * muW;
+    vF = vF < 0.0 ? 0.0 : vF;
+    vW = vW < 0.0 ? 0.0 : vW;
+    const double cv = s[4] * inv_n - muF * muW;
+    if (!(vF < 1e-5 || vW < 1e-5)) {  // similarity.cpp:13, 151-154
+        const double inv_den = 1.0 / (vF * vW);
+        const double alpha = cv * inv_den;       // cv / (vF vW)
+        r.cc2 = alpha * cv;                      // cv^2 / (vF vW)
+        const double beta = r.cc2 * vF * inv_den;  // cv^2 / (vF vW^2)
+        r.an = alpha * inv_n;
+        r.amu = r.an * muF;
+        r.bn = beta * inv_n;
+        r.bmu = r.bn * muW;
+    }
+    return r;
+}
+
+// dL/dW at one voxel from the box sums of the 4 coefficients (similarity.cpp:182)
+__device__ __forceinline__ double lncc_dw(double m2n, double f, double w, const double s[4]) {
+    return m2n * (f * s[0] - s[1] - w * s[2] + s[3]);
+}
+
+// ---------------------------------------------------------------------------
+// Adam division / square root: fp32 uses the MUFU approximations (<= 2 ulp;
+// the fp32 path is held to 1e-5 relative), fp64 the IEEE operations.
+__device__ __forceinline__ float adam_div(float a, float b) { return __fdividef(a, b); }
+__device__ __forceinline__ double adam_div(double a, double b) { return a / b; }
+__device__ __forceinline__ float adam_sqrt(float a) {
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(a));
+    return r;
+}
+__device__ __forceinline__ double adam_sqrt(double a) { return sqrt(a); }
+
+// Adam constants of one launch (optim.cpp:22-42, diffeo.cpp:47-57)
+template <class T>
+struct AdamK {
+    T b1, omb1, b2, omb2, eps, eta, cap;
+};
+
+template <class T>
+inline AdamK<T> adam_k(const AdamParams& ap) {
+    return AdamK<T>{T(ap.b1), T(1.0 - ap.b1), T(ap.b2), T(1.0 - ap.b2),
+                    T(ap.eps), T(ap.eta),     T(ap.cap)};
+}
+
+// One component: v = -smoothed grad (diffeo.cpp:17-24); m, nu updated in
+// place; returns the capped step; sets bad on a non-finite step.
+template <class T>
+__device__ __forceinline__ T adam_component(const AdamK<T>& k, T g, T& m, T& nu, T ic1, T ic2,
+                                            bool& bad) {
+    const T v = -g;
+    m = k.b1 * m + k.omb1 * v;
+    nu = k.b2 * nu + k.omb2 * v * v;
+    const T dir = adam_div(m * ic1, adam_sqrt(nu * ic2) + k.eps);  // (m/c1)/(sqrt(nu/c2)+eps)
+    const T sv = k.eta * dir;
+    bad |= !isfinite(sv);
+    return fmin(fmax(sv, -k.cap), k.cap);
+}
+
+}  // namespace dfm

@@ -18,7 +18,8 @@ import numpy as np
 
 from . import _abi as A
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdifform_cuda.so")
+LIB_PATH = os.environ.get(  # DFM_LIB: an alternative build (tuning A/B only)
+    "DFM_LIB", os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdifform_cuda.so"))
 
 # every entry point include/difform_gpu.h declares (checked by tests/test_abi.py)
 EXPORTS = [
@@ -32,7 +33,12 @@ EXPORTS = [
     "dfm_eulerian_direction", "dfm_apply_update", "dfm_singularity_fraction", "dfm_register",
     "dfm_dev_register", "dfm_ctx_set_profiling", "dfm_ctx_kernel_times",
     "dfm_slab_bounds", "dfm_slab_halo", "dfm_slab_unique_id", "dfm_dev_register_slab",
+    "dfm_ctx_set_option",
 ]
+
+OPT_BRICK_MAX = 1
+OPT_FORCE_LEGACY = 2
+OPT_PERSIST = 3
 
 _lib: Optional[C.CDLL] = None
 
@@ -66,6 +72,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         lib.dfm_downsample_grid.restype = C.c_int
         lib.dfm_ctx_set_profiling.argtypes = [C.c_void_p, C.c_int]
         lib.dfm_ctx_set_profiling.restype = C.c_int
+        lib.dfm_ctx_set_option.argtypes = [C.c_void_p, C.c_int, C.c_int64]
+        lib.dfm_ctx_set_option.restype = C.c_int
         lib.dfm_ctx_kernel_times.argtypes = [C.c_void_p, C.POINTER(C.c_double),
                                              C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         lib.dfm_ctx_kernel_times.restype = C.c_int
@@ -138,6 +146,11 @@ class Context(A.HostAPI):
 
     def set_profiling(self, on: bool):
         self.t.check(self.lib.dfm_ctx_set_profiling(self.handle, int(on)), "set_profiling")
+
+    def set_option(self, key: int, value: int):
+        """dfm_ctx_set_option: OPT_BRICK_MAX (voxels) / OPT_FORCE_LEGACY (0|1)."""
+        self.t.check(self.lib.dfm_ctx_set_option(self.handle, int(key), int(value)),
+                     "set_option")
 
     def kernel_times(self) -> dict:
         ms = (C.c_double * A.NUM_KCLASS)()

@@ -1,0 +1,26 @@
+"""Builds a tuning variant of the library with extra nvcc -D flags:
+    python tools/build_variant.py NAME -DDFM_S_FWD=6 ...
+-> build/variants/libdifform_NAME.so (load it with DFM_LIB=<path>)."""
+import os, subprocess, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2404_01249_b200 import build as B
+
+name, defs = sys.argv[1], sys.argv[2:]
+out = os.path.join(B.ROOT, "build", "variants", name)
+os.makedirs(out, exist_ok=True)
+B.build(verbose=False)
+objs = []
+for f in sorted(os.listdir(B.CSRC)):
+    if not f.endswith(".cu"):
+        continue
+    src = os.path.join(B.CSRC, f)
+    if f == "kernels_tma.cu":
+        obj = os.path.join(out, f.replace(".cu", ".o"))
+        subprocess.run([B.NVCC] + B.ARCH + B.FLAGS + defs + ["-c", src, "-o", obj], check=True)
+    else:
+        obj = os.path.join(B.OBJ, f.replace(".cu", ".o"))
+    objs.append(obj)
+lib = os.path.join(B.ROOT, "build", "variants", f"libdifform_{name}.so")
+subprocess.run([B.NVCC] + B.ARCH + ["-shared", "-cudart", "static", "-o", lib] + objs +
+               ["-Xlinker", "--exclude-libs,ALL", "-lrt", "-ldl", "-lpthread"], check=True)
+print(lib)
