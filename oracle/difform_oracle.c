@@ -226,6 +226,125 @@ int orc_compose(const dfm_grid* g, const double* phi, const double* psi, double*
     return 0;
 }
 
+/* ---------------------------------------------------------------------- */
+/* SVF: diffeo.cpp:66-167                                                   */
+
+/* diffeo.cpp:66-77: u = v / 2^M, then M self-compositions */
+static void exp_map_raw(const dfm_grid* g, const double* v, int M, double* u, double* tmp) {
+    const int64_t nd = nvox(g) * g->ndim;
+    const double scale = ldexp(1.0, -M);
+    for (int64_t i = 0; i < nd; ++i) u[i] = v[i] * scale;
+    for (int k = 0; k < M; ++k) {
+        compose_raw(g, u, u, tmp);
+        memcpy(u, tmp, (size_t)nd * sizeof(double));
+    }
+}
+
+int orc_exp_map(const dfm_grid* g, const double* v, int M, double* out) {
+    if (M < 0) return fail(1, "exp_map: M must be >= 0");
+    CHECK(orc_validate_grid(g));
+    double* tmp = dalloc(nvox(g) * g->ndim);
+    exp_map_raw(g, v, M, out, tmp);
+    free(tmp);
+    return 0;
+}
+
+/* interp.cpp:205-227 sample_field_jacobian: J[comp][a] over the cell corners
+ * in (cz, cy, cx) order, zero on flat or clamped axes */
+static void sample_field_jacobian(const dfm_grid* m, const double* f, const double p[3],
+                                  double J[3][3]) {
+    const cell_t c = locate(m, p);
+    const int d = m->ndim;
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) J[a][b] = 0.0;
+    for (int a = 0; a < d; ++a) {
+        if (m->dims[a] == 1 || c.clamped[a]) continue;
+        for (int cz = 0; cz < nzc(m); ++cz)
+            for (int cy = 0; cy < 2; ++cy)
+                for (int cx = 0; cx < 2; ++cx) {
+                    const int k[3] = {cx, cy, cz};
+                    const double sgn = k[a] ? 1.0 : -1.0;
+                    const double w = sgn * corner_w(&c, cx, cy, cz, a);
+                    const int64_t j = corner_index(m, &c, cx, cy, cz);
+                    for (int comp = 0; comp < d; ++comp) J[comp][a] += w * f[j * d + comp];
+                }
+    }
+}
+
+/* diffeo.cpp:79-167: discrete adjoint of exp_map.  Per level (reverse order):
+ * wn = w + J(u_k)(x+u_k)^T w (voxel-parallel in the reference), then the
+ * serial scatter of the lerp weights of every voxel's sample onto its cell
+ * corners, in voxel order; finally w * 2^-M. */
+int orc_svf_pullback(const dfm_grid* g, const double* v, const double* grad_phi, int M,
+                     double* out) {
+    if (M < 0) return fail(1, "svf_pullback: M must be >= 0");
+    CHECK(orc_validate_grid(g));
+    const int d = g->ndim;
+    const int64_t n = nvox(g), nd = n * d;
+    const double scale = ldexp(1.0, -M);
+    double* levels = dalloc(nd * (M + 1));
+    for (int64_t i = 0; i < nd; ++i) levels[i] = v[i] * scale;
+    for (int k = 0; k < M; ++k) compose_raw(g, levels + k * nd, levels + k * nd, levels + (k + 1) * nd);
+    double* w = dalloc(nd);
+    double* wn = dalloc(nd);
+    double* pts = dalloc(n * 3);
+    memcpy(w, grad_phi, (size_t)nd * sizeof(double));
+    const int nz = (d == 3) ? 2 : 1;
+    for (int k = M - 1; k >= 0; --k) {
+        const double* uk = levels + k * nd;
+        memcpy(wn, w, (size_t)nd * sizeof(double));
+        for (int64_t i = 0; i < n; ++i) {
+            double* p = pts + 3 * i;
+            voxel_xyz(g, i, p);
+            for (int c = 0; c < d; ++c) p[c] += uk[i * d + c];
+            double J[3][3];
+            sample_field_jacobian(g, uk, p, J);
+            const double* wi = w + i * d;
+            double* wo = wn + i * d;
+            for (int a = 0; a < d; ++a) {
+                double acc = 0.0;
+                for (int comp = 0; comp < d; ++comp) acc += J[comp][a] * wi[comp];
+                wo[a] += acc;
+            }
+        }
+        for (int64_t i = 0; i < n; ++i) {
+            const double* p = pts + 3 * i;
+            int64_t i0[3] = {0, 0, 0};
+            double f[3] = {0.0, 0.0, 0.0};
+            for (int a = 0; a < 3; ++a) {
+                if (a >= d || g->dims[a] == 1) continue;
+                double pc = p[a];
+                const double hi = (double)(g->dims[a] - 1);
+                if (pc < 0.0) pc = 0.0;
+                if (hi < pc) pc = hi;
+                int64_t q = (int64_t)floor(pc);
+                if (q < 0) q = 0;
+                if (g->dims[a] - 2 < q) q = g->dims[a] - 2;
+                i0[a] = q;
+                f[a] = pc - (double)q;
+            }
+            const double* wi = w + i * d;
+            for (int cz = 0; cz < nz; ++cz)
+                for (int cy = 0; cy < 2; ++cy)
+                    for (int cx = 0; cx < 2; ++cx) {
+                        const double wt = (cx ? f[0] : 1.0 - f[0]) * (cy ? f[1] : 1.0 - f[1]) *
+                                          ((nz == 2) ? (cz ? f[2] : 1.0 - f[2]) : 1.0);
+                        if (wt == 0.0) continue;
+                        const int64_t zz = (nz == 2) ? i0[2] + cz : 0;
+                        const int64_t idx = (zz * g->dims[1] + (i0[1] + cy)) * g->dims[0] + i0[0] + cx;
+                        for (int c = 0; c < d; ++c) wn[idx * d + c] += wt * wi[c];
+                    }
+        }
+        memcpy(w, wn, (size_t)nd * sizeof(double));
+    }
+    for (int64_t i = 0; i < nd; ++i) out[i] = w[i] * scale;
+    free(levels);
+    free(w);
+    free(wn);
+    free(pts);
+    return 0;
+}
+
 /* interp.cpp:291-328: J = I + central differences (one-sided at borders),
  * row = component, column = axis. */
 static void jacobian_at(const dfm_grid* m, const double* phi, int64_t i, double J[9]) {
@@ -782,7 +901,7 @@ static int validate_config(const dfm_config* c) {
     if (c->conv_tol < 0.0) return fail(1, "config: conv_tol must be >= 0");
     if (c->mode == DFM_MODE_SVF && c->loss == DFM_LOSS_DICE)
         return fail(1, "config: dice loss is not available in svf mode");
-    if (c->mode != DFM_MODE_DIRECT) return fail(1, "register: only direct mode is on this path");
+    if (c->mode != DFM_MODE_DIRECT && c->mode != DFM_MODE_SVF) return fail(1, "config: unknown mode");
     return 0;
 }
 
@@ -877,6 +996,7 @@ int orc_register(const dfm_grid* g, const double* fixed, const double* moving,
     double* tmp = dalloc(nfull * d);
     double* tmp2 = dalloc(nfull * d);
     double* grad = dalloc(nfull * d);
+    double* phis = dalloc(nfull * d); /* exp(v) in svf mode */
     int64_t total_iters = 0;
     for (int i = 0; i < nscales; ++i) total_iters += iters[i];
     double* losses = dalloc(total_iters + 1);
@@ -907,7 +1027,12 @@ int orc_register(const dfm_grid* g, const double* fixed, const double* moving,
         for (int it = 0; it < iters[si]; ++it) {
             const double t_it = now_ms();
             double value;
-            if ((rc = eval_loss(&wg, f, mv, u, cfg, &value, grad))) break;
+            const double* phi = u;
+            if (cfg->mode == DFM_MODE_SVF) {  /* pipeline.cpp:166-167 */
+                exp_map_raw(&wg, u, cfg->svf_M, phis, tmp);
+                phi = phis;
+            }
+            if ((rc = eval_loss(&wg, f, mv, phi, cfg, &value, grad))) break;
             if (!isfinite(value)) {
                 rc = fail(2, "register_images: non-finite loss at scale %f, iteration %d",
                           scales[si], it);
@@ -920,6 +1045,29 @@ int orc_register(const dfm_grid* g, const double* fixed, const double* moving,
                 if (nrec < max_records) records[nrec] = rec;
                 ++nrec;
                 break;
+            }
+            if (cfg->mode == DFM_MODE_SVF) {  /* pipeline.cpp:189-206 */
+                if ((rc = orc_svf_pullback(&wg, u, grad, cfg->svf_M, tmp))) break;
+                if (cfg->sigma_grad > 0.0)
+                    for (int a = 0; a < d; ++a) smooth_axis(tmp, &wg, d, a, cfg->sigma_grad);
+                for (int64_t i = 0; i < n * d; ++i) tmp[i] = -tmp[i];
+                if ((rc = orc_adam_step(&wg, m, nu, &t_adam, cfg->beta1, cfg->beta2,
+                                        cfg->eps_adam, tmp, tmp2)))
+                    break;
+                double mx = 0.0;
+                for (int64_t i = 0; i < n * d; ++i) {
+                    const double sv = fabs(clampd(cfg->eta * tmp2[i], -cfg->step_cap, cfg->step_cap));
+                    mx = mx > sv ? mx : sv;
+                }
+                rec.max_step = mx;
+                for (int64_t i = 0; i < n * d; ++i)
+                    u[i] += clampd(cfg->eta * tmp2[i], -cfg->step_cap, cfg->step_cap);
+                if (cfg->sigma_warp > 0.0)
+                    for (int a = 0; a < d; ++a) smooth_axis(u, &wg, d, a, cfg->sigma_warp);
+                rec.wall_ms = now_ms() - t_it;
+                if (nrec < max_records) records[nrec] = rec;
+                ++nrec;
+                continue;
             }
             if (cfg->sigma_grad > 0.0) {
                 const double s3[3] = {cfg->sigma_grad, cfg->sigma_grad, cfg->sigma_grad};
@@ -949,6 +1097,10 @@ int orc_register(const dfm_grid* g, const double* fixed, const double* moving,
         if (!rc) memcpy(u, tmp, (size_t)(nfull * d) * sizeof(double));
     }
     double final_loss = 0.0, sing = 0.0;
+    if (!rc && cfg->mode == DFM_MODE_SVF) {  /* pipeline.cpp:214-215: phi = exp(v) */
+        exp_map_raw(g, u, cfg->svf_M, phis, tmp);
+        memcpy(u, phis, (size_t)(nfull * d) * sizeof(double));
+    }
     if (!rc) rc = eval_loss(g, fixed, moving, u, cfg, &final_loss, NULL);
     if (!rc) rc = orc_singularity_fraction(g, u, &sing);
     if (!rc) {
@@ -958,7 +1110,8 @@ int orc_register(const dfm_grid* g, const double* fixed, const double* moving,
         log->final_loss = final_loss;
         log->final_singularity_fraction = sing;
         log->total_ms = now_ms() - t0;
-        if (sing > 0.0) rc = fail(2, "register_images: folded warp (det J <= 0 somewhere)");
+        if (cfg->mode == DFM_MODE_DIRECT && sing > 0.0)
+            rc = fail(2, "register_images: folded warp (det J <= 0 somewhere)");
     }
     free(f);
     free(mv);
@@ -968,6 +1121,7 @@ int orc_register(const dfm_grid* g, const double* fixed, const double* moving,
     free(tmp);
     free(tmp2);
     free(grad);
+    free(phis);
     free(losses);
     return rc;
 }

@@ -61,6 +61,9 @@ int orc_eulerian_direction(const dfm_grid* g, const double* grad, const double* 
 int orc_apply_update(const dfm_grid* g, const double* phi, const double* v, double eta,
                      double sigma_warp, double cap, double* out);
 int orc_singularity_fraction(const dfm_grid* g, const double* phi, double* frac);
+int orc_exp_map(const dfm_grid* g, const double* v, int M, double* out);
+int orc_svf_pullback(const dfm_grid* g, const double* v, const double* grad_phi, int M,
+                     double* out);
 int orc_register(const dfm_grid* g, const double* fixed, const double* moving,
                  const dfm_config* cfg, const double* scales, const int32_t* iters,
                  int32_t nscales, const dfm_init* init, double* out_field,

@@ -165,6 +165,15 @@ int dfmref_compose(const dfm_grid* g, const double* phi, const double* psi, doub
     return guarded([&] { put(compose(to_field(g, phi), to_field(g, psi)).data, out); });
 }
 
+int dfmref_exp_map(const dfm_grid* g, const double* v, int M, double* out) {
+    return guarded([&] { put(exp_map(to_field(g, v), M).data, out); });
+}
+
+int dfmref_svf_pullback(const dfm_grid* g, const double* v, const double* grad_phi, int M,
+                        double* out) {
+    return guarded([&] { put(svf_pullback(to_field(g, v), to_field(g, grad_phi), M).data, out); });
+}
+
 int dfmref_jacobian_det(const dfm_grid* g, const double* phi, double* out) {
     return guarded([&] { put(jacobian_det(to_field(g, phi)).data, out); });
 }

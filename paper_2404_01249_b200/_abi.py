@@ -202,6 +202,8 @@ PROTOS = {
     "warp_image": [_G, _D, _D, _D],
     "warp_labels": [_G, _I, _D, _I],
     "compose": [_G, _D, _D, _D],
+    "exp_map": [_G, _D, C.c_int, _D],
+    "svf_pullback": [_G, _D, _D, C.c_int, _D],
     "jacobian_det": [_G, _D, _D],
     "gaussian_smooth": [_G, _D, _D, _D],
     "gaussian_smooth_field": [_G, _D, _D, _D],
@@ -329,6 +331,21 @@ class HostAPI:
         phi, psi = as_f64(phi, g.field_shape), as_f64(psi, g.field_shape)
         out = np.empty(g.field_shape)
         self.t.call("compose", C.byref(g.c()), _dptr(phi), _dptr(psi), _dptr(out))
+        return out
+
+    def exp_map(self, g, v, M):
+        """exp_map (diffeo.hpp:19-20, diffeo.cpp:66-77): scaling and squaring."""
+        v = as_f64(v, g.field_shape)
+        out = np.empty(g.field_shape)
+        self.t.call("exp_map", C.byref(g.c()), _dptr(v), int(M), _dptr(out))
+        return out
+
+    def svf_pullback(self, g, v, grad_phi, M):
+        """svf_pullback (diffeo.hpp:22-26, diffeo.cpp:79-167): adjoint of exp_map."""
+        v = as_f64(v, g.field_shape)
+        gp = as_f64(grad_phi, g.field_shape)
+        out = np.empty(g.field_shape)
+        self.t.call("svf_pullback", C.byref(g.c()), _dptr(v), _dptr(gp), int(M), _dptr(out))
         return out
 
     def jacobian_det(self, g, phi):

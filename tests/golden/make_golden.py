@@ -52,8 +52,48 @@ def ndimage_smooth(a):
     return ndimage.gaussian_filter(a, 1.0)
 
 
+SVF_MS = (0, 1, 4, 6)
+
+
+def svf_golden(ref):
+    """exp_map / svf_pullback (diffeo.cpp:66-167) and SVF-mode registrations."""
+    rng = np.random.default_rng(4321)
+    out = {}
+    for tag, g in (("3d", A.GridMeta.make_3d(13, 11, 9)), ("2d", A.GridMeta.make_2d(17, 12))):
+        v = f32(rng.normal(0, 1.5, g.field_shape))   # large enough to clamp at the faces
+        w = f32(rng.normal(0, 1.0, g.field_shape))
+        out[f"{tag}_dims"] = np.array(g.dims)
+        out[f"{tag}_ndim"] = np.array(g.ndim)
+        out[f"{tag}_v"] = v
+        out[f"{tag}_w"] = w
+        for M in SVF_MS:
+            out[f"{tag}_exp{M}"] = ref.exp_map(g, v, M)
+            out[f"{tag}_pull{M}"] = ref.svf_pullback(g, v, w, M)
+    np.savez_compressed(os.path.join(HERE, "svf.npz"), **out)
+    for loss, name in ((A.LOSS_LNCC, "svf_lncc"), (A.LOSS_SSD, "svf_ssd")):
+        p = synth.make_pair(0, seed=11, shape=(24, 24, 24), iters=(12, 8, 4))
+        cfg = synth.baseline_config(loss, 2, 1.0, max_iters=12)
+        cfg.mode = A.MODE_SVF
+        cfg.svf_M = 4
+        fld, log = ref.register_images(p.grid, p.fixed, p.moving, cfg, p.schedule)
+        np.savez_compressed(
+            os.path.join(HERE, f"register_{name}.npz"), fixed=p.fixed, moving=p.moving,
+            fixed_labels=p.fixed_labels, moving_labels=p.moving_labels,
+            dims=np.array(p.grid.dims), scales=np.array(p.schedule.scales),
+            iters=np.array(p.schedule.iterations), field=fld, mode=np.array(A.MODE_SVF),
+            svf_M=np.array(4), losses=np.array([r.loss for r in log.iterations]),
+            max_steps=np.array([r.max_step for r in log.iterations]),
+            scale_index=np.array([r.scale_index for r in log.iterations]),
+            final_loss=np.array(log.final_loss), sing=np.array(log.final_singularity_fraction))
+
+
 def main():
     ref = pyoracle.reference()
+    if "--only-svf" in sys.argv:
+        svf_golden(ref)
+        print("svf golden vectors written to", HERE)
+        return
+    svf_golden(ref)
     C = cases()
     for tag in ("3d", "2d"):
         c = C[tag]

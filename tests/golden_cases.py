@@ -96,3 +96,29 @@ def register_inputs(name):
     sched = A.PyramidSchedule(tuple(float(s) for s in z["scales"]),
                               tuple(int(i) for i in z["iters"]))
     return z, g, sched
+
+
+def register_config(name, z, sched):
+    """The RegistrationConfig a register_<name>.npz golden was made with."""
+    from paper_2404_01249_b200 import synth
+    loss = A.LOSS_LNCC if name.endswith("lncc") else A.LOSS_SSD
+    cfg = synth.baseline_config(loss, 2, 1.0, max_iters=max(sched.iterations))
+    if "mode" in z:
+        cfg.mode = int(z["mode"])
+        cfg.svf_M = int(z["svf_M"])
+    return cfg
+
+
+SVF_MS = (0, 1, 4, 6)
+
+
+def compute_svf(api, tag):
+    """exp_map / svf_pullback on the svf.npz inputs -> {key: (got, want)}."""
+    z = load("svf.npz")
+    g = A.GridMeta(int(z[f"{tag}_ndim"]), tuple(int(v) for v in z[f"{tag}_dims"]))
+    out = {}
+    for M in SVF_MS:
+        out[f"exp{M}"] = (api.exp_map(g, z[f"{tag}_v"], M), z[f"{tag}_exp{M}"])
+        out[f"pull{M}"] = (api.svf_pullback(g, z[f"{tag}_v"], z[f"{tag}_w"], M),
+                           z[f"{tag}_pull{M}"])
+    return out

@@ -39,6 +39,26 @@ def test_restatement_register_bitwise(oracle_port, name):
     assert log.final_loss == float(z["final_loss"])
 
 
+@pytest.mark.parametrize("tag", ["3d", "2d"])
+def test_restatement_svf_bitwise(oracle_port, tag):
+    """exp_map / svf_pullback (diffeo.cpp:66-167): scaling and squaring and its
+    discrete adjoint with the serial lerp-weight scatter, M in {0, 1, 4, 6}."""
+    for key, (got, want) in G.compute_svf(oracle_port, tag).items():
+        assert np.array_equal(got, want), key
+
+
+@pytest.mark.parametrize("name", ["svf_lncc", "svf_ssd"])
+def test_restatement_register_svf_bitwise(oracle_port, name):
+    """SVF mode of register_images (pipeline.cpp:166-167, 189-206, 213-215)."""
+    z, g, sched = G.register_inputs(name)
+    cfg = G.register_config(name, z, sched)
+    fld, log = oracle_port.register_images(g, z["fixed"], z["moving"], cfg, sched)
+    assert np.array_equal(fld, z["field"])
+    assert np.array_equal([r.loss for r in log.iterations], z["losses"])
+    assert np.array_equal([r.max_step for r in log.iterations], z["max_steps"])
+    assert log.final_loss == float(z["final_loss"])
+
+
 def test_restatement_early_stop_record_count(oracle_port):
     """test_pipeline.cpp:69-93 semantics: default window 10 on a self pair."""
     z = G.load("register_self.npz")
