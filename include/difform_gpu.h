@@ -82,7 +82,7 @@ typedef struct {
     double sigma_grad;
     double sigma_warp;
     int32_t use_jac;
-    int32_t mode;        /* dfm_mode; only DFM_MODE_DIRECT is on this path */
+    int32_t mode;        /* dfm_mode: direct (the hot path) or svf (exp_map + pullback) */
     int32_t svf_M;
     double beta1;
     double beta2;
@@ -166,6 +166,16 @@ DFM_API dfm_status dfm_warp_labels(dfm_ctx* ctx, const dfm_grid* g, const int32_
 /* compose (interp.hpp:35): out = u_psi + lerp(u_phi)(x + u_psi) */
 DFM_API dfm_status dfm_compose(dfm_ctx* ctx, const dfm_grid* g, const double* phi,
                        const double* psi, double* out);
+/* exp_map (diffeo.hpp:19-20, diffeo.cpp:66-77): v / 2^M, then M
+ * self-compositions.  M < 0 -> DFM_E_INVALID. */
+DFM_API dfm_status dfm_exp_map(dfm_ctx* ctx, const dfm_grid* g, const double* v, int M,
+                               double* out);
+/* svf_pullback (diffeo.hpp:22-26, diffeo.cpp:79-167): the discrete adjoint of
+ * exp_map applied to the cotangent grad_phi.  The reference's serial scatter
+ * is a stable-sorted gather on the device: same per-node summation order,
+ * bit-stable across runs.  Needs 8 * voxels < 2^31. */
+DFM_API dfm_status dfm_svf_pullback(dfm_ctx* ctx, const dfm_grid* g, const double* v,
+                                    const double* grad_phi, int M, double* out);
 /* jacobian_det (interp.hpp:50) */
 DFM_API dfm_status dfm_jacobian_det(dfm_ctx* ctx, const dfm_grid* g, const double* phi, double* out);
 /* gaussian_smooth / gaussian_smooth_field (interp.hpp:54-57) */

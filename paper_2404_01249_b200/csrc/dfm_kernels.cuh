@@ -255,6 +255,32 @@ struct PersistScale {
 template <class T>
 int launch_persist_scale(const Launch& L, const PersistScale<T>& p);
 
+// -------- SVF mode (kernels_svf.cu): exp_map and the deterministic
+// svf_pullback (stable-sorted gather in place of the reference's serial
+// scatter).  Fields are packed 3-plane bases; levels = (M+1) packed fields.
+template <class T>
+struct SvfWork {
+    T* wa;
+    T* wb;              // 3n each: cotangent ping-pong
+    int32_t* keys[2];   // 8n each
+    int32_t* vals[2];   // 8n each
+    int32_t* start;     // n+1
+    void* temp;
+    size_t temp_bytes;  // >= svf_sort_temp_bytes(n)
+};
+size_t svf_sort_temp_bytes(int64_t n);
+template <class T>
+void launch_exp_map(const Launch& L, const T* v, Dims d, int M, T* levels,
+                    const LoopState* st = nullptr);
+template <class T>
+void launch_svf_pullback(const Launch& L, const T* levels, Dims d, int M, const T* grad_phi,
+                         T* out, const SvfWork<T>& ws, const LoopState* st = nullptr);
+// SVF update (pipeline.cpp:199-205): out = G_sigma_warp * (v + step); skips
+// when the scale is done, counts the update (kernels_stencil.cu)
+template <class T>
+void launch_svf_update(const Launch& L, int R, const GaussW<T>& w, CPlanes3<T> v,
+                       CPlanes3<T> step, Planes3<T> out, Dims d, LoopState* st);
+
 // -------- loop control
 // kind: 0 ssd, 1 lncc, 2 dice (3 partial arrays of np each)
 void launch_monitor(const Launch& L, int kind, const double* partials, int np, double nvox,

@@ -699,6 +699,58 @@ dfm_status dfm_compose(dfm_ctx* ctx, const dfm_grid* g, const double* phi, const
     });
 }
 
+dfm_status dfm_exp_map(dfm_ctx* ctx, const dfm_grid* g, const double* v, int M, double* out) {
+    return guarded([&] {
+        if (M < 0) fail(DFM_E_INVALID, "exp_map: M must be >= 0");
+        validate_grid(g);
+        const Dims d = to_dims(g);
+        DFM_DISPATCH(ctx, {
+            Field<T> a = dev_field<T>(ctx, "api_f0", d.n);
+            upload_field<T>(ctx, v, d.n, d.ndim, a);
+            T* lev = ctx->arr<T>("api_svf_levels", 3 * d.n * (M + 1));
+            launch_exp_map<T>(ctx->L(), a.p[0], d, M, lev);
+            const T* r = lev + 3 * d.n * M;
+            download_field<T, double>(ctx, CPlanes3<T>{{r, r + d.n, r + 2 * d.n}}, d.n, d.ndim,
+                                      out);
+            ctx->sync();
+        });
+    });
+}
+
+dfm_status dfm_svf_pullback(dfm_ctx* ctx, const dfm_grid* g, const double* v,
+                            const double* grad_phi, int M, double* out) {
+    return guarded([&] {
+        if (M < 0) fail(DFM_E_INVALID, "svf_pullback: M must be >= 0");
+        validate_grid(g);
+        const Dims d = to_dims(g);
+        if (8 * d.n >= (int64_t(1) << 31))
+            fail(DFM_E_INVALID, "svf_pullback: volume too large (8 * voxels must be < 2^31)");
+        DFM_DISPATCH(ctx, {
+            Field<T> a = dev_field<T>(ctx, "api_f0", d.n);
+            Field<T> b = dev_field<T>(ctx, "api_f1", d.n);
+            Field<T> o = dev_field<T>(ctx, "api_f2", d.n);
+            upload_field<T>(ctx, v, d.n, d.ndim, a);
+            upload_field<T>(ctx, grad_phi, d.n, d.ndim, b);
+            T* lev = ctx->arr<T>("api_svf_levels", 3 * d.n * (M + 1));
+            launch_exp_map<T>(ctx->L(), a.p[0], d, M, lev);
+            SvfWork<T> ws{};
+            ws.wa = ctx->arr<T>("api_svf_wa", 3 * d.n);
+            ws.wb = ctx->arr<T>("api_svf_wb", 3 * d.n);
+            int32_t* kv = ctx->arr<int32_t>("api_svf_kv", 4 * 8 * d.n);
+            for (int k = 0; k < 2; ++k) {
+                ws.keys[k] = kv + (2 * k) * 8 * d.n;
+                ws.vals[k] = kv + (2 * k + 1) * 8 * d.n;
+            }
+            ws.start = ctx->arr<int32_t>("api_svf_start", d.n + 1);
+            ws.temp_bytes = svf_sort_temp_bytes(d.n);
+            ws.temp = ctx->get("api_svf_temp", ws.temp_bytes);
+            launch_svf_pullback<T>(ctx->L(), lev, d, M, b.p[0], o.p[0], ws);
+            download_field<T, double>(ctx, o.r(), d.n, d.ndim, out);
+            ctx->sync();
+        });
+    });
+}
+
 dfm_status dfm_jacobian_det(dfm_ctx* ctx, const dfm_grid* g, const double* phi, double* out) {
     return guarded([&] {
         validate_grid(g);
@@ -1031,8 +1083,7 @@ void validate_config(const dfm_config* c) {
     if (c->conv_tol < 0.0) fail(DFM_E_INVALID, "config: conv_tol must be >= 0");
     if (c->mode == DFM_MODE_SVF && c->loss == DFM_LOSS_DICE)
         fail(DFM_E_INVALID, "config: dice loss is not available in svf mode");
-    if (c->mode != DFM_MODE_DIRECT)
-        fail(DFM_E_INVALID, "register: svf mode is not on the device path (direct mode only)");
+    if (c->mode != DFM_MODE_DIRECT && c->mode != DFM_MODE_SVF) fail(DFM_E_INVALID, "config: unknown mode");
     if (c->loss < 0 || c->loss > 2) fail(DFM_E_INVALID, "unknown loss");
     if (c->loss == DFM_LOSS_LNCC && c->lncc_radius > kRMax)
         fail(DFM_E_INVALID, "lncc_radius > %d unsupported on the device path", kRMax);
@@ -1077,6 +1128,10 @@ struct Registrar {
     T* Gb = nullptr;  // grad M(x+u), 3 planes
     bool use_tma = false;    // fused W/G-carrying loop (plane-streaming and/or brick kernels)
     bool use_brick = false;  // this scale runs the brick kernels
+    // SVF mode (pipeline.cpp:166-167, 189-206): exp_map levels + pullback work
+    T* svf_levels = nullptr;
+    T* svf_g = nullptr;  // pulled-back gradient (3 planes)
+    SvfWork<T> svf{};
     // profiling
     std::vector<cudaEvent_t> evpool;
     std::vector<std::pair<int, int>> evuse;  // (class, pool index of start)
@@ -1095,6 +1150,23 @@ struct Registrar {
         for (int k = 0; k < 4; ++k) coef[k] = cb + k * n;
         Wb = ctx->arr<T>("reg_W", n);
         Gb = ctx->arr<T>("reg_G", 3 * n);
+        if (cfg->mode == DFM_MODE_SVF) {
+            if (8 * n >= (int64_t(1) << 31))
+                fail(DFM_E_INVALID, "svf mode: volume too large (8 * voxels must be < 2^31)");
+            const int M = cfg->svf_M;
+            svf_levels = ctx->arr<T>("svf_levels", 3 * n * (M + 1));
+            svf_g = ctx->arr<T>("svf_g", 3 * n);
+            svf.wa = ctx->arr<T>("svf_wa", 3 * n);
+            svf.wb = ctx->arr<T>("svf_wb", 3 * n);
+            int32_t* kv = ctx->arr<int32_t>("svf_kv", 4 * 8 * n);
+            for (int k = 0; k < 2; ++k) {
+                svf.keys[k] = kv + (2 * k) * 8 * n;
+                svf.vals[k] = kv + (2 * k + 1) * 8 * n;
+            }
+            svf.start = ctx->arr<int32_t>("svf_start", n + 1);
+            svf.temp_bytes = svf_sort_temp_bytes(n);
+            svf.temp = ctx->get("svf_temp", svf.temp_bytes);
+        }
         partials = ctx->arr<double>("reg_partials", 3 * 65536);
         st = ctx->arr<LoopState>("reg_state", 1);
         const int64_t cap = total_iters + 2;
@@ -1238,10 +1310,61 @@ struct Registrar {
         ev_end();
     }
 
+    // one SVF iteration (pipeline.cpp:166-167, 189-206), v = u[src] -> u[1-src]:
+    // phi = exp(v); loss + grad at phi; g = pullback; sigma_grad; -g; Adam;
+    // v' = G_sigma_warp * (v + clamp(eta dir))
+    void enqueue_iteration_svf(const Dims& d, int src, int Rg, int Rw, const GaussW<T>& wg,
+                               const GaussW<T>& ww, const DevAxisGauss* big_g,
+                               const DevAxisGauss* big_w) {
+        Launch L = ctx->L();
+        const int M = cfg->svf_M;
+        const int64_t n = d.n;
+        const int loss_kind = cfg->loss;
+        ev_begin(KC_FWD);
+        launch_exp_map<T>(L, u[src].p[0], d, M, svf_levels, st);
+        const T* ph = svf_levels + 3 * n * M;
+        const CPlanes3<T> phi{{ph, ph + n, ph + 2 * n}};
+        const int np = loss_kind_launch_fwd<T>(ctx, loss_kind, cfg->lncc_radius, Fs, Ms, d, d,
+                                               phi, coef, grad.w(), partials, st);
+        ev_end();
+        ev_begin(KC_MON);
+        launch_monitor(L, monitor_kind(loss_kind), partials, np, static_cast<double>(n), st,
+                       loss, stamp, cfg->conv_window, cfg->conv_tol);
+        ev_end();
+        if (loss_kind == DFM_LOSS_LNCC) {
+            const T* cc[4] = {coef[0], coef[1], coef[2], coef[3]};
+            ev_begin(KC_BWD);
+            launch_lncc_bwd<T>(L, cfg->lncc_radius, Fs, Ms, d, d, phi, cc, grad.w(), st);
+            ev_end();
+        }
+        ev_begin(KC_ADAM);
+        launch_svf_pullback<T>(L, svf_levels, d, M, grad.p[0], svf_g, svf, st);
+        const CPlanes3<T> g{{svf_g, svf_g + n, svf_g + 2 * n}};
+        if (big_g)
+            for (int c = 0; c < 3; ++c)
+                axis_smooth_plane<T>(ctx, d, *big_g, svf_g + c * n, svf_g + c * n, step.p[c], st);
+        AdamParams ap{cfg->beta1, cfg->beta2, cfg->eps_adam, cfg->eta, cfg->step_cap,
+                      corr1, corr2, 0};
+        launch_smooth_adam<T>(L, big_g ? 0 : Rg, wg, g, u[src].r(), m.w(), nu.w(), step.w(), d,
+                              ap, st, maxstep);
+        ev_end();
+        ev_begin(KC_COMPOSE);
+        launch_svf_update<T>(L, big_w ? 0 : Rw, ww, u[src].r(), step.r(), u[1 - src].w(), d, st);
+        if (big_w)
+            for (int c = 0; c < 3; ++c)
+                axis_smooth_plane<T>(ctx, d, *big_w, u[1 - src].p[c], u[1 - src].p[c], grad.p[c],
+                                     st);
+        ev_end();
+    }
+
     // one iteration of the hot loop on grid d, u[src] -> u[1-src]
     void enqueue_iteration(const Dims& d, int src, int Rg, int Rw, const GaussW<T>& wg,
                            const GaussW<T>& ww, const DevAxisGauss* big_g,
                            const DevAxisGauss* big_w) {
+        if (cfg->mode == DFM_MODE_SVF) {
+            enqueue_iteration_svf(d, src, Rg, Rw, wg, ww, big_g, big_w);
+            return;
+        }
         if (use_tma) {
             enqueue_iteration_tma(d, src, Rg, Rw, wg, ww);
             return;
@@ -1334,6 +1457,13 @@ struct Registrar {
             upsample_field_only(cd, full);
         }
         Dims d = full;
+        if (cfg->mode == DFM_MODE_SVF) {  // pipeline.cpp:214-215: phi = exp(v)
+            launch_exp_map<T>(L, u[cur].p[0], d, cfg->svf_M, svf_levels);
+            relayout(u[1 - cur], d.n);
+            CK(cudaMemcpyAsync(u[1 - cur].p[0], svf_levels + 3 * d.n * cfg->svf_M,
+                               sizeof(T) * 3 * d.n, cudaMemcpyDeviceToDevice, ctx->stream));
+            cur = 1 - cur;
+        }
         T* coef0[4] = {nullptr, nullptr, nullptr, nullptr};
         check_loss_inputs(F, M, g);
         const int np = loss_kind_launch_fwd<T>(ctx, cfg->loss, cfg->lncc_radius, F, M, d, d,
@@ -1503,10 +1633,11 @@ struct Registrar {
         const int Rw = hw.R > kRMax ? 0 : hw.R;
         const int start = cur;
         const bool big = pbg || pbw;
-        use_brick = !ctx->force_legacy && !big && !cfg->use_jac && d.n <= ctx->brick_max &&
+        const bool direct = cfg->mode == DFM_MODE_DIRECT;
+        use_brick = direct && !ctx->force_legacy && !big && !cfg->use_jac && d.n <= ctx->brick_max &&
                     brick_supported(d, static_cast<int>(sizeof(T)),
                                     cfg->loss == DFM_LOSS_LNCC ? cfg->lncc_radius : 1, Rg, Rw);
-        use_tma = use_brick || (!ctx->force_legacy && tma_eligible(d, Rg, Rw, big));
+        use_tma = use_brick || (direct && !ctx->force_legacy && tma_eligible(d, Rg, Rw, big));
         if (use_tma && cfg->loss == DFM_LOSS_LNCC)
             launch_warpgrad<T>(ctx->L(), Ms, d, u[cur].r(), d, Wb, Gb);
         bool persisted = false;
@@ -1701,7 +1832,8 @@ dfm_status dfm_register(dfm_ctx* ctx, const dfm_grid* g, const void* fixed, cons
         });
         o.total_ms = now_ms() - t0;
         fill_log(o, records, max_records, log);
-        if (o.sing > 0.0) fail(DFM_E_NUMERICAL, "register_images: folded warp (det J <= 0 somewhere)");
+        if (cfg->mode == DFM_MODE_DIRECT && o.sing > 0.0)
+            fail(DFM_E_NUMERICAL, "register_images: folded warp (det J <= 0 somewhere)");
     });
 }
 
@@ -1729,7 +1861,8 @@ dfm_status dfm_dev_register(dfm_ctx* ctx, const dfm_grid* g, const void* d_fixed
             ctx->sync();
         });
         fill_log(o, records, max_records, log);
-        if (o.sing > 0.0) fail(DFM_E_NUMERICAL, "register_images: folded warp (det J <= 0 somewhere)");
+        if (cfg->mode == DFM_MODE_DIRECT && o.sing > 0.0)
+            fail(DFM_E_NUMERICAL, "register_images: folded warp (det J <= 0 somewhere)");
     });
 }
 
@@ -2091,8 +2224,8 @@ struct SlabRun {
     void run(const T* F, const T* M, const double* scales, const int32_t* iters, int ns,
              RegOut& out, T* d_out, int64_t* ozlo, int64_t* ozhi) {
         const double t0 = now_ms();
-        if (cfg->loss != DFM_LOSS_LNCC || cfg->use_jac)
-            fail(DFM_E_INVALID, "slab decomposition: LNCC loss, use_jac off only");
+        if (cfg->loss != DFM_LOSS_LNCC || cfg->use_jac || cfg->mode != DFM_MODE_DIRECT)
+            fail(DFM_E_INVALID, "slab decomposition: direct mode, LNCC loss, use_jac off only");
         if (!tma_supported(full, sizeof(T)))
             fail(DFM_E_INVALID, "slab decomposition: x extent must be a multiple of 16 bytes");
         H = slab_halo(cfg);

@@ -446,6 +446,38 @@ struct GaussOp {
     __device__ void finish(int, double, double) const {}
 };
 
+// SVF update (pipeline.cpp:199-205): field + capped step, then sigma_warp
+// smoothing; one counted update per iteration, nothing once the scale is done
+template <class T, int R>
+struct SvfUpdateOp {
+    using Acc = T;
+    static constexpr int C = 3;
+    static constexpr bool kBox = false, kSum = false, kMax = false;
+    GaussW<T> w;
+    CPlanes3<T> v, step;
+    Planes3<T> out;
+    LoopState* st;
+    Dims d;
+
+    __device__ bool skip() const { return st && st->done; }
+    __device__ Acc wgt(int a, int j) const { return w.taps[a][j]; }
+    __device__ Acc nrm(int a, int i) const { return __ldg(w.norm[a] + i); }
+    __device__ void load(int x, int y, int z, T s[3]) const {
+        const int64_t i = d.idx(x, y, z);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) s[c] = c < d.ndim ? v.c[c][i] + step.c[c][i] : T(0);
+    }
+    __device__ Red emit(int x, int y, int z, const T s[3]) const {
+        const int64_t i = d.idx(x, y, z);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) out.c[c][i] = s[c];
+        return {0.0, 0.0};
+    }
+    __device__ void finish(int, double, double) const {
+        if (st) st->nupdates += 1;
+    }
+};
+
 // ---------------------------------------------------------------------------
 // launch plumbing
 
@@ -610,6 +642,22 @@ void launch_gauss_fused(const Launch& L, int R, const GaussW<T>& w, CPlanes3<T> 
     });
 }
 
+template <class T>
+void launch_svf_update(const Launch& L, int R, const GaussW<T>& w, CPlanes3<T> v,
+                       CPlanes3<T> step, Planes3<T> out, Dims d, LoopState* st) {
+    with_radius<0>(R, [&](auto rc) {
+        constexpr int RR = decltype(rc)::value;
+        SvfUpdateOp<T, RR> op;
+        op.w = w;
+        op.v = v;
+        op.step = step;
+        op.out = out;
+        op.st = st;
+        op.d = d;
+        return run_zmarch<RR>(L, op, d);
+    });
+}
+
 #define DFM_INST_S(T)                                                                          \
     template int launch_lncc_fwd<T>(const Launch&, int, const T*, const T*, Dims, Dims,        \
                                     CPlanes3<T>, T* const*, double*, const LoopState*);        \
@@ -622,7 +670,9 @@ void launch_gauss_fused(const Launch& L, int R, const GaussW<T>& w, CPlanes3<T> 
     template void launch_compose_smooth<T>(const Launch&, int, const GaussW<T>&, CPlanes3<T>,  \
                                            CPlanes3<T>, Planes3<T>, Dims, LoopState*);         \
     template void launch_gauss_fused<T>(const Launch&, int, const GaussW<T>&, CPlanes3<T>,     \
-                                        Planes3<T>, int, Dims);
+                                        Planes3<T>, int, Dims);                                \
+    template void launch_svf_update<T>(const Launch&, int, const GaussW<T>&, CPlanes3<T>,      \
+                                       CPlanes3<T>, Planes3<T>, Dims, LoopState*);
 
 DFM_INST_S(float)
 DFM_INST_S(double)
