@@ -115,6 +115,17 @@ typedef struct {
     const double* field; /* DFM_INIT_FIELD: AoS doubles (host) */
 } dfm_init;
 
+/* difform::AffineResult (affine.hpp:18-23): best-loss iterate of
+ * affine_register (the last finite one on divergence). */
+typedef struct {
+    int32_t ndim;
+    double A[9];         /* row-major, ndim x ndim used */
+    double t[3];
+    double loss;
+    int32_t diverged;
+    int64_t iterations;
+} dfm_affine_result;
+
 /* Result summary of dfm_register: difform::RunLog (pipeline.hpp:55-60). */
 typedef struct {
     int64_t n_records;   /* records written (<= capacity passed in)   */
@@ -166,6 +177,26 @@ DFM_API dfm_status dfm_warp_labels(dfm_ctx* ctx, const dfm_grid* g, const int32_
 /* compose (interp.hpp:35): out = u_psi + lerp(u_phi)(x + u_psi) */
 DFM_API dfm_status dfm_compose(dfm_ctx* ctx, const dfm_grid* g, const double* phi,
                        const double* psi, double* out);
+/* ---- affine.hpp: pre-alignment (the step before the diffeomorphic path) ----- */
+/* affine_to_field (affine.hpp:29-30): u(x) = (A - I) x + t on grid g. */
+DFM_API dfm_status dfm_affine_to_field(dfm_ctx* ctx, const dfm_grid* g, const double A[9],
+                                       const double t[3], double* out);
+/* affine_param_gradient (affine.hpp:43-46, affine.cpp:95-122): loss of the
+ * affine warp u = S^-1 (A S x + t) - x on a working-scale pair and its
+ * parameter gradient dL/dA (row-major), dL/dt. */
+DFM_API dfm_status dfm_affine_param_gradient(dfm_ctx* ctx, const dfm_grid* g,
+                                             const double* fixed, const double* moving,
+                                             int loss, const double A[9], const double t[3],
+                                             const double scale_to_full[3], int lncc_radius,
+                                             double* value, double dA[9], double dt[3]);
+/* affine_register (affine.hpp:25-30, affine.cpp:124-183): multi-scale Adam
+ * (beta 0.9/0.999, eps 1e-8) on (A, t) from identity; best-loss iterate;
+ * non-finite loss -> diverged (no error); |det A| < 1e-3 -> DFM_E_NUMERICAL. */
+DFM_API dfm_status dfm_affine_register(dfm_ctx* ctx, const dfm_grid* g, const double* fixed,
+                                       const double* moving, int loss, const double* scales,
+                                       const int32_t* iters, int32_t nscales, double eta,
+                                       int lncc_radius, dfm_affine_result* out);
+
 /* exp_map (diffeo.hpp:19-20, diffeo.cpp:66-77): v / 2^M, then M
  * self-compositions.  M < 0 -> DFM_E_INVALID. */
 DFM_API dfm_status dfm_exp_map(dfm_ctx* ctx, const dfm_grid* g, const double* v, int M,

@@ -1126,6 +1126,144 @@ int orc_register(const dfm_grid* g, const double* fixed, const double* moving,
     return rc;
 }
 
+/* ---------------------------------------------------------------------- */
+/* affine pre-alignment: affine.cpp:50-183                                  */
+
+static int affine_eval(const dfm_grid* g, const double* f, const double* mv, int loss, int r,
+                       double* phi, double* value, double* grad) {
+    dfm_config c;
+    memset(&c, 0, sizeof(c));
+    c.loss = loss;
+    c.lncc_radius = r;
+    return eval_loss(g, f, mv, phi, &c, value, grad);
+}
+
+/* affine.cpp:72-77 */
+int orc_affine_to_field(const dfm_grid* g, const double A[9], const double t[3], double* out) {
+    CHECK(orc_validate_grid(g));
+    dfm_init T;
+    memset(&T, 0, sizeof(T));
+    memcpy(T.A, A, sizeof(T.A));
+    memcpy(T.t, t, sizeof(T.t));
+    const double S[3] = {1.0, 1.0, 1.0};
+    affine_working_field(&T, g, S, out);
+    return 0;
+}
+
+/* affine.cpp:95-122: dL/dA_rc = sum_x (g_r / S_r) S_c x_c, dL/dt_r = sum_x g_r / S_r,
+ * each a 4096-block ordered sum (parallel.cpp:153-169) */
+int orc_affine_param_gradient(const dfm_grid* g, const double* fixed, const double* moving,
+                              int loss, const double A[9], const double t[3], const double S[3],
+                              int lncc_radius, double* value, double dA[9], double dt[3]) {
+    CHECK(orc_validate_grid(g));
+    const int d = g->ndim;
+    const int64_t n = nvox(g);
+    dfm_init T;
+    memset(&T, 0, sizeof(T));
+    memcpy(T.A, A, sizeof(T.A));
+    memcpy(T.t, t, sizeof(T.t));
+    double* u = dalloc(n * d);
+    double* gr = dalloc(n * d);
+    double* term = dalloc(n);
+    affine_working_field(&T, g, S, u);
+    int rc = affine_eval(g, fixed, moving, loss, lncc_radius, u, value, gr);
+    for (int k = 0; k < 9; ++k) dA[k] = 0.0;
+    for (int k = 0; k < 3; ++k) dt[k] = 0.0;
+    if (!rc) {
+        for (int r = 0; r < d; ++r) {
+            for (int c = 0; c < d; ++c) {
+                for (int64_t i = 0; i < n; ++i) {
+                    double xw[3];
+                    voxel_xyz(g, i, xw);
+                    term[i] = gr[i * d + r] / S[r] * S[c] * xw[c];
+                }
+                dA[r * d + c] = block_sum(term, n);
+            }
+            for (int64_t i = 0; i < n; ++i) term[i] = gr[i * d + r] / S[r];
+            dt[r] = block_sum(term, n);
+        }
+    }
+    free(u);
+    free(gr);
+    free(term);
+    return rc;
+}
+
+/* affine.cpp:124-183 */
+int orc_affine_register(const dfm_grid* g, const double* fixed, const double* moving, int loss,
+                        const double* scales, const int32_t* iters, int32_t nscales, double eta,
+                        int lncc_radius, dfm_affine_result* out) {
+    CHECK(orc_validate_grid(g));
+    if (nscales < 1) return fail(1, "affine_register: bad schedule");
+    const int d = g->ndim, np = d * d + d;
+    const int64_t nfull = nvox(g);
+    double A[9] = {0}, t[3] = {0}, bA[9], bt[3];
+    for (int i = 0; i < d; ++i) A[i * d + i] = 1.0;
+    memcpy(bA, A, sizeof(A));
+    memcpy(bt, t, sizeof(t));
+    double best = INFINITY;
+    double am[12] = {0}, anu[12] = {0};
+    int64_t ta = 0, total = 0;
+    const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
+    double* f = dalloc(nfull);
+    double* mv = dalloc(nfull);
+    int rc = 0, diverged = 0;
+    for (int si = 0; si < nscales && !rc && !diverged; ++si) {
+        const double fac[3] = {scales[si], scales[si], scales[si]};
+        dfm_grid wg;
+        if ((rc = orc_downsample_image(g, fixed, fac, &wg, f))) break;
+        if ((rc = orc_downsample_image(g, moving, fac, &wg, mv))) break;
+        double S[3] = {1.0, 1.0, 1.0};
+        for (int a = 0; a < d; ++a) S[a] = (double)(g->dims[a] - 1) / (double)(wg.dims[a] - 1);
+        for (int it = 0; it < iters[si]; ++it) {
+            double value, dA[9], dt[3];
+            if ((rc = orc_affine_param_gradient(&wg, f, mv, loss, A, t, S, lncc_radius, &value,
+                                                dA, dt)))
+                break;
+            ++total;
+            if (!isfinite(value)) {
+                diverged = 1;
+                break;
+            }
+            if (value < best) {
+                best = value;
+                memcpy(bA, A, sizeof(A));
+                memcpy(bt, t, sizeof(t));
+            }
+            ++ta;
+            const double c1 = 1.0 - pow(b1, (double)ta);
+            const double c2 = 1.0 - pow(b2, (double)ta);
+            for (int p = 0; p < np; ++p) {
+                const double gp = p < d * d ? dA[p] : dt[p - d * d];
+                am[p] = b1 * am[p] + (1.0 - b1) * gp;
+                anu[p] = b2 * anu[p] + (1.0 - b2) * gp * gp;
+                const double dir = (am[p] / c1) / (sqrt(anu[p] / c2) + eps);
+                if (p < d * d)
+                    A[p] -= eta * dir;
+                else
+                    t[p - d * d] -= eta * dir;
+            }
+        }
+    }
+    free(f);
+    free(mv);
+    if (rc) return rc;
+    out->ndim = d;
+    memcpy(out->A, bA, sizeof(bA));
+    memcpy(out->t, bt, sizeof(bt));
+    out->loss = best;
+    out->diverged = diverged;
+    out->iterations = total;
+    if (!diverged) {
+        const double det = d == 2 ? bA[0] * bA[3] - bA[1] * bA[2]
+                                  : bA[0] * (bA[4] * bA[8] - bA[5] * bA[7]) -
+                                        bA[1] * (bA[3] * bA[8] - bA[5] * bA[6]) +
+                                        bA[2] * (bA[3] * bA[7] - bA[4] * bA[6]);
+        if (fabs(det) < 1e-3) return fail(2, "affine_register: transform collapsed (|det A| < 1e-3)");
+    }
+    return 0;
+}
+
 /* analysis.cpp:169-247, MO (Dice) columns only.  Labels are ints; regions are
  * visited in ascending label order like std::map. */
 int orc_overlap_dice(const dfm_grid* g, const int32_t* warped, const int32_t* fixed,

@@ -61,6 +61,13 @@ int orc_eulerian_direction(const dfm_grid* g, const double* grad, const double* 
 int orc_apply_update(const dfm_grid* g, const double* phi, const double* v, double eta,
                      double sigma_warp, double cap, double* out);
 int orc_singularity_fraction(const dfm_grid* g, const double* phi, double* frac);
+int orc_affine_to_field(const dfm_grid* g, const double A[9], const double t[3], double* out);
+int orc_affine_param_gradient(const dfm_grid* g, const double* fixed, const double* moving,
+                              int loss, const double A[9], const double t[3], const double S[3],
+                              int lncc_radius, double* value, double dA[9], double dt[3]);
+int orc_affine_register(const dfm_grid* g, const double* fixed, const double* moving, int loss,
+                        const double* scales, const int32_t* iters, int32_t nscales, double eta,
+                        int lncc_radius, dfm_affine_result* out);
 int orc_exp_map(const dfm_grid* g, const double* v, int M, double* out);
 int orc_svf_pullback(const dfm_grid* g, const double* v, const double* grad_phi, int M,
                      double* out);

@@ -15,6 +15,7 @@
 #include <variant>
 #include <vector>
 
+#include "difform/affine.hpp"
 #include "difform/analysis.hpp"
 #include "difform/core.hpp"
 #include "difform/diffeo.hpp"
@@ -163,6 +164,51 @@ int dfmref_warp_labels(const dfm_grid* g, const int32_t* labels, const double* p
 
 int dfmref_compose(const dfm_grid* g, const double* phi, const double* psi, double* out) {
     return guarded([&] { put(compose(to_field(g, phi), to_field(g, psi)).data, out); });
+}
+
+static AffineTransform to_affine(int ndim, const double A[9], const double t[3]) {
+    AffineTransform T;
+    T.ndim = ndim;
+    for (int k = 0; k < 9; ++k) T.A[k] = A[k];
+    for (int k = 0; k < 3; ++k) T.t[k] = t[k];
+    return T;
+}
+
+int dfmref_affine_to_field(const dfm_grid* g, const double A[9], const double t[3],
+                           double* out) {
+    return guarded([&] { put(affine_to_field(to_affine(g->ndim, A, t), to_meta(g)).data, out); });
+}
+
+int dfmref_affine_param_gradient(const dfm_grid* g, const double* fixed, const double* moving,
+                                 int loss, const double A[9], const double t[3],
+                                 const double S[3], int lncc_radius, double* value, double dA[9],
+                                 double dt[3]) {
+    return guarded([&] {
+        const AffineGrad r = affine_param_gradient(
+            to_image(g, fixed), to_image(g, moving), static_cast<LossKind>(loss),
+            to_affine(g->ndim, A, t), {S[0], S[1], S[2]}, lncc_radius);
+        *value = r.value;
+        for (int k = 0; k < 9; ++k) dA[k] = r.dA[k];
+        for (int k = 0; k < 3; ++k) dt[k] = r.dt[k];
+    });
+}
+
+int dfmref_affine_register(const dfm_grid* g, const double* fixed, const double* moving,
+                           int loss, const double* scales, const int32_t* iters,
+                           int32_t nscales, double eta, int lncc_radius,
+                           dfm_affine_result* out) {
+    return guarded([&] {
+        const AffineResult r = affine_register(
+            to_image(g, fixed), to_image(g, moving), static_cast<LossKind>(loss),
+            std::vector<double>(scales, scales + nscales), std::vector<int>(iters, iters + nscales),
+            eta, lncc_radius);
+        out->ndim = r.transform.ndim;
+        for (int k = 0; k < 9; ++k) out->A[k] = r.transform.A[k];
+        for (int k = 0; k < 3; ++k) out->t[k] = r.transform.t[k];
+        out->loss = r.loss;
+        out->diverged = r.diverged ? 1 : 0;
+        out->iterations = r.iterations;
+    });
 }
 
 int dfmref_exp_map(const dfm_grid* g, const double* v, int M, double* out) {

@@ -66,6 +66,11 @@ class dfm_runlog(C.Structure):
                 ("total_ms", C.c_double)]
 
 
+class dfm_affine_result(C.Structure):
+    _fields_ = [("ndim", C.c_int32), ("A", C.c_double * 9), ("t", C.c_double * 3),
+                ("loss", C.c_double), ("diverged", C.c_int32), ("iterations", C.c_int64)]
+
+
 # --------------------------------------------------------------------------
 # host-side value types (difform::GridMeta / RegistrationConfig / ...)
 
@@ -185,6 +190,21 @@ def _ipptr(a: np.ndarray):
     return a.ctypes.data_as(C.POINTER(C.c_int32))
 
 
+def _affine_A(A, ndim) -> np.ndarray:
+    """row-major ndim x ndim matrix packed into the 9-slot C array"""
+    a = np.asarray(A, dtype=np.float64).reshape(ndim, ndim)
+    out = np.zeros(9)
+    out[:ndim * ndim] = a.ravel()
+    return out
+
+
+def _vec3(v) -> np.ndarray:
+    out = np.zeros(3)
+    v = np.asarray(v, dtype=np.float64).ravel()
+    out[:len(v)] = v
+    return out
+
+
 def as_f64(a, shape=None) -> np.ndarray:
     out = np.ascontiguousarray(a, dtype=np.float64)
     if shape is not None and out.shape != tuple(shape):
@@ -203,6 +223,10 @@ PROTOS = {
     "warp_labels": [_G, _I, _D, _I],
     "compose": [_G, _D, _D, _D],
     "exp_map": [_G, _D, C.c_int, _D],
+    "affine_to_field": [_G, _D, _D, _D],
+    "affine_param_gradient": [_G, _D, _D, C.c_int, _D, _D, _D, C.c_int, _D, _D, _D],
+    "affine_register": [_G, _D, _D, C.c_int, _D, _I, C.c_int32, C.c_double, C.c_int,
+                        C.POINTER(dfm_affine_result)],
     "svf_pullback": [_G, _D, _D, C.c_int, _D],
     "jacobian_det": [_G, _D, _D],
     "gaussian_smooth": [_G, _D, _D, _D],
@@ -332,6 +356,39 @@ class HostAPI:
         out = np.empty(g.field_shape)
         self.t.call("compose", C.byref(g.c()), _dptr(phi), _dptr(psi), _dptr(out))
         return out
+
+    def affine_to_field(self, g, A, t):
+        """affine_to_field (affine.hpp:29-30): u(x) = (A - I) x + t."""
+        out = np.empty(g.field_shape)
+        self.t.call("affine_to_field", C.byref(g.c()), _dptr(_affine_A(A, g.ndim)),
+                    _dptr(_vec3(t)), _dptr(out))
+        return out
+
+    def affine_param_gradient(self, g, fixed, moving, loss, A, t, scale_to_full=(1, 1, 1),
+                              lncc_radius=2):
+        """affine_param_gradient (affine.hpp:43-46) -> (value, dA (d x d), dt (d))."""
+        f, m = as_f64(fixed, g.shape), as_f64(moving, g.shape)
+        val = C.c_double()
+        dA = np.zeros(9)
+        dt = np.zeros(3)
+        self.t.call("affine_param_gradient", C.byref(g.c()), _dptr(f), _dptr(m), int(loss),
+                    _dptr(_affine_A(A, g.ndim)), _dptr(_vec3(t)), _dptr(_vec3(scale_to_full)),
+                    int(lncc_radius), C.byref(val), _dptr(dA), _dptr(dt))
+        d = g.ndim
+        return val.value, dA[:d * d].reshape(d, d), dt[:d]
+
+    def affine_register(self, g, fixed, moving, loss, scales, iters, eta, lncc_radius=2):
+        """affine_register (affine.hpp:25-30) -> dict(A, t, loss, diverged, iterations)."""
+        f, m = as_f64(fixed, g.shape), as_f64(moving, g.shape)
+        s = np.ascontiguousarray(scales, dtype=np.float64)
+        it = np.ascontiguousarray(iters, dtype=np.int32)
+        r = dfm_affine_result()
+        self.t.call("affine_register", C.byref(g.c()), _dptr(f), _dptr(m), int(loss), _dptr(s),
+                    it.ctypes.data_as(C.POINTER(C.c_int32)), len(s), float(eta),
+                    int(lncc_radius), C.byref(r))
+        d = g.ndim
+        return dict(A=np.array(r.A[:d * d]).reshape(d, d), t=np.array(r.t[:d]), loss=r.loss,
+                    diverged=bool(r.diverged), iterations=int(r.iterations))
 
     def exp_map(self, g, v, M):
         """exp_map (diffeo.hpp:19-20, diffeo.cpp:66-77): scaling and squaring."""

@@ -87,13 +87,58 @@ def svf_golden(ref):
             final_loss=np.array(log.final_loss), sing=np.array(log.final_singularity_fraction))
 
 
+def affine_moving(p, A, t):
+    """the pair's fixed image warped by the affine map x -> A x + t (pre-alignment case)"""
+    g = p.grid
+    u = pyoracle.reference().affine_to_field(g, A, t)
+    return f32(pyoracle.reference().warp_image(g, p.fixed, u))
+
+
+def affine_golden(ref):
+    """affine_to_field / affine_param_gradient / affine_register (affine.cpp:50-183)."""
+    rng = np.random.default_rng(777)
+    out = {}
+    for tag, g in (("3d", A.GridMeta.make_3d(13, 11, 9)), ("2d", A.GridMeta.make_2d(17, 12))):
+        d = g.ndim
+        Am = np.eye(d) + rng.normal(0, 0.05, (d, d))
+        t = rng.normal(0, 0.5, d)
+        F = f32(rng.random(g.shape))
+        M = f32(ndimage_smooth(rng.random(g.shape)))
+        S = (1.3, 1.1, 0.9)
+        out.update({f"{tag}_dims": np.array(g.dims), f"{tag}_ndim": np.array(d), f"{tag}_A": Am,
+                    f"{tag}_t": t, f"{tag}_F": F, f"{tag}_M": M, f"{tag}_S": np.array(S),
+                    f"{tag}_field": ref.affine_to_field(g, Am, t)})
+        for loss in (A.LOSS_SSD, A.LOSS_LNCC, A.LOSS_DICE):
+            Fm, Mm = (np.clip(F, 0, 1), np.clip(M, 0, 1)) if loss == A.LOSS_DICE else (F, M)
+            v, dA, dt = ref.affine_param_gradient(g, Fm, Mm, loss, Am, t, S, 2)
+            out[f"{tag}_grad{loss}_val"] = np.array(v)
+            out[f"{tag}_grad{loss}_dA"] = dA
+            out[f"{tag}_grad{loss}_dt"] = dt
+    p = synth.make_pair(0, seed=21, shape=(32, 28, 24))
+    Am = np.array([[1.05, 0.03, 0.0], [-0.02, 0.96, 0.04], [0.0, 0.02, 1.03]])
+    moving = affine_moving(p, Am, np.array([1.2, -0.8, 0.5]))
+    out["reg_dims"] = np.array(p.grid.dims)
+    out["reg_fixed"] = p.fixed
+    out["reg_moving"] = moving
+    for loss in (A.LOSS_SSD, A.LOSS_LNCC):
+        r = ref.affine_register(p.grid, p.fixed, moving, loss, [4, 2, 1], [40, 20, 10], 0.01)
+        for k in ("A", "t", "loss", "iterations"):
+            out[f"reg{loss}_{k}"] = np.array(r[k])
+    np.savez_compressed(os.path.join(HERE, "affine.npz"), **out)
+
+
 def main():
     ref = pyoracle.reference()
+    if "--only-affine" in sys.argv:
+        affine_golden(ref)
+        print("affine golden vectors written to", HERE)
+        return
     if "--only-svf" in sys.argv:
         svf_golden(ref)
         print("svf golden vectors written to", HERE)
         return
     svf_golden(ref)
+    affine_golden(ref)
     C = cases()
     for tag in ("3d", "2d"):
         c = C[tag]

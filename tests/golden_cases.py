@@ -122,3 +122,26 @@ def compute_svf(api, tag):
         out[f"pull{M}"] = (api.svf_pullback(g, z[f"{tag}_v"], z[f"{tag}_w"], M),
                            z[f"{tag}_pull{M}"])
     return out
+
+
+def compute_affine(api, tag):
+    """affine_to_field / affine_param_gradient on affine.npz -> {key: (got, want)}."""
+    z = load("affine.npz")
+    g = A.GridMeta(int(z[f"{tag}_ndim"]), tuple(int(v) for v in z[f"{tag}_dims"]))
+    Am, t, S = z[f"{tag}_A"], z[f"{tag}_t"], z[f"{tag}_S"]
+    out = {"field": (api.affine_to_field(g, Am, t), z[f"{tag}_field"])}
+    for loss in (A.LOSS_SSD, A.LOSS_LNCC, A.LOSS_DICE):
+        F, M = z[f"{tag}_F"], z[f"{tag}_M"]
+        if loss == A.LOSS_DICE:
+            F, M = np.clip(F, 0, 1), np.clip(M, 0, 1)
+        v, dA, dt = api.affine_param_gradient(g, F, M, loss, Am, t, S, 2)
+        out[f"grad{loss}_val"] = (np.asarray(v), z[f"{tag}_grad{loss}_val"])
+        out[f"grad{loss}_dA"] = (dA, z[f"{tag}_grad{loss}_dA"])
+        out[f"grad{loss}_dt"] = (dt, z[f"{tag}_grad{loss}_dt"])
+    return out
+
+
+def affine_register_inputs():
+    z = load("affine.npz")
+    g = A.GridMeta(3, tuple(int(v) for v in z["reg_dims"]))
+    return z, g

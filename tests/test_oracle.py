@@ -59,6 +59,41 @@ def test_restatement_register_svf_bitwise(oracle_port, name):
     assert log.final_loss == float(z["final_loss"])
 
 
+@pytest.mark.parametrize("tag", ["3d", "2d"])
+def test_restatement_affine_bitwise(oracle_port, tag):
+    """affine_to_field / affine_param_gradient (affine.cpp:50-122), 3 losses."""
+    for key, (got, want) in G.compute_affine(oracle_port, tag).items():
+        assert np.array_equal(got, want), key
+
+
+@pytest.mark.parametrize("loss", [A.LOSS_SSD, A.LOSS_LNCC])
+def test_restatement_affine_register_bitwise(oracle_port, loss):
+    """affine_register (affine.cpp:124-183): multi-scale parameter Adam."""
+    z, g = G.affine_register_inputs()
+    r = oracle_port.affine_register(g, z["reg_fixed"], z["reg_moving"], loss, [4, 2, 1],
+                                    [40, 20, 10], 0.01)
+    assert np.array_equal(r["A"], z[f"reg{loss}_A"])
+    assert np.array_equal(r["t"], z[f"reg{loss}_t"])
+    assert r["loss"] == float(z[f"reg{loss}_loss"])
+    assert r["iterations"] == int(z[f"reg{loss}_iterations"])
+
+
+def test_restatement_affine_errors(oracle_port):
+    g = A.GridMeta.make_3d(12, 12, 12)
+    F = np.zeros(g.shape)
+    with pytest.raises(A.InvalidArgument):
+        oracle_port.affine_register(g, F, F, A.LOSS_SSD, [], [], 0.1)
+    # eta so large that A collapses / the loss stays finite: |det A| < 1e-3 -> runtime_error
+    rng = np.random.default_rng(0)
+    F = rng.random(g.shape)
+    M = np.roll(F, 2, axis=0)
+    try:
+        r = oracle_port.affine_register(g, F, M, A.LOSS_SSD, [1], [40], 50.0)
+        assert r["diverged"] or abs(np.linalg.det(r["A"])) >= 1e-3
+    except A.NumericalError:
+        pass
+
+
 def test_restatement_early_stop_record_count(oracle_port):
     """test_pipeline.cpp:69-93 semantics: default window 10 on a self pair."""
     z = G.load("register_self.npz")
