@@ -281,6 +281,17 @@ template <class T>
 void launch_svf_update(const Launch& L, int R, const GaussW<T>& w, CPlanes3<T> v,
                        CPlanes3<T> step, Planes3<T> out, Dims d, LoopState* st);
 
+// -------- affine pre-alignment (kernels_affine.cu): the 12 parameter sums
+// of affine_param_gradient; out12 = dA (row-major, ndim x ndim packed) then dt
+// at [9..11]; partials needs affine_grad_partials() doubles.
+struct AffineS {
+    double S[3];
+};
+int affine_grad_partials();
+template <class T>
+void launch_affine_grad(const Launch& L, CPlanes3<T> g, Dims d, AffineS S, double* partials,
+                        double* out12);
+
 // -------- loop control
 // kind: 0 ssd, 1 lncc, 2 dice (3 partial arrays of np each)
 void launch_monitor(const Launch& L, int kind, const double* partials, int np, double nvox,

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <map>
 #include <stdexcept>
 #include <string>
@@ -695,6 +696,178 @@ dfm_status dfm_compose(dfm_ctx* ctx, const dfm_grid* g, const double* phi, const
             launch_compose<T>(ctx->L(), a.r(), b.r(), d, o.w());
             download_field<T, double>(ctx, o.r(), d.n, d.ndim, out);
             ctx->sync();
+        });
+    });
+}
+
+// ---------------------------------------------------------------------------
+// affine pre-alignment (affine.cpp:50-183)
+
+}  // extern "C"
+
+static void check_lncc_window(int loss, int R, const Dims& d) {
+    if (loss != DFM_LOSS_LNCC) return;
+    if (R < 1) fail(DFM_E_INVALID, "lncc_eval: window_radius must be >= 1");
+    const int n[3] = {d.nx, d.ny, d.nz};
+    for (int a = 0; a < d.ndim; ++a)
+        if (2 * static_cast<int64_t>(R) + 1 > n[a])
+            fail(DFM_E_INVALID, "lncc_eval: window larger than image");
+    if (R > kRMax) fail(DFM_E_INVALID, "lncc_eval: window_radius > %d unsupported", kRMax);
+}
+
+static void check_dice_masks(int loss, const double* fixed, const double* moving, int64_t n) {
+    if (loss != DFM_LOSS_DICE) return;
+    for (int64_t i = 0; i < n; ++i)
+        if (!(fixed[i] >= 0.0 && fixed[i] <= 1.0))
+            fail(DFM_E_INVALID, "dice_soft_eval: fixed mask values outside [0,1]");
+    for (int64_t i = 0; i < n; ++i)
+        if (!(moving[i] >= 0.0 && moving[i] <= 1.0))
+            fail(DFM_E_INVALID, "dice_soft_eval: moving mask values outside [0,1]");
+}
+
+// affine.cpp:95-122 on device images of grid d: value, dA (packed), dt
+template <class T>
+static double affine_grad_dev(dfm_ctx* ctx, int loss, int R, const T* F, const T* M,
+                              const Dims& d, const double A[9], const double t[3],
+                              const double S[3], double dA[9], double dt[3]) {
+    Launch L = ctx->L();
+    Field<T> u = dev_field<T>(ctx, "aff_u", d.n);
+    Field<T> gr = dev_field<T>(ctx, "aff_g", d.n);
+    launch_affine_field<T>(L, A, t, S, d, u.w());
+    const double value = eval_loss_dev<T>(ctx, loss, R, F, M, d, d, u.r(), true, gr.w());
+    double* part = ctx->arr<double>("aff_partials", affine_grad_partials());
+    double* out = ctx->arr<double>("aff_out", 12);
+    AffineS s;
+    for (int a = 0; a < 3; ++a) s.S[a] = S[a];
+    launch_affine_grad<T>(L, gr.r(), d, s, part, out);
+    double h[12];
+    CK(cudaMemcpyAsync(h, out, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    for (int k = 0; k < 9; ++k) dA[k] = 0.0;
+    for (int k = 0; k < d.ndim * d.ndim; ++k) dA[k] = h[k];
+    for (int k = 0; k < 3; ++k) dt[k] = k < d.ndim ? h[9 + k] : 0.0;
+    return value;
+}
+
+extern "C" {
+
+dfm_status dfm_affine_to_field(dfm_ctx* ctx, const dfm_grid* g, const double A[9],
+                               const double t[3], double* out) {
+    return guarded([&] {
+        validate_grid(g);
+        const Dims d = to_dims(g);
+        const double S[3] = {1.0, 1.0, 1.0};
+        DFM_DISPATCH(ctx, {
+            Field<T> o = dev_field<T>(ctx, "api_f2", d.n);
+            launch_affine_field<T>(ctx->L(), A, t, S, d, o.w());
+            download_field<T, double>(ctx, o.r(), d.n, d.ndim, out);
+            ctx->sync();
+        });
+    });
+}
+
+dfm_status dfm_affine_param_gradient(dfm_ctx* ctx, const dfm_grid* g, const double* fixed,
+                                     const double* moving, int loss, const double A[9],
+                                     const double t[3], const double S[3], int lncc_radius,
+                                     double* value, double dA[9], double dt[3]) {
+    return guarded([&] {
+        validate_grid(g);
+        if (loss < 0 || loss > 2) fail(DFM_E_INVALID, "unknown loss");
+        const Dims d = to_dims(g);
+        check_lncc_window(loss, lncc_radius, d);
+        check_dice_masks(loss, fixed, moving, d.n);
+        DFM_DISPATCH(ctx, {
+            T* F = ctx->arr<T>("api_img0", d.n);
+            T* M = ctx->arr<T>("api_img1", d.n);
+            upload_image<T, double>(ctx, fixed, d.n, F);
+            upload_image<T, double>(ctx, moving, d.n, M);
+            *value = affine_grad_dev<T>(ctx, loss, lncc_radius, F, M, d, A, t, S, dA, dt);
+        });
+    });
+}
+
+dfm_status dfm_affine_register(dfm_ctx* ctx, const dfm_grid* g, const double* fixed,
+                               const double* moving, int loss, const double* scales,
+                               const int32_t* iters, int32_t nscales, double eta,
+                               int lncc_radius, dfm_affine_result* out) {
+    return guarded([&] {
+        validate_grid(g);
+        if (nscales < 1 || !scales || !iters) fail(DFM_E_INVALID, "affine_register: bad schedule");
+        if (loss < 0 || loss > 2) fail(DFM_E_INVALID, "unknown loss");
+        const Dims full = to_dims(g);
+        const int nd = g->ndim, np = nd * nd + nd;
+        check_dice_masks(loss, fixed, moving, full.n);
+        DFM_DISPATCH(ctx, {
+            T* F = ctx->arr<T>("aff_F", full.n);
+            T* M = ctx->arr<T>("aff_M", full.n);
+            T* Fw = ctx->arr<T>("aff_Fw", full.n);
+            T* Mw = ctx->arr<T>("aff_Mw", full.n);
+            upload_image<T, double>(ctx, fixed, full.n, F);
+            upload_image<T, double>(ctx, moving, full.n, M);
+            double A[9] = {0}, t[3] = {0}, bA[9], bt[3];
+            for (int i = 0; i < nd; ++i) A[i * nd + i] = 1.0;
+            std::memcpy(bA, A, sizeof(A));
+            std::memcpy(bt, t, sizeof(t));
+            double best = std::numeric_limits<double>::infinity();
+            double am[12] = {0}, anu[12] = {0};
+            int64_t ta = 0, total = 0;
+            const double b1 = 0.9, b2 = 0.999, eps = 1e-8;  // affine.cpp:139
+            bool diverged = false;
+            for (int si = 0; si < nscales && !diverged; ++si) {
+                const double fac[3] = {scales[si], scales[si], scales[si]};
+                dfm_grid wgd;
+                downsample_grid(g, fac, &wgd);
+                const Dims d = to_dims(&wgd);
+                check_lncc_window(loss, lncc_radius, d);
+                Impl<T>{ctx}.downsample_dev(full, F, fac, d, Fw, "aff_pyr");
+                Impl<T>{ctx}.downsample_dev(full, M, fac, d, Mw, "aff_pyr");
+                double S[3] = {1.0, 1.0, 1.0};
+                const int fd[3] = {full.nx, full.ny, full.nz}, wd[3] = {d.nx, d.ny, d.nz};
+                for (int a = 0; a < nd; ++a)
+                    S[a] = static_cast<double>(fd[a] - 1) / static_cast<double>(wd[a] - 1);
+                for (int it = 0; it < iters[si]; ++it) {
+                    double dA[9], dt[3];
+                    const double value =
+                        affine_grad_dev<T>(ctx, loss, lncc_radius, Fw, Mw, d, A, t, S, dA, dt);
+                    ++total;
+                    if (!std::isfinite(value)) {
+                        diverged = true;
+                        break;
+                    }
+                    if (value < best) {
+                        best = value;
+                        std::memcpy(bA, A, sizeof(A));
+                        std::memcpy(bt, t, sizeof(t));
+                    }
+                    ++ta;
+                    const double c1 = 1.0 - std::pow(b1, static_cast<double>(ta));
+                    const double c2 = 1.0 - std::pow(b2, static_cast<double>(ta));
+                    for (int p = 0; p < np; ++p) {
+                        const double gp = p < nd * nd ? dA[p] : dt[p - nd * nd];
+                        am[p] = b1 * am[p] + (1.0 - b1) * gp;
+                        anu[p] = b2 * anu[p] + (1.0 - b2) * gp * gp;
+                        const double dir = (am[p] / c1) / (std::sqrt(anu[p] / c2) + eps);
+                        if (p < nd * nd)
+                            A[p] -= eta * dir;
+                        else
+                            t[p - nd * nd] -= eta * dir;
+                    }
+                }
+            }
+            out->ndim = nd;
+            std::memcpy(out->A, bA, sizeof(bA));
+            std::memcpy(out->t, bt, sizeof(bt));
+            out->loss = best;
+            out->diverged = diverged ? 1 : 0;
+            out->iterations = total;
+            if (!diverged) {
+                const double det = nd == 2 ? bA[0] * bA[3] - bA[1] * bA[2]
+                                           : bA[0] * (bA[4] * bA[8] - bA[5] * bA[7]) -
+                                                 bA[1] * (bA[3] * bA[8] - bA[5] * bA[6]) +
+                                                 bA[2] * (bA[3] * bA[7] - bA[4] * bA[6]);
+                if (std::fabs(det) < 1e-3)
+                    fail(DFM_E_NUMERICAL, "affine_register: transform collapsed (|det A| < 1e-3)");
+            }
         });
     });
 }

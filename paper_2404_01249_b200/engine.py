@@ -33,7 +33,8 @@ EXPORTS = [
     "dfm_eulerian_direction", "dfm_apply_update", "dfm_singularity_fraction", "dfm_register",
     "dfm_dev_register", "dfm_ctx_set_profiling", "dfm_ctx_kernel_times",
     "dfm_slab_bounds", "dfm_slab_halo", "dfm_slab_unique_id", "dfm_dev_register_slab",
-    "dfm_ctx_set_option", "dfm_exp_map", "dfm_svf_pullback",
+    "dfm_ctx_set_option", "dfm_exp_map", "dfm_svf_pullback", "dfm_affine_to_field",
+    "dfm_affine_param_gradient", "dfm_affine_register",
 ]
 
 OPT_BRICK_MAX = 1
