@@ -126,6 +126,23 @@ typedef struct {
     int64_t iterations;
 } dfm_affine_result;
 
+/* difform::RegionOverlap (analysis.hpp:46-59) */
+typedef struct {
+    int32_t label;
+    int32_t has_to, has_fn, has_fp;
+    int64_t fixed_count;   /* |T_r| */
+    int64_t warped_count;  /* |S_r| */
+    int64_t intersection;  /* |S_r n T_r| */
+    double to, mo, fn, fp, vs;
+} dfm_region_overlap;
+
+/* difform::OverlapReport aggregates (analysis.hpp:61-65) */
+typedef struct {
+    double to_mean, mo_mean, fn_mean, fp_mean, vs_mean;
+    double to_klein, mo_klein, fn_klein, fp_klein, vs_klein;
+    int64_t n_regions;     /* regions in the report (may exceed the capacity passed) */
+} dfm_overlap_summary;
+
 /* Result summary of dfm_register: difform::RunLog (pipeline.hpp:55-60). */
 typedef struct {
     int64_t n_records;   /* records written (<= capacity passed in)   */
@@ -283,6 +300,33 @@ DFM_API dfm_status dfm_dev_register(dfm_ctx* ctx, const dfm_grid* g, const void*
                             const double* scales, const int32_t* iterations,
                             int32_t nscales, void* d_out_soa_field,
                             dfm_iter_record* records, int64_t max_records, dfm_runlog* log);
+
+/* ---- evaluation epilogue (analysis.hpp, interp.hpp) -------------------- */
+/* overlap_report (analysis.hpp:67, analysis.cpp:169-247): per-region and
+ * aggregate TO/MO/FN/FP/VS of a warped vs a fixed label map; regions in
+ * ascending label order, at most max_regions written.  Labels above 2^24 ->
+ * DFM_E_INVALID (MHD label maps are MET_SHORT).  Grid mismatch -> DFM_E_INVALID. */
+DFM_API dfm_status dfm_overlap_report(dfm_ctx* ctx, const dfm_grid* warped_grid,
+                                      const int32_t* warped, const dfm_grid* fixed_grid,
+                                      const int32_t* fixed, dfm_overlap_summary* out,
+                                      dfm_region_overlap* regions, int64_t max_regions);
+/* Same on device label maps (no host round trip of the volumes). */
+DFM_API dfm_status dfm_dev_overlap_report(dfm_ctx* ctx, const dfm_grid* g,
+                                          const int32_t* d_warped, const int32_t* d_fixed,
+                                          dfm_overlap_summary* out, dfm_region_overlap* regions,
+                                          int64_t max_regions);
+/* warp_labels (interp.hpp:33) on device buffers: d_field_soa is a 3-plane SoA
+ * field in the context precision (as dfm_dev_register writes it). */
+DFM_API dfm_status dfm_dev_warp_labels(dfm_ctx* ctx, const dfm_grid* g, const int32_t* d_labels,
+                                       const void* d_field_soa, int32_t* d_out);
+/* landmark_error (analysis.hpp:77-79, analysis.cpp:249-283): fixed-space
+ * points (mm, n x 3) mapped through phi (AoS doubles on phi_grid == fixed
+ * grid) into the moving frame; Euclidean mm distances to the moving points. */
+DFM_API dfm_status dfm_landmark_error(dfm_ctx* ctx, const dfm_grid* fixed_grid,
+                                      const dfm_grid* moving_grid, const dfm_grid* phi_grid,
+                                      const double* phi, int64_t n, const double* fixed_mm,
+                                      const double* moving_mm, double* distances, double* mean,
+                                      double* max);
 
 /* ---- z-slab decomposition (BASELINE config 4) ------------ */
 /* Owned planes [zlo, zhi) and halo depths (hlo, hhi) of slab `part` of

@@ -1301,3 +1301,118 @@ int orc_overlap_dice(const dfm_grid* g, const int32_t* warped, const int32_t* fi
     free(I);
     return 0;
 }
+
+/* analysis.cpp:169-247: full report; regions in ascending label order */
+int orc_overlap_report(const dfm_grid* gw, const int32_t* warped, const dfm_grid* gf,
+                       const int32_t* fixed, dfm_overlap_summary* rep,
+                       dfm_region_overlap* regions, int64_t cap) {
+    CHECK(orc_validate_grid(gw));
+    CHECK(orc_validate_grid(gf));
+    if (!same_grid(gw, gf)) return fail(1, "overlap_report: grid mismatch");
+    const int64_t n = nvox(gw);
+    int32_t maxl = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        if (warped[i] > maxl) maxl = warped[i];
+        if (fixed[i] > maxl) maxl = fixed[i];
+    }
+    int64_t* S = calloc((size_t)maxl + 1, sizeof(int64_t));
+    int64_t* T = calloc((size_t)maxl + 1, sizeof(int64_t));
+    int64_t* I = calloc((size_t)maxl + 1, sizeof(int64_t));
+    for (int64_t i = 0; i < n; ++i) {
+        const int32_t s = warped[i], t = fixed[i];
+        if (s > 0) ++S[s];
+        if (t > 0) ++T[t];
+        if (s > 0 && s == t) ++I[s];
+    }
+    memset(rep, 0, sizeof(*rep));
+    int64_t ps = 0, pt = 0, pi = 0, pfn = 0, pfp = 0, nr = 0;
+    int to_n = 0, fp_n = 0, vs_n = 0;
+    for (int32_t l = 1; l <= maxl; ++l) {
+        if (S[l] == 0 && T[l] == 0) continue;
+        dfm_region_overlap r;
+        memset(&r, 0, sizeof(r));
+        r.label = l;
+        r.warped_count = S[l];
+        r.fixed_count = T[l];
+        r.intersection = I[l];
+        const int64_t fn = T[l] - I[l], fp = S[l] - I[l];
+        if (T[l] > 0) {
+            r.has_to = r.has_fn = 1;
+            r.to = (double)I[l] / (double)T[l];
+            r.fn = (double)fn / (double)T[l];
+            rep->to_mean += r.to;
+            rep->fn_mean += r.fn;
+            ++to_n;
+        }
+        if (S[l] > 0) {
+            r.has_fp = 1;
+            r.fp = (double)fp / (double)S[l];
+            rep->fp_mean += r.fp;
+            ++fp_n;
+        }
+        const int64_t den = S[l] + T[l];
+        r.mo = 2.0 * (double)I[l] / (double)den;
+        r.vs = 2.0 * (double)(S[l] - T[l]) / (double)den;
+        rep->mo_mean += r.mo;
+        rep->vs_mean += r.vs;
+        ++vs_n;
+        ps += S[l];
+        pt += T[l];
+        pi += I[l];
+        pfn += fn;
+        pfp += fp;
+        if (nr < cap) regions[nr] = r;
+        ++nr;
+    }
+    if (to_n > 0) {
+        rep->to_mean /= to_n;
+        rep->fn_mean /= to_n;
+    }
+    if (fp_n > 0) rep->fp_mean /= fp_n;
+    if (vs_n > 0) {
+        rep->mo_mean /= vs_n;
+        rep->vs_mean /= vs_n;
+    }
+    if (pt > 0) {
+        rep->to_klein = (double)pi / (double)pt;
+        rep->fn_klein = (double)pfn / (double)pt;
+    }
+    if (ps > 0) rep->fp_klein = (double)pfp / (double)ps;
+    if (ps + pt > 0) {
+        rep->mo_klein = 2.0 * (double)pi / (double)(ps + pt);
+        rep->vs_klein = 2.0 * (double)(ps - pt) / (double)(ps + pt);
+    }
+    rep->n_regions = nr;
+    free(S);
+    free(T);
+    free(I);
+    return 0;
+}
+
+/* analysis.cpp:249-283 */
+int orc_landmark_error(const dfm_grid* fg, const dfm_grid* mg, const dfm_grid* pg,
+                       const double* phi, int64_t n, const double* fixed_mm,
+                       const double* moving_mm, double* dist, double* mean, double* mx) {
+    if (!same_grid(pg, fg)) /* core.hpp:20-22: ndim and dims */
+        return fail(1, "landmark_error: field must live on the fixed grid");
+    *mean = 0.0;
+    *mx = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        double vox[3] = {0.0, 0.0, 0.0}, u[3];
+        for (int a = 0; a < fg->ndim; ++a)
+            vox[a] = (fixed_mm[3 * i + a] - fg->origin[a]) / fg->spacing[a];
+        sample_field(pg, phi, vox, u);
+        double d2 = 0.0;
+        for (int a = 0; a < fg->ndim; ++a) {
+            const double mapped = (vox[a] + u[a]) * mg->spacing[a] + mg->origin[a];
+            const double diff = mapped - moving_mm[3 * i + a];
+            d2 += diff * diff;
+        }
+        const double d = sqrt(d2);
+        dist[i] = d;
+        *mean += d;
+        *mx = *mx > d ? *mx : d;
+    }
+    if (n > 0) *mean /= (double)n;
+    return 0;
+}

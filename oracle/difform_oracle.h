@@ -75,6 +75,12 @@ int orc_register(const dfm_grid* g, const double* fixed, const double* moving,
                  const dfm_config* cfg, const double* scales, const int32_t* iters,
                  int32_t nscales, const dfm_init* init, double* out_field,
                  dfm_iter_record* records, int64_t max_records, dfm_runlog* log);
+int orc_overlap_report(const dfm_grid* gw, const int32_t* warped, const dfm_grid* gf,
+                       const int32_t* fixed, dfm_overlap_summary* rep,
+                       dfm_region_overlap* regions, int64_t cap);
+int orc_landmark_error(const dfm_grid* fg, const dfm_grid* mg, const dfm_grid* pg,
+                       const double* phi, int64_t n, const double* fixed_mm,
+                       const double* moving_mm, double* dist, double* mean, double* mx);
 int orc_overlap_dice(const dfm_grid* g, const int32_t* warped, const int32_t* fixed,
                      double* mo_mean, double* mo_klein);
 

@@ -393,4 +393,62 @@ int dfmref_overlap_dice(const dfm_grid* g, const int32_t* warped, const int32_t*
     });
 }
 
+int dfmref_overlap_report(const dfm_grid* gw, const int32_t* warped, const dfm_grid* gf,
+                          const int32_t* fixed, dfm_overlap_summary* rep,
+                          dfm_region_overlap* regions, int64_t cap) {
+    return guarded([&] {
+        LabelImage W, F;
+        W.meta = to_meta(gw);
+        F.meta = to_meta(gf);
+        W.data.assign(warped, warped + W.meta.voxel_count());
+        F.data.assign(fixed, fixed + F.meta.voxel_count());
+        const OverlapReport r = overlap_report(W, F);
+        rep->to_mean = r.to_mean;
+        rep->mo_mean = r.mo_mean;
+        rep->fn_mean = r.fn_mean;
+        rep->fp_mean = r.fp_mean;
+        rep->vs_mean = r.vs_mean;
+        rep->to_klein = r.to_klein;
+        rep->mo_klein = r.mo_klein;
+        rep->fn_klein = r.fn_klein;
+        rep->fp_klein = r.fp_klein;
+        rep->vs_klein = r.vs_klein;
+        rep->n_regions = static_cast<int64_t>(r.regions.size());
+        for (size_t k = 0; k < r.regions.size() && static_cast<int64_t>(k) < cap; ++k) {
+            const RegionOverlap& q = r.regions[k];
+            dfm_region_overlap& o = regions[k];
+            o.label = q.label;
+            o.has_to = q.has_to;
+            o.has_fn = q.has_fn;
+            o.has_fp = q.has_fp;
+            o.fixed_count = q.fixed_count;
+            o.warped_count = q.warped_count;
+            o.intersection = q.intersection;
+            o.to = q.to;
+            o.mo = q.mo;
+            o.fn = q.fn;
+            o.fp = q.fp;
+            o.vs = q.vs;
+        }
+    });
+}
+
+int dfmref_landmark_error(const dfm_grid* fg, const dfm_grid* mg, const dfm_grid* pg,
+                          const double* phi, int64_t n, const double* fixed_mm,
+                          const double* moving_mm, double* dist, double* mean, double* mx) {
+    return guarded([&] {
+        LandmarkSet a(static_cast<size_t>(n)), b(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i)
+            for (int k = 0; k < 3; ++k) {
+                a[static_cast<size_t>(i)].point_mm[k] = fixed_mm[3 * i + k];
+                b[static_cast<size_t>(i)].point_mm[k] = moving_mm[3 * i + k];
+            }
+        const LandmarkErrors r =
+            landmark_error(a, b, to_field(pg, phi), to_meta(fg), to_meta(mg));
+        for (int64_t i = 0; i < n; ++i) dist[i] = r.distances_mm[static_cast<size_t>(i)];
+        *mean = r.mean;
+        *mx = r.max;
+    });
+}
+
 }  // extern "C"

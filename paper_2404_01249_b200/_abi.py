@@ -71,6 +71,19 @@ class dfm_affine_result(C.Structure):
                 ("loss", C.c_double), ("diverged", C.c_int32), ("iterations", C.c_int64)]
 
 
+class dfm_region_overlap(C.Structure):
+    _fields_ = [("label", C.c_int32), ("has_to", C.c_int32), ("has_fn", C.c_int32),
+                ("has_fp", C.c_int32), ("fixed_count", C.c_int64), ("warped_count", C.c_int64),
+                ("intersection", C.c_int64), ("to", C.c_double), ("mo", C.c_double),
+                ("fn", C.c_double), ("fp", C.c_double), ("vs", C.c_double)]
+
+
+class dfm_overlap_summary(C.Structure):
+    _fields_ = [(k, C.c_double) for k in ("to_mean", "mo_mean", "fn_mean", "fp_mean", "vs_mean",
+                                          "to_klein", "mo_klein", "fn_klein", "fp_klein",
+                                          "vs_klein")] + [("n_regions", C.c_int64)]
+
+
 # --------------------------------------------------------------------------
 # host-side value types (difform::GridMeta / RegistrationConfig / ...)
 
@@ -223,6 +236,9 @@ PROTOS = {
     "warp_labels": [_G, _I, _D, _I],
     "compose": [_G, _D, _D, _D],
     "exp_map": [_G, _D, C.c_int, _D],
+    "overlap_report": [_G, _I, _G, _I, C.POINTER(dfm_overlap_summary),
+                       C.POINTER(dfm_region_overlap), C.c_int64],
+    "landmark_error": [_G, _G, _G, _D, C.c_int64, _D, _D, _D, _D, _D],
     "affine_to_field": [_G, _D, _D, _D],
     "affine_param_gradient": [_G, _D, _D, C.c_int, _D, _D, _D, C.c_int, _D, _D, _D],
     "affine_register": [_G, _D, _D, C.c_int, _D, _I, C.c_int32, C.c_double, C.c_int,
@@ -389,6 +405,31 @@ class HostAPI:
         d = g.ndim
         return dict(A=np.array(r.A[:d * d]).reshape(d, d), t=np.array(r.t[:d]), loss=r.loss,
                     diverged=bool(r.diverged), iterations=int(r.iterations))
+
+    def overlap_report(self, g, warped, fixed, gf=None, max_regions=4096):
+        """overlap_report (analysis.hpp:67) -> dict(summary..., regions=[dict])."""
+        w = np.ascontiguousarray(warped, dtype=np.int32).ravel()
+        f = np.ascontiguousarray(fixed, dtype=np.int32).ravel()
+        rep = dfm_overlap_summary()
+        regs = (dfm_region_overlap * max_regions)()
+        self.t.call("overlap_report", C.byref(g.c()), _ipptr(w), C.byref((gf or g).c()),
+                    _ipptr(f), C.byref(rep), regs, max_regions)
+        out = {k: getattr(rep, k) for k, _ in dfm_overlap_summary._fields_}
+        out["regions"] = [{k: getattr(regs[i], k) for k, _ in dfm_region_overlap._fields_}
+                          for i in range(min(rep.n_regions, max_regions))]
+        return out
+
+    def landmark_error(self, fixed_grid, moving_grid, phi, fixed_mm, moving_mm):
+        """landmark_error (analysis.hpp:77-79) -> (distances_mm, mean, max)."""
+        phi = as_f64(phi, fixed_grid.field_shape)
+        a = np.ascontiguousarray(fixed_mm, dtype=np.float64).reshape(-1, 3)
+        b = np.ascontiguousarray(moving_mm, dtype=np.float64).reshape(-1, 3)
+        dist = np.zeros(len(a))
+        mean, mx = C.c_double(), C.c_double()
+        self.t.call("landmark_error", C.byref(fixed_grid.c()), C.byref(moving_grid.c()),
+                    C.byref(fixed_grid.c()), _dptr(phi), len(a), _dptr(a), _dptr(b), _dptr(dist),
+                    C.byref(mean), C.byref(mx))
+        return dist, mean.value, mx.value
 
     def exp_map(self, g, v, M):
         """exp_map (diffeo.hpp:19-20, diffeo.cpp:66-77): scaling and squaring."""

@@ -292,6 +292,12 @@ template <class T>
 void launch_affine_grad(const Launch& L, CPlanes3<T> g, Dims d, AffineS S, double* partials,
                         double* out12);
 
+// -------- evaluation epilogue (kernels_eval.cu): label maxima and per-label
+// counts (3 rows of maxl+1: |S_l|, |T_l|, |S_l n T_l|) for overlap_report
+int launch_label_max(const Launch& L, const int32_t* a, const int32_t* b, int64_t n, int* out);
+void launch_label_hist(const Launch& L, const int32_t* warped, const int32_t* fixed, int64_t n,
+                       int maxl, unsigned long long* counts);
+
 // -------- loop control
 // kind: 0 ssd, 1 lncc, 2 dice (3 partial arrays of np each)
 void launch_monitor(const Launch& L, int kind, const double* partials, int np, double nvox,

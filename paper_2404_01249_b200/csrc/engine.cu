@@ -5,6 +5,7 @@
 // dfm_ctx owns a CUDA stream, a named workspace arena (grown on demand, reused
 // across calls), two captured CUDA graphs per pyramid scale (ping-pong of the
 // displacement buffers) and an event pool for optional per-kernel timing.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
@@ -869,6 +870,189 @@ dfm_status dfm_affine_register(dfm_ctx* ctx, const dfm_grid* g, const double* fi
                     fail(DFM_E_NUMERICAL, "affine_register: transform collapsed (|det A| < 1e-3)");
             }
         });
+    });
+}
+
+// ---------------------------------------------------------------------------
+// evaluation epilogue (analysis.cpp:169-283)
+
+}  // extern "C"
+
+// analysis.cpp:192-246 from the device label counts (integers: exact)
+static void assemble_overlap(const std::vector<unsigned long long>& c, int maxl,
+                             dfm_overlap_summary* rep, dfm_region_overlap* regions, int64_t cap) {
+    const size_t L = static_cast<size_t>(maxl) + 1;
+    *rep = dfm_overlap_summary{};
+    int64_t ps = 0, pt = 0, pi = 0, pfn = 0, pfp = 0, nr = 0;
+    int to_n = 0, fp_n = 0, vs_n = 0;
+    for (size_t l = 1; l < L; ++l) {
+        const int64_t S = static_cast<int64_t>(c[l]), T = static_cast<int64_t>(c[L + l]),
+                      I = static_cast<int64_t>(c[2 * L + l]);
+        if (S == 0 && T == 0) continue;
+        dfm_region_overlap r{};
+        r.label = static_cast<int32_t>(l);
+        r.warped_count = S;
+        r.fixed_count = T;
+        r.intersection = I;
+        const int64_t fn = T - I, fp = S - I;
+        if (T > 0) {
+            r.has_to = r.has_fn = 1;
+            r.to = static_cast<double>(I) / static_cast<double>(T);
+            r.fn = static_cast<double>(fn) / static_cast<double>(T);
+            rep->to_mean += r.to;
+            rep->fn_mean += r.fn;
+            ++to_n;
+        }
+        if (S > 0) {
+            r.has_fp = 1;
+            r.fp = static_cast<double>(fp) / static_cast<double>(S);
+            rep->fp_mean += r.fp;
+            ++fp_n;
+        }
+        const int64_t den = S + T;
+        r.mo = 2.0 * static_cast<double>(I) / static_cast<double>(den);
+        r.vs = 2.0 * static_cast<double>(S - T) / static_cast<double>(den);
+        rep->mo_mean += r.mo;
+        rep->vs_mean += r.vs;
+        ++vs_n;
+        ps += S;
+        pt += T;
+        pi += I;
+        pfn += fn;
+        pfp += fp;
+        if (regions && nr < cap) regions[nr] = r;
+        ++nr;
+    }
+    if (to_n > 0) {
+        rep->to_mean /= to_n;
+        rep->fn_mean /= to_n;
+    }
+    if (fp_n > 0) rep->fp_mean /= fp_n;
+    if (vs_n > 0) {
+        rep->mo_mean /= vs_n;
+        rep->vs_mean /= vs_n;
+    }
+    if (pt > 0) {
+        rep->to_klein = static_cast<double>(pi) / static_cast<double>(pt);
+        rep->fn_klein = static_cast<double>(pfn) / static_cast<double>(pt);
+    }
+    if (ps > 0) rep->fp_klein = static_cast<double>(pfp) / static_cast<double>(ps);
+    if (ps + pt > 0) {
+        rep->mo_klein = 2.0 * static_cast<double>(pi) / static_cast<double>(ps + pt);
+        rep->vs_klein = 2.0 * static_cast<double>(ps - pt) / static_cast<double>(ps + pt);
+    }
+    rep->n_regions = nr;
+}
+
+static void overlap_dev(dfm_ctx* ctx, int64_t n, const int32_t* dw, const int32_t* df,
+                        dfm_overlap_summary* out, dfm_region_overlap* regions, int64_t cap) {
+    int* dmax = ctx->arr<int>("ev_max", 1);
+    launch_label_max(ctx->L(), dw, df, n, dmax);
+    int maxl = 0;
+    CK(cudaMemcpyAsync(&maxl, dmax, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    if (maxl >= (1 << 24)) fail(DFM_E_INVALID, "overlap_report: label values >= 2^24 unsupported");
+    const size_t L = static_cast<size_t>(maxl) + 1;
+    auto* cnt = ctx->arr<unsigned long long>("ev_counts", static_cast<int64_t>(3 * L));
+    launch_label_hist(ctx->L(), dw, df, n, maxl, cnt);
+    std::vector<unsigned long long> h(3 * L);
+    CK(cudaMemcpyAsync(h.data(), cnt, sizeof(unsigned long long) * 3 * L, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    ctx->sync();
+    assemble_overlap(h, maxl, out, regions, cap);
+}
+
+extern "C" {
+
+dfm_status dfm_overlap_report(dfm_ctx* ctx, const dfm_grid* gw, const int32_t* warped,
+                              const dfm_grid* gf, const int32_t* fixed, dfm_overlap_summary* out,
+                              dfm_region_overlap* regions, int64_t max_regions) {
+    return guarded([&] {
+        validate_grid(gw);
+        validate_grid(gf);
+        if (!same_grid(gw, gf)) fail(DFM_E_INVALID, "overlap_report: grid mismatch");
+        const Dims d = to_dims(gw);
+        int32_t* dw = ctx->arr<int32_t>("ev_w", d.n);
+        int32_t* df = ctx->arr<int32_t>("ev_f", d.n);
+        CK(cudaMemcpyAsync(dw, warped, sizeof(int32_t) * d.n, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(df, fixed, sizeof(int32_t) * d.n, cudaMemcpyHostToDevice, ctx->stream));
+        overlap_dev(ctx, d.n, dw, df, out, regions, max_regions);
+    });
+}
+
+dfm_status dfm_dev_overlap_report(dfm_ctx* ctx, const dfm_grid* g, const int32_t* d_warped,
+                                  const int32_t* d_fixed, dfm_overlap_summary* out,
+                                  dfm_region_overlap* regions, int64_t max_regions) {
+    return guarded([&] {
+        validate_grid(g);
+        overlap_dev(ctx, to_dims(g).n, d_warped, d_fixed, out, regions, max_regions);
+    });
+}
+
+dfm_status dfm_dev_warp_labels(dfm_ctx* ctx, const dfm_grid* g, const int32_t* d_labels,
+                               const void* d_field_soa, int32_t* d_out) {
+    return guarded([&] {
+        validate_grid(g);
+        const Dims d = to_dims(g);
+        DFM_DISPATCH(ctx, {
+            const T* u = static_cast<const T*>(d_field_soa);
+            launch_warp_labels<T>(ctx->L(), d_labels, CPlanes3<T>{{u, u + d.n, u + 2 * d.n}}, d,
+                                  d_out);
+            ctx->sync();
+        });
+    });
+}
+
+dfm_status dfm_landmark_error(dfm_ctx* ctx, const dfm_grid* fg, const dfm_grid* mg,
+                              const dfm_grid* pg, const double* phi, int64_t n,
+                              const double* fixed_mm, const double* moving_mm, double* dist,
+                              double* mean, double* mx) {
+    return guarded([&] {
+        validate_grid(fg);
+        validate_grid(mg);
+        validate_grid(pg);
+        if (!same_grid(pg, fg))
+            fail(DFM_E_INVALID, "landmark_error: field must live on the fixed grid");
+        if (n < 0) fail(DFM_E_INVALID, "landmark_error: negative landmark count");
+        *mean = 0.0;
+        *mx = 0.0;
+        if (n == 0) return;
+        const Dims d = to_dims(pg);
+        // fixed-space mm -> fixed voxel coordinates (analysis.cpp:262-266)
+        std::vector<double> vox(3 * static_cast<size_t>(n), 0.0);
+        for (int64_t i = 0; i < n; ++i)
+            for (int a = 0; a < fg->ndim; ++a)
+                vox[3 * i + a] = (fixed_mm[3 * i + a] - fg->origin[a]) / fg->spacing[a];
+        std::vector<double> u(3 * static_cast<size_t>(n), 0.0);
+        DFM_DISPATCH(ctx, {
+            Field<T> f = dev_field<T>(ctx, "api_f0", d.n);
+            upload_field<T>(ctx, phi, d.n, d.ndim, f);
+            double* dp = ctx->arr<double>("lm_pts", 3 * n);
+            double* dv = ctx->arr<double>("lm_vals", 3 * n);
+            CK(cudaMemcpyAsync(dp, vox.data(), sizeof(double) * 3 * n, cudaMemcpyHostToDevice,
+                               ctx->stream));
+            for (int c = 0; c < d.ndim; ++c)  // sample_field = per-component lerp
+                launch_sample_points<T>(ctx->L(), f.p[c], d, dp, n, dv + c * n, nullptr);
+            std::vector<double> hv(3 * static_cast<size_t>(n));
+            CK(cudaMemcpyAsync(hv.data(), dv, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+            ctx->sync();
+            for (int64_t i = 0; i < n; ++i)
+                for (int c = 0; c < d.ndim; ++c) u[3 * i + c] = hv[c * n + i];
+        });
+        for (int64_t i = 0; i < n; ++i) {  // analysis.cpp:267-279
+            double d2 = 0.0;
+            for (int a = 0; a < fg->ndim; ++a) {
+                const double mapped = (vox[3 * i + a] + u[3 * i + a]) * mg->spacing[a] + mg->origin[a];
+                const double diff = mapped - moving_mm[3 * i + a];
+                d2 += diff * diff;
+            }
+            const double dd = std::sqrt(d2);
+            dist[i] = dd;
+            *mean += dd;
+            *mx = std::max(*mx, dd);
+        }
+        *mean /= static_cast<double>(n);
     });
 }
 

@@ -34,7 +34,8 @@ EXPORTS = [
     "dfm_dev_register", "dfm_ctx_set_profiling", "dfm_ctx_kernel_times",
     "dfm_slab_bounds", "dfm_slab_halo", "dfm_slab_unique_id", "dfm_dev_register_slab",
     "dfm_ctx_set_option", "dfm_exp_map", "dfm_svf_pullback", "dfm_affine_to_field",
-    "dfm_affine_param_gradient", "dfm_affine_register",
+    "dfm_affine_param_gradient", "dfm_affine_register", "dfm_overlap_report",
+    "dfm_dev_overlap_report", "dfm_dev_warp_labels", "dfm_landmark_error",
 ]
 
 OPT_BRICK_MAX = 1
@@ -73,6 +74,13 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         lib.dfm_downsample_grid.restype = C.c_int
         lib.dfm_ctx_set_profiling.argtypes = [C.c_void_p, C.c_int]
         lib.dfm_ctx_set_profiling.restype = C.c_int
+        lib.dfm_dev_warp_labels.argtypes = [C.c_void_p, C.POINTER(A.dfm_grid), C.c_void_p,
+                                            C.c_void_p, C.c_void_p]
+        lib.dfm_dev_warp_labels.restype = C.c_int
+        lib.dfm_dev_overlap_report.argtypes = [
+            C.c_void_p, C.POINTER(A.dfm_grid), C.c_void_p, C.c_void_p,
+            C.POINTER(A.dfm_overlap_summary), C.POINTER(A.dfm_region_overlap), C.c_int64]
+        lib.dfm_dev_overlap_report.restype = C.c_int
         lib.dfm_ctx_set_option.argtypes = [C.c_void_p, C.c_int, C.c_int64]
         lib.dfm_ctx_set_option.restype = C.c_int
         lib.dfm_ctx_kernel_times.argtypes = [C.c_void_p, C.POINTER(C.c_double),

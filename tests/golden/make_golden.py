@@ -127,8 +127,43 @@ def affine_golden(ref):
     np.savez_compressed(os.path.join(HERE, "affine.npz"), **out)
 
 
+def eval_golden(ref):
+    """overlap_report / landmark_error (analysis.cpp:169-283)."""
+    rng = np.random.default_rng(99)
+    out = {}
+    gf = A.GridMeta(3, (21, 17, 13), (1.2, 0.9, 1.5), (3.0, -2.0, 10.0))
+    gm = A.GridMeta(3, (21, 17, 13), (1.1, 1.0, 1.4), (-1.0, 4.0, 0.5))
+    lab_f = rng.integers(-1, 9, gf.shape).astype(np.int32)      # includes 0 / negative
+    lab_w = np.where(rng.random(gf.shape) < 0.7, lab_f,
+                     rng.integers(0, 12, gf.shape)).astype(np.int32)  # labels only in one map
+    r = ref.overlap_report(gf, lab_w, lab_f)
+    out["lab_f"], out["lab_w"] = lab_f, lab_w
+    for k, v in r.items():
+        if k != "regions":
+            out[f"ov_{k}"] = np.array(v)
+    out["ov_regions"] = np.array([[q[k] for k, _ in A.dfm_region_overlap._fields_]
+                                  for q in r["regions"]], dtype=np.float64)
+    phi = f32(rng.normal(0, 2.0, gf.field_shape))
+    npts = 40
+    lo = np.array(gf.origin)
+    hi = lo + (np.array(gf.dims) - 1) * np.array(gf.spacing)
+    fixed_mm = rng.uniform(lo - 3, hi + 3, (npts, 3))              # some outside the grid
+    moving_mm = fixed_mm + rng.normal(0, 2.0, (npts, 3))
+    dist, mean, mx = ref.landmark_error(gf, gm, phi, fixed_mm, moving_mm)
+    out.update(dict(phi=phi, fixed_mm=fixed_mm, moving_mm=moving_mm, lm_dist=dist,
+                    lm_mean=np.array(mean), lm_max=np.array(mx)))
+    for tag, g in (("f", gf), ("m", gm)):
+        out[f"{tag}_dims"], out[f"{tag}_spacing"], out[f"{tag}_origin"] = (
+            np.array(g.dims), np.array(g.spacing), np.array(g.origin))
+    np.savez_compressed(os.path.join(HERE, "eval.npz"), **out)
+
+
 def main():
     ref = pyoracle.reference()
+    if "--only-eval" in sys.argv:
+        eval_golden(ref)
+        print("eval golden vectors written to", HERE)
+        return
     if "--only-affine" in sys.argv:
         affine_golden(ref)
         print("affine golden vectors written to", HERE)
@@ -139,6 +174,7 @@ def main():
         return
     svf_golden(ref)
     affine_golden(ref)
+    eval_golden(ref)
     C = cases()
     for tag in ("3d", "2d"):
         c = C[tag]

@@ -145,3 +145,17 @@ def affine_register_inputs():
     z = load("affine.npz")
     g = A.GridMeta(3, tuple(int(v) for v in z["reg_dims"]))
     return z, g
+
+
+def eval_inputs():
+    z = load("eval.npz")
+    gf = A.GridMeta(3, tuple(int(v) for v in z["f_dims"]), tuple(z["f_spacing"]),
+                    tuple(z["f_origin"]))
+    gm = A.GridMeta(3, tuple(int(v) for v in z["m_dims"]), tuple(z["m_spacing"]),
+                    tuple(z["m_origin"]))
+    return z, gf, gm
+
+
+def region_rows(rep):
+    return np.array([[q[k] for k, _ in A.dfm_region_overlap._fields_] for q in rep["regions"]],
+                    dtype=np.float64)

@@ -94,6 +94,20 @@ def test_restatement_affine_errors(oracle_port):
         pass
 
 
+def test_restatement_overlap_and_landmarks_bitwise(oracle_port):
+    """overlap_report (analysis.cpp:169-247) incl. negative / one-sided labels,
+    and landmark_error (249-283) on grids with spacing and origin."""
+    z, gf, gm = G.eval_inputs()
+    r = oracle_port.overlap_report(gf, z["lab_w"], z["lab_f"])
+    for k, v in r.items():
+        if k != "regions":
+            assert v == float(z[f"ov_{k}"]), k
+    assert np.array_equal(G.region_rows(r), z["ov_regions"])
+    dist, mean, mx = oracle_port.landmark_error(gf, gm, z["phi"], z["fixed_mm"], z["moving_mm"])
+    assert np.array_equal(dist, z["lm_dist"])
+    assert mean == float(z["lm_mean"]) and mx == float(z["lm_max"])
+
+
 def test_restatement_early_stop_record_count(oracle_port):
     """test_pipeline.cpp:69-93 semantics: default window 10 on a self pair."""
     z = G.load("register_self.npz")
