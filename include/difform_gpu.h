@@ -328,6 +328,45 @@ DFM_API dfm_status dfm_landmark_error(dfm_ctx* ctx, const dfm_grid* fixed_grid,
                                       const double* moving_mm, double* distances, double* mean,
                                       double* max);
 
+/* ---- hyperparameter sweep (pipeline.hpp:75-104, pipeline.cpp:226-313) -- */
+/* difform::SweepPair: images on one grid (host AoS doubles); labels optional
+ * (NULL) unless the metric is overlap. */
+typedef struct {
+    const dfm_grid* grid;
+    const double* fixed;
+    const double* moving;
+    const int32_t* fixed_labels;
+    const int32_t* moving_labels;
+} dfm_sweep_pair;
+
+/* difform::SweepRow */
+typedef struct {
+    double eta, sigma_warp, sigma_grad;
+    double metric_mean, metric_sd;
+    double wall_ms;
+    int32_t failed;
+    int32_t computed;     /* 1 for the rows of this call's shard */
+    char error[256];
+} dfm_sweep_row;
+
+typedef enum { DFM_SWEEP_LOSS = 0, DFM_SWEEP_OVERLAP = 1 } dfm_sweep_metric;
+
+/* sweep: grid eta x sigma_warp x sigma_grad (config k = (ei * n_sw + wi) *
+ * n_sg + gi, as pipeline.cpp:254-257); each config registers every pair;
+ * metric = final loss or overlap TO mean (analysis.cpp), mean and SD over the
+ * pairs; failures are recorded per row.  Configs run concurrently on
+ * `ndevices` GPUs x `workers_per_device` contexts (the reference's worker
+ * threads, one CUDA stream each); pairs are uploaded once per context.  Only
+ * configs k = shard_begin + j * shard_step are computed (multi-process
+ * sharding; 0, 1 = all).  rows has n_eta * n_sw * n_sg entries. */
+DFM_API dfm_status dfm_sweep(const int* devices, int ndevices, int workers_per_device,
+                             int precision, const dfm_sweep_pair* pairs, int npairs,
+                             const dfm_config* base, const double* scales,
+                             const int32_t* iterations, int32_t nscales, const double* etas,
+                             int n_eta, const double* sigma_warps, int n_sw,
+                             const double* sigma_grads, int n_sg, int metric,
+                             int64_t shard_begin, int64_t shard_step, dfm_sweep_row* rows);
+
 /* ---- z-slab decomposition (BASELINE config 4) ------------ */
 /* Owned planes [zlo, zhi) and halo depths (hlo, hhi) of slab `part` of
  * `nparts` over nz planes with halo H: out = {zlo, zhi, hlo, hhi}. */

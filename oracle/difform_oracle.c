@@ -1416,3 +1416,77 @@ int orc_landmark_error(const dfm_grid* fg, const dfm_grid* mg, const dfm_grid* p
     if (n > 0) *mean /= (double)n;
     return 0;
 }
+
+/* pipeline.cpp:226-313 sweep, serial (workers = 1): config k = (ei*n_sw + wi)*n_sg + gi */
+int orc_sweep(const dfm_sweep_pair* pairs, int npairs, const dfm_config* base,
+              const double* scales, const int32_t* iters, int32_t nscales, const double* etas,
+              int n_eta, const double* sws, int n_sw, const double* sgs, int n_sg, int metric,
+              dfm_sweep_row* rows) {
+    if (npairs < 1) return fail(1, "sweep: at least one image pair required");
+    if (n_eta < 1 || n_sw < 1 || n_sg < 1) return fail(1, "sweep: grid axes must be non-empty");
+    if (metric == DFM_SWEEP_OVERLAP)
+        for (int p = 0; p < npairs; ++p)
+            if (!pairs[p].fixed_labels || !pairs[p].moving_labels)
+                return fail(1, "sweep: overlap metric needs label maps on every pair");
+    const int64_t n_cfg = (int64_t)n_eta * n_sw * n_sg;
+    int64_t cap = 1;
+    for (int i = 0; i < nscales; ++i) cap += iters[i];
+    dfm_iter_record* recs = calloc((size_t)cap, sizeof(dfm_iter_record));
+    for (int64_t k = 0; k < n_cfg; ++k) {
+        const int64_t gi = k % n_sg, wi = (k / n_sg) % n_sw, ei = k / ((int64_t)n_sg * n_sw);
+        dfm_sweep_row* row = &rows[k];
+        memset(row, 0, sizeof(*row));
+        row->eta = etas[ei];
+        row->sigma_warp = sws[wi];
+        row->sigma_grad = sgs[gi];
+        row->computed = 1;
+        dfm_config cfg = *base;
+        cfg.eta = row->eta;
+        cfg.sigma_warp = row->sigma_warp;
+        cfg.sigma_grad = row->sigma_grad;
+        cfg.seed = base->seed + (uint64_t)k;
+        const double t0 = now_ms();
+        double sum = 0.0, sum2 = 0.0;
+        int failed = 0;
+        for (int p = 0; p < npairs && !failed; ++p) {
+            const dfm_grid* g = pairs[p].grid;
+            const int64_t n = nvox(g);
+            double* phi = dalloc(n * g->ndim);
+            dfm_runlog log;
+            double m = 0.0;
+            int rc = orc_register(g, pairs[p].fixed, pairs[p].moving, &cfg, scales, iters, nscales,
+                                  NULL, phi, recs, cap, &log);
+            if (!rc) {
+                if (metric == DFM_SWEEP_LOSS) {
+                    m = log.final_loss;
+                } else {
+                    int32_t* w = calloc((size_t)n, sizeof(int32_t));
+                    orc_warp_labels(g, pairs[p].moving_labels, phi, w);
+                    dfm_overlap_summary rep;
+                    orc_overlap_report(g, w, g, pairs[p].fixed_labels, &rep, NULL, 0);
+                    m = rep.to_mean;
+                    free(w);
+                }
+            } else {
+                failed = 1;
+                orc_last_error(row->error, sizeof(row->error));
+            }
+            free(phi);
+            sum += m;
+            sum2 += m * m;
+        }
+        if (failed) {
+            row->failed = 1;
+            row->metric_mean = NAN;
+            row->metric_sd = NAN;
+        } else {
+            const double nn = (double)npairs;
+            row->metric_mean = sum / nn;
+            const double v = sum2 / nn - row->metric_mean * row->metric_mean;
+            row->metric_sd = sqrt(v > 0.0 ? v : 0.0);
+        }
+        row->wall_ms = now_ms() - t0;
+    }
+    free(recs);
+    return 0;
+}

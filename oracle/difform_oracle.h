@@ -81,6 +81,10 @@ int orc_overlap_report(const dfm_grid* gw, const int32_t* warped, const dfm_grid
 int orc_landmark_error(const dfm_grid* fg, const dfm_grid* mg, const dfm_grid* pg,
                        const double* phi, int64_t n, const double* fixed_mm,
                        const double* moving_mm, double* dist, double* mean, double* mx);
+int orc_sweep(const dfm_sweep_pair* pairs, int npairs, const dfm_config* base,
+              const double* scales, const int32_t* iters, int32_t nscales, const double* etas,
+              int n_eta, const double* sws, int n_sw, const double* sgs, int n_sg, int metric,
+              dfm_sweep_row* rows);
 int orc_overlap_dice(const dfm_grid* g, const int32_t* warped, const int32_t* fixed,
                      double* mo_mean, double* mo_klein);
 

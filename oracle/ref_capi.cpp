@@ -393,6 +393,53 @@ int dfmref_overlap_dice(const dfm_grid* g, const int32_t* warped, const int32_t*
     });
 }
 
+int dfmref_sweep(const dfm_sweep_pair* pairs, int npairs, const dfm_config* base,
+                 const double* scales, const int32_t* iters, int32_t nscales, const double* etas,
+                 int n_eta, const double* sws, int n_sw, const double* sgs, int n_sg, int metric,
+                 int workers, dfm_sweep_row* rows) {
+    return guarded([&] {
+        std::vector<SweepPair> ps(static_cast<size_t>(npairs));
+        for (int p = 0; p < npairs; ++p) {
+            ps[p].fixed = to_image(pairs[p].grid, pairs[p].fixed);
+            ps[p].moving = to_image(pairs[p].grid, pairs[p].moving);
+            const int64_t n = ps[p].fixed.meta.voxel_count();
+            if (pairs[p].fixed_labels) {
+                LabelImage L;
+                L.meta = ps[p].fixed.meta;
+                L.data.assign(pairs[p].fixed_labels, pairs[p].fixed_labels + n);
+                ps[p].fixed_labels = L;
+            }
+            if (pairs[p].moving_labels) {
+                LabelImage L;
+                L.meta = ps[p].fixed.meta;
+                L.data.assign(pairs[p].moving_labels, pairs[p].moving_labels + n);
+                ps[p].moving_labels = L;
+            }
+        }
+        PyramidSchedule sched;
+        sched.scales.assign(scales, scales + nscales);
+        sched.iterations.assign(iters, iters + nscales);
+        const SweepResult r =
+            sweep(ps, to_cfg(base), sched, std::vector<double>(etas, etas + n_eta),
+                  std::vector<double>(sws, sws + n_sw), std::vector<double>(sgs, sgs + n_sg),
+                  metric == DFM_SWEEP_OVERLAP ? SweepMetric::overlap : SweepMetric::loss, workers);
+        for (size_t k = 0; k < r.rows.size(); ++k) {
+            dfm_sweep_row& o = rows[k];
+            std::memset(&o, 0, sizeof(o));
+            const SweepRow& q = r.rows[k];
+            o.eta = q.eta;
+            o.sigma_warp = q.sigma_warp;
+            o.sigma_grad = q.sigma_grad;
+            o.metric_mean = q.metric_mean;
+            o.metric_sd = q.metric_sd;
+            o.wall_ms = q.wall_ms;
+            o.failed = q.failed ? 1 : 0;
+            o.computed = 1;
+            std::strncpy(o.error, q.error.c_str(), sizeof(o.error) - 1);
+        }
+    });
+}
+
 int dfmref_overlap_report(const dfm_grid* gw, const int32_t* warped, const dfm_grid* gf,
                           const int32_t* fixed, dfm_overlap_summary* rep,
                           dfm_region_overlap* regions, int64_t cap) {

@@ -84,6 +84,21 @@ class dfm_overlap_summary(C.Structure):
                                           "vs_klein")] + [("n_regions", C.c_int64)]
 
 
+class dfm_sweep_pair(C.Structure):
+    _fields_ = [("grid", C.c_void_p), ("fixed", C.POINTER(C.c_double)),
+                ("moving", C.POINTER(C.c_double)), ("fixed_labels", C.POINTER(C.c_int32)),
+                ("moving_labels", C.POINTER(C.c_int32))]
+
+
+class dfm_sweep_row(C.Structure):
+    _fields_ = [("eta", C.c_double), ("sigma_warp", C.c_double), ("sigma_grad", C.c_double),
+                ("metric_mean", C.c_double), ("metric_sd", C.c_double), ("wall_ms", C.c_double),
+                ("failed", C.c_int32), ("computed", C.c_int32), ("error", C.c_char * 256)]
+
+
+SWEEP_LOSS, SWEEP_OVERLAP = 0, 1
+
+
 # --------------------------------------------------------------------------
 # host-side value types (difform::GridMeta / RegistrationConfig / ...)
 

@@ -32,6 +32,16 @@ namespace {
 
 thread_local std::string g_err;
 
+}  // namespace
+
+// the thread's error message, for host modules built on the C-ABI (sweep.cu)
+dfm_status dfm_internal_set_error(dfm_status code, const char* msg) {
+    g_err = msg;
+    return code;
+}
+
+namespace {
+
 struct DfmError {
     int code;
     std::string msg;

@@ -35,7 +35,7 @@ EXPORTS = [
     "dfm_slab_bounds", "dfm_slab_halo", "dfm_slab_unique_id", "dfm_dev_register_slab",
     "dfm_ctx_set_option", "dfm_exp_map", "dfm_svf_pullback", "dfm_affine_to_field",
     "dfm_affine_param_gradient", "dfm_affine_register", "dfm_overlap_report",
-    "dfm_dev_overlap_report", "dfm_dev_warp_labels", "dfm_landmark_error",
+    "dfm_dev_overlap_report", "dfm_dev_warp_labels", "dfm_landmark_error", "dfm_sweep",
 ]
 
 OPT_BRICK_MAX = 1
