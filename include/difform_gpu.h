@@ -367,6 +367,39 @@ DFM_API dfm_status dfm_sweep(const int* devices, int ndevices, int workers_per_d
                              const double* sigma_grads, int n_sg, int metric,
                              int64_t shard_begin, int64_t shard_step, dfm_sweep_row* rows);
 
+/* ---- MetaImage I/O (io.hpp; io.cpp:117-328 format) ---------------------- */
+typedef enum { DFM_MET_OTHER = -1, DFM_MET_FLOAT = 0, DFM_MET_SHORT = 1 } dfm_met_type;
+typedef struct {
+    dfm_grid grid;
+    int32_t element_type;         /* dfm_met_type */
+    int32_t channels;
+    char element_type_name[32];
+    char raw_path[1024];          /* ElementDataFile resolved against the header dir */
+} dfm_mhd_info;
+/* read_mhd_header (io.cpp:152-216); errors "path: byte N: ..." -> DFM_E_INVALID */
+DFM_API dfm_status dfm_mhd_read_header(const char* path, dfm_mhd_info* out);
+/* write_image_mhd / read_image_mhd (io.cpp:245-269): MET_FLOAT, 1 channel.
+ * Readers: out == NULL queries the grid; capacity in elements. */
+DFM_API dfm_status dfm_mhd_write_image(const char* path, const dfm_grid* g, const double* img);
+DFM_API dfm_status dfm_mhd_read_image(const char* path, dfm_grid* g, double* out,
+                                      int64_t capacity);
+/* write_labels_mhd / read_labels_mhd (io.cpp:271-304): MET_SHORT */
+DFM_API dfm_status dfm_mhd_write_labels(const char* path, const dfm_grid* g,
+                                        const int32_t* labels);
+DFM_API dfm_status dfm_mhd_read_labels(const char* path, dfm_grid* g, int32_t* out,
+                                       int64_t capacity);
+/* write_field_mhd / read_field_mhd (io.cpp:306-328): MET_FLOAT, ndim channels */
+DFM_API dfm_status dfm_mhd_write_field(const char* path, const dfm_grid* g, const double* field);
+DFM_API dfm_status dfm_mhd_read_field(const char* path, dfm_grid* g, double* out,
+                                      int64_t capacity);
+/* Streaming device feed: an MET_FLOAT image straight into HBM (context
+ * precision) through pinned double-buffered chunks; d_out == NULL queries the
+ * grid.  And a device SoA field (as dfm_dev_register writes it) to .mhd/.raw. */
+DFM_API dfm_status dfm_dev_load_image_mhd(dfm_ctx* ctx, const char* path, dfm_grid* g,
+                                          void* d_out);
+DFM_API dfm_status dfm_dev_save_field_mhd(dfm_ctx* ctx, const char* path, const dfm_grid* g,
+                                          const void* d_field_soa);
+
 /* ---- z-slab decomposition (BASELINE config 4) ------------ */
 /* Owned planes [zlo, zhi) and halo depths (hlo, hhi) of slab `part` of
  * `nparts` over nz planes with halo H: out = {zlo, zhi, hlo, hhi}. */

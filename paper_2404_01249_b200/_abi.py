@@ -97,6 +97,12 @@ class dfm_sweep_row(C.Structure):
 
 
 SWEEP_LOSS, SWEEP_OVERLAP = 0, 1
+MET_OTHER, MET_FLOAT, MET_SHORT = -1, 0, 1
+
+
+class dfm_mhd_info(C.Structure):
+    _fields_ = [("grid", dfm_grid), ("element_type", C.c_int32), ("channels", C.c_int32),
+                ("element_type_name", C.c_char * 32), ("raw_path", C.c_char * 1024)]
 
 
 # --------------------------------------------------------------------------

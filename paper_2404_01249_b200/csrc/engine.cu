@@ -118,6 +118,21 @@ struct dfm_ctx {
         return hstate;
     }
 
+    std::map<std::string, std::pair<void*, size_t>> pinned;  // page-locked host staging
+    void* get_pinned(const std::string& name, size_t bytes) {
+        auto it = pinned.find(name);
+        if (it != pinned.end() && it->second.second >= bytes) return it->second.first;
+        if (it != pinned.end()) {
+            CK(cudaStreamSynchronize(stream));
+            CK(cudaFreeHost(it->second.first));
+            pinned.erase(it);
+        }
+        void* p = nullptr;
+        CK(cudaMallocHost(&p, bytes));
+        pinned[name] = {p, bytes};
+        return p;
+    }
+
     void* get(const std::string& name, size_t bytes) {
         if (bytes == 0) bytes = 16;
         auto it = bufs.find(name);
@@ -537,6 +552,7 @@ void dfm_ctx_destroy(dfm_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     for (auto& kv : ctx->bufs) cudaFree(kv.second.first);
+    for (auto& kv : ctx->pinned) cudaFreeHost(kv.second.first);
     if (ctx->hstate) cudaFreeHost(ctx->hstate);
     for (int k = 0; k < 2; ++k)
         if (ctx->chunk_ev[k]) cudaEventDestroy(ctx->chunk_ev[k]);
@@ -547,6 +563,26 @@ void dfm_ctx_destroy(dfm_ctx* ctx) {
 int dfm_ctx_precision(const dfm_ctx* ctx) { return ctx ? ctx->prec : -1; }
 void* dfm_ctx_stream(dfm_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
 int64_t dfm_ctx_launch_count(const dfm_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+}  // extern "C"
+
+// context plumbing for host modules (mhd_io.cu): precision + stream, named
+// device ("name") or pinned host ("@pinned:name") buffers, launch counting
+dfm_status dfm_internal_ctx_info(dfm_ctx* ctx, int* precision, cudaStream_t* stream) {
+    if (!ctx) return DFM_E_INVALID;
+    CK(cudaSetDevice(ctx->device));
+    *precision = ctx->prec;
+    *stream = ctx->stream;
+    return DFM_OK;
+}
+void* dfm_internal_ctx_buffer(dfm_ctx* ctx, const char* name, size_t bytes) {
+    const std::string n(name);
+    if (n.rfind("@pinned:", 0) == 0) return ctx->get_pinned(n, bytes);
+    return ctx->get(n, bytes);
+}
+void dfm_internal_bump(dfm_ctx* ctx) { ++ctx->launches; }
+
+extern "C" {
 
 dfm_status dfm_ctx_set_profiling(dfm_ctx* ctx, int enable) {
     return guarded([&] {

@@ -36,6 +36,9 @@ EXPORTS = [
     "dfm_ctx_set_option", "dfm_exp_map", "dfm_svf_pullback", "dfm_affine_to_field",
     "dfm_affine_param_gradient", "dfm_affine_register", "dfm_overlap_report",
     "dfm_dev_overlap_report", "dfm_dev_warp_labels", "dfm_landmark_error", "dfm_sweep",
+    "dfm_mhd_read_header", "dfm_mhd_write_image", "dfm_mhd_read_image", "dfm_mhd_write_labels",
+    "dfm_mhd_read_labels", "dfm_mhd_write_field", "dfm_mhd_read_field", "dfm_dev_load_image_mhd",
+    "dfm_dev_save_field_mhd",
 ]
 
 OPT_BRICK_MAX = 1
@@ -81,6 +84,10 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
             C.c_void_p, C.POINTER(A.dfm_grid), C.c_void_p, C.c_void_p,
             C.POINTER(A.dfm_overlap_summary), C.POINTER(A.dfm_region_overlap), C.c_int64]
         lib.dfm_dev_overlap_report.restype = C.c_int
+        lib.dfm_dev_load_image_mhd.argtypes = [C.c_void_p, C.c_char_p, C.POINTER(A.dfm_grid),
+                                               C.c_void_p]
+        lib.dfm_dev_save_field_mhd.argtypes = [C.c_void_p, C.c_char_p, C.POINTER(A.dfm_grid),
+                                               C.c_void_p]
         lib.dfm_ctx_set_option.argtypes = [C.c_void_p, C.c_int, C.c_int64]
         lib.dfm_ctx_set_option.restype = C.c_int
         lib.dfm_ctx_kernel_times.argtypes = [C.c_void_p, C.POINTER(C.c_double),
