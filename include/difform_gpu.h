@@ -450,6 +450,11 @@ DFM_API dfm_status dfm_ctx_kernel_times(const dfm_ctx* ctx, double* ms, int64_t*
  * one persistent cooperative launch per level; 0 = one CUDA graph per
  * iteration (default 0: measured faster).  Env DFM_PERSIST. */
 #define DFM_OPT_PERSIST 3
+/* DFM_OPT_PDL: 1 = the loop kernels use programmatic dependent
+ * launch (each kernel's CTAs are scheduled while its predecessor drains and
+ * wait on griddepcontrol); 0 (default, measured no faster) = plain stream
+ * order.  Env DFM_PDL. */
+#define DFM_OPT_PDL 4
 DFM_API dfm_status dfm_ctx_set_option(dfm_ctx* ctx, int key, int64_t value);
 
 #ifdef __cplusplus

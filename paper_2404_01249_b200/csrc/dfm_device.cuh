@@ -30,6 +30,16 @@ struct Dims {
     __host__ __device__ bool is3d() const { return nz > 1; }
 };
 
+// Programmatic dependent launch (sm_90+): a kernel launched with
+// programmatic stream serialization may start while its predecessor drains;
+// pdl_wait() blocks until the predecessor grid has completed and its writes
+// are visible (a no-op for a normally launched kernel); pdl_trigger() lets the
+// successor's CTAs be scheduled once every CTA of this grid has issued it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 template <class T>
 struct Planes3 {  // SoA vector field
     T* c[3];

@@ -73,10 +73,29 @@ struct Launch {
     cudaStream_t stream;
     int64_t* counter;  // incremented per kernel launch (host side)
     int num_sms;
+    bool pdl = false;  // launch the loop kernels with programmatic dependent launch
     void bump() const {
         if (counter) ++*counter;
     }
 };
+
+// Launches `kern` with programmatic stream serialization when L.pdl (the
+// kernel must call pdl_wait() before touching its predecessor's outputs).
+template <class Kern, class... Args>
+inline cudaError_t launch_maybe_pdl(const Launch& L, Kern kern, dim3 grid, dim3 block,
+                                    size_t smem, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = L.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = L.pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
 
 // Gaussian weights of one smoothing call (interp.cpp:114-123), per axis, padded
 // with zero taps to a common radius; norm = 1 / (in-range tap sum) per position.

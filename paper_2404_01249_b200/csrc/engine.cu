@@ -107,7 +107,8 @@ struct dfm_ctx {
     LoopState* hstate = nullptr;  // 2 pinned slots for the chunked launch loop
     cudaEvent_t chunk_ev[2] = {nullptr, nullptr};
 
-    Launch L() { return Launch{stream, &launches, num_sms}; }
+    bool pdl = getenv("DFM_PDL") ? atoi(getenv("DFM_PDL")) != 0 : false;
+    Launch L() { return Launch{stream, &launches, num_sms, pdl}; }
 
     LoopState* pinned_state() {
         if (!hstate) {
@@ -601,6 +602,8 @@ dfm_status dfm_ctx_set_option(dfm_ctx* ctx, int key, int64_t value) {
             ctx->force_legacy = value != 0;
         } else if (key == DFM_OPT_PERSIST) {
             ctx->persist = value != 0;
+        } else if (key == DFM_OPT_PDL) {
+            ctx->pdl = value != 0;
         } else {
             fail(DFM_E_INVALID, "unknown context option %d", key);
         }

@@ -66,7 +66,7 @@ struct BrickLayout {
 // One brick of one op: stage, x, y, z passes, per-voxel epilogue and the
 // CTA reduction; op.finish(b, ...) records brick b's partial.  Ends with the
 // CTA's threads synchronised (smem reusable).
-template <class Op>
+template <class Op, int NTB>
 __device__ __forceinline__ void brick_body(const Op& op, const BG& g, int b, unsigned char* smem,
                                            double* s_red) {
     using Lay = BrickLayout<Op>;
@@ -194,8 +194,10 @@ template <class Op>
 __global__ void __launch_bounds__(NTB, 2) k_brick(const __grid_constant__ Op op, const BG g) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double s_red[32];
+    pdl_trigger();
+    pdl_wait();
     if (op.skip()) return;
-    brick_body(op, g, blockIdx.x, smem, s_red);
+    brick_body<Op, NTB>(op, g, blockIdx.x, smem, s_red);
     if constexpr (Op::kSum) {
         if (op.mon.st)
             monitor_tail<NTB>(op.mon, op.partials, gridDim.x,
@@ -482,8 +484,10 @@ struct PersistArgs {
     double tol;
 };
 
+constexpr int NTP = 256;  // persistent solver: 2 CTAs of 256 threads per SM
+
 template <class T, int R, int RG, int RW>
-__global__ void __launch_bounds__(NTB, 1)
+__global__ void __launch_bounds__(NTP, 2)
     k_persist(const __grid_constant__ PersistArgs<T, R, RG, RW> a, const BG g, int nb) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
@@ -494,11 +498,11 @@ __global__ void __launch_bounds__(NTB, 1)
     int nupd = 0;
     for (int it = 0; it < a.iters; ++it) {
         // loss: fused LNCC forward over every brick
-        for (int b = blockIdx.x; b < nb; b += gridDim.x) brick_body(a.fwd, g, b, smem, s_red);
+        for (int b = blockIdx.x; b < nb; b += gridDim.x) brick_body<decltype(a.fwd), NTP>(a.fwd, g, b, smem, s_red);
         grid.sync();
         double acc = 0.0;
-        for (int k = threadIdx.x; k < nb; k += NTB) acc += __ldcg(a.fwd.partials + k);
-        const double v = -bsum<NTB>(acc, s_red) / nvox;
+        for (int k = threadIdx.x; k < nb; k += NTP) acc += __ldcg(a.fwd.partials + k);
+        const double v = -bsum<NTP>(acc, s_red) / nvox;
         // the monitor's decision (monitor_commit), taken identically by all CTAs
         const int slot = it;
         bool stop = !isfinite(v);
@@ -510,9 +514,9 @@ __global__ void __launch_bounds__(NTB, 1)
         if (blockIdx.x == 0 && threadIdx.x == 0)
             monitor_commit(st, v, 0.0, 0.0, a.loss, a.stamp, a.window, a.tol);
         if (stop) break;
-        for (int b = blockIdx.x; b < nb; b += gridDim.x) brick_body(a.bwd, g, b, smem, s_red);
+        for (int b = blockIdx.x; b < nb; b += gridDim.x) brick_body<decltype(a.bwd), NTP>(a.bwd, g, b, smem, s_red);
         grid.sync();  // also publishes CTA 0's st->t / st->slot to the Adam prologue
-        for (int b = blockIdx.x; b < nb; b += gridDim.x) brick_body(a.sa, g, b, smem, s_red);
+        for (int b = blockIdx.x; b < nb; b += gridDim.x) brick_body<decltype(a.sa), NTP>(a.sa, g, b, smem, s_red);
         grid.sync();
         if (*reinterpret_cast<volatile int*>(&st->bad_step)) {  // diffeo.cpp:52-53
             if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -526,7 +530,7 @@ __global__ void __launch_bounds__(NTB, 1)
             co.u = a.co.uout;
             co.uout = const_cast<T*>(a.co.u);
         }
-        for (int b = blockIdx.x; b < nb; b += gridDim.x) brick_body(co, g, b, smem, s_red);
+        for (int b = blockIdx.x; b < nb; b += gridDim.x) brick_body<decltype(co), NTP>(co, g, b, smem, s_red);
         ++nupd;
         grid.sync();
     }
@@ -552,7 +556,7 @@ int run_persist(const Launch& L, const PersistArgs<T, R, RG, RW>& a, const Dims&
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(bytes));
             if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_persist<T, R, RG, RW>,
-                                                              NTB, bytes) != cudaSuccess)
+                                                              NTP, bytes) != cudaSuccess)
                 per_sm = 0;
         });
         if (per_sm < 1) return -3;
@@ -565,7 +569,7 @@ int run_persist(const Launch& L, const PersistArgs<T, R, RG, RW>& a, const Dims&
         const int grid = nb < cap ? nb : cap;
         void* args[] = {const_cast<A*>(&a), &g, &nb};
         const cudaError_t e = cudaLaunchCooperativeKernel(
-            reinterpret_cast<const void*>(k_persist<T, R, RG, RW>), dim3(grid), dim3(NTB), args,
+            reinterpret_cast<const void*>(k_persist<T, R, RG, RW>), dim3(grid), dim3(NTP), args,
             bytes, L.stream);
         if (e != cudaSuccess) {
             cudaGetLastError();
@@ -592,7 +596,7 @@ int run_brick(const Launch& L, const Op& op, const Dims& d) {
     g.nbx = (d.nx + BX - 1) / BX;
     g.nby = (d.ny + BY - 1) / BY;
     const int nb = g.nbx * g.nby * ((d.nz + BZ - 1) / BZ);
-    k_brick<Op><<<nb, NTB, Lay::bytes, L.stream>>>(op, g);
+    launch_maybe_pdl(L, k_brick<Op>, dim3(nb), dim3(NTB), Lay::bytes, op, g);
     L.bump();
     return nb;
     }

@@ -19,6 +19,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 
 #include "dfm_device.cuh"
@@ -44,6 +45,19 @@ constexpr int TX = kTX, TY = kTY, NT = TX * TY;
 #endif
 #ifndef DFM_S_CO_EXTRA
 #define DFM_S_CO_EXTRA 0
+#endif
+// CTA tile heights (rows of 32 columns) per op; overridable for tuning builds
+#ifndef DFM_TY_FWD
+#define DFM_TY_FWD 8
+#endif
+#ifndef DFM_TY_BWD
+#define DFM_TY_BWD 8
+#endif
+#ifndef DFM_TY_SA
+#define DFM_TY_SA 16
+#endif
+#ifndef DFM_TY_CO
+#define DFM_TY_CO 8
 #endif
 
 template <class T>
@@ -78,6 +92,8 @@ __global__ void __launch_bounds__(TX * Op::TYv) k_zm2(const __grid_constant__ Op
     __shared__ __align__(8) uint64_t bars[S];
     __shared__ double s_red[32];
 
+    pdl_trigger();  // successor CTAs may be scheduled into our tail
+    pdl_wait();     // predecessor's outputs (and LoopState) are visible from here
     if (op.skip()) return;
     const Dims& d = g.d;
     const int tid = threadIdx.x;
@@ -239,7 +255,7 @@ struct NoProl {};
 struct NoCarry {};
 
 // similarity.cpp:122-168 — box moments of F and W = M(x+u), window coefficients
-template <class T, int R_, int TY_ = 8>
+template <class T, int R_, int TY_ = DFM_TY_FWD>
 struct LnccFwd2 {
     using Acc = double;
     using Center = NoCenter;
@@ -311,7 +327,7 @@ struct LnccFwd2 {
 };
 
 // similarity.cpp:170-189 — box sums of the coefficients, dW, grad = dW * G
-template <class T, int R_, int TY_ = 8>
+template <class T, int R_, int TY_ = DFM_TY_BWD>
 struct LnccBwd2 {
     using Acc = double;
     using Prol = NoProl;
@@ -378,7 +394,7 @@ struct LnccBwd2 {
 };
 
 // pipeline.cpp:182-186 + optim.cpp:22-42 + diffeo.cpp:47-57
-template <class T, int R_, int TY_ = 16>
+template <class T, int R_, int TY_ = DFM_TY_SA>
 struct SmoothAdam2 {
     using Acc = T;
     using Carry = NoCarry;
@@ -476,7 +492,7 @@ struct SmoothAdam2 {
 // Gaussian, then W = M(x+u') and G = grad M(x+u') for the next loss pass.  The
 // M gather of plane zo is issued at its emit and consumed at the emit of plane
 // zo+1 (Carry), so its latency hides behind a whole plane of work.
-template <class T, int R_, int CAPH, int TY_ = 8>
+template <class T, int R_, int CAPH, int TY_ = DFM_TY_CO>
 struct Compose2 {
     using Acc = T;
     using Center = NoCenter;
@@ -787,11 +803,16 @@ int run_zm2(const Launch& L, const Op& op, Dims d) {
     }
     g.tiles_x = (d.nx + TX - 1) / TX;
     const int tiles = g.tiles_x * ((d.ny + Op::TYv - 1) / Op::TYv);
-    const int slots = occ * (L.num_sms > 0 ? L.num_sms : 148);
+    // resident-CTA slots the chunking may plan for (DFM_SLOT_CAP caps CTAs per
+    // SM: beyond ~2 the per-SM issue rate saturates and extra chunks only add
+    // halo planes)
+    static const int slot_cap = getenv("DFM_SLOT_CAP") ? atoi(getenv("DFM_SLOT_CAP")) : 0;
+    const int per_sm = slot_cap > 0 && slot_cap < occ ? slot_cap : occ;
+    const int slots = per_sm * (L.num_sms > 0 ? L.num_sms : 148);
     Dims dr = d;  // chunk the produced plane range only
     dr.nz = d.out_end() - d.out_begin();
     const int nchunks = pick_chunks(dr, tiles, slots, 2 * Op::R + Op::BACK + Op::AHEAD, &g.zchunk);
-    k_zm2<Op><<<dim3(tiles, nchunks), TX * Op::TYv, smem, L.stream>>>(op, g);
+    launch_maybe_pdl(L, k_zm2<Op>, dim3(tiles, nchunks), dim3(TX * Op::TYv), smem, op, g);
     L.bump();
     return tiles * nchunks;
 }

@@ -44,6 +44,7 @@ EXPORTS = [
 OPT_BRICK_MAX = 1
 OPT_FORCE_LEGACY = 2
 OPT_PERSIST = 3
+OPT_PDL = 4
 
 _lib: Optional[C.CDLL] = None
 

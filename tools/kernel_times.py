@@ -16,12 +16,15 @@ prec = sys.argv[5] if len(sys.argv) > 5 else "f32"
 p = synth.make_pair(1, seed=0, shape=(nx, ny, nz), iters=(iters,))
 sched = A.PyramidSchedule((1.0,), (iters,))
 cfg = synth.baseline_config(A.LOSS_LNCC, 2, 1.0, max_iters=iters)
-for fam, bm in (("stream", 0), ("brick", 1 << 40)):
+for fam, bm in [("stream", 0), ("brick", 1 << 40)][:int(os.environ.get("KT_FAMS", "2"))]:
     ctx = Context(0, prec)
     ctx.set_option(OPT_BRICK_MAX, bm)
     ctx.set_option(OPT_PERSIST, 0)
     ctx.set_profiling(True)
-    ctx.register_images(p.grid, p.fixed, p.moving, cfg, sched)
+    try:
+        ctx.register_images(p.grid, p.fixed, p.moving, cfg, sched)
+    except A.NumericalError:
+        pass  # a single full-resolution level from identity may fold: timings still stand
     kt = ctx.kernel_times()
     parts = []
     for k in ("loss_fwd", "lncc_bwd", "smooth_adam", "compose_smooth"):
