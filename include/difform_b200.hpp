@@ -17,6 +17,8 @@
 #pragma once
 
 #include <array>
+#include <algorithm>
+#include <optional>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -444,6 +446,261 @@ inline std::pair<DisplacementField, RunLog> register_images(
                                   r.max_step, r.wall_ms});
     }
     return {std::move(phi), std::move(log)};
+}
+
+// ---- diffeo.hpp: SVF -----------------------------------------------------------
+using VelocityField = VectorField;
+
+inline DisplacementField exp_map(const VelocityField& v, int M) {
+    const dfm_grid g = gpu::grid(v.meta);
+    DisplacementField out = gpu::field_like(v.meta);
+    gpu::check(dfm_exp_map(gpu::ctx(), &g, v.data.data(), M, out.data.data()));
+    return out;
+}
+
+inline VectorField svf_pullback(const VelocityField& v, const VectorField& grad_phi, int M) {
+    if (!v.meta.same_grid(grad_phi.meta))
+        throw std::invalid_argument("svf_pullback: grid mismatch");
+    const dfm_grid g = gpu::grid(v.meta);
+    VectorField out = gpu::field_like(v.meta);
+    gpu::check(dfm_svf_pullback(gpu::ctx(), &g, v.data.data(), grad_phi.data.data(), M,
+                                out.data.data()));
+    return out;
+}
+
+// ---- affine.hpp ----------------------------------------------------------------
+struct AffineResult {
+    AffineTransform transform;
+    double loss = 0.0;
+    bool diverged = false;
+    int64_t iterations = 0;
+};
+
+struct AffineGrad {
+    double value = 0.0;
+    std::array<double, 9> dA{};
+    std::array<double, 3> dt{};
+};
+
+inline AffineTransform identity_affine(int ndim) {
+    AffineTransform T;
+    T.ndim = ndim;
+    T.A.fill(0.0);
+    for (int i = 0; i < ndim; ++i) T.A[static_cast<size_t>(i * ndim + i)] = 1.0;
+    T.t = {0.0, 0.0, 0.0};
+    return T;
+}
+
+inline double affine_det(const AffineTransform& T) {
+    const auto& a = T.A;
+    if (T.ndim == 2) return a[0] * a[3] - a[1] * a[2];
+    return a[0] * (a[4] * a[8] - a[5] * a[7]) - a[1] * (a[3] * a[8] - a[5] * a[6]) +
+           a[2] * (a[3] * a[7] - a[4] * a[6]);
+}
+
+inline DisplacementField affine_to_field(const AffineTransform& T, const GridMeta& meta) {
+    if (T.ndim != meta.ndim)
+        throw std::invalid_argument("affine_to_field: dimensionality mismatch");
+    const dfm_grid g = gpu::grid(meta);
+    DisplacementField out = gpu::field_like(meta);
+    gpu::check(dfm_affine_to_field(gpu::ctx(), &g, T.A.data(), T.t.data(), out.data.data()));
+    return out;
+}
+
+inline AffineGrad affine_param_gradient(const ScalarImage& fixed, const ScalarImage& moving,
+                                        LossKind loss, const AffineTransform& T,
+                                        const std::array<double, 3>& scale_to_full,
+                                        int lncc_radius = 2) {
+    const dfm_grid g = gpu::grid(fixed.meta);
+    AffineGrad r;
+    gpu::check(dfm_affine_param_gradient(gpu::ctx(), &g, fixed.data.data(), moving.data.data(),
+                                         static_cast<int>(loss), T.A.data(), T.t.data(),
+                                         scale_to_full.data(), lncc_radius, &r.value,
+                                         r.dA.data(), r.dt.data()));
+    return r;
+}
+
+inline AffineResult affine_register(const ScalarImage& fixed, const ScalarImage& moving,
+                                    LossKind loss, const std::vector<double>& scales,
+                                    const std::vector<int>& iters, double eta,
+                                    int lncc_radius = 2) {
+    if (!fixed.meta.same_grid(moving.meta))
+        throw std::invalid_argument("affine_register: images must share a grid");
+    if (scales.size() != iters.size() || scales.empty())
+        throw std::invalid_argument("affine_register: bad schedule");
+    const dfm_grid g = gpu::grid(fixed.meta);
+    std::vector<int32_t> it(iters.begin(), iters.end());
+    dfm_affine_result r{};
+    gpu::check(dfm_affine_register(gpu::ctx(), &g, fixed.data.data(), moving.data.data(),
+                                   static_cast<int>(loss), scales.data(), it.data(),
+                                   static_cast<int32_t>(scales.size()), eta, lncc_radius, &r));
+    AffineResult out;
+    out.transform.ndim = r.ndim;
+    for (int k = 0; k < 9; ++k) out.transform.A[static_cast<size_t>(k)] = r.A[k];
+    for (int k = 0; k < 3; ++k) out.transform.t[static_cast<size_t>(k)] = r.t[k];
+    out.loss = r.loss;
+    out.diverged = r.diverged != 0;
+    out.iterations = r.iterations;
+    return out;
+}
+
+// ---- analysis.hpp: evaluation ------------------------------------------------------
+struct RegionOverlap {
+    int32_t label = 0;
+    int64_t fixed_count = 0, warped_count = 0, intersection = 0;
+    bool has_to = false;
+    double to = 0.0, mo = 0.0;
+    bool has_fn = false;
+    double fn = 0.0;
+    bool has_fp = false;
+    double fp = 0.0, vs = 0.0;
+};
+
+struct OverlapReport {
+    std::vector<RegionOverlap> regions;
+    double to_mean = 0.0, mo_mean = 0.0, fn_mean = 0.0, fp_mean = 0.0, vs_mean = 0.0;
+    double to_klein = 0.0, mo_klein = 0.0, fn_klein = 0.0, fp_klein = 0.0, vs_klein = 0.0;
+};
+
+inline OverlapReport overlap_report(const LabelImage& warped, const LabelImage& fixed) {
+    const dfm_grid gw = gpu::grid(warped.meta), gf = gpu::grid(fixed.meta);
+    dfm_overlap_summary s{};
+    std::vector<dfm_region_overlap> regs(1024);
+    for (;;) {
+        gpu::check(dfm_overlap_report(gpu::ctx(), &gw, warped.data.data(), &gf,
+                                      fixed.data.data(), &s, regs.data(),
+                                      static_cast<int64_t>(regs.size())));
+        if (s.n_regions <= static_cast<int64_t>(regs.size())) break;
+        regs.resize(static_cast<size_t>(s.n_regions));
+    }
+    OverlapReport r;
+    r.to_mean = s.to_mean;
+    r.mo_mean = s.mo_mean;
+    r.fn_mean = s.fn_mean;
+    r.fp_mean = s.fp_mean;
+    r.vs_mean = s.vs_mean;
+    r.to_klein = s.to_klein;
+    r.mo_klein = s.mo_klein;
+    r.fn_klein = s.fn_klein;
+    r.fp_klein = s.fp_klein;
+    r.vs_klein = s.vs_klein;
+    for (int64_t k = 0; k < s.n_regions; ++k) {
+        const dfm_region_overlap& q = regs[static_cast<size_t>(k)];
+        r.regions.push_back({q.label, q.fixed_count, q.warped_count, q.intersection,
+                             q.has_to != 0, q.to, q.mo, q.has_fn != 0, q.fn, q.has_fp != 0,
+                             q.fp, q.vs});
+    }
+    return r;
+}
+
+struct Landmark {
+    std::array<double, 3> point_mm{0.0, 0.0, 0.0};
+    std::string id;
+};
+using LandmarkSet = std::vector<Landmark>;
+
+struct LandmarkErrors {
+    std::vector<double> distances_mm;
+    double mean = 0.0;
+    double max = 0.0;
+};
+
+inline LandmarkErrors landmark_error(const LandmarkSet& fixed_pts, const LandmarkSet& moving_pts,
+                                     const DisplacementField& phi, const GridMeta& fixed_meta,
+                                     const GridMeta& moving_meta) {
+    if (fixed_pts.size() != moving_pts.size())
+        throw std::invalid_argument("landmark_error: landmark counts differ");
+    const dfm_grid gf = gpu::grid(fixed_meta), gm = gpu::grid(moving_meta),
+                   gp = gpu::grid(phi.meta);
+    std::vector<double> a, b;
+    for (size_t i = 0; i < fixed_pts.size(); ++i)
+        for (int k = 0; k < 3; ++k) {
+            a.push_back(fixed_pts[i].point_mm[static_cast<size_t>(k)]);
+            b.push_back(moving_pts[i].point_mm[static_cast<size_t>(k)]);
+        }
+    LandmarkErrors r;
+    r.distances_mm.resize(fixed_pts.size());
+    gpu::check(dfm_landmark_error(gpu::ctx(), &gf, &gm, &gp, phi.data.data(),
+                                  static_cast<int64_t>(fixed_pts.size()), a.data(), b.data(),
+                                  r.distances_mm.data(), &r.mean, &r.max));
+    return r;
+}
+
+// ---- pipeline.hpp: sweep --------------------------------------------------------
+enum class SweepMetric { loss, overlap };
+
+struct SweepPair {
+    ScalarImage fixed, moving;
+    std::optional<LabelImage> fixed_labels, moving_labels;
+    std::string name;
+};
+
+struct SweepRow {
+    double eta = 0.0, sigma_warp = 0.0, sigma_grad = 0.0;
+    double metric_mean = 0.0, metric_sd = 0.0;
+    double wall_ms = 0.0;
+    bool failed = false;
+    std::string error;
+};
+
+struct SweepResult {
+    std::vector<SweepRow> rows;
+    std::vector<std::vector<std::vector<double>>> heatmaps;
+    std::vector<double> etas, sigma_warps, sigma_grads;
+};
+
+// `workers` maps to worker contexts on the current device (the reference's
+// worker threads); difform::gpu::set_sweep_devices() spreads them over GPUs.
+inline std::vector<int>& sweep_devices() {
+    static std::vector<int> d{0};
+    return d;
+}
+
+inline SweepResult sweep(const std::vector<SweepPair>& pairs, const RegistrationConfig& base,
+                         const PyramidSchedule& sched, const std::vector<double>& etas,
+                         const std::vector<double>& sigma_warps,
+                         const std::vector<double>& sigma_grads, SweepMetric metric,
+                         int workers) {
+    std::vector<dfm_grid> grids;
+    grids.reserve(pairs.size());
+    std::vector<dfm_sweep_pair> ps;
+    for (const SweepPair& p : pairs) {
+        grids.push_back(gpu::grid(p.fixed.meta));
+        ps.push_back({&grids.back(), p.fixed.data.data(), p.moving.data.data(),
+                      p.fixed_labels ? p.fixed_labels->data.data() : nullptr,
+                      p.moving_labels ? p.moving_labels->data.data() : nullptr});
+    }
+    const dfm_config c = gpu::config(base);
+    std::vector<int32_t> it(sched.iterations.begin(), sched.iterations.end());
+    const size_t n_cfg = etas.size() * sigma_warps.size() * sigma_grads.size();
+    std::vector<dfm_sweep_row> rows(n_cfg > 0 ? n_cfg : 1);
+    const std::vector<int>& dev = sweep_devices();
+    const int per_dev = std::max(1, workers / static_cast<int>(dev.size()));
+    gpu::check(dfm_sweep(dev.data(), static_cast<int>(dev.size()), per_dev,
+                         gpu::thread_precision(), ps.data(), static_cast<int>(ps.size()), &c,
+                         sched.scales.data(), it.data(), static_cast<int32_t>(it.size()),
+                         etas.data(), static_cast<int>(etas.size()), sigma_warps.data(),
+                         static_cast<int>(sigma_warps.size()), sigma_grads.data(),
+                         static_cast<int>(sigma_grads.size()),
+                         metric == SweepMetric::overlap ? DFM_SWEEP_OVERLAP : DFM_SWEEP_LOSS, 0,
+                         1, rows.data()));
+    SweepResult r;
+    r.etas = etas;
+    r.sigma_warps = sigma_warps;
+    r.sigma_grads = sigma_grads;
+    r.heatmaps.assign(etas.size(), std::vector<std::vector<double>>(
+                                       sigma_warps.size(),
+                                       std::vector<double>(sigma_grads.size(), 0.0)));
+    for (size_t k = 0; k < n_cfg; ++k) {
+        const dfm_sweep_row& q = rows[k];
+        r.rows.push_back({q.eta, q.sigma_warp, q.sigma_grad, q.metric_mean, q.metric_sd,
+                          q.wall_ms, q.failed != 0, q.error});
+        const size_t gi = k % sigma_grads.size();
+        const size_t wi = (k / sigma_grads.size()) % sigma_warps.size();
+        const size_t ei = k / (sigma_grads.size() * sigma_warps.size());
+        r.heatmaps[ei][wi][gi] = q.metric_mean;
+    }
+    return r;
 }
 
 }  // namespace difform

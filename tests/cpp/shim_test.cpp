@@ -79,6 +79,52 @@ int main() {
             threw = true;
         }
         EXPECT(threw);
+        // SVF: exp_map of zero is zero; pullback of zero is zero; SVF registration runs
+        VelocityField v0 = phi2;
+        for (double& x : v0.data) x = 0.0;
+        const DisplacementField e0 = exp_map(v0, 4);
+        for (double x : e0.data) EXPECT(x == 0.0);
+        const VectorField p0 = svf_pullback(phi2, v0, 4);
+        for (double x : p0.data) EXPECT(x == 0.0);
+        RegistrationConfig scfg = cfg;
+        scfg.mode = RegMode::svf;
+        scfg.svf_M = 4;
+        auto [phis, logs] = register_images(F, M, scfg, {{2.0, 1.0}, {10, 10}});
+        EXPECT(logs.iterations.size() == 20u);
+        EXPECT(logs.final_loss < logs.iterations.front().loss);
+
+        // affine: identity maps to a zero field; registration of a shifted copy
+        const DisplacementField az = affine_to_field(identity_affine(3), m);
+        for (double x : az.data) EXPECT(x == 0.0);
+        const AffineResult ar = affine_register(F, M, LossKind::lncc, {2.0, 1.0}, {15, 10}, 0.01);
+        EXPECT(!ar.diverged && ar.iterations == 25);
+        EXPECT(std::abs(affine_det(ar.transform)) > 0.5);
+        const AffineGrad ag =
+            affine_param_gradient(F, M, LossKind::ssd, identity_affine(3), {1.0, 1.0, 1.0});
+        EXPECT(std::isfinite(ag.value) && ag.value > 0.0);
+
+        // evaluation: a label map against itself; landmarks through phi = 0
+        LabelImage L{m, std::vector<int32_t>(static_cast<size_t>(m.voxel_count()), 0)};
+        for (size_t i = 0; i < L.data.size(); ++i) L.data[i] = static_cast<int32_t>(i % 5);
+        const OverlapReport ov = overlap_report(L, L);
+        EXPECT(ov.regions.size() == 4u && ov.mo_mean == 1.0 && ov.vs_klein == 0.0);
+        LandmarkSet a(3), b(3);
+        for (int i = 0; i < 3; ++i) {
+            a[static_cast<size_t>(i)].point_mm = {1.0 + i, 2.0, 3.0};
+            b[static_cast<size_t>(i)].point_mm = {1.0 + i, 2.0, 3.0 + i};
+        }
+        const LandmarkErrors le = landmark_error(a, b, e0, m, m);
+        EXPECT(std::abs(le.max - 2.0) < 1e-12 && std::abs(le.mean - 1.0) < 1e-12);
+
+        // sweep over 2 x 1 x 1 configs on the pair (loss metric)
+        std::vector<SweepPair> pairs(1);
+        pairs[0].fixed = F;
+        pairs[0].moving = M;
+        const SweepResult sw = sweep(pairs, cfg, {{2.0, 1.0}, {5, 5}}, {0.3, 0.6}, {0.5}, {1.0},
+                                     SweepMetric::loss, 2);
+        EXPECT(sw.rows.size() == 2u && !sw.rows[0].failed && !sw.rows[1].failed);
+        EXPECT(sw.heatmaps[1][0][0] == sw.rows[1].metric_mean);
+
         std::printf("precision %s: self records %zu, lncc loss %.5f -> %.5f\n",
                     prec == DFM_PREC_F64 ? "f64" : "f32", log.iterations.size(),
                     log2.iterations.front().loss, log2.final_loss);
