@@ -47,6 +47,32 @@ constexpr int TX = kTX, TY = kTY, NT = TX * TY;
 #define DFM_S_CO_EXTRA 0
 #endif
 // CTA tile heights (rows of 32 columns) per op; overridable for tuning builds
+// minimum resident CTAs per SM requested from ptxas (register budget)
+#ifndef DFM_MINB_FWD
+#define DFM_MINB_FWD 3
+#endif
+#ifndef DFM_MINB_BWD
+#define DFM_MINB_BWD 4
+#endif
+#ifndef DFM_MINB_SA
+#define DFM_MINB_SA 2
+#endif
+#ifndef DFM_MINB_CO
+#define DFM_MINB_CO 3
+#endif
+// rows per thread (coarsening) per op
+#ifndef DFM_CY_FWD
+#define DFM_CY_FWD 1
+#endif
+#ifndef DFM_CY_BWD
+#define DFM_CY_BWD 1
+#endif
+#ifndef DFM_CY_SA
+#define DFM_CY_SA 1
+#endif
+#ifndef DFM_CY_CO
+#define DFM_CY_CO 1
+#endif
 #ifndef DFM_TY_FWD
 #define DFM_TY_FWD 8
 #endif
@@ -73,15 +99,18 @@ struct ZG2 {
 };
 
 // ---------------------------------------------------------------------------
-// the streaming z-march driver.  A CTA is TX x Op::TYv threads, one output
-// column per thread; per-thread constants (norm factors of its x and y, the
-// op's prologue such as Adam bias corrections) are computed once; Op::Carry
-// lets an op defer work of plane zo into plane zo+1 (latency hiding).
+// the streaming z-march driver.  A CTA is TX x (TYv / CY) threads; each thread
+// owns CY output columns of its x (rows ty, ty + TYv/CY, ...): per-plane
+// overheads (barrier, mbarrier wait, loop control, address math) are shared by
+// CY voxels.  Per-thread constants (norm factors, the op's prologue such as
+// Adam bias corrections) are computed once; Op::Carry lets an op defer work of
+// plane zo into plane zo+1 (latency hiding).
 template <class Op>
-__global__ void __launch_bounds__(TX * Op::TYv) k_zm2(const __grid_constant__ Op op,
-                                                      const ZG2 g) {
+__global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
+    k_zm2(const __grid_constant__ Op op, const ZG2 g) {
     using Acc = typename Op::Acc;
-    constexpr int TYv = Op::TYv, NTh = TX * TYv;
+    constexpr int TYv = Op::TYv, CY = Op::kCY, TYt = TYv / CY, NTh = TX * TYt;
+    static_assert(TYt * CY == TYv, "tile rows must be a multiple of the coarsening");
     constexpr int R = Op::R, C = Op::C, S = Op::S, K = 2 * R + 1;
     constexpr int HI = TYv + 2 * R, WI = TX + 2 * R;
     constexpr int SB = Op::kStageBytes;
@@ -102,8 +131,7 @@ __global__ void __launch_bounds__(TX * Op::TYv) k_zm2(const __grid_constant__ Op
     const int y0 = (blockIdx.x / g.tiles_x) * TYv;
     const int z0 = d.out_begin() + blockIdx.y * g.zchunk;
     const int z1 = min(z0 + g.zchunk, d.out_end());
-    const int x = x0 + tx, y = y0 + ty;
-    const bool own = x < d.nx && y < d.ny;
+    const int x = x0 + tx;
     const int q0 = z0 - R - Op::BACK;
     const int qend = z1 + R + Op::AHEAD;
 
@@ -119,119 +147,129 @@ __global__ void __launch_bounds__(TX * Op::TYv) k_zm2(const __grid_constant__ Op
             op.issue(stages + ((q - q0) % S) * SB, &bars[(q - q0) % S], x0, y0, q);
 
     const Acc nxv = x < d.nx ? op.nrm(0, x) : Acc(0);
-    const Acc nyv = own ? op.nrm(1, y) : Acc(0);
+    int yk[CY];
+    bool own[CY];
+    Acc nyv[CY];
+#pragma unroll
+    for (int k = 0; k < CY; ++k) {
+        yk[k] = y0 + ty + k * TYt;
+        own[k] = x < d.nx && yk[k] < d.ny;
+        nyv[k] = own[k] ? op.nrm(1, yk[k]) : Acc(0);
+    }
     const typename Op::Prol pr = op.prologue();
-    typename Op::Carry carry{};
+    typename Op::Carry carry[CY] = {};
 
-    // register ring of the last K xy-filtered planes; the plane loop is
-    // unrolled by K so every ring slot is a compile-time register (no moves)
-    Acc ring[C][K];
+    // register ring of the last K xy-filtered planes per owned row; it shifts
+    // by register moves (C*(K-1) MOVs per plane and row) rather than unrolling
+    // the plane loop by K: the unrolled body overflowed the instruction cache
+    Acc ring[CY][C][K];
 #pragma unroll
-    for (int c = 0; c < C; ++c)
+    for (int r = 0; r < CY; ++r)
 #pragma unroll
-        for (int k = 0; k < K; ++k) ring[c][k] = Acc(0);
+        for (int c = 0; c < C; ++c)
+#pragma unroll
+            for (int k = 0; k < K; ++k) ring[r][c][k] = Acc(0);
     double rsum = 0.0, rmax = 0.0;
     int waited = q0 - 1;
     int buf = 0;
     const int zend = z1 + R;
 
-    // the ring shifts by register moves (C*(K-1) MOVs per plane) rather than
-    // unrolling the plane loop by K: the unrolled body overflowed the
-    // instruction cache (26% no_instruction stalls at the coarse scales)
-    {
-        {
-            for (int zi = z0 - R; zi < zend; ++zi) {
-                constexpr int kk = K - 1;
-                const int zo = zi - R;
-                const bool em = (zo >= z0) && own;
-                typename Op::Center cen;
-                if (em) op.load_center(x, y, zo, cen);
-                while (waited < zi + Op::AHEAD) {
-                    ++waited;
-                    const int k = waited - q0;
-                    mbar_wait(&bars[k % S], (k / S) & 1);
+    for (int zi = z0 - R; zi < zend; ++zi) {
+        constexpr int kk = K - 1;
+        const int zo = zi - R;
+        typename Op::Center cen[CY];
+#pragma unroll
+        for (int r = 0; r < CY; ++r)
+            if (zo >= z0 && own[r]) op.load_center(x, yk[r], zo, cen[r]);
+        while (waited < zi + Op::AHEAD) {
+            ++waited;
+            const int k = waited - q0;
+            mbar_wait(&bars[k % S], (k / S) & 1);
+        }
+        Acc* sx = s_x + buf * (C * HI * TX);
+        if constexpr (Op::kStaged) {
+            const typename Op::PlaneCtx pc = op.plane_ctx(stages, q0, zi);
+            if (op.interior(x0, y0, zi)) {  // CTA-uniform: no clamping, no bounds
+                for (int e = tid; e < HI * WI; e += NTh) {
+                    const int row = e / WI, col = e - row * WI;
+                    Acc v[C];
+                    op.stage_fast(pc, x0, y0, zi, row, col, v);
+#pragma unroll
+                    for (int c = 0; c < C; ++c) s_in[(c * HI + row) * WI + col] = v[c];
                 }
-                Acc* sx = s_x + buf * (C * HI * TX);
-                if constexpr (Op::kStaged) {
-                    const typename Op::PlaneCtx pc = op.plane_ctx(stages, q0, zi);
-                    if (op.interior(x0, y0, zi)) {  // CTA-uniform: no clamping, no bounds
-                        for (int e = tid; e < HI * WI; e += NTh) {
-                            const int row = e / WI, col = e - row * WI;
-                            Acc v[C];
-                            op.stage_fast(pc, x0, y0, zi, row, col, v);
+            } else {
+                for (int e = tid; e < HI * WI; e += NTh) {
+                    const int row = e / WI, col = e - row * WI;
+                    Acc v[C];
+                    op.stage(pc, x0, y0, zi, row, col, v);
 #pragma unroll
-                            for (int c = 0; c < C; ++c) s_in[(c * HI + row) * WI + col] = v[c];
-                        }
-                    } else {
-                        for (int e = tid; e < HI * WI; e += NTh) {
-                            const int row = e / WI, col = e - row * WI;
-                            Acc v[C];
-                            op.stage(pc, x0, y0, zi, row, col, v);
-#pragma unroll
-                            for (int c = 0; c < C; ++c) s_in[(c * HI + row) * WI + col] = v[c];
-                        }
-                    }
-                    __syncthreads();
-#pragma unroll
-                    for (int row = ty; row < HI; row += TYv) {
-#pragma unroll
-                        for (int c = 0; c < C; ++c) {
-                            const Acc* src = s_in + (c * HI + row) * WI + tx;
-                            Acc a = Acc(0);
-#pragma unroll
-                            for (int j = 0; j < K; ++j) a += op.wgt(0, j) * src[j];
-                            sx[(c * HI + row) * TX + tx] = a * nxv;
-                        }
-                    }
-                } else {
-                    const unsigned char* st = stages + ((zi - q0) % S) * SB;
-#pragma unroll
-                    for (int row = ty; row < HI; row += TYv) {
-                        Acc v[C];
-                        op.xpass(st, row, tx, nxv, v);
-#pragma unroll
-                        for (int c = 0; c < C; ++c) sx[(c * HI + row) * TX + tx] = v[c];
-                    }
+                    for (int c = 0; c < C; ++c) s_in[(c * HI + row) * WI + col] = v[c];
                 }
-                __syncthreads();
-                if (tid == 0) {
-                    const int qf = zi - Op::BACK + S;
-                    if (qf < qend) {
-                        const int k = qf - q0;
-                        op.issue(stages + (k % S) * SB, &bars[k % S], x0, y0, qf);
-                    }
-                }
-                // y pass into ring slot kk (the newest plane)
+            }
+            __syncthreads();
+#pragma unroll
+            for (int row = ty; row < HI; row += TYt) {
 #pragma unroll
                 for (int c = 0; c < C; ++c) {
-                    const Acc* src = sx + (c * HI + ty) * TX + tx;
+                    const Acc* src = s_in + (c * HI + row) * WI + tx;
                     Acc a = Acc(0);
 #pragma unroll
-                    for (int j = 0; j < K; ++j) a += op.wgt(1, j) * src[j * TX];
-#pragma unroll
-                    for (int k = 0; k < K - 1; ++k) ring[c][k] = ring[c][k + 1];
-                    ring[c][kk] = a * nyv;
+                    for (int j = 0; j < K; ++j) a += op.wgt(0, j) * src[j];
+                    sx[(c * HI + row) * TX + tx] = a * nxv;
                 }
-                if (em) {
-                    // oldest plane (zo - R) sits in slot 0 (slot (kk + 1) % K)
-                    const Acc nz = op.nrm(2, zo + d.zoff);
-                    Acc sv[C];
+            }
+        } else {
+            const unsigned char* st = stages + ((zi - q0) % S) * SB;
 #pragma unroll
-                    for (int c = 0; c < C; ++c) {
-                        Acc a = Acc(0);
+            for (int row = ty; row < HI; row += TYt) {
+                Acc v[C];
+                op.xpass(st, row, tx, nxv, v);
 #pragma unroll
-                        for (int j = 0; j < K; ++j) a += op.wgt(2, j) * ring[c][(kk + 1 + j) % K];
-                        sv[c] = a * nz;
-                    }
-                    const Red2 r = op.emit(x, y, zo, sv, cen, pr, carry);
-                    rsum += r.sum;
-                    rmax = fmax(rmax, r.mx);
-                }
-                buf ^= 1;
+                for (int c = 0; c < C; ++c) sx[(c * HI + row) * TX + tx] = v[c];
             }
         }
+        __syncthreads();
+        if (tid == 0) {
+            const int qf = zi - Op::BACK + S;
+            if (qf < qend) {
+                const int k = qf - q0;
+                op.issue(stages + (k % S) * SB, &bars[k % S], x0, y0, qf);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < CY; ++r) {
+            // y pass into ring slot kk (the newest plane)
+            const int row = ty + r * TYt;
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                const Acc* src = sx + (c * HI + row) * TX + tx;
+                Acc a = Acc(0);
+#pragma unroll
+                for (int j = 0; j < K; ++j) a += op.wgt(1, j) * src[j * TX];
+#pragma unroll
+                for (int k = 0; k < K - 1; ++k) ring[r][c][k] = ring[r][c][k + 1];
+                ring[r][c][kk] = a * nyv[r];
+            }
+            if (zo >= z0 && own[r]) {
+                // oldest plane (zo - R) sits in slot 0 (slot (kk + 1) % K)
+                const Acc nz = op.nrm(2, zo + d.zoff);
+                Acc sv[C];
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    Acc a = Acc(0);
+#pragma unroll
+                    for (int j = 0; j < K; ++j) a += op.wgt(2, j) * ring[r][c][(kk + 1 + j) % K];
+                    sv[c] = a * nz;
+                }
+                const Red2 rr = op.emit(x, yk[r], zo, sv, cen[r], pr, carry[r]);
+                rsum += rr.sum;
+                rmax = fmax(rmax, rr.mx);
+            }
+        }
+        buf ^= 1;
     }
-    op.flush(carry);
+#pragma unroll
+    for (int r = 0; r < CY; ++r) op.flush(carry[r]);
     if constexpr (Op::kSum || Op::kMax) {
         const int blk = blockIdx.y * gridDim.x + blockIdx.x;
         const double bs = Op::kSum ? bsum<NTh>(rsum, s_red) : 0.0;
@@ -262,6 +300,7 @@ struct LnccFwd2 {
     using Prol = NoProl;
     using Carry = NoCarry;
     static constexpr int R = R_, C = 5, BACK = 0, AHEAD = 0, S = DFM_S_FWD, TYv = TY_;
+    static constexpr int kMinB = DFM_MINB_FWD, kCY = DFM_CY_FWD;
     static constexpr bool kStaged = false, kSum = true, kMax = false;
     static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TYv + 2 * R;
     static constexpr int kBytes = BX * BY * int(sizeof(T));
@@ -333,6 +372,7 @@ struct LnccBwd2 {
     using Prol = NoProl;
     using Carry = NoCarry;
     static constexpr int R = R_, C = 4, BACK = 0, AHEAD = 0, S = DFM_S_BWD, TYv = TY_;
+    static constexpr int kMinB = DFM_MINB_BWD, kCY = DFM_CY_BWD;
     static constexpr bool kStaged = false, kSum = false, kMax = false;
     static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TYv + 2 * R;
     static constexpr int kBytes = BX * BY * int(sizeof(T));
@@ -399,6 +439,7 @@ struct SmoothAdam2 {
     using Acc = T;
     using Carry = NoCarry;
     static constexpr int R = R_, C = 3, BACK = 0, AHEAD = 0, S = DFM_S_SA, TYv = TY_;
+    static constexpr int kMinB = DFM_MINB_SA, kCY = DFM_CY_SA;
     static constexpr bool kStaged = false, kSum = false, kMax = true;
     static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TYv + 2 * R;
     static constexpr int kBytes = BX * BY * int(sizeof(T));
@@ -497,6 +538,7 @@ struct Compose2 {
     using Acc = T;
     using Center = NoCenter;
     using Prol = NoProl;
+    static constexpr int kMinB = DFM_MINB_CO, kCY = DFM_CY_CO;
     static constexpr int R = R_, C = 3, BACK = CAPH, AHEAD = CAPH,
                          S = 2 * CAPH + 2 + DFM_S_CO_EXTRA, TYv = TY_;
     static constexpr bool kStaged = true, kSum = false, kMax = false;
@@ -797,7 +839,8 @@ int run_zm2(const Launch& L, const Op& op, Dims d) {
     if (occ == 0) {
         cudaFuncSetAttribute(k_zm2<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_zm2<Op>, TX * Op::TYv, smem) !=
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_zm2<Op>, TX * Op::TYv / Op::kCY,
+                                                          smem) !=
                 cudaSuccess || occ < 1)
             occ = 1;
     }
@@ -812,7 +855,8 @@ int run_zm2(const Launch& L, const Op& op, Dims d) {
     Dims dr = d;  // chunk the produced plane range only
     dr.nz = d.out_end() - d.out_begin();
     const int nchunks = pick_chunks(dr, tiles, slots, 2 * Op::R + Op::BACK + Op::AHEAD, &g.zchunk);
-    launch_maybe_pdl(L, k_zm2<Op>, dim3(tiles, nchunks), dim3(TX * Op::TYv), smem, op, g);
+    launch_maybe_pdl(L, k_zm2<Op>, dim3(tiles, nchunks), dim3(TX * Op::TYv / Op::kCY), smem, op,
+                     g);
     L.bump();
     return tiles * nchunks;
 }
