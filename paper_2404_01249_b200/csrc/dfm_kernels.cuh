@@ -207,6 +207,14 @@ int launch_lncc_fwd_tma(const Launch& L, int R, const T* F, const T* W, Dims d, 
 template <class T>
 int launch_lncc_bwd_tma(const Launch& L, int R, const T* coef, const T* F, const T* W,
                         const T* G, Dims d, T* grad, const LoopState* st);
+// per-level window statistics of F (fstat: 2 fp64 planes muF, vF), then the
+// 3-moment forward that reads them — bit-identical to launch_lncc_fwd_tma
+template <class T>
+int launch_fstats_tma(const Launch& L, int R, const T* F, Dims d, double* fstat);
+template <class T>
+int launch_lncc_fwd3_tma(const Launch& L, int R, const T* F, const T* W, const double* fstat,
+                         Dims d, T* coef, double* partials, const LoopState* st,
+                         const MonitorArgs* mon = nullptr);
 template <class T>
 int launch_smooth_adam_tma(const Launch& L, int R, const GaussW<T>& w, const T* grad, T* m,
                            T* nu, T* step, Dims d, AdamParams ap, LoopState* st,

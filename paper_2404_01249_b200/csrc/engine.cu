@@ -108,6 +108,8 @@ struct dfm_ctx {
     cudaEvent_t chunk_ev[2] = {nullptr, nullptr};
 
     bool pdl = getenv("DFM_PDL") ? atoi(getenv("DFM_PDL")) != 0 : false;
+    // LNCC forward with per-level F statistics (3 fp64 moments per iteration)
+    bool fwd3 = getenv("DFM_FWD3") ? atoi(getenv("DFM_FWD3")) != 0 : true;
     Launch L() { return Launch{stream, &launches, num_sms, pdl}; }
 
     LoopState* pinned_state() {
@@ -1530,6 +1532,8 @@ struct Registrar {
     double* corr1;
     double* corr2;
     int cur = 0;
+    double* fstat = nullptr;   // per-level muF, vF (2 planes) for the 3-moment forward
+    bool fstat_ready = false;  // this level's F statistics are current
     T* Wb = nullptr;  // W = M(x+u) for the current u (TMA path)
     T* Gb = nullptr;  // grad M(x+u), 3 planes
     bool use_tma = false;    // fused W/G-carrying loop (plane-streaming and/or brick kernels)
@@ -1556,6 +1560,7 @@ struct Registrar {
         for (int k = 0; k < 4; ++k) coef[k] = cb + k * n;
         Wb = ctx->arr<T>("reg_W", n);
         Gb = ctx->arr<T>("reg_G", 3 * n);
+        if (cfg->loss == DFM_LOSS_LNCC && ctx->fwd3) fstat = ctx->arr<double>("reg_fstat", 2 * n);
         if (cfg->mode == DFM_MODE_SVF) {
             if (8 * n >= (int64_t(1) << 31))
                 fail(DFM_E_INVALID, "svf mode: volume too large (8 * voxels must be < 2^31)");
@@ -1656,10 +1661,15 @@ struct Registrar {
         const bool fused = lncc && (mask & 1);
         if (fused) {  // LNCC moments + window coefficients + loss + monitor, one launch
             const MonitorArgs mon{st, loss, stamp, cfg->conv_window, cfg->conv_tol};
-            np = use_brick ? launch_lncc_fwd_brick<T>(L, cfg->lncc_radius, Fs, Wb, d, coef[0],
-                                                      partials, st, &mon)
-                           : launch_lncc_fwd_tma<T>(L, cfg->lncc_radius, Fs, Wb, d, coef[0],
-                                                    partials, st, &mon);
+            if (use_brick)
+                np = launch_lncc_fwd_brick<T>(L, cfg->lncc_radius, Fs, Wb, d, coef[0], partials,
+                                              st, &mon);
+            else if (fstat_ready)
+                np = launch_lncc_fwd3_tma<T>(L, cfg->lncc_radius, Fs, Wb, fstat, d, coef[0],
+                                             partials, st, &mon);
+            else
+                np = launch_lncc_fwd_tma<T>(L, cfg->lncc_radius, Fs, Wb, d, coef[0], partials,
+                                            st, &mon);
         } else {
             np = loss_kind_launch_fwd<T>(ctx, loss_kind, cfg->lncc_radius, Fs, Ms, d, d, uin,
                                          coef, grad.w(), partials, st);
@@ -2046,6 +2056,9 @@ struct Registrar {
         use_tma = use_brick || (direct && !ctx->force_legacy && tma_eligible(d, Rg, Rw, big));
         if (use_tma && cfg->loss == DFM_LOSS_LNCC)
             launch_warpgrad<T>(ctx->L(), Ms, d, u[cur].r(), d, Wb, Gb);
+        fstat_ready = false;
+        if (use_tma && !use_brick && fstat && (ctx->tma_mask & 1))
+            fstat_ready = launch_fstats_tma<T>(ctx->L(), cfg->lncc_radius, Fs, d, fstat) >= 0;
         bool persisted = false;
         if (!ctx->profiling && ctx->persist && use_brick && cfg->loss == DFM_LOSS_LNCC) {
             PersistScale<T> ps{};

@@ -51,6 +51,9 @@ constexpr int TX = kTX, TY = kTY, NT = TX * TY;
 #ifndef DFM_MINB_FWD
 #define DFM_MINB_FWD 3
 #endif
+#ifndef DFM_MINB_FWD3
+#define DFM_MINB_FWD3 3
+#endif
 #ifndef DFM_MINB_BWD
 #define DFM_MINB_BWD 4
 #endif
@@ -359,6 +362,136 @@ struct LnccFwd2 {
             coef[2 * d.n + i] = static_cast<T>(k.bn);
             coef[3 * d.n + i] = static_cast<T>(k.bmu);
         }
+        return {k.cc2, 0.0};
+    }
+    __device__ void flush(Carry&) const {}
+    __device__ void finish(int blk, double s, double, const Prol&) const { partials[blk] = s; }
+};
+
+// similarity.cpp:122-150, fixed-image half: per-voxel window mean and variance
+// of F, once per pyramid level (F does not change between iterations)
+template <class T, int R_, int TY_ = DFM_TY_FWD>
+struct FStats2 {
+    using Acc = double;
+    using Center = NoCenter;
+    using Prol = NoProl;
+    using Carry = NoCarry;
+    static constexpr int R = R_, C = 2, BACK = 0, AHEAD = 0, S = DFM_S_FWD, TYv = TY_;
+    static constexpr int kMinB = DFM_MINB_FWD, kCY = 1;
+    static constexpr bool kStaged = false, kSum = false, kMax = false;
+    static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TYv + 2 * R;
+    static constexpr int kBytes = BX * BY * int(sizeof(T));
+    static constexpr int kBox = align128(kBytes);
+    static constexpr int kStageBytes = kBox;
+    CUtensorMap mF;
+    double* fstat;  // 2 planes: muF, vF
+    Dims d;
+
+    __device__ bool skip() const { return false; }
+    __device__ void prefetch_maps() const { prefetch_tmap(&mF); }
+    __device__ void issue(unsigned char* dst, uint64_t* bar, int x0, int y0, int q) const {
+        mbar_expect_tx(bar, kBytes);
+        tma_load_4d(dst, &mF, bar, x0 - XA, y0 - R, q, 0);
+    }
+    __device__ Acc wgt(int, int) const { return 1.0; }
+    __device__ Acc nrm(int, int) const { return 1.0; }
+    __device__ Prol prologue() const { return {}; }
+    __device__ void xpass(const unsigned char* st_, int row, int col, Acc, Acc v[2]) const {
+        const T* F = reinterpret_cast<const T*>(st_) + row * BX + col + (XA - R);
+        double a0 = 0, a1 = 0;
+#pragma unroll
+        for (int j = 0; j < 2 * R + 1; ++j) {
+            const double f = static_cast<double>(F[j]);
+            a0 += f;
+            a1 += f * f;
+        }
+        v[0] = a0;
+        v[1] = a1;
+    }
+    __device__ void load_center(int, int, int, Center&) const {}
+    __device__ Red2 emit(int x, int y, int z, const double s[2], const Center&, const Prol&,
+                         Carry&) const {
+        const double n = static_cast<double>(box_len(x, d.nx, R) * box_len(y, d.ny, R) *
+                                             (d.gz() > 1 ? box_len(z + d.zoff, d.gz(), R) : 1));
+        double muF, vF;
+        lncc_fstats(s[0], s[1], n, muF, vF);
+        const int i = d.idx32(x, y, z);
+        fstat[i] = muF;
+        fstat[d.n + i] = vF;
+        return {0.0, 0.0};
+    }
+    __device__ void flush(Carry&) const {}
+    __device__ void finish(int, double, double, const Prol&) const {}
+};
+
+// similarity.cpp:122-168 with the F statistics precomputed (FStats2): three
+// fp64 box moments of W per iteration instead of five
+template <class T, int R_, int TY_ = DFM_TY_FWD>
+struct LnccFwd3 {
+    using Acc = double;
+    using Prol = NoProl;
+    using Carry = NoCarry;
+    static constexpr int R = R_, C = 3, BACK = 0, AHEAD = 0, S = DFM_S_FWD, TYv = TY_;
+    static constexpr int kMinB = DFM_MINB_FWD3, kCY = 1;
+    static constexpr bool kStaged = false, kSum = true, kMax = false;
+    static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TYv + 2 * R;
+    static constexpr int kBytes = BX * BY * int(sizeof(T));
+    static constexpr int kBox = align128(kBytes);
+    static constexpr int kStageBytes = 2 * kBox;
+    CUtensorMap mF, mW;
+    const double* fstat;
+    T* coef;
+    double* partials;
+    const LoopState* st;
+    MonitorArgs mon;
+    Dims d;
+    struct Center {
+        double muF, vF;
+    };
+
+    __device__ bool skip() const { return st && st->done; }
+    __device__ void prefetch_maps() const {
+        prefetch_tmap(&mF);
+        prefetch_tmap(&mW);
+    }
+    __device__ void issue(unsigned char* dst, uint64_t* bar, int x0, int y0, int q) const {
+        mbar_expect_tx(bar, 2 * kBytes);
+        tma_load_4d(dst, &mF, bar, x0 - XA, y0 - R, q, 0);
+        tma_load_4d(dst + kBox, &mW, bar, x0 - XA, y0 - R, q, 0);
+    }
+    __device__ Acc wgt(int, int) const { return 1.0; }
+    __device__ Acc nrm(int, int) const { return 1.0; }
+    __device__ Prol prologue() const { return {}; }
+    __device__ void xpass(const unsigned char* st_, int row, int col, Acc, Acc v[3]) const {
+        const T* F = reinterpret_cast<const T*>(st_) + row * BX + col + (XA - R);
+        const T* W = F + kBox / int(sizeof(T));
+        double a0 = 0, a1 = 0, a2 = 0;
+#pragma unroll
+        for (int j = 0; j < 2 * R + 1; ++j) {
+            const double w = static_cast<double>(W[j]);
+            a0 += w;
+            a1 += w * w;
+            a2 += static_cast<double>(F[j]) * w;
+        }
+        v[0] = a0;
+        v[1] = a1;
+        v[2] = a2;
+    }
+    __device__ void load_center(int x, int y, int z, Center& c) const {
+        const int i = d.idx32(x, y, z);
+        c.muF = __ldg(fstat + i);
+        c.vF = __ldg(fstat + d.n + i);
+    }
+    __device__ Red2 emit(int x, int y, int z, const double s[3], const Center& c, const Prol&,
+                         Carry&) const {
+        const double n = static_cast<double>(box_len(x, d.nx, R) * box_len(y, d.ny, R) *
+                                             (d.gz() > 1 ? box_len(z + d.zoff, d.gz(), R) : 1));
+        const LnccCoef k = lncc_coef_f(c.muF, c.vF, s[0], s[1], s[2], n);
+        const int i = d.idx32(x, y, z);
+        coef[i] = static_cast<T>(k.an);
+        coef[d.n + i] = static_cast<T>(k.amu);
+        coef[2 * d.n + i] = static_cast<T>(k.bn);
+        coef[3 * d.n + i] = static_cast<T>(k.bmu);
         return {k.cc2, 0.0};
     }
     __device__ void flush(Carry&) const {}
@@ -900,6 +1033,40 @@ int launch_lncc_fwd_tma(const Launch& L, int R, const T* F, const T* W, Dims d, 
 }
 
 template <class T>
+int launch_fstats_tma(const Launch& L, int R, const T* F, Dims d, double* fstat) {
+    return with_r<1, 5>(R, [&](auto rc) {
+        constexpr int RR = decltype(rc)::value;
+        using Op = FStats2<T, RR>;
+        Op op;
+        if (!make_map<T>(&op.mF, F, d, 1, Op::BX, Op::BY)) return -1;
+        op.fstat = fstat;
+        op.d = d;
+        return run_zm2(L, op, d);
+    });
+}
+
+template <class T>
+int launch_lncc_fwd3_tma(const Launch& L, int R, const T* F, const T* W, const double* fstat,
+                         Dims d, T* coef, double* partials, const LoopState* st,
+                         const MonitorArgs* mon) {
+    return with_r<1, 5>(R, [&](auto rc) {
+        constexpr int RR = decltype(rc)::value;
+        using Op = LnccFwd3<T, RR>;
+        Op op;
+        if (!make_map<T>(&op.mF, F, d, 1, Op::BX, Op::BY) ||
+            !make_map<T>(&op.mW, W, d, 1, Op::BX, Op::BY))
+            return -1;
+        op.fstat = fstat;
+        op.coef = coef;
+        op.partials = partials;
+        op.st = st;
+        op.mon = mon ? *mon : MonitorArgs{nullptr, nullptr, nullptr, 0, 0.0};
+        op.d = d;
+        return run_zm2(L, op, d);
+    });
+}
+
+template <class T>
 int launch_lncc_bwd_tma(const Launch& L, int R, const T* coef, const T* F, const T* W,
                         const T* G, Dims d, T* grad, const LoopState* st) {
     return with_r<1, 5>(R, [&](auto rc) {
@@ -983,6 +1150,10 @@ void launch_warpgrad(const Launch& L, const T* M, Dims dm, CPlanes3<T> u, Dims d
                                         double*, const LoopState*, const MonitorArgs*);        \
     template int launch_lncc_bwd_tma<T>(const Launch&, int, const T*, const T*, const T*,      \
                                         const T*, Dims, T*, const LoopState*);                 \
+    template int launch_fstats_tma<T>(const Launch&, int, const T*, Dims, double*);           \
+    template int launch_lncc_fwd3_tma<T>(const Launch&, int, const T*, const T*,               \
+                                         const double*, Dims, T*, double*, const LoopState*,   \
+                                         const MonitorArgs*);                                  \
     template int launch_smooth_adam_tma<T>(const Launch&, int, const GaussW<T>&, const T*, T*, \
                                            T*, T*, Dims, AdamParams, LoopState*,               \
                                            unsigned long long*);                               \

@@ -81,20 +81,32 @@ struct LnccCoef {
     double cc2, an, amu, bn, bmu;
 };
 
-__device__ __forceinline__ LnccCoef lncc_coef(const double s[5], double n) {
+// The fixed image's window statistics (similarity.cpp:145-150, F half):
+// constant over the iterations of a pyramid level, so computable once per
+// level.  Products and differences are explicit (no FMA contraction) so the
+// split and the fused forms below round identically.
+__device__ __forceinline__ void lncc_fstats(double sF, double sF2, double n, double& muF,
+                                            double& vF) {
+    const double inv_n = 1.0 / n;
+    muF = __dmul_rn(sF, inv_n);
+    vF = __dsub_rn(__dmul_rn(sF2, inv_n), __dmul_rn(muF, muF));
+    vF = vF < 0.0 ? 0.0 : vF;
+}
+
+// window coefficients given the F statistics and the three W moments
+// (ΣW, ΣW², ΣFW)
+__device__ __forceinline__ LnccCoef lncc_coef_f(double muF, double vF, double sW, double sW2,
+                                                double sFW, double n) {
     LnccCoef r{0.0, 0.0, 0.0, 0.0, 0.0};
     const double inv_n = 1.0 / n;
-    const double muF = s[0] * inv_n;
-    const double muW = s[1] * inv_n;
-    double vF = s[2] * inv_n - muF * muF;
-    double vW = s[3] * inv_n - muW * muW;
-    vF = vF < 0.0 ? 0.0 : vF;
+    const double muW = __dmul_rn(sW, inv_n);
+    double vW = __dsub_rn(__dmul_rn(sW2, inv_n), __dmul_rn(muW, muW));
     vW = vW < 0.0 ? 0.0 : vW;
-    const double cv = s[4] * inv_n - muF * muW;
+    const double cv = __dsub_rn(__dmul_rn(sFW, inv_n), __dmul_rn(muF, muW));
     if (!(vF < 1e-5 || vW < 1e-5)) {  // similarity.cpp:13, 151-154
         const double inv_den = 1.0 / (vF * vW);
-        const double alpha = cv * inv_den;       // cv / (vF vW)
-        r.cc2 = alpha * cv;                      // cv^2 / (vF vW)
+        const double alpha = cv * inv_den;         // cv / (vF vW)
+        r.cc2 = alpha * cv;                        // cv^2 / (vF vW)
         const double beta = r.cc2 * vF * inv_den;  // cv^2 / (vF vW^2)
         r.an = alpha * inv_n;
         r.amu = r.an * muF;
@@ -102,6 +114,14 @@ __device__ __forceinline__ LnccCoef lncc_coef(const double s[5], double n) {
         r.bmu = r.bn * muW;
     }
     return r;
+}
+
+// from the five raw moments: the same two steps, hence bit-identical to the
+// precomputed-F form
+__device__ __forceinline__ LnccCoef lncc_coef(const double s[5], double n) {
+    double muF, vF;
+    lncc_fstats(s[0], s[2], n, muF, vF);
+    return lncc_coef_f(muF, vF, s[1], s[3], s[4], n);
 }
 
 // dL/dW at one voxel from the box sums of the 4 coefficients (similarity.cpp:182)
