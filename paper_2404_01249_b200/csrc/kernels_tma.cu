@@ -52,6 +52,9 @@ constexpr int64_t kSaCoarsenVoxels = 2000000;
 #ifndef DFM_MINB_FWD
 #define DFM_MINB_FWD 3
 #endif
+#ifndef DFM_BWD_ACC32
+#define DFM_BWD_ACC32 1
+#endif
 #ifndef DFM_MINB_FWD3
 #define DFM_MINB_FWD3 3
 #endif
@@ -502,7 +505,10 @@ struct LnccFwd3 {
 // similarity.cpp:170-189 — box sums of the coefficients, dW, grad = dW * G
 template <class T, int R_, int TY_ = DFM_TY_BWD>
 struct LnccBwd2 {
-    using Acc = double;
+    // fp32 context: the box sums of the (fp32-stored) coefficients may run in
+    // fp32 (DFM_BWD_ACC32); the dW combination stays fp64
+    using Acc = typename std::conditional<(DFM_BWD_ACC32 != 0) && sizeof(T) == 4, float,
+                                          double>::type;
     using Prol = NoProl;
     using Carry = NoCarry;
     static constexpr int R = R_, C = 4, BACK = 0, AHEAD = 0, S = DFM_S_BWD, TYv = TY_;
@@ -538,10 +544,10 @@ struct LnccBwd2 {
         const T* p = reinterpret_cast<const T*>(st_) + row * BX + col + (XA - R);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            double a = 0.0;
+            Acc a = Acc(0);
 #pragma unroll
             for (int j = 0; j < 2 * R + 1; ++j)
-                a += static_cast<double>(p[c * (kBox / int(sizeof(T))) + j]);
+                a += static_cast<Acc>(p[c * (kBox / int(sizeof(T))) + j]);
             v[c] = a;
         }
     }
@@ -553,10 +559,12 @@ struct LnccBwd2 {
         c.g1 = __ldg(G + d.n + i);
         c.g2 = d.ndim == 3 ? __ldg(G + 2 * d.n + i) : T(0);
     }
-    __device__ Red2 emit(int x, int y, int z, const double s[4], const Center& c, const Prol&,
+    __device__ Red2 emit(int x, int y, int z, const Acc sa[4], const Center& c, const Prol&,
                          Carry&) const {
         const int64_t i = d.idx32(x, y, z);
         const double f = static_cast<double>(c.f), w = static_cast<double>(c.w);
+        const double s[4] = {static_cast<double>(sa[0]), static_cast<double>(sa[1]),
+                             static_cast<double>(sa[2]), static_cast<double>(sa[3])};
         const double dW = lncc_dw(m2n, f, w, s);
         grad[i] = static_cast<T>(dW * static_cast<double>(c.g0));
         grad[d.n + i] = static_cast<T>(dW * static_cast<double>(c.g1));
