@@ -28,6 +28,7 @@
 //   ComposeB    step, u       -> u' = smooth(step + u(x+step)), W, G
 #include <cstdint>
 #include <mutex>
+#include <type_traits>
 
 #include <cooperative_groups.h>
 
@@ -269,8 +270,9 @@ struct LnccFwdB {
 // similarity.cpp:170-189 — box sums of the 4 coefficients, dW, grad = dW * G
 template <class T, int R_>
 struct LnccBwdB {
-    using Acc = double;
-    using Raw = double;
+    // fp32 context: coefficient box sums in fp32 (as LnccBwd2, DFM_BWD_ACC32)
+    using Acc = typename std::conditional<sizeof(T) == 4, float, double>::type;
+    using Raw = Acc;
     using Prol = NoProl;
     static constexpr int R = R_, C = 4, NR = 4, kStageBatch = 8;
     static constexpr bool kSum = false, kMax = false;
@@ -284,24 +286,26 @@ struct LnccBwdB {
     Dims d;
 
     __device__ bool skip() const { return st && st->done; }
-    __device__ void stage(int x, int y, int z, double v[4]) const {
+    __device__ void stage(int x, int y, int z, Acc v[4]) const {
         const int i = d.idx32(x, y, z);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) v[k] = static_cast<double>(coef[k * d.n + i]);
+        for (int k = 0; k < 4; ++k) v[k] = static_cast<Acc>(coef[k * d.n + i]);
     }
-    __device__ void xpass(const double* p, int cs, double v[4]) const {
+    __device__ void xpass(const Acc* p, int cs, Acc v[4]) const {
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            double a = 0.0;
+            Acc a = Acc(0);
 #pragma unroll
             for (int j = 0; j < 2 * R + 1; ++j) a += p[c * cs + j];
             v[c] = a;
         }
     }
-    __device__ double wgt(int, int) const { return 1.0; }
-    __device__ double nrm(int, int) const { return 1.0; }
+    __device__ Acc wgt(int, int) const { return Acc(1); }
+    __device__ Acc nrm(int, int) const { return Acc(1); }
     __device__ Prol prologue() const { return {}; }
-    __device__ Red2 emit(int x, int y, int z, const double s[4], const Prol&) const {
+    __device__ Red2 emit(int x, int y, int z, const Acc sa[4], const Prol&) const {
+        const double s[4] = {static_cast<double>(sa[0]), static_cast<double>(sa[1]),
+                             static_cast<double>(sa[2]), static_cast<double>(sa[3])};
         const int i = d.idx32(x, y, z);
         const double f = static_cast<double>(__ldg(F + i)), w = static_cast<double>(W[i]);
         const double dW = lncc_dw(m2n, f, w, s);
