@@ -37,6 +37,9 @@ ALG_ELEMS = {
     "smooth_adam": 3 + 3 + 3 + 3 + 3 + 3,  # read grad m nu; write m nu step
     "compose_smooth": 3 + 3 + 1 + 3 + 1 + 3,  # read step u M; write u' W G(3)
 }
+# fixed extra bytes per voxel independent of the precision: the forward reads
+# the level's precomputed F window statistics (muF, vF as fp64)
+ALG_EXTRA_BYTES = {"loss_fwd": 16}
 # the iteration's irreducible state traffic: read u m nu F M,
 # write u m nu = 20 elements (80 B fp32)
 ITER_MIN_ELEMS = 20
@@ -309,7 +312,7 @@ def main():
         if kt[k]["launches"]:
             avg_ms = kt[k]["ms"] / kt[k]["launches"]
             vox = kt[k]["voxels"] / kt[k]["launches"]
-            bytes_launch = vox * elems * esz
+            bytes_launch = vox * (elems * esz + ALG_EXTRA_BYTES.get(k, 0))
             per[k] = {"avg_ms": avg_ms, "launches": kt[k]["launches"],
                       "alg_bytes": bytes_launch, "gbs": bytes_launch / (avg_ms * 1e6)}
     dom = max(per, key=lambda k: per[k]["avg_ms"] * per[k]["launches"]) if per else None
@@ -322,7 +325,7 @@ def main():
                 "per_kernel_ms": {k: v["avg_ms"] for k, v in per.items()}}
         it_ms = sum(v["avg_ms"] for v in per.values()) + (
             kt["monitor"]["ms"] / kt["monitor"]["launches"] if kt["monitor"]["launches"] else 0)
-        vox = per[dom]["alg_bytes"] / (ALG_ELEMS[dom] * esz)
+        vox = per[dom]["alg_bytes"] / (ALG_ELEMS[dom] * esz + ALG_EXTRA_BYTES.get(dom, 0))
         roof["iteration"] = {"ms": it_ms, "min_bytes_per_voxel": ITER_MIN_ELEMS * esz,
                              "achieved": vox * ITER_MIN_ELEMS * esz / (it_ms * 1e6),
                              "frac": vox * ITER_MIN_ELEMS * esz / (it_ms * 1e6) / peak}
@@ -331,6 +334,8 @@ def main():
             try:
                 with open(tr) as f:
                     roof["traffic"] = json.load(f).get(args.precision, {}).get(dom)
+                roof["traffic_unit"] = "DRAM bytes per launch (ncu, profiles/traffic.json)"
+                roof["alg_bytes_per_launch"] = per[dom]["alg_bytes"]
             except (OSError, ValueError):
                 pass
 
