@@ -225,6 +225,70 @@ __device__ __forceinline__ void lerp_grad(const Cell3<T>& c, const Corners<T>& k
     }
 }
 
+// ---------------------------------------------------------------------------
+// 3-D fast form of warp_with_gradient at one voxel (similarity.cpp:25-45):
+// all dims >= 2 (validate_meta), 32-bit offsets, no flat-axis cases.  Same
+// arithmetic as locate3 + lerp_value + lerp_grad, in fewer instructions.
+template <class T>
+struct WG3 {
+    int base;       // lower corner index
+    T fx, fy, fz;
+    unsigned clamp;  // bit a: axis a clamped (zero gradient)
+    T v[8];          // corners in (cz, cy, cx) order
+};
+
+template <class T, bool NC = true>
+__device__ __forceinline__ void wg3_fetch(const T* __restrict__ M, const Dims& m, int x, int y,
+                                          int z, T ux, T uy, T uz, WG3<T>& w) {
+    const AxisCell<T> ax = locate_axis(x, ux, m.nx);
+    const AxisCell<T> ay = locate_axis(y, uy, m.ny);
+    const AxisCell<T> az = locate_axis(z, uz, m.nz);
+    w.fx = ax.f;
+    w.fy = ay.f;
+    w.fz = az.f;
+    w.clamp = (ax.clamped ? 1u : 0u) | (ay.clamped ? 2u : 0u) | (az.clamped ? 4u : 0u);
+    const int sy = m.nx, sz = m.nx * m.ny;
+    w.base = (az.i0 * m.ny + ay.i0) * m.nx + ax.i0;
+    const T* p = M + w.base;
+    w.v[0] = ld_<T, NC>(p);
+    w.v[1] = ld_<T, NC>(p + 1);
+    w.v[2] = ld_<T, NC>(p + sy);
+    w.v[3] = ld_<T, NC>(p + sy + 1);
+    w.v[4] = ld_<T, NC>(p + sz);
+    w.v[5] = ld_<T, NC>(p + sz + 1);
+    w.v[6] = ld_<T, NC>(p + sz + sy);
+    w.v[7] = ld_<T, NC>(p + sz + sy + 1);
+}
+
+template <class T>
+__device__ __forceinline__ T wg3_value(const WG3<T>& w) {
+    const T wx0 = T(1) - w.fx, wx1 = w.fx;
+    const T wy0 = T(1) - w.fy, wy1 = w.fy;
+    const T wz0 = T(1) - w.fz, wz1 = w.fz;
+    T acc = (wx0 * wy0 * wz0) * w.v[0] + (wx1 * wy0 * wz0) * w.v[1] +
+            (wx0 * wy1 * wz0) * w.v[2] + (wx1 * wy1 * wz0) * w.v[3];
+    acc += (wx0 * wy0 * wz1) * w.v[4] + (wx1 * wy0 * wz1) * w.v[5] +
+           (wx0 * wy1 * wz1) * w.v[6] + (wx1 * wy1 * wz1) * w.v[7];
+    return acc;
+}
+
+template <class T>
+__device__ __forceinline__ void wg3_grad(const WG3<T>& w, T g[3]) {
+    const T wx0 = T(1) - w.fx, wx1 = w.fx;
+    const T wy0 = T(1) - w.fy, wy1 = w.fy;
+    const T wz0 = T(1) - w.fz, wz1 = w.fz;
+    const T* k = w.v;
+    T a = (wy0 * wz0) * (k[1] - k[0]) + (wy1 * wz0) * (k[3] - k[2]);
+    a += (wy0 * wz1) * (k[5] - k[4]) + (wy1 * wz1) * (k[7] - k[6]);
+    g[0] = (w.clamp & 1u) ? T(0) : a;
+    T b = (wx0 * wz0) * (k[2] - k[0]) + (wx1 * wz0) * (k[3] - k[1]);
+    b += (wx0 * wz1) * (k[6] - k[4]) + (wx1 * wz1) * (k[7] - k[5]);
+    g[1] = (w.clamp & 2u) ? T(0) : b;
+    const T c = (wx0 * wy0) * (k[4] - k[0]) + (wx1 * wy0) * (k[5] - k[1]) +
+                (wx0 * wy1) * (k[6] - k[2]) + (wx1 * wy1) * (k[7] - k[3]);
+    g[2] = (w.clamp & 4u) ? T(0) : c;
+}
+
 // per-component field sample (interp.cpp:188-203)
 template <class T, bool NC = true>
 __device__ __forceinline__ void lerp_field(const Cell3<T>& c, const T* __restrict__ f0,

@@ -1642,6 +1642,7 @@ struct Registrar {
     // can this scale run the plane-streaming (TMA) kernels?
     bool tma_eligible(const Dims& d, int Rg, int Rw, bool big) const {
         return !big && !cfg->use_jac && cfg->step_cap <= 1.5 && Rg <= 6 && Rw <= 4 &&
+               d.ndim == 3 &&  // Compose2's fused W/G gather is 3-D only
                (cfg->loss != DFM_LOSS_LNCC || cfg->lncc_radius <= 5) &&
                tma_supported(d, sizeof(T));
     }
@@ -2647,6 +2648,7 @@ struct SlabRun {
             fail(DFM_E_INVALID, "slab decomposition: direct mode, LNCC loss, use_jac off only");
         if (!tma_supported(full, sizeof(T)))
             fail(DFM_E_INVALID, "slab decomposition: x extent must be a multiple of 16 bytes");
+        if (full.ndim != 3) fail(DFM_E_INVALID, "slab decomposition: 3-D volumes only");
         H = slab_halo(cfg);
         int64_t total = 0;
         for (int i = 0; i < ns; ++i) total += iters[i];

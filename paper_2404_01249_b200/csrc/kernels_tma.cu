@@ -702,11 +702,10 @@ struct Compose2 {
     LoopState* st;
     int count_update;  // 0 for all but one slab of an emulated decomposition
     Dims d;
-    struct Carry {
+    struct Carry {  // the M gather of the previous plane's voxel (3-D fast form)
         bool valid;
-        int64_t i;
-        Cell3<T> c;
-        Corners<T> k;
+        int i;
+        WG3<T> w;
     };
 
     __device__ bool skip() const {
@@ -852,9 +851,9 @@ struct Compose2 {
     __device__ void xpass(const unsigned char*, int, int, Acc, Acc*) const {}
     __device__ void load_center(int, int, int, Center&) const {}
     __device__ void finish_wg(const Carry& c) const {
-        W[c.i] = lerp_value(c.c, c.k);
+        W[c.i] = wg3_value(c.w);
         T gr[3];
-        lerp_grad(c.c, c.k, d.ndim, gr);
+        wg3_grad(c.w, gr);
         G[c.i] = gr[0];
         G[d.n + c.i] = gr[1];
         G[2 * d.n + c.i] = gr[2];
@@ -865,11 +864,10 @@ struct Compose2 {
         uout[i] = u[0];
         uout[d.n + i] = u[1];
         uout[2 * d.n + i] = d.ndim == 3 ? u[2] : T(0);
-        if (W) {  // similarity.cpp:25-45 for the next loss evaluation
+        if (W) {  // similarity.cpp:25-45 for the next loss evaluation (3-D only: launcher)
             if (cr.valid) finish_wg(cr);
-            cr.c = locate3<T>(dm, x, y, z + d.zoff, u[0], u[1], d.ndim == 3 ? u[2] : T(0));
-            cr.k = fetch_corners<T>(M, cr.c);
-            cr.i = i;
+            wg3_fetch<T>(M, dm, x, y, z + d.zoff, u[0], u[1], u[2], cr.w);
+            cr.i = static_cast<int>(i);
             cr.valid = true;
         }
         return {0.0, 0.0};
@@ -1129,6 +1127,7 @@ int launch_compose_tma(const Launch& L, int R, double cap, const GaussW<T>& w, c
                        LoopState* st, bool count_update) {
     const int caph = cap <= 0.5 ? 1 : (cap <= 1.5 ? 2 : 0);
     if (caph == 0) return -2;
+    if (W && d.ndim != 3) return -2;  // the fused M gather is the 3-D fast form
     return with_r<0, 4>(R, [&](auto rc) {
         constexpr int RR = decltype(rc)::value;
         auto go = [&](auto ch) {
