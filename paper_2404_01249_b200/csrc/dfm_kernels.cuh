@@ -235,7 +235,9 @@ bool brick_supported(Dims d, int esz, int lncc_r, int rg, int rw);
 template <class T>
 int launch_lncc_fwd_brick(const Launch& L, int R, const T* F, const T* W, Dims d, T* coef,
                           double* partials, const LoopState* st,
-                          const MonitorArgs* mon = nullptr);
+                          const MonitorArgs* mon = nullptr, const double* fstat = nullptr);
+template <class T>
+int launch_fstats_brick(const Launch& L, int R, const T* F, Dims d, double* fstat);
 template <class T>
 int launch_lncc_bwd_brick(const Launch& L, int R, const T* coef, const T* F, const T* W,
                           const T* G, Dims d, T* grad, const LoopState* st);

@@ -1664,7 +1664,7 @@ struct Registrar {
             const MonitorArgs mon{st, loss, stamp, cfg->conv_window, cfg->conv_tol};
             if (use_brick)
                 np = launch_lncc_fwd_brick<T>(L, cfg->lncc_radius, Fs, Wb, d, coef[0], partials,
-                                              st, &mon);
+                                              st, &mon, fstat_ready ? fstat : nullptr);
             else if (fstat_ready)
                 np = launch_lncc_fwd3_tma<T>(L, cfg->lncc_radius, Fs, Wb, fstat, d, coef[0],
                                              partials, st, &mon);
@@ -2058,8 +2058,11 @@ struct Registrar {
         if (use_tma && cfg->loss == DFM_LOSS_LNCC)
             launch_warpgrad<T>(ctx->L(), Ms, d, u[cur].r(), d, Wb, Gb);
         fstat_ready = false;
-        if (use_tma && !use_brick && fstat && (ctx->tma_mask & 1))
-            fstat_ready = launch_fstats_tma<T>(ctx->L(), cfg->lncc_radius, Fs, d, fstat) >= 0;
+        if (use_tma && fstat && (ctx->tma_mask & 1))
+            fstat_ready = (use_brick ? launch_fstats_brick<T>(ctx->L(), cfg->lncc_radius, Fs, d,
+                                                              fstat)
+                                     : launch_fstats_tma<T>(ctx->L(), cfg->lncc_radius, Fs, d,
+                                                            fstat)) >= 0;
         bool persisted = false;
         if (!ctx->profiling && ctx->persist && use_brick && cfg->loss == DFM_LOSS_LNCC) {
             PersistScale<T> ps{};

@@ -208,17 +208,19 @@ __global__ void __launch_bounds__(NTB, 2) k_brick(const __grid_constant__ Op op,
 
 struct NoProl {};
 
-// similarity.cpp:122-168 — five box moments of F and W = M(x+u) (fp64), the
-// window coefficients and cc^2
-template <class T, int R_>
+// similarity.cpp:122-168 — box moments (fp64) of F and W = M(x+u), the window
+// coefficients and cc^2.  FS: the level's F statistics (muF, vF) come
+// precomputed (FStatsB) and only the three W moments are summed.
+template <class T, int R_, bool FS = false>
 struct LnccFwdB {
     using Acc = double;
     using Raw = double;
     using Prol = NoProl;
-    static constexpr int R = R_, C = 5, NR = 2, kStageBatch = 8;
+    static constexpr int R = R_, C = FS ? 3 : 5, NR = 2, kStageBatch = 8;
     static constexpr bool kSum = true, kMax = false;
     const T* F;
     const T* W;
+    const double* fstat;  // FS: 2 planes muF, vF
     T* coef;  // 4 planes; nullptr -> value only
     double* partials;
     const LoopState* st;
@@ -231,32 +233,50 @@ struct LnccFwdB {
         v[0] = static_cast<double>(__ldg(F + i));
         v[1] = static_cast<double>(W[i]);
     }
-    __device__ void xpass(const double* p, int cs, double v[5]) const {
-        double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
+    __device__ void xpass(const double* p, int cs, double v[C]) const {
+        if constexpr (FS) {
+            double a0 = 0, a1 = 0, a2 = 0;
 #pragma unroll
-        for (int j = 0; j < 2 * R + 1; ++j) {
-            const double f = p[j], w = p[cs + j];
-            a0 += f;
-            a1 += w;
-            a2 += f * f;
-            a3 += w * w;
-            a4 += f * w;
+            for (int j = 0; j < 2 * R + 1; ++j) {
+                const double f = p[j], w = p[cs + j];
+                a0 += w;
+                a1 += w * w;
+                a2 += f * w;
+            }
+            v[0] = a0;
+            v[1] = a1;
+            v[2] = a2;
+        } else {
+            double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
+#pragma unroll
+            for (int j = 0; j < 2 * R + 1; ++j) {
+                const double f = p[j], w = p[cs + j];
+                a0 += f;
+                a1 += w;
+                a2 += f * f;
+                a3 += w * w;
+                a4 += f * w;
+            }
+            v[0] = a0;
+            v[1] = a1;
+            v[2] = a2;
+            v[3] = a3;
+            v[4] = a4;
         }
-        v[0] = a0;
-        v[1] = a1;
-        v[2] = a2;
-        v[3] = a3;
-        v[4] = a4;
     }
     __device__ double wgt(int, int) const { return 1.0; }
     __device__ double nrm(int, int) const { return 1.0; }
     __device__ Prol prologue() const { return {}; }
-    __device__ Red2 emit(int x, int y, int z, const double s[5], const Prol&) const {
+    __device__ Red2 emit(int x, int y, int z, const double s[C], const Prol&) const {
         const double n = static_cast<double>(box_len(x, d.nx, R) * box_len(y, d.ny, R) *
                                              box_len(z, d.nz, R));
-        const LnccCoef k = lncc_coef(s, n);
+        const int i = d.idx32(x, y, z);
+        LnccCoef k;
+        if constexpr (FS)
+            k = lncc_coef_f(__ldg(fstat + i), __ldg(fstat + d.n + i), s[0], s[1], s[2], n);
+        else
+            k = lncc_coef(s, n);
         if (coef) {
-            const int i = d.idx32(x, y, z);
             coef[i] = static_cast<T>(k.an);
             coef[d.n + i] = static_cast<T>(k.amu);
             coef[2 * d.n + i] = static_cast<T>(k.bn);
@@ -265,6 +285,48 @@ struct LnccFwdB {
         return {k.cc2, 0.0};
     }
     __device__ void finish(int blk, double s, double, const Prol&) const { partials[blk] = s; }
+};
+
+// similarity.cpp:145-150, F half, once per level: muF and vF per voxel
+template <class T, int R_>
+struct FStatsB {
+    using Acc = double;
+    using Raw = double;
+    using Prol = NoProl;
+    static constexpr int R = R_, C = 2, NR = 1, kStageBatch = 8;
+    static constexpr bool kSum = false, kMax = false;
+    const T* F;
+    double* fstat;
+    Dims d;
+
+    __device__ bool skip() const { return false; }
+    __device__ void stage(int x, int y, int z, double v[1]) const {
+        v[0] = static_cast<double>(__ldg(F + d.idx32(x, y, z)));
+    }
+    __device__ void xpass(const double* p, int, double v[2]) const {
+        double a0 = 0, a1 = 0;
+#pragma unroll
+        for (int j = 0; j < 2 * R + 1; ++j) {
+            a0 += p[j];
+            a1 += p[j] * p[j];
+        }
+        v[0] = a0;
+        v[1] = a1;
+    }
+    __device__ double wgt(int, int) const { return 1.0; }
+    __device__ double nrm(int, int) const { return 1.0; }
+    __device__ Prol prologue() const { return {}; }
+    __device__ Red2 emit(int x, int y, int z, const double s[2], const Prol&) const {
+        const double n = static_cast<double>(box_len(x, d.nx, R) * box_len(y, d.ny, R) *
+                                             box_len(z, d.nz, R));
+        double muF, vF;
+        lncc_fstats(s[0], s[1], n, muF, vF);
+        const int i = d.idx32(x, y, z);
+        fstat[i] = muF;
+        fstat[d.n + i] = vF;
+        return {0.0, 0.0};
+    }
+    __device__ void finish(int, double, double, const Prol&) const {}
 };
 
 // similarity.cpp:170-189 — box sums of the 4 coefficients, dW, grad = dW * G
@@ -449,11 +511,11 @@ struct ComposeB {
         uout[d.n + i] = s[1];
         uout[2 * d.n + i] = s[2];
         if (W) {
-            const Cell3<T> c = locate3<T>(dm, x, y, z, s[0], s[1], s[2]);
-            const Corners<T> k = fetch_corners<T>(M, c);
-            W[i] = lerp_value(c, k);
+            WG3<T> w;
+            wg3_fetch<T>(M, dm, x, y, z, s[0], s[1], s[2], w);
+            W[i] = wg3_value(w);
             T gr[3];
-            lerp_grad(c, k, 3, gr);
+            wg3_grad(w, gr);
             G[i] = gr[0];
             G[d.n + i] = gr[1];
             G[2 * d.n + i] = gr[2];
@@ -631,16 +693,31 @@ bool brick_supported(Dims d, int esz, int lncc_r, int rg, int rw) {
 
 template <class T>
 int launch_lncc_fwd_brick(const Launch& L, int R, const T* F, const T* W, Dims d, T* coef,
-                          double* partials, const LoopState* st, const MonitorArgs* mon) {
+                          double* partials, const LoopState* st, const MonitorArgs* mon,
+                          const double* fstat) {
     return with_rb<1, kBrickLnccRMax>(R, [&](auto rc) {
-        using Op = LnccFwdB<T, decltype(rc)::value>;
-        Op op;
+        auto go = [&](auto op) {
+            op.F = F;
+            op.W = W;
+            op.fstat = fstat;
+            op.coef = coef;
+            op.partials = partials;
+            op.st = st;
+            op.mon = mon ? *mon : MonitorArgs{nullptr, nullptr, nullptr, 0, 0.0};
+            op.d = d;
+            return run_brick(L, op, d);
+        };
+        if (fstat) return go(LnccFwdB<T, decltype(rc)::value, true>{});
+        return go(LnccFwdB<T, decltype(rc)::value, false>{});
+    });
+}
+
+template <class T>
+int launch_fstats_brick(const Launch& L, int R, const T* F, Dims d, double* fstat) {
+    return with_rb<1, kBrickLnccRMax>(R, [&](auto rc) {
+        FStatsB<T, decltype(rc)::value> op;
         op.F = F;
-        op.W = W;
-        op.coef = coef;
-        op.partials = partials;
-        op.st = st;
-        op.mon = mon ? *mon : MonitorArgs{nullptr, nullptr, nullptr, 0, 0.0};
+        op.fstat = fstat;
         op.d = d;
         return run_brick(L, op, d);
     });
@@ -717,6 +794,7 @@ int launch_persist_scale(const Launch& L, const PersistScale<T>& p) {
         PersistArgs<T, R, 3, 2> a;
         a.fwd.F = p.F;
         a.fwd.W = p.W;
+        a.fwd.fstat = nullptr;
         a.fwd.coef = p.coef;
         a.fwd.partials = p.partials;
         a.fwd.st = p.st;
@@ -771,7 +849,9 @@ int launch_persist_scale(const Launch& L, const PersistScale<T>& p) {
 
 #define DFM_INST_BRICK(T)                                                                      \
     template int launch_lncc_fwd_brick<T>(const Launch&, int, const T*, const T*, Dims, T*,    \
-                                          double*, const LoopState*, const MonitorArgs*);      \
+                                          double*, const LoopState*, const MonitorArgs*,       \
+                                          const double*);                                      \
+    template int launch_fstats_brick<T>(const Launch&, int, const T*, Dims, double*);         \
     template int launch_lncc_bwd_brick<T>(const Launch&, int, const T*, const T*, const T*,    \
                                           const T*, Dims, T*, const LoopState*);               \
     template int launch_smooth_adam_brick<T>(const Launch&, int, const GaussW<T>&, const T*,   \
