@@ -2419,7 +2419,7 @@ struct SlabRun {
     int64_t plane() const { return static_cast<int64_t>(parts.empty() ? full.nx * full.ny
                                                                        : parts[0].dl.nx * parts[0].dl.ny); }
 
-    void alloc(int64_t total_iters) {
+    void alloc(int64_t total_iters, int64_t prev_n) {
         const int64_t pl = static_cast<int64_t>(full.nx) * full.ny;
         // local capacity: the largest owned range at full resolution + 2H
         int maxn = 0;
@@ -2436,7 +2436,8 @@ struct SlabRun {
                                                comps[k] * cap);
         Fs = ctx->arr<T>("slab_Fs", full.n);
         Ms = ctx->arr<T>("slab_Ms", full.n);
-        for (int k = 0; k < 3; ++k) gath[k] = ctx->arr<T>("slab_gath" + std::to_string(k), 3 * full.n);
+        for (int k = 0; k < 3; ++k)  // u: also the final gathered field (full grid)
+            gath[k] = ctx->arr<T>("slab_gath" + std::to_string(k), 3 * (k == 0 ? full.n : prev_n));
         st = ctx->arr<LoopState>("slab_state", 1);
         const int64_t ni = total_iters + 2;
         loss = ctx->arr<double>("slab_loss", ni);
@@ -2655,7 +2656,17 @@ struct SlabRun {
         H = slab_halo(cfg);
         int64_t total = 0;
         for (int i = 0; i < ns; ++i) total += iters[i];
-        alloc(total);
+        // m and nu are gathered only when leaving a level that is not the full
+        // grid: size their gather buffers for the largest such level
+        int64_t prev_n = 1;
+        for (int i = 0; i < ns; ++i) {
+            const double fac[3] = {scales[i], scales[i], scales[i]};
+            dfm_grid wgd;
+            downsample_grid(g, fac, &wgd);
+            const Dims di = to_dims(&wgd);
+            if (!dims_equal(di, full)) prev_n = std::max(prev_n, di.n);
+        }
+        alloc(total, prev_n);
         Dims prev{};
         bool have = false;
         int64_t global = 0;

@@ -13,7 +13,7 @@ namespace {
 constexpr int kNT = 256;
 constexpr int kRedBlocks = 1184;  // fixed => partial-sum order independent of the device
 
-inline int grid_for(int64_t n, int cap = 1 << 20) {
+inline int grid_for(int64_t n, int cap = 0x7fffffff) {  // callers with a cap grid-stride
     int64_t b = (n + kNT - 1) / kNT;
     if (b < 1) b = 1;
     return static_cast<int>(b < cap ? b : cap);
