@@ -2665,6 +2665,10 @@ struct SlabRun {
             downsample_grid(g, fac, &wgd);
             const Dims di = to_dims(&wgd);
             if (!dims_equal(di, full)) prev_n = std::max(prev_n, di.n);
+            if (!tma_supported(di, sizeof(T)))
+                fail(DFM_E_INVALID,
+                     "slab decomposition: the x extent of every pyramid level must be a multiple "
+                     "of 16 bytes (level %d has %d voxels)", i, di.nx);
         }
         alloc(total, prev_n);
         Dims prev{};
