@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--config", type=int, default=1, choices=[0, 1, 3])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--pairs-per-gpu", type=int, default=1,
+                    help="config-2 style batch: K concurrent pairs per GPU, one context "
+                         "(stream) and host thread each; value = aggregate voxel-iter/s")
     return ap.parse_args()
 
 
@@ -193,6 +196,82 @@ def run_reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_batch(args, rank, world, local):
+    """K independent pairs per GPU registered concurrently (config 2's batch
+    of pairs; the reference's sweep worker pattern with streams): device time
+    from one start event to the last context's end event, max over ranks."""
+    import threading
+    import torch
+    from paper_2404_01249_b200 import synth
+    from paper_2404_01249_b200.engine import Context
+    K = args.pairs_per_gpu
+    pairs = [synth.make_pair(args.config, seed=rank * K + k) for k in range(K)]
+    tdt = torch.float32 if args.precision == "f32" else torch.float64
+    dev = f"cuda:{local}"
+    bufs = [(torch.from_numpy(p.fixed.astype(np.float32)).to(dev, dtype=tdt),
+             torch.from_numpy(p.moving.astype(np.float32)).to(dev, dtype=tdt),
+             torch.empty((3,) + p.grid.shape, dtype=tdt, device=dev)) for p in pairs]
+    ctxs = [Context(local, args.precision) for _ in range(K)]
+    streams = [torch.cuda.ExternalStream(c.stream_ptr, device=dev) for c in ctxs]
+
+    def run(k, n):
+        c, p, (F, M, o) = ctxs[k], pairs[k], bufs[k]
+        for _ in range(n):
+            c.register_device(p.grid, F.data_ptr(), M.data_ptr(), p.config, p.schedule,
+                              o.data_ptr())
+
+    def all_threads(n):
+        th = [threading.Thread(target=run, args=(k, n)) for k in range(K)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+
+    all_threads(args.warmup)
+    vi = voxel_iters(pairs[0])
+    clocks = ClockSampler(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    l0 = sum(c.launch_count for c in ctxs)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for st in streams:
+        st.wait_event(e0)
+    all_threads(args.steps)
+    ends = []
+    for st in streams:
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(st)
+        ends.append(e)
+    torch.cuda.synchronize()
+    ms = max(e0.elapsed_time(e) for e in ends) / args.steps
+    launches = sum(c.launch_count for c in ctxs) - l0
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    clk = clocks.stop()
+    for c in ctxs:
+        c.close()
+    if rank == 0:
+        line = {"metric": "voxel-iterations/sec", "value": world * K * vi / (ms / 1e3),
+                "unit": "voxel-iter/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms,
+                "pairs_per_s": world * K / (ms / 1e3), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": args.precision,
+                "data": "synthetic (BASELINE config recipe, seeded per pair)",
+                "config": {"workload": pairs[0].name + "_batch", "pairs_per_gpu": K,
+                           "shape_xyz": list(pairs[0].grid.dims),
+                           "note": "one step = K concurrent pairs per GPU"},
+                "gpu_launches": launches, "clocks": clk}
+        print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
@@ -212,6 +291,8 @@ def main():
     from paper_2404_01249_b200 import synth, _abi as A
     from paper_2404_01249_b200.engine import Context
 
+    if args.pairs_per_gpu > 1:
+        return run_batch(args, rank, world, local)
     pair = synth.make_pair(args.config, seed=rank)
     g = pair.grid
     cfg = pair.config
