@@ -225,6 +225,18 @@ int launch_compose_tma(const Launch& L, int R, double cap, const GaussW<T>& w, c
                        LoopState* st, bool count_update = true);
 template <class T>
 void launch_warpgrad(const Launch& L, const T* M, Dims dm, CPlanes3<T> u, Dims d, T* W, T* G);
+// split update (3-D): smooth+Adam whose epilogue also composes, writing the
+// composed field c = step + u(x+step) to `cout`; then the sigma_warp smoothing
+// of c with the fused W/G gather.  Same values as launch_smooth_adam_tma +
+// launch_compose_tma without recomposing halo elements.
+template <class T>
+int launch_smooth_adam_compose_tma(const Launch& L, int R, const GaussW<T>& w, const T* grad,
+                                   T* m, T* nu, const T* uin, T* cout, double cap, Dims d,
+                                   AdamParams ap, LoopState* st, unsigned long long* maxstep);
+template <class T>
+int launch_compose_smooth_tma(const Launch& L, int R, const GaussW<T>& w, const T* c, T* uout,
+                              const T* M, Dims dm, Dims d, T* W, T* G, LoopState* st,
+                              bool count_update = true);
 
 // -------- brick kernels (kernels_brick.cu): 8x8x8 bricks, every pass in
 // parallel; used on the small pyramid levels where the z-march is

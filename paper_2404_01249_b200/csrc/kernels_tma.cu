@@ -52,6 +52,18 @@ constexpr int64_t kSaCoarsenVoxels = 2000000;
 #ifndef DFM_MINB_FWD
 #define DFM_MINB_FWD 3
 #endif
+#ifndef DFM_TY_SAC
+#define DFM_TY_SAC 8
+#endif
+#ifndef DFM_MINB_SAC
+#define DFM_MINB_SAC 2
+#endif
+#ifndef DFM_TY_CS
+#define DFM_TY_CS 8
+#endif
+#ifndef DFM_MINB_CS
+#define DFM_MINB_CS 3
+#endif
 #ifndef DFM_BWD_ACC32
 #define DFM_BWD_ACC32 1
 #endif
@@ -576,10 +588,13 @@ struct LnccBwd2 {
 };
 
 // pipeline.cpp:182-186 + optim.cpp:22-42 + diffeo.cpp:47-57
-template <class T, int R_, int TY_ = DFM_TY_SA, int CY_ = DFM_CY_SA, int MINB_ = DFM_MINB_SA>
+// CAPH_ > 0: the emit also composes, writing c = step + u(x + step) (the
+// composed field ComposeS2 smooths) into `step` instead of the step itself
+template <class T, int R_, int TY_ = DFM_TY_SA, int CY_ = DFM_CY_SA, int MINB_ = DFM_MINB_SA,
+          int CAPH_ = 0>
 struct SmoothAdam2 {
     using Acc = T;
-    using Carry = NoCarry;
+    using Carry = typename std::conditional<(CAPH_ > 0), ComposeCarry<T>, NoCarry>::type;
     static constexpr int R = R_, C = 3, BACK = 0, AHEAD = 0, S = DFM_S_SA, TYv = TY_;
     static constexpr int kMinB = MINB_, kCY = CY_;
     static constexpr bool kStaged = false, kSum = false, kMax = true;
@@ -592,6 +607,7 @@ struct SmoothAdam2 {
     T* m;   // 3 planes
     T* nu;  // 3 planes
     T* step;
+    const T* uin;  // CAPH_ > 0: the current field (3 planes)
     AdamK<T> ak;
     const double* corr1;
     const double* corr2;
@@ -644,28 +660,47 @@ struct SmoothAdam2 {
             c.nu[k] = k < d.ndim ? nu[k * d.n + i] : T(0);
         }
     }
+    __device__ void finish_c(const Carry& cr) const {
+        if constexpr (CAPH_ > 0) {
+            T cv[3];
+            compose_finish(cr, cv);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) step[k * d.n + cr.i] = cv[k];
+        }
+    }
     __device__ Red2 emit(int x, int y, int z, const T s[3], const Center& c, const Prol& p,
-                         Carry&) const {
+                         Carry& cr) const {
         const int64_t i = static_cast<int64_t>((z * d.ny + y) * d.nx + x);
         T mx = T(0);
         bool bad = false;
+        T cl[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             if (k >= d.ndim) {
-                step[k * d.n + i] = T(0);
+                cl[k] = T(0);
                 continue;
             }
             T mm = c.m[k], nn = c.nu[k];
-            const T cl = adam_component(ak, s[k], mm, nn, p.ic1, p.ic2, bad);
+            cl[k] = adam_component(ak, s[k], mm, nn, p.ic1, p.ic2, bad);
             m[k * d.n + i] = mm;
             nu[k * d.n + i] = nn;
-            step[k * d.n + i] = cl;
-            mx = fmax(mx, fabs(cl));
+            mx = fmax(mx, fabs(cl[k]));
+        }
+        if constexpr (CAPH_ > 0) {  // diffeo.cpp:60 compose, pointwise (interp.cpp:269-289)
+            if (cr.valid) finish_c(cr);  // the previous plane's voxel
+            compose_fetch<T, CAPH_>(uin, d, x, y, z + d.zoff, cl, i, cr);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) step[k * d.n + i] = cl[k];
         }
         if (bad && st) st->bad_step = 1;
         return {0.0, static_cast<double>(mx)};
     }
-    __device__ void flush(Carry&) const {}
+    __device__ void flush(Carry& cr) const {
+        if constexpr (CAPH_ > 0) {
+            if (cr.valid) finish_c(cr);
+        }
+    }
     __device__ void finish(int, double, double mx, const Prol& p) const {
         if (maxstep) atomic_max_nonneg(maxstep + p.slot, mx);
     }
@@ -868,6 +903,102 @@ struct Compose2 {
             if (cr.valid) finish_wg(cr);
             wg3_fetch<T>(M, dm, x, y, z + d.zoff, u[0], u[1], u[2], cr.w);
             cr.i = static_cast<int>(i);
+            cr.valid = true;
+        }
+        return {0.0, 0.0};
+    }
+    __device__ void flush(Carry& cr) const {
+        if (W && cr.valid) finish_wg(cr);
+    }
+    __device__ void finish(int, double, double, const Prol&) const {
+        if (st && count_update) st->nupdates += 1;
+    }
+};
+
+// interp.cpp:362-371 + similarity.cpp:25-45: sigma_warp smoothing of the
+// composed field c (SmoothAdam2<..., CAPH> wrote it), u' = G * c, then the
+// fused W = M(x+u'), G = grad M(x+u') epilogue (3-D fast gather, carried one
+// plane).  With the pointwise compose in the Adam kernel this replaces
+// Compose2, which recomposed every halo element of its tile (1.7x work).
+template <class T, int R_, int TY_ = DFM_TY_CS>
+struct ComposeS2 {
+    using Acc = T;
+    using Center = NoCenter;
+    using Prol = NoProl;
+    static constexpr int R = R_, C = 3, BACK = 0, AHEAD = 0, S = DFM_S_SA, TYv = TY_;
+    static constexpr int kMinB = DFM_MINB_CS, kCY = 1;
+    static constexpr bool kStaged = false, kSum = false, kMax = false;
+    static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TYv + 2 * R;
+    static constexpr int kBytes = BX * BY * int(sizeof(T));
+    static constexpr int kBox = align128(kBytes);
+    static constexpr int kStageBytes = 3 * kBox;
+    CUtensorMap mC;
+    GaussW<T> w;
+    T* uout;
+    const T* M;
+    Dims dm;
+    T* W;
+    T* G;
+    LoopState* st;
+    int count_update;
+    Dims d;
+    struct Carry {
+        bool valid;
+        int i;
+        WG3<T> w;
+    };
+
+    __device__ bool skip() const {
+        if (!st) return false;
+        if (st->done) return true;
+        if (st->bad_step) {  // diffeo.cpp:52-53: throw before composing
+            if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+                st->err = 2;
+                st->done = 1;
+            }
+            return true;
+        }
+        return false;
+    }
+    __device__ void prefetch_maps() const { prefetch_tmap(&mC); }
+    __device__ void issue(unsigned char* dst, uint64_t* bar, int x0, int y0, int q) const {
+        mbar_expect_tx(bar, 3 * kBytes);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) tma_load_4d(dst + k * kBox, &mC, bar, x0 - XA, y0 - R, q, k);
+    }
+    __device__ Acc wgt(int a, int j) const { return w.taps[a][j]; }
+    __device__ Acc nrm(int a, int i) const { return __ldg(w.norm[a] + i); }
+    __device__ Prol prologue() const { return {}; }
+    __device__ void xpass(const unsigned char* st_, int row, int col, Acc nx, Acc v[3]) const {
+        const T* p = reinterpret_cast<const T*>(st_) + row * BX + col + (XA - R);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const T* q = p + c * (kBox / int(sizeof(T)));
+            T a = T(0);
+#pragma unroll
+            for (int j = 0; j < 2 * R + 1; ++j) a += w.taps[0][j] * q[j];
+            v[c] = a * nx;
+        }
+    }
+    __device__ void load_center(int, int, int, Center&) const {}
+    __device__ void finish_wg(const Carry& c) const {
+        W[c.i] = wg3_value(c.w);
+        T gr[3];
+        wg3_grad(c.w, gr);
+        G[c.i] = gr[0];
+        G[d.n + c.i] = gr[1];
+        G[2 * d.n + c.i] = gr[2];
+    }
+    __device__ Red2 emit(int x, int y, int z, const T u[3], const Center&, const Prol&,
+                         Carry& cr) const {
+        const int i = d.idx32(x, y, z);
+        uout[i] = u[0];
+        uout[d.n + i] = u[1];
+        uout[2 * d.n + i] = u[2];
+        if (W) {
+            if (cr.valid) finish_wg(cr);
+            wg3_fetch<T>(M, dm, x, y, z + d.zoff, u[0], u[1], u[2], cr.w);
+            cr.i = i;
             cr.valid = true;
         }
         return {0.0, 0.0};
@@ -1154,6 +1285,62 @@ int launch_compose_tma(const Launch& L, int R, double cap, const GaussW<T>& w, c
 }
 
 template <class T>
+int launch_smooth_adam_compose_tma(const Launch& L, int R, const GaussW<T>& w, const T* grad,
+                                   T* m, T* nu, const T* uin, T* cout, double cap, Dims d,
+                                   AdamParams ap, LoopState* st, unsigned long long* maxstep) {
+    const int caph = cap <= 0.5 ? 1 : (cap <= 1.5 ? 2 : 0);
+    if (caph == 0 || d.ndim != 3) return -2;
+    return with_r<0, 6>(R, [&](auto rc) {
+        constexpr int RR = decltype(rc)::value;
+        auto go = [&](auto op) {
+            using Op = decltype(op);
+            if (!make_map<T>(&op.mG, grad, d, 3, Op::BX, Op::BY)) return -1;
+            op.w = w;
+            op.m = m;
+            op.nu = nu;
+            op.step = cout;
+            op.uin = uin;
+            op.ak = adam_k<T>(ap);
+            op.corr1 = ap.corr1;
+            op.corr2 = ap.corr2;
+            op.st = st;
+            op.maxstep = maxstep;
+            op.d = d;
+            return run_zm2(L, op, d);
+        };
+        auto pick = [&](auto ch) {  // the carried gather needs ~100 registers
+            constexpr int CH = decltype(ch)::value;
+            return go(SmoothAdam2<T, RR, DFM_TY_SAC, 1, DFM_MINB_SAC, CH>{});
+        };
+        return caph == 1 ? pick(std::integral_constant<int, 1>{})
+                         : pick(std::integral_constant<int, 2>{});
+    });
+}
+
+template <class T>
+int launch_compose_smooth_tma(const Launch& L, int R, const GaussW<T>& w, const T* c, T* uout,
+                              const T* M, Dims dm, Dims d, T* W, T* G, LoopState* st,
+                              bool count_update) {
+    if (d.ndim != 3) return -2;
+    return with_r<0, 4>(R, [&](auto rc) {
+        constexpr int RR = decltype(rc)::value;
+        using Op = ComposeS2<T, RR>;
+        Op op;
+        if (!make_map<T>(&op.mC, c, d, 3, Op::BX, Op::BY)) return -1;
+        op.w = w;
+        op.uout = uout;
+        op.M = M;
+        op.dm = dm;
+        op.W = W;
+        op.G = G;
+        op.st = st;
+        op.count_update = count_update ? 1 : 0;
+        op.d = d;
+        return run_zm2(L, op, d);
+    });
+}
+
+template <class T>
 void launch_warpgrad(const Launch& L, const T* M, Dims dm, CPlanes3<T> u, Dims d, T* W, T* G) {
     k_warpgrad<T><<<static_cast<unsigned>((d.n + 255) / 256), 256, 0, L.stream>>>(M, dm, u, d, W, G);
     L.bump();
@@ -1174,7 +1361,14 @@ void launch_warpgrad(const Launch& L, const T* M, Dims dm, CPlanes3<T> u, Dims d
     template int launch_compose_tma<T>(const Launch&, int, double, const GaussW<T>&, const T*, \
                                        const T*, T*, const T*, Dims, Dims, T*, T*,             \
                                        LoopState*, bool);                                      \
-    template void launch_warpgrad<T>(const Launch&, const T*, Dims, CPlanes3<T>, Dims, T*, T*);
+    template void launch_warpgrad<T>(const Launch&, const T*, Dims, CPlanes3<T>, Dims, T*, T*); \
+    template int launch_smooth_adam_compose_tma<T>(const Launch&, int, const GaussW<T>&,        \
+                                                   const T*, T*, T*, const T*, T*, double,     \
+                                                   Dims, AdamParams, LoopState*,               \
+                                                   unsigned long long*);                       \
+    template int launch_compose_smooth_tma<T>(const Launch&, int, const GaussW<T>&, const T*,  \
+                                              T*, const T*, Dims, Dims, T*, T*, LoopState*,    \
+                                              bool);
 
 DFM_INST_TMA(float)
 DFM_INST_TMA(double)
