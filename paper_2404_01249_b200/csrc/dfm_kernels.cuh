@@ -262,6 +262,16 @@ int launch_compose_brick(const Launch& L, int R, const GaussW<T>& w, const T* st
                          const T* uin, T* uout, const T* M, Dims dm, Dims d, T* W, T* G,
                          LoopState* st, bool count_update = true);
 
+// brick forms of the split update (see launch_smooth_adam_compose_tma)
+template <class T>
+int launch_smooth_adam_compose_brick(const Launch& L, int R, const GaussW<T>& w, const T* grad,
+                                     T* m, T* nu, const T* uin, T* cout, double cap, Dims d,
+                                     AdamParams ap, LoopState* st, unsigned long long* maxstep);
+template <class T>
+int launch_compose_smooth_brick(const Launch& L, int R, const GaussW<T>& w, const T* c, T* uout,
+                                const T* M, Dims dm, Dims d, T* W, T* G, LoopState* st,
+                                bool count_update = true);
+
 // Persistent scale solver (kernels_brick.cu): every iteration of one small
 // LNCC pyramid level in ONE cooperative launch, grid barriers between the
 // brick phases, device-side monitor.  u0 -> u1 on even iterations (ping-pong);

@@ -1709,6 +1709,20 @@ struct Registrar {
         // iteration) and loses on the full 160x192x224 level (610 -> 650 us)
         const bool split = !use_brick && ctx->split_compose && (mask & 4) && (mask & 8) &&
                            d.ndim == 3 && d.n < kSplitMaxVoxels;
+        if (use_brick && ctx->split_compose) {  // brick: compose once per voxel, not per halo
+            ev_begin(KC_ADAM);
+            const int r1 = launch_smooth_adam_compose_brick<T>(
+                L, Rg, wg, grad.p[0], m.p[0], nu.p[0], u[src].p[0], step.p[0], cfg->step_cap, d,
+                ap, st, maxstep);
+            ev_end();
+            ev_begin(KC_COMPOSE);
+            const int r2 = launch_compose_smooth_brick<T>(L, Rw, ww, step.p[0], u[1 - src].p[0],
+                                                          Ms, d, d, lncc ? Wb : nullptr,
+                                                          lncc ? Gb : nullptr, st);
+            ev_end();
+            if (r1 < 0 || r2 < 0) fail(DFM_E_CUDA, "split update launch failed");
+            return;
+        }
         if (split) {
             ev_begin(KC_ADAM);
             const int r1 = launch_smooth_adam_compose_tma<T>(L, Rg, wg, grad.p[0], m.p[0],

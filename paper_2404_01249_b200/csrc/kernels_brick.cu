@@ -396,7 +396,7 @@ __device__ __forceinline__ void gauss_xpass(const GaussW<T>& w, const T* p, int 
 
 // pipeline.cpp:182-186 + optim.cpp:22-42 + diffeo.cpp:47-57: sigma_grad
 // smoothing, v = -g, Adam, capped step, max |step|
-template <class T, int R_>
+template <class T, int R_, int CAPH_ = 0>
 struct SmoothAdamB {
     using Acc = T;
     using Raw = T;
@@ -406,7 +406,8 @@ struct SmoothAdamB {
     GaussW<T> w;
     T* m;
     T* nu;
-    T* step;
+    T* step;        // CAPH_ > 0: receives the composed field c = step + u(x+step)
+    const T* uin;   // CAPH_ > 0: the current field
     AdamK<T> ak;
     const double* corr1;
     const double* corr2;
@@ -440,13 +441,22 @@ struct SmoothAdamB {
         T mx = T(0);
         bool bad = false;
 #pragma unroll
+        T cl[3];
         for (int k = 0; k < 3; ++k) {
             T mm = m[k * d.n + i], nn = nu[k * d.n + i];
-            const T cl = adam_component(ak, s[k], mm, nn, p.ic1, p.ic2, bad);
+            cl[k] = adam_component(ak, s[k], mm, nn, p.ic1, p.ic2, bad);
             m[k * d.n + i] = mm;
             nu[k * d.n + i] = nn;
-            step[k * d.n + i] = cl;
-            mx = fmax(mx, fabs(cl));
+            mx = fmax(mx, fabs(cl[k]));
+        }
+        if constexpr (CAPH_ > 0) {  // pointwise compose (interp.cpp:269-289)
+            T cv[3];
+            compose_at<T, CAPH_>(uin, d, x, y, z, cl, cv);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) step[k * d.n + i] = cv[k];
+        } else {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) step[k * d.n + i] = cl[k];
         }
         if (bad && st) st->bad_step = 1;
         return {0.0, static_cast<double>(mx)};
@@ -516,6 +526,69 @@ struct ComposeB {
             W[i] = wg3_value(w);
             T gr[3];
             wg3_grad(w, gr);
+            G[i] = gr[0];
+            G[d.n + i] = gr[1];
+            G[2 * d.n + i] = gr[2];
+        }
+        return {0.0, 0.0};
+    }
+    __device__ void finish(int, double, double, const Prol&) const {
+        if (st && count_update) st->nupdates += 1;
+    }
+};
+
+// split update, second half: sigma_warp smoothing of the composed field c
+// (SmoothAdamB<..., CAPH> wrote it) and the fused W/G epilogue
+template <class T, int R_>
+struct ComposeSB {
+    using Acc = T;
+    using Raw = T;
+    using Prol = NoProl;
+    static constexpr int R = R_, C = 3, NR = 3, kStageBatch = 8;
+    static constexpr bool kSum = false, kMax = false;
+    const T* c;  // 3 planes
+    GaussW<T> w;
+    T* uout;
+    const T* M;
+    Dims dm;
+    T* W;
+    T* G;
+    LoopState* st;
+    int count_update;
+    Dims d;
+
+    __device__ bool skip() const {
+        if (!st) return false;
+        if (st->done) return true;
+        if (st->bad_step) {  // diffeo.cpp:52-53: throw before composing
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                st->err = 2;
+                st->done = 1;
+            }
+            return true;
+        }
+        return false;
+    }
+    __device__ void stage(int x, int y, int z, T v[3]) const {
+        const int i = d.idx32(x, y, z);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) v[k] = c[k * d.n + i];
+    }
+    __device__ void xpass(const T* p, int cs, T v[3]) const { gauss_xpass<T, R>(w, p, cs, v); }
+    __device__ T wgt(int a, int j) const { return w.taps[a][j]; }
+    __device__ T nrm(int a, int i) const { return __ldg(w.norm[a] + i); }
+    __device__ Prol prologue() const { return {}; }
+    __device__ Red2 emit(int x, int y, int z, const T s[3], const Prol&) const {
+        const int i = d.idx32(x, y, z);
+        uout[i] = s[0];
+        uout[d.n + i] = s[1];
+        uout[2 * d.n + i] = s[2];
+        if (W) {
+            WG3<T> wg;
+            wg3_fetch<T>(M, dm, x, y, z, s[0], s[1], s[2], wg);
+            W[i] = wg3_value(wg);
+            T gr[3];
+            wg3_grad(wg, gr);
             G[i] = gr[0];
             G[d.n + i] = gr[1];
             G[2 * d.n + i] = gr[2];
@@ -847,6 +920,53 @@ int launch_persist_scale(const Launch& L, const PersistScale<T>& p) {
     return -2;
 }
 
+template <class T>
+int launch_smooth_adam_compose_brick(const Launch& L, int R, const GaussW<T>& w, const T* grad,
+                                     T* m, T* nu, const T* uin, T* cout, double cap, Dims d,
+                                     AdamParams ap, LoopState* st, unsigned long long* maxstep) {
+    return with_rb<0, kBrickGaussRMax>(R, [&](auto rc) {
+        auto go = [&](auto op) {
+            op.grad = grad;
+            op.w = w;
+            op.m = m;
+            op.nu = nu;
+            op.step = cout;
+            op.uin = uin;
+            op.ak = adam_k<T>(ap);
+            op.corr1 = ap.corr1;
+            op.corr2 = ap.corr2;
+            op.st = st;
+            op.maxstep = maxstep;
+            op.d = d;
+            return run_brick(L, op, d);
+        };
+        constexpr int RR = decltype(rc)::value;
+        if (cap <= 0.5) return go(SmoothAdamB<T, RR, 1>{});
+        if (cap <= 1.5) return go(SmoothAdamB<T, RR, 2>{});
+        return go(SmoothAdamB<T, RR, 1 << 20>{});  // any cap: the clamped general form
+    });
+}
+
+template <class T>
+int launch_compose_smooth_brick(const Launch& L, int R, const GaussW<T>& w, const T* c, T* uout,
+                                const T* M, Dims dm, Dims d, T* W, T* G, LoopState* st,
+                                bool count_update) {
+    return with_rb<0, kBrickComposeRMax>(R, [&](auto rc) {
+        ComposeSB<T, decltype(rc)::value> op;
+        op.c = c;
+        op.w = w;
+        op.uout = uout;
+        op.M = M;
+        op.dm = dm;
+        op.W = W;
+        op.G = G;
+        op.st = st;
+        op.count_update = count_update ? 1 : 0;
+        op.d = d;
+        return run_brick(L, op, d);
+    });
+}
+
 #define DFM_INST_BRICK(T)                                                                      \
     template int launch_lncc_fwd_brick<T>(const Launch&, int, const T*, const T*, Dims, T*,    \
                                           double*, const LoopState*, const MonitorArgs*,       \
@@ -860,7 +980,14 @@ int launch_persist_scale(const Launch& L, const PersistScale<T>& p) {
     template int launch_compose_brick<T>(const Launch&, int, const GaussW<T>&, const T*,       \
                                          const T*, T*, const T*, Dims, Dims, T*, T*,           \
                                          LoopState*, bool);                                    \
-    template int launch_persist_scale<T>(const Launch&, const PersistScale<T>&);
+    template int launch_persist_scale<T>(const Launch&, const PersistScale<T>&);              \
+    template int launch_smooth_adam_compose_brick<T>(const Launch&, int, const GaussW<T>&,      \
+                                                     const T*, T*, T*, const T*, T*, double,   \
+                                                     Dims, AdamParams, LoopState*,             \
+                                                     unsigned long long*);                     \
+    template int launch_compose_smooth_brick<T>(const Launch&, int, const GaussW<T>&,           \
+                                                const T*, T*, const T*, Dims, Dims, T*, T*,    \
+                                                LoopState*, bool);
 
 DFM_INST_BRICK(float)
 DFM_INST_BRICK(double)

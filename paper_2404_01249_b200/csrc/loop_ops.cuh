@@ -256,4 +256,12 @@ __device__ __forceinline__ void compose_finish(const ComposeCarry<T>& c, T out[3
     }
 }
 
+template <class T, int CAPH>
+__device__ __forceinline__ void compose_at(const T* __restrict__ u, const Dims& d, int x, int y,
+                                           int zg, const T s[3], T out[3]) {
+    ComposeCarry<T> c;
+    compose_fetch<T, CAPH>(u, d, x, y, zg, s, 0, c);
+    compose_finish(c, out);
+}
+
 }  // namespace dfm
