@@ -234,6 +234,9 @@ int launch_smooth_adam_compose_tma(const Launch& L, int R, const GaussW<T>& w, c
                                    T* m, T* nu, const T* uin, T* cout, double cap, Dims d,
                                    AdamParams ap, LoopState* st, unsigned long long* maxstep);
 template <class T>
+int launch_compose_pointwise(const Launch& L, const T* step, const T* u, double cap, Dims d,
+                             T* c, const LoopState* st);
+template <class T>
 int launch_compose_smooth_tma(const Launch& L, int R, const GaussW<T>& w, const T* c, T* uout,
                               const T* M, Dims dm, Dims d, T* W, T* G, LoopState* st,
                               bool count_update = true);

@@ -114,6 +114,7 @@ struct dfm_ctx {
     bool fwd3 = getenv("DFM_FWD3") ? atoi(getenv("DFM_FWD3")) != 0 : true;
     // split update: pointwise compose in the Adam epilogue + smoothing kernel
     bool split_compose = getenv("DFM_SPLIT") ? atoi(getenv("DFM_SPLIT")) != 0 : true;
+    bool split3 = getenv("DFM_SPLIT3") ? atoi(getenv("DFM_SPLIT3")) != 0 : true;
     Launch L() { return Launch{stream, &launches, num_sms, pdl}; }
 
     LoopState* pinned_state() {
@@ -1536,6 +1537,7 @@ struct Registrar {
     double* corr1;
     double* corr2;
     int cur = 0;
+    GaussW<T> w_id{};          // identity (sigma 0) weights of the current level
     double* fstat = nullptr;   // per-level muF, vF (2 planes) for the 3-moment forward
     bool fstat_ready = false;  // this level's F statistics are current
     T* Wb = nullptr;  // W = M(x+u) for the current u (TMA path)
@@ -1721,6 +1723,30 @@ struct Registrar {
                                                           lncc ? Gb : nullptr, st);
             ev_end();
             if (r1 < 0 || r2 < 0) fail(DFM_E_CUDA, "split update launch failed");
+            return;
+        }
+        // large levels: plain smooth+Adam, a pointwise compose kernel, then the
+        // smoothing + W/G kernel (compose once per voxel, at full occupancy)
+        const bool split3 = !use_brick && ctx->split_compose && ctx->split3 && (mask & 4) &&
+                            (mask & 8) && d.ndim == 3 && d.n >= kSplitMaxVoxels;
+        if (split3) {
+            ev_begin(KC_ADAM);
+            launch_smooth_adam_tma<T>(L, Rg, wg, grad.p[0], m.p[0], nu.p[0], step.p[0], d, ap, st,
+                                      maxstep);
+            ev_end();
+            ev_begin(KC_COMPOSE);
+            T* cbuf = grad.p[0];  // grad is dead after smooth+Adam: it holds c
+            // the plane-streaming compose at Gaussian radius 0: c = step + u(x+step)
+            // from TMA-staged u tiles, no halo recomposition, no W/G, no count
+            if (launch_compose_tma<T>(L, 0, cfg->step_cap, w_id, step.p[0], u[src].p[0], cbuf,
+                                      Ms, d, d, nullptr, nullptr, st, false) < 0)
+                launch_compose_pointwise<T>(L, step.p[0], u[src].p[0], cfg->step_cap, d, cbuf,
+                                            st);
+            const int r2 = launch_compose_smooth_tma<T>(L, Rw, ww, cbuf, u[1 - src].p[0], Ms, d,
+                                                        d, lncc ? Wb : nullptr,
+                                                        lncc ? Gb : nullptr, st);
+            ev_end();
+            if (r2 < 0) fail(DFM_E_CUDA, "split update launch failed");
             return;
         }
         if (split) {
@@ -2067,6 +2093,10 @@ struct Registrar {
         const HostGauss hg = make_gauss(d, sg), hw = make_gauss(d, sw);
         GaussW<T> wg = upload_gauss<T>(ctx, hg, d, "loop_g");
         GaussW<T> ww = upload_gauss<T>(ctx, hw, d, "loop_w");
+        {
+            const double zero[3] = {0, 0, 0};
+            w_id = upload_gauss<T>(ctx, make_gauss(d, zero), d, "loop_id");
+        }
         DevAxisGauss bg{}, bw{};
         const DevAxisGauss* pbg = nullptr;
         const DevAxisGauss* pbw = nullptr;

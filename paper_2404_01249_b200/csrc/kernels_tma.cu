@@ -1317,6 +1317,41 @@ int launch_smooth_adam_compose_tma(const Launch& L, int R, const GaussW<T>& w, c
     });
 }
 
+// pointwise compose c = step + u(x + step) (interp.cpp:269-289), one voxel
+// per thread, for the split update on large levels: a light streaming kernel
+// at full occupancy hides the 24 gathers better than the Adam epilogue can
+template <class T, int CAPH>
+__global__ void __launch_bounds__(256) k_compose_pw(const T* __restrict__ step,
+                                                    const T* __restrict__ u, Dims d,
+                                                    T* __restrict__ c, const LoopState* st) {
+    if (st && (st->done || st->bad_step)) return;
+    const int64_t i = blockIdx.x * 256ll + threadIdx.x;
+    if (i >= d.n) return;
+    const int x = static_cast<int>(i % d.nx);
+    const int64_t r = i / d.nx;
+    const int y = static_cast<int>(r % d.ny), z = static_cast<int>(r / d.ny);
+    const T s[3] = {step[i], step[d.n + i], step[2 * d.n + i]};
+    T cv[3];
+    compose_at<T, CAPH>(u, d, x, y, z + d.zoff, s, cv);
+    c[i] = cv[0];
+    c[d.n + i] = cv[1];
+    c[2 * d.n + i] = cv[2];
+}
+
+template <class T>
+int launch_compose_pointwise(const Launch& L, const T* step, const T* u, double cap, Dims d,
+                             T* c, const LoopState* st) {
+    const unsigned nb = static_cast<unsigned>((d.n + 255) / 256);
+    if (cap <= 0.5)
+        k_compose_pw<T, 1><<<nb, 256, 0, L.stream>>>(step, u, d, c, st);
+    else if (cap <= 1.5)
+        k_compose_pw<T, 2><<<nb, 256, 0, L.stream>>>(step, u, d, c, st);
+    else
+        k_compose_pw<T, (1 << 20)><<<nb, 256, 0, L.stream>>>(step, u, d, c, st);
+    L.bump();
+    return static_cast<int>(nb);
+}
+
 template <class T>
 int launch_compose_smooth_tma(const Launch& L, int R, const GaussW<T>& w, const T* c, T* uout,
                               const T* M, Dims dm, Dims d, T* W, T* G, LoopState* st,
@@ -1366,6 +1401,8 @@ void launch_warpgrad(const Launch& L, const T* M, Dims dm, CPlanes3<T> u, Dims d
                                                    const T*, T*, T*, const T*, T*, double,     \
                                                    Dims, AdamParams, LoopState*,               \
                                                    unsigned long long*);                       \
+    template int launch_compose_pointwise<T>(const Launch&, const T*, const T*, double, Dims,   \
+                                             T*, const LoopState*);                            \
     template int launch_compose_smooth_tma<T>(const Launch&, int, const GaussW<T>&, const T*,  \
                                               T*, const T*, Dims, Dims, T*, T*, LoopState*,    \
                                               bool);
