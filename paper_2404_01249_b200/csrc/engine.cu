@@ -30,7 +30,6 @@ using namespace dfm;
 
 namespace {
 
-constexpr int64_t kSplitMaxVoxels = 2000000;  // split update below this level size
 
 thread_local std::string g_err;
 
@@ -115,6 +114,10 @@ struct dfm_ctx {
     // split update: pointwise compose in the Adam epilogue + smoothing kernel
     bool split_compose = getenv("DFM_SPLIT") ? atoi(getenv("DFM_SPLIT")) != 0 : true;
     bool split3 = getenv("DFM_SPLIT3") ? atoi(getenv("DFM_SPLIT3")) != 0 : true;
+    // levels below this size fold the compose into the Adam epilogue, larger
+    // ones run it as its own radius-0 streaming kernel
+    int64_t split_fold_max = getenv("DFM_SPLIT_FOLD_MAX") ? atoll(getenv("DFM_SPLIT_FOLD_MAX"))
+                                                          : 2000000;
     Launch L() { return Launch{stream, &launches, num_sms, pdl}; }
 
     LoopState* pinned_state() {
@@ -1710,7 +1713,7 @@ struct Registrar {
         // measured: the split wins on mid-size levels (80x96x112: 127 -> 115 us per
         // iteration) and loses on the full 160x192x224 level (610 -> 650 us)
         const bool split = !use_brick && ctx->split_compose && (mask & 4) && (mask & 8) &&
-                           d.ndim == 3 && d.n < kSplitMaxVoxels;
+                           d.ndim == 3 && d.n < ctx->split_fold_max;
         if (use_brick && ctx->split_compose) {  // brick: compose once per voxel, not per halo
             ev_begin(KC_ADAM);
             const int r1 = launch_smooth_adam_compose_brick<T>(
@@ -1728,7 +1731,7 @@ struct Registrar {
         // large levels: plain smooth+Adam, a pointwise compose kernel, then the
         // smoothing + W/G kernel (compose once per voxel, at full occupancy)
         const bool split3 = !use_brick && ctx->split_compose && ctx->split3 && (mask & 4) &&
-                            (mask & 8) && d.ndim == 3 && d.n >= kSplitMaxVoxels;
+                            (mask & 8) && d.ndim == 3 && d.n >= ctx->split_fold_max;
         if (split3) {
             ev_begin(KC_ADAM);
             launch_smooth_adam_tma<T>(L, Rg, wg, grad.p[0], m.p[0], nu.p[0], step.p[0], d, ap, st,
