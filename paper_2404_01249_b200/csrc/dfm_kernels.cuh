@@ -152,9 +152,11 @@ void launch_range_check(const Launch& L, const T* p, int64_t n, int* bad);
 
 // -------- losses
 // per-CTA partial sums (double) into `partials`; returns number of partials.
+struct MonitorArgs;
 template <class T>
 int launch_ssd(const Launch& L, const T* F, const T* M, Dims d, Dims dm, CPlanes3<T> u,
-               Planes3<T> grad, double* partials, const LoopState* st);
+               Planes3<T> grad, double* partials, const LoopState* st,
+               const MonitorArgs* mon = nullptr);
 template <class T>
 int launch_dice_sums(const Launch& L, const T* F, const T* M, Dims d, Dims dm, CPlanes3<T> u,
                      double* partials, const LoopState* st);

@@ -1680,12 +1680,15 @@ struct Registrar {
             else
                 np = launch_lncc_fwd_tma<T>(L, cfg->lncc_radius, Fs, Wb, d, coef[0], partials,
                                             st, &mon);
+        } else if (loss_kind == DFM_LOSS_SSD) {  // loss + grad + monitor, one launch
+            const MonitorArgs mon{st, loss, stamp, cfg->conv_window, cfg->conv_tol};
+            np = launch_ssd<T>(L, Fs, Ms, d, d, uin, grad.w(), partials, st, &mon);
         } else {
             np = loss_kind_launch_fwd<T>(ctx, loss_kind, cfg->lncc_radius, Fs, Ms, d, d, uin,
                                          coef, grad.w(), partials, st);
         }
         ev_end();
-        if (!fused) {
+        if (!fused && loss_kind != DFM_LOSS_SSD) {
             ev_begin(KC_MON);
             launch_monitor(L, monitor_kind(loss_kind), partials, np, static_cast<double>(d.n),
                            st, loss, stamp, cfg->conv_window, cfg->conv_tol);

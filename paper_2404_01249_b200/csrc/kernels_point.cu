@@ -5,6 +5,7 @@
 
 #include "dfm_device.cuh"
 #include "dfm_kernels.cuh"
+#include "loop_ops.cuh"
 
 namespace dfm {
 
@@ -445,11 +446,33 @@ void launch_range_check(const Launch& L, const T* p, int64_t n, int* bad) {
 template <class T>
 __global__ void __launch_bounds__(kNT) k_ssd(const T* __restrict__ F, const T* __restrict__ M,
                                              Dims d, Dims dm, CPlanes3<T> u, Planes3<T> grad,
-                                             double* partials, const LoopState* st) {
+                                             double* partials, const LoopState* st,
+                                             MonitorArgs mon) {
     __shared__ double sh[32];
     if (st && st->done) return;
     double acc = 0.0;
     const T nn = static_cast<T>(d.n);
+    if (d.ndim == 3) {  // 3-D fast form: 32-bit gather, grad * (1/N) in fp32
+        const T inv = sizeof(T) == 4 ? T(1) / nn : T(0);
+        for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < d.n;
+             i += (int64_t)gridDim.x * kNT) {
+            int x, y, z;
+            voxel_xyz(d, i, x, y, z);
+            WG3<T> wg;
+            wg3_fetch<T, false>(M, dm, x, y, z, ld(u.c[0], i), ld(u.c[1], i), ld(u.c[2], i), wg);
+            const T w = wg3_value(wg);
+            const T f = ld(F, i);
+            const double r = static_cast<double>(f) - static_cast<double>(w);
+            acc += r * r;
+            if (grad.c[0]) {
+                T g[3];
+                wg3_grad(wg, g);
+                const T rr = w - f;
+                for (int a = 0; a < 3; ++a)
+                    grad.c[a][i] = sizeof(T) == 4 ? rr * g[a] * inv : rr * g[a] / nn;
+            }
+        }
+    } else {
     for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < d.n;
          i += (int64_t)gridDim.x * kNT) {
         int x, y, z;
@@ -468,15 +491,21 @@ __global__ void __launch_bounds__(kNT) k_ssd(const T* __restrict__ F, const T* _
             for (int a = 0; a < 3; ++a) grad.c[a][i] = rr * g[a] / nn;
         }
     }
+    }
     const double s = block_sum<kNT>(acc, sh);
     if (threadIdx.x == 0) partials[blockIdx.x] = s;
+    if (mon.st) {  // fused convergence monitor (value = +sum / N)
+        __syncthreads();
+        monitor_tail<kNT>(mon, partials, gridDim.x, static_cast<double>(d.n), sh, 1.0);
+    }
 }
 
 template <class T>
 int launch_ssd(const Launch& L, const T* F, const T* M, Dims d, Dims dm, CPlanes3<T> u,
-               Planes3<T> grad, double* partials, const LoopState* st) {
+               Planes3<T> grad, double* partials, const LoopState* st, const MonitorArgs* mon) {
     const int nb = grid_for(d.n, kRedBlocks);
-    k_ssd<T><<<nb, kNT, 0, L.stream>>>(F, M, d, dm, u, grad, partials, st);
+    k_ssd<T><<<nb, kNT, 0, L.stream>>>(F, M, d, dm, u, grad, partials, st,
+                                       mon ? *mon : MonitorArgs{nullptr, nullptr, nullptr, 0, 0.0});
     L.bump();
     return nb;
 }
@@ -652,7 +681,7 @@ void launch_stamp(const Launch& L, unsigned long long* slot) {
                                        const double*, const double*, const LoopState*);        \
     template void launch_range_check<T>(const Launch&, const T*, int64_t, int*);               \
     template int launch_ssd<T>(const Launch&, const T*, const T*, Dims, Dims, CPlanes3<T>,     \
-                               Planes3<T>, double*, const LoopState*);                         \
+                               Planes3<T>, double*, const LoopState*, const MonitorArgs*);                         \
     template int launch_dice_sums<T>(const Launch&, const T*, const T*, Dims, Dims,            \
                                      CPlanes3<T>, double*, const LoopState*);                  \
     template void launch_dice_grad<T>(const Launch&, const T*, const T*, Dims, Dims,           \

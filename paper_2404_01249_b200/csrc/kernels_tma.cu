@@ -1246,8 +1246,12 @@ int launch_smooth_adam_tma(const Launch& L, int R, const GaussW<T>& w, const T* 
         };
         // large levels: two rows per thread (measured -8% at 160x192x224,
         // +8% at 80x96x112); fp64 keeps one row (register budget)
-        if (sizeof(T) == 4 && d.n >= kSaCoarsenVoxels)
-            return go(SmoothAdam2<T, RR, 16, 2, 3>{});
+        // (register ring of 2 x 3 x (2R+1): only for the BASELINE sigma_grad 1.0;
+        // at R = 5 it spills, 504 vs ~160 us)
+        if constexpr (RR <= 3) {
+            if (sizeof(T) == 4 && d.n >= kSaCoarsenVoxels)
+                return go(SmoothAdam2<T, RR, 16, 2, 3>{});
+        }
         return go(SmoothAdam2<T, RR>{});
     });
 }

@@ -50,10 +50,11 @@ __device__ double bmax(double v, double* sh) {
 
 // Fused loss + convergence monitor tail: every CTA has written its partial;
 // the last CTA to arrive sums all partials in fixed order (deterministic) and
-// runs monitor_commit (pipeline.cpp:157-179).  nvox = global voxel count.
+// runs monitor_commit (pipeline.cpp:157-179) on sign * sum / nvox (LNCC -1,
+// SSD +1).  nvox = global voxel count.
 template <int NTH>
 __device__ void monitor_tail(const MonitorArgs& mon, const double* partials, int nb, double nvox,
-                             double* s_red) {
+                             double* s_red, double sign = -1.0) {
     __shared__ int s_last;
     if (threadIdx.x == 0) {
         __threadfence();
@@ -67,8 +68,8 @@ __device__ void monitor_tail(const MonitorArgs& mon, const double* partials, int
         const double tot = bsum<NTH>(acc, s_red);
         if (threadIdx.x == 0) {
             mon.st->arrive = 0;
-            monitor_commit(mon.st, -tot / nvox, 0.0, 0.0, mon.loss, mon.stamp, mon.window,
-                           mon.tol);
+            monitor_commit(mon.st, sign * tot / nvox, 0.0, 0.0, mon.loss, mon.stamp,
+                           mon.window, mon.tol);
         }
     }
 }
