@@ -1951,9 +1951,19 @@ struct Registrar {
         }
         T* coef0[4] = {nullptr, nullptr, nullptr, nullptr};
         check_loss_inputs(F, M, g);
-        const int np = loss_kind_launch_fwd<T>(ctx, cfg->loss, cfg->lncc_radius, F, M, d, d,
-                                               u[cur].r(), coef0, Planes3<T>{{nullptr, nullptr, nullptr}},
-                                               partials, nullptr);
+        int np = -1;
+        if (cfg->loss == DFM_LOSS_LNCC && cfg->lncc_radius <= 5 && d.ndim == 3 &&
+            tma_supported(d, sizeof(T))) {
+            // value only through the plane-streaming forward: W = M(x+u), then moments
+            launch_warpgrad<T>(L, M, d, u[cur].r(), d, Wb, nullptr);
+            np = launch_lncc_fwd_tma<T>(L, cfg->lncc_radius, F, Wb, d, nullptr, partials,
+                                        nullptr);
+        }
+        if (np < 0)
+            np = loss_kind_launch_fwd<T>(ctx, cfg->loss, cfg->lncc_radius, F, M, d, d,
+                                         u[cur].r(), coef0,
+                                         Planes3<T>{{nullptr, nullptr, nullptr}}, partials,
+                                         nullptr);
         double* val = ctx->arr<double>("reg_value3", 4);
         launch_reduce_value(L, monitor_kind(cfg->loss), partials, np, static_cast<double>(d.n),
                             val);
