@@ -422,7 +422,15 @@ struct Impl {
             return;
         }
         const T* src = img;
-        if (blur) {
+        if (blur && make_gauss(d, sigma).R <= kRMax) {
+            // one fused 3-axis pass (z-march, x/y in shared memory, z in registers)
+            const HostGauss h = make_gauss(d, sigma);
+            const GaussW<T> w = upload_gauss<T>(ctx, h, d, "down_" + key);
+            T* b0 = ctx->arr<T>("down_tmp0", d.n);
+            launch_gauss_fused<T>(L, h.R, w, CPlanes3<T>{{img, nullptr, nullptr}},
+                                  Planes3<T>{{b0, nullptr, nullptr}}, 1, d);
+            src = b0;
+        } else if (blur) {
             const HostGauss h = make_gauss(d, sigma);
             const DevAxisGauss g = upload_axis_gauss(ctx, h, d, "down_" + key);
             T* b0 = ctx->arr<T>("down_tmp0", d.n);
