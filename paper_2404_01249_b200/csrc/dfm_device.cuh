@@ -335,22 +335,23 @@ __device__ __forceinline__ void jacobian_at(CPlanes3<T> u, const Dims& d, int x,
     for (int k = 0; k < 9; ++k) J[k] = T(0);
     for (int a = 0; a < d.ndim; ++a) {
         int64_t lo, hi;
-        T den;
+        T scale;  // 1/den: x / 2 == x * 0.5 exactly, x / 1 == x
         if (pos[a] == 0) {
             lo = i;
             hi = i + stride[a];
-            den = T(1);
+            scale = T(1);
         } else if (pos[a] == n[a] - 1) {
             lo = i - stride[a];
             hi = i;
-            den = T(1);
+            scale = T(1);
         } else {
             lo = i - stride[a];
             hi = i + stride[a];
-            den = T(2);
+            scale = T(0.5);
         }
         for (int c = 0; c < d.ndim; ++c)
-            J[c * d.ndim + a] = (__ldg(u.c[c] + hi) - __ldg(u.c[c] + lo)) / den + (c == a ? T(1) : T(0));
+            J[c * d.ndim + a] =
+                (__ldg(u.c[c] + hi) - __ldg(u.c[c] + lo)) * scale + (c == a ? T(1) : T(0));
     }
 }
 
