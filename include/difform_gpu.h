@@ -455,6 +455,13 @@ DFM_API dfm_status dfm_ctx_kernel_times(const dfm_ctx* ctx, double* ms, int64_t*
  * wait on griddepcontrol); 0 (default, measured no faster) = plain stream
  * order.  Env DFM_PDL. */
 #define DFM_OPT_PDL 4
+/* DFM_OPT_SPLIT: 1 (default) = the split update (compose once per voxel, then
+ * smooth); 0 = the fused compose+smooth kernel (recomposes halo elements).
+ * DFM_OPT_SPLIT_FOLD_MAX: levels below this many voxels fold the compose into
+ * the smooth+Adam epilogue, larger ones run it as its own kernel (default
+ * 2000000).  Both give bit-identical fields.  Env DFM_SPLIT, DFM_SPLIT_FOLD_MAX. */
+#define DFM_OPT_SPLIT 5
+#define DFM_OPT_SPLIT_FOLD_MAX 6
 DFM_API dfm_status dfm_ctx_set_option(dfm_ctx* ctx, int key, int64_t value);
 
 #ifdef __cplusplus

@@ -622,6 +622,11 @@ dfm_status dfm_ctx_set_option(dfm_ctx* ctx, int key, int64_t value) {
             ctx->persist = value != 0;
         } else if (key == DFM_OPT_PDL) {
             ctx->pdl = value != 0;
+        } else if (key == DFM_OPT_SPLIT) {
+            ctx->split_compose = value != 0;
+        } else if (key == DFM_OPT_SPLIT_FOLD_MAX) {
+            if (value < 0) fail(DFM_E_INVALID, "split_fold_max must be >= 0");
+            ctx->split_fold_max = value;
         } else {
             fail(DFM_E_INVALID, "unknown context option %d", key);
         }

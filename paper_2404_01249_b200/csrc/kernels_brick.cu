@@ -40,8 +40,14 @@ namespace dfm {
 
 namespace {
 
-constexpr int NTB = 512;
-constexpr int BX = 8, BY = 8, BZ = 8;
+#ifndef DFM_BRICK_BY
+#define DFM_BRICK_BY 8
+#endif
+#ifndef DFM_BRICK_NTB
+#define DFM_BRICK_NTB 512
+#endif
+constexpr int NTB = DFM_BRICK_NTB;
+constexpr int BX = 8, BY = DFM_BRICK_BY, BZ = 8;
 constexpr size_t kBrickSmemMax = 227 * 1024;
 
 struct BG {

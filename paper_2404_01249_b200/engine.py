@@ -45,6 +45,8 @@ OPT_BRICK_MAX = 1
 OPT_FORCE_LEGACY = 2
 OPT_PERSIST = 3
 OPT_PDL = 4
+OPT_SPLIT = 5
+OPT_SPLIT_FOLD_MAX = 6
 
 _lib: Optional[C.CDLL] = None
 

@@ -12,7 +12,8 @@ import pytest
 
 import golden_cases as G
 from paper_2404_01249_b200 import _abi as A, synth
-from paper_2404_01249_b200.engine import Context, OPT_BRICK_MAX, OPT_PERSIST
+from paper_2404_01249_b200.engine import (Context, OPT_BRICK_MAX, OPT_PERSIST, OPT_SPLIT,
+                                          OPT_SPLIT_FOLD_MAX)
 
 pytestmark = pytest.mark.gpu
 
@@ -106,6 +107,26 @@ def test_persistent_solver_early_stop_and_replay(prec):
     lb = [r.loss for r in runs["brick"][1].iterations]
     assert len(la) == len(lb) < sum(p.schedule.iterations)
     assert np.allclose(la, lb, rtol=1e-12 if prec == "f64" else 1e-5)
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_update_variants_bit_identical(prec):
+    """The fused compose+smooth kernel, the split update with the compose folded
+    into smooth+Adam, and the split update with a separate radius-0 compose
+    kernel produce the same bits (stream family, every level)."""
+    z, g, sched = G.register_inputs("lncc")
+    fields = []
+    for split, fold_max in ((0, 0), (1, 1 << 40), (1, 0)):
+        ctx = Context(0, prec)
+        ctx.set_option(OPT_BRICK_MAX, 0)
+        ctx.set_option(OPT_SPLIT, split)
+        ctx.set_option(OPT_SPLIT_FOLD_MAX, fold_max)
+        f, log = ctx.register_images(g, z["fixed"], z["moving"], _cfg("lncc", sched), sched)
+        ctx.close()
+        fields.append((f, [r.loss for r in log.iterations]))
+    for f, ls in fields[1:]:
+        assert np.array_equal(f, fields[0][0])
+        assert ls == fields[0][1]
 
 
 def test_set_option_rejects_unknown_key():
