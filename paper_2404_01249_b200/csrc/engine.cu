@@ -129,6 +129,25 @@ struct dfm_ctx {
         return hstate;
     }
 
+    // per-(level, ping-pong variant) executable graphs kept across calls: a
+    // re-capture is applied with cudaGraphExecUpdate (cheap) instead of a new
+    // cudaGraphInstantiate (hundreds of us of host time the GPU waits for)
+    std::map<int, cudaGraphExec_t> graph_cache;
+    cudaGraphExec_t graph_exec(int key, cudaGraph_t graph) {
+        auto it = graph_cache.find(key);
+        if (it != graph_cache.end()) {
+            cudaGraphExecUpdateResultInfo info;
+            if (cudaGraphExecUpdate(it->second, graph, &info) == cudaSuccess) return it->second;
+            cudaGetLastError();  // topology changed: instantiate afresh
+            CK(cudaGraphExecDestroy(it->second));
+            graph_cache.erase(it);
+        }
+        cudaGraphExec_t e = nullptr;
+        CK(cudaGraphInstantiate(&e, graph, 0));
+        graph_cache[key] = e;
+        return e;
+    }
+
     std::map<std::string, std::pair<void*, size_t>> pinned;  // page-locked host staging
     void* get_pinned(const std::string& name, size_t bytes) {
         auto it = pinned.find(name);
@@ -572,6 +591,7 @@ void dfm_ctx_destroy(dfm_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (auto& kv : ctx->bufs) cudaFree(kv.second.first);
     for (auto& kv : ctx->pinned) cudaFreeHost(kv.second.first);
+    for (auto& kv : ctx->graph_cache) cudaGraphExecDestroy(kv.second);
     if (ctx->hstate) cudaFreeHost(ctx->hstate);
     for (int k = 0; k < 2; ++k)
         if (ctx->chunk_ev[k]) cudaEventDestroy(ctx->chunk_ev[k]);
@@ -2210,7 +2230,7 @@ struct Registrar {
                 CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
                 enqueue_iteration(d, (start + v) % 2, Rg, Rw, wg, ww, pbg, pbw);
                 CK(cudaStreamEndCapture(ctx->stream, &graph));
-                CK(cudaGraphInstantiate(&exec[v], graph, 0));
+                exec[v] = ctx->graph_exec(2 * si + v, graph);
                 CK(cudaGraphDestroy(graph));
                 nodes_per = ctx->launches - before;
                 ctx->launches = before;
@@ -2239,8 +2259,7 @@ struct Registrar {
                 ++nchunk;
             }
             launch_stamp(ctx->L(), stamp + T_si);
-            ctx->sync();
-            for (int v = 0; v < 2; ++v) CK(cudaGraphExecDestroy(exec[v]));
+            ctx->sync();  // the execs stay in ctx->graph_cache for the next call
         }
         // read back the scale's log (one readback per scale)
         LoopState hs;
