@@ -9,6 +9,7 @@
 
 #include <cstdint>
 #include <cuda_runtime.h>
+#include "tma_util.cuh"
 
 namespace dfm {
 
@@ -260,15 +261,56 @@ __device__ __forceinline__ void wg3_fetch(const T* __restrict__ M, const Dims& m
     w.v[7] = ld_<T, NC>(p + sz + sy + 1);
 }
 
+// the same gather issued as cp.async copies of the 8 corners into s[k * ss]
+// (shared memory); wg3_load pulls them into w.v once cp_async_wait_all() ran
+template <class T>
+__device__ __forceinline__ void wg3_fetch_async(const T* __restrict__ M, const Dims& m, int x,
+                                                int y, int z, T ux, T uy, T uz, WG3<T>& w,
+                                                T* s, int ss) {
+    const AxisCell<T> ax = locate_axis(x, ux, m.nx);
+    const AxisCell<T> ay = locate_axis(y, uy, m.ny);
+    const AxisCell<T> az = locate_axis(z, uz, m.nz);
+    w.fx = ax.f;
+    w.fy = ay.f;
+    w.fz = az.f;
+    w.clamp = (ax.clamped ? 1u : 0u) | (ay.clamped ? 2u : 0u) | (az.clamped ? 4u : 0u);
+    const int sy = m.nx, sz = m.nx * m.ny;
+    w.base = (az.i0 * m.ny + ay.i0) * m.nx + ax.i0;
+    const T* p = M + w.base;
+    const int off[8] = {0, 1, sy, sy + 1, sz, sz + 1, sz + sy, sz + sy + 1};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) cp_async<int(sizeof(T))>(s + k * ss, p + off[k]);
+    cp_async_commit();
+}
+
+template <class T>
+__device__ __forceinline__ void wg3_load(WG3<T>& w, const T* s, int ss) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w.v[k] = s[k * ss];
+}
+
+// The 8-corner sums below are written as explicit fma chains: left to the
+// compiler, mul+add contraction depends on the surrounding code, and the
+// gather's kernels (fused, split, brick, streamed, synchronous or cp.async
+// gather) must round identically.
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+
 template <class T>
 __device__ __forceinline__ T wg3_value(const WG3<T>& w) {
     const T wx0 = T(1) - w.fx, wx1 = w.fx;
     const T wy0 = T(1) - w.fy, wy1 = w.fy;
     const T wz0 = T(1) - w.fz, wz1 = w.fz;
-    T acc = (wx0 * wy0 * wz0) * w.v[0] + (wx1 * wy0 * wz0) * w.v[1] +
-            (wx0 * wy1 * wz0) * w.v[2] + (wx1 * wy1 * wz0) * w.v[3];
-    acc += (wx0 * wy0 * wz1) * w.v[4] + (wx1 * wy0 * wz1) * w.v[5] +
-           (wx0 * wy1 * wz1) * w.v[6] + (wx1 * wy1 * wz1) * w.v[7];
+    const T a00 = mul_rn(wy0, wz0), a10 = mul_rn(wy1, wz0), a01 = mul_rn(wy0, wz1),
+            a11 = mul_rn(wy1, wz1);
+    T acc = mul_rn(mul_rn(wx0, a00), w.v[0]);
+    acc = fma(mul_rn(wx1, a00), w.v[1], acc);
+    acc = fma(mul_rn(wx0, a10), w.v[2], acc);
+    acc = fma(mul_rn(wx1, a10), w.v[3], acc);
+    acc = fma(mul_rn(wx0, a01), w.v[4], acc);
+    acc = fma(mul_rn(wx1, a01), w.v[5], acc);
+    acc = fma(mul_rn(wx0, a11), w.v[6], acc);
+    acc = fma(mul_rn(wx1, a11), w.v[7], acc);
     return acc;
 }
 
@@ -278,14 +320,20 @@ __device__ __forceinline__ void wg3_grad(const WG3<T>& w, T g[3]) {
     const T wy0 = T(1) - w.fy, wy1 = w.fy;
     const T wz0 = T(1) - w.fz, wz1 = w.fz;
     const T* k = w.v;
-    T a = (wy0 * wz0) * (k[1] - k[0]) + (wy1 * wz0) * (k[3] - k[2]);
-    a += (wy0 * wz1) * (k[5] - k[4]) + (wy1 * wz1) * (k[7] - k[6]);
+    T a = mul_rn(mul_rn(wy0, wz0), k[1] - k[0]);
+    a = fma(mul_rn(wy1, wz0), k[3] - k[2], a);
+    a = fma(mul_rn(wy0, wz1), k[5] - k[4], a);
+    a = fma(mul_rn(wy1, wz1), k[7] - k[6], a);
     g[0] = (w.clamp & 1u) ? T(0) : a;
-    T b = (wx0 * wz0) * (k[2] - k[0]) + (wx1 * wz0) * (k[3] - k[1]);
-    b += (wx0 * wz1) * (k[6] - k[4]) + (wx1 * wz1) * (k[7] - k[5]);
+    T b = mul_rn(mul_rn(wx0, wz0), k[2] - k[0]);
+    b = fma(mul_rn(wx1, wz0), k[3] - k[1], b);
+    b = fma(mul_rn(wx0, wz1), k[6] - k[4], b);
+    b = fma(mul_rn(wx1, wz1), k[7] - k[5], b);
     g[1] = (w.clamp & 2u) ? T(0) : b;
-    const T c = (wx0 * wy0) * (k[4] - k[0]) + (wx1 * wy0) * (k[5] - k[1]) +
-                (wx0 * wy1) * (k[6] - k[2]) + (wx1 * wy1) * (k[7] - k[3]);
+    T c = mul_rn(mul_rn(wx0, wy0), k[4] - k[0]);
+    c = fma(mul_rn(wx1, wy0), k[5] - k[1], c);
+    c = fma(mul_rn(wx0, wy1), k[6] - k[2], c);
+    c = fma(mul_rn(wx1, wy1), k[7] - k[3], c);
     g[2] = (w.clamp & 4u) ? T(0) : c;
 }
 

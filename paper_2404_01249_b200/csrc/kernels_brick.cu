@@ -274,14 +274,13 @@ struct LnccFwdB {
     __device__ double nrm(int, int) const { return 1.0; }
     __device__ Prol prologue() const { return {}; }
     __device__ Red2 emit(int x, int y, int z, const double s[C], const Prol&) const {
-        const double n = static_cast<double>(box_len(x, d.nx, R) * box_len(y, d.ny, R) *
-                                             box_len(z, d.nz, R));
+        const double inv_n = window_inv<R>(x, y, z, d);
         const int i = d.idx32(x, y, z);
         LnccCoef k;
         if constexpr (FS)
-            k = lncc_coef_f(__ldg(fstat + i), __ldg(fstat + d.n + i), s[0], s[1], s[2], n);
+            k = lncc_coef_f(__ldg(fstat + i), __ldg(fstat + d.n + i), s[0], s[1], s[2], inv_n);
         else
-            k = lncc_coef(s, n);
+            k = lncc_coef(s, inv_n);
         if (coef) {
             coef[i] = static_cast<T>(k.an);
             coef[d.n + i] = static_cast<T>(k.amu);
@@ -323,10 +322,9 @@ struct FStatsB {
     __device__ double nrm(int, int) const { return 1.0; }
     __device__ Prol prologue() const { return {}; }
     __device__ Red2 emit(int x, int y, int z, const double s[2], const Prol&) const {
-        const double n = static_cast<double>(box_len(x, d.nx, R) * box_len(y, d.ny, R) *
-                                             box_len(z, d.nz, R));
+        const double inv_n = window_inv<R>(x, y, z, d);
         double muF, vF;
-        lncc_fstats(s[0], s[1], n, muF, vF);
+        lncc_fstats(s[0], s[1], inv_n, muF, vF);
         const int i = d.idx32(x, y, z);
         fstat[i] = muF;
         fstat[d.n + i] = vF;

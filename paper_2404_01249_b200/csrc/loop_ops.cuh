@@ -82,13 +82,13 @@ struct LnccCoef {
     double cc2, an, amu, bn, bmu;
 };
 
-// The fixed image's window statistics (similarity.cpp:145-150, F half):
+// The fixed image's window statistics (similarity.cpp:145-150, F half),
+// given inv_n = 1 / (clipped window size):
 // constant over the iterations of a pyramid level, so computable once per
 // level.  Products and differences are explicit (no FMA contraction) so the
 // split and the fused forms below round identically.
-__device__ __forceinline__ void lncc_fstats(double sF, double sF2, double n, double& muF,
+__device__ __forceinline__ void lncc_fstats(double sF, double sF2, double inv_n, double& muF,
                                             double& vF) {
-    const double inv_n = 1.0 / n;
     muF = __dmul_rn(sF, inv_n);
     vF = __dsub_rn(__dmul_rn(sF2, inv_n), __dmul_rn(muF, muF));
     vF = vF < 0.0 ? 0.0 : vF;
@@ -97,9 +97,8 @@ __device__ __forceinline__ void lncc_fstats(double sF, double sF2, double n, dou
 // window coefficients given the F statistics and the three W moments
 // (ΣW, ΣW², ΣFW)
 __device__ __forceinline__ LnccCoef lncc_coef_f(double muF, double vF, double sW, double sW2,
-                                                double sFW, double n) {
+                                                double sFW, double inv_n) {
     LnccCoef r{0.0, 0.0, 0.0, 0.0, 0.0};
-    const double inv_n = 1.0 / n;
     const double muW = __dmul_rn(sW, inv_n);
     double vW = __dsub_rn(__dmul_rn(sW2, inv_n), __dmul_rn(muW, muW));
     vW = vW < 0.0 ? 0.0 : vW;
@@ -119,10 +118,26 @@ __device__ __forceinline__ LnccCoef lncc_coef_f(double muF, double vF, double sW
 
 // from the five raw moments: the same two steps, hence bit-identical to the
 // precomputed-F form
-__device__ __forceinline__ LnccCoef lncc_coef(const double s[5], double n) {
+__device__ __forceinline__ LnccCoef lncc_coef(const double s[5], double inv_n) {
     double muF, vF;
-    lncc_fstats(s[0], s[2], n, muF, vF);
-    return lncc_coef_f(muF, vF, s[1], s[3], s[4], n);
+    lncc_fstats(s[0], s[2], inv_n, muF, vF);
+    return lncc_coef_f(muF, vF, s[1], s[3], s[4], inv_n);
+}
+
+// 1 / (clipped window size) at voxel (x, y, z local; zoff/gnz from the view):
+// interior voxels take the compile-time constant (the same correctly rounded
+// value a division would give), border voxels divide
+template <int R>
+__device__ __forceinline__ double window_inv(int x, int y, int z, const Dims& d) {
+    constexpr double K = 2 * R + 1;
+    const int gz = d.gz(), zg = z + d.zoff;
+    const bool three = gz > 1;
+    if (x >= R && x < d.nx - R && y >= R && y < d.ny - R &&
+        (!three || (zg >= R && zg < gz - R)))
+        return three ? 1.0 / (K * K * K) : 1.0 / (K * K);
+    const double n = static_cast<double>(box_len(x, d.nx, R) * box_len(y, d.ny, R) *
+                                         (three ? box_len(zg, gz, R) : 1));
+    return 1.0 / n;
 }
 
 // dL/dW at one voxel from the box sums of the 4 coefficients (similarity.cpp:182)

@@ -69,6 +69,23 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
+// per-thread asynchronous gathers (cp.async, SASS LDGSTS): the data lands in
+// shared memory and is waited for with cp.async.wait_all where it is consumed,
+// so a gather in flight across a loop iteration occupies no register
+// scoreboard (ptxas drains shared scoreboards at loop heads)
+template <int B>
+__device__ __forceinline__ void cp_async(void* s, const void* g) {
+    static_assert(B == 4 || B == 8 || B == 16, "cp.async size");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(s)), "l"(g), "n"(B)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
