@@ -259,6 +259,21 @@ __device__ __forceinline__ void compose_fetch(const T* __restrict__ u, const Dim
     c.valid = true;
 }
 
+// trilinear combination of the 8 corners, as explicit fma chains: every
+// compose path (fused, folded, split, brick, register or cp.async gather)
+// rounds identically whatever the compiler would contract around it
+template <class T>
+__device__ __forceinline__ T bilerp4(T w00, T w10, T w01, T w11, T a0, T a1, T a2, T a3) {
+    T r = mul_rn(w00, a0);
+    r = fma(w10, a1, r);
+    r = fma(w01, a2, r);
+    return fma(w11, a3, r);
+}
+template <class T>
+__device__ __forceinline__ T zlerp(T wz0, T lo, T wz1, T hi) {
+    return fma(wz0, lo, mul_rn(wz1, hi));
+}
+
 template <class T>
 __device__ __forceinline__ void compose_finish(const ComposeCarry<T>& c, T out[3]) {
     const T wx0 = T(1) - c.fx, wy0 = T(1) - c.fy, wz0 = T(1) - c.fz;
@@ -266,9 +281,74 @@ __device__ __forceinline__ void compose_finish(const ComposeCarry<T>& c, T out[3
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         const T* a = c.a[k];
-        const T lo = w00 * a[0] + w10 * a[1] + w01 * a[2] + w11 * a[3];
-        const T hi = w00 * a[4] + w10 * a[5] + w01 * a[6] + w11 * a[7];
-        out[k] = c.s[k] + (wz0 * lo + c.fz * hi);
+        const T lo = bilerp4(w00, w10, w01, w11, a[0], a[1], a[2], a[3]);
+        const T hi = bilerp4(w00, w10, w01, w11, a[4], a[5], a[6], a[7]);
+        out[k] = c.s[k] + zlerp(wz0, lo, c.fz, hi);
+    }
+}
+
+// the same compose with the 24 corner values gathered by cp.async into
+// shared memory (buf[(k * 8 + j) * ss], k component, j corner): the carry
+// holds 7 values instead of 30 registers of loads in flight
+template <class T>
+struct ComposeCarryA {
+    bool valid;
+    int slot;
+    int64_t i;
+    T s[3];
+    T fx, fy, fz;
+};
+
+template <class T, int CAPH>
+__device__ __forceinline__ void compose_fetch_async(const T* const* u, const Dims& d, int x,
+                                                    int y, int zg, const T s[3], int64_t i,
+                                                    ComposeCarryA<T>& c, T* buf, int ss) {
+    const int gz = d.gz();
+    int ix, iy, iz;
+    if (x >= CAPH && x < d.nx - CAPH && y >= CAPH && y < d.ny - CAPH && zg >= CAPH &&
+        zg < gz - CAPH) {
+        cell_exact<T>(x, s[0], ix, c.fx);
+        cell_exact<T>(y, s[1], iy, c.fy);
+        cell_exact<T>(zg, s[2], iz, c.fz);
+    } else {
+        const AxisCell<T> ax = locate_axis(x, s[0], d.nx);
+        const AxisCell<T> ay = locate_axis(y, s[1], d.ny);
+        const AxisCell<T> az = locate_axis(zg, s[2], gz);
+        ix = ax.i0;
+        iy = ay.i0;
+        iz = az.i0;
+        c.fx = ax.f;
+        c.fy = ay.f;
+        c.fz = az.f;
+    }
+    const int sy = d.nx;
+    const int64_t sz = static_cast<int64_t>(d.nx) * d.ny;
+    const int64_t base = (static_cast<int64_t>(iz - d.zoff) * d.ny + iy) * d.nx + ix;
+    const int64_t off[8] = {0, 1, sy, sy + 1, sz, sz + 1, sz + sy, sz + sy + 1};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const T* a = u[k] + base;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) cp_async<int(sizeof(T))>(buf + (k * 8 + j) * ss, a + off[j]);
+        c.s[k] = s[k];
+    }
+    cp_async_commit();
+    c.i = i;
+    c.valid = true;
+}
+
+// after cp_async_wait_all()
+template <class T>
+__device__ __forceinline__ void compose_finish_async(const ComposeCarryA<T>& c, const T* buf,
+                                                     int ss, T out[3]) {
+    const T wx0 = T(1) - c.fx, wy0 = T(1) - c.fy, wz0 = T(1) - c.fz;
+    const T w00 = wx0 * wy0, w10 = c.fx * wy0, w01 = wx0 * c.fy, w11 = c.fx * c.fy;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const T* a = buf + k * 8 * ss;
+        const T lo = bilerp4(w00, w10, w01, w11, a[0], a[ss], a[2 * ss], a[3 * ss]);
+        const T hi = bilerp4(w00, w10, w01, w11, a[4 * ss], a[5 * ss], a[6 * ss], a[7 * ss]);
+        out[k] = c.s[k] + zlerp(wz0, lo, c.fz, hi);
     }
 }
 
