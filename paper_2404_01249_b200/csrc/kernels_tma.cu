@@ -146,6 +146,8 @@ template <class Op>
 __host__ __device__ constexpr int zm2_core_bytes() {
     using Acc = typename Op::Acc;
     constexpr int HI = Op::TYv + 2 * Op::R, WI = kTX + 2 * Op::R;
+    if constexpr (Op::kStaged && Op::R == 0)  // pointwise: no filter buffers
+        return Op::S * Op::kStageBytes;
     return Op::S * Op::kStageBytes +
            (Op::kStaged ? int(sizeof(Acc)) * Op::C * HI * WI : 0) +
            2 * int(sizeof(Acc)) * Op::C * HI * kTX;
@@ -258,6 +260,39 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
     const int zend = z1 + R;
 
     for (int zi = z0 - R; zi < zend; ++zi) {
+        if constexpr (Op::kStaged && R == 0) {
+            // pointwise staged op (e.g. the radius-0 compose of the split
+            // update): the staged value is the output, no filter passes
+            while (waited < zi + Op::AHEAD) {
+                ++waited;
+                const int k = waited - q0;
+                mbar_wait(&bars[k % S], (k / S) & 1);
+            }
+            const typename Op::PlaneCtx pc = op.plane_ctx(stages, q0, zi);
+            const bool fast = op.interior(x0, y0, zi);  // CTA-uniform
+            typename Op::Center cen{};
+#pragma unroll
+            for (int r = 0; r < CY; ++r) {
+                if (!own[r]) continue;
+                Acc v[C];
+                if (fast)
+                    op.stage_fast(pc, x0, y0, zi, ty + r * TYt, tx, v);
+                else
+                    op.stage(pc, x0, y0, zi, ty + r * TYt, tx, v);
+                const Red2 rr = op.emit(x, yk[r], zi, v, cen, pr, carry[r]);
+                rsum += rr.sum;
+                rmax = fmax(rmax, rr.mx);
+            }
+            __syncthreads();  // plane zi - BACK's slot is free for the next plane
+            if (tid == 0) {
+                const int qf = zi - Op::BACK + S;
+                if (qf < qend) {
+                    const int k = qf - q0;
+                    op.issue(stages + (k % S) * SB, &bars[k % S], x0, y0, qf);
+                }
+            }
+            continue;
+        }
         constexpr int kk = K - 1;
         const int zo = zi - R;
         typename Op::Center cen[CY];
