@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
     Acc nyv[CY];
 #pragma unroll
     for (int k = 0; k < CY; ++k) {
-        yk[k] = y0 + ty + k * TYt;
+        yk[k] = y0 + ty * CY + k;  // consecutive rows: their y windows share K-1 loads
         own[k] = x < d.nx && yk[k] < d.ny;
         nyv[k] = own[k] ? op.nrm(1, yk[k]) : Acc(0);
     }
@@ -276,9 +276,9 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
                 if (!own[r]) continue;
                 Acc v[C];
                 if (fast)
-                    op.stage_fast(pc, x0, y0, zi, ty + r * TYt, tx, v);
+                    op.stage_fast(pc, x0, y0, zi, ty * CY + r, tx, v);
                 else
-                    op.stage(pc, x0, y0, zi, ty + r * TYt, tx, v);
+                    op.stage(pc, x0, y0, zi, ty * CY + r, tx, v);
                 const Red2 rr = op.emit(x, yk[r], zi, v, cen, pr, carry[r]);
                 rsum += rr.sum;
                 rmax = fmax(rmax, rr.mx);
@@ -354,10 +354,11 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
                 op.issue(stages + (k % S) * SB, &bars[k % S], x0, y0, qf);
             }
         }
+        // y pass of every owned row into ring slot kk (the newest plane) before
+        // any emit: the rows' windows overlap and their loads are shared
 #pragma unroll
         for (int r = 0; r < CY; ++r) {
-            // y pass into ring slot kk (the newest plane)
-            const int row = ty + r * TYt;
+            const int row = ty * CY + r;
 #pragma unroll
             for (int c = 0; c < C; ++c) {
                 const Acc* src = sx + (c * HI + row) * TX + tx;
@@ -368,6 +369,9 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
                 for (int k = 0; k < K - 1; ++k) ring[r][c][k] = ring[r][c][k + 1];
                 ring[r][c][kk] = a * nyv[r];
             }
+        }
+#pragma unroll
+        for (int r = 0; r < CY; ++r) {
             if (zo >= z0 && own[r]) {
                 // oldest plane (zo - R) sits in slot 0 (slot (kk + 1) % K)
                 const Acc nz = op.nrm(2, zo + d.zoff);
@@ -837,7 +841,7 @@ struct Compose2 {
     using Acc = T;
     using Center = NoCenter;
     using Prol = NoProl;
-    static constexpr int kMinB = DFM_MINB_CO, kCY = DFM_CY_CO;
+    static constexpr int kMinB = DFM_MINB_CO, kCY = R_ == 0 ? 2 : DFM_CY_CO;  // pointwise: 2 rows
     static constexpr int R = R_, C = 3, BACK = CAPH, AHEAD = CAPH,
                          S = 2 * CAPH + 2 + DFM_S_CO_EXTRA, TYv = TY_;
     static constexpr bool kStaged = true, kSum = false, kMax = false;
