@@ -58,6 +58,15 @@ constexpr int64_t kSaCoarsenVoxels = 2000000;
 #ifndef DFM_CS_ASYNC
 #define DFM_CS_ASYNC 1
 #endif
+#ifndef DFM_SA_QUAD1
+#define DFM_SA_QUAD1 1
+#endif
+#ifndef DFM_SA_QUAD2
+#define DFM_SA_QUAD2 0
+#endif
+#ifndef DFM_MINB_SA2
+#define DFM_MINB_SA2 3
+#endif
 #ifndef DFM_SAC_ASYNC
 #define DFM_SAC_ASYNC 0
 #endif
@@ -69,6 +78,9 @@ constexpr int64_t kSaCoarsenVoxels = 2000000;
 #endif
 #ifndef DFM_TY_CS
 #define DFM_TY_CS 8
+#endif
+#ifndef DFM_CY_CS
+#define DFM_CY_CS 1
 #endif
 #ifndef DFM_MINB_CS
 #define DFM_MINB_CS 3
@@ -93,7 +105,7 @@ constexpr int64_t kSaCoarsenVoxels = 2000000;
 #define DFM_CY_FWD 1
 #endif
 #ifndef DFM_CY_BWD
-#define DFM_CY_BWD 1
+#define DFM_CY_BWD 2
 #endif
 #ifndef DFM_CY_SA
 #define DFM_CY_SA 1
@@ -164,6 +176,39 @@ __device__ __forceinline__ unsigned char* zm2_extra() {
     return zm2_smem_base() + ((zm2_core_bytes<Op>() + 15) & ~15);
 }
 
+// x filter four columns per thread (Op::kXQuad, fp32 ops): 128-bit shared
+// loads of the row window, one 128-bit store of the four results
+template <class Op, class = void>
+struct XQuad {
+    static constexpr bool value = false;
+};
+template <class Op>
+struct XQuad<Op, std::void_t<decltype(Op::kXQuad)>> {
+    static constexpr bool value = Op::kXQuad;
+};
+
+// the float4 chunks [col, col + 4 * NCH) of a stage row, col % 4 == 0
+template <int NCH>
+__device__ __forceinline__ void load_row4(const float* p, float w[4 * NCH]) {
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+        const float4 t = reinterpret_cast<const float4*>(p)[k];
+        w[4 * k] = t.x;
+        w[4 * k + 1] = t.y;
+        w[4 * k + 2] = t.z;
+        w[4 * k + 3] = t.w;
+    }
+}
+
+// optional per-row carry initialisation (Op::init_carry(carry, row))
+template <class Op, class C>
+__device__ __forceinline__ auto carry_init(const Op& op, C& c, int r, int)
+    -> decltype(op.init_carry(c, r), void()) {
+    op.init_carry(c, r);
+}
+template <class Op, class C>
+__device__ __forceinline__ void carry_init(const Op&, C&, int, long) {}
+
 struct ZG2 {
     Dims d;
     int zchunk;
@@ -219,6 +264,14 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
             op.issue(stages + ((q - q0) % S) * SB, &bars[(q - q0) % S], x0, y0, q);
 
     const Acc nxv = x < d.nx ? op.nrm(0, x) : Acc(0);
+    constexpr bool kQuad = XQuad<Op>::value;
+    constexpr int NQ = TX / 4;  // quads per tile row
+    static_assert(!kQuad || NTh % NQ == 0, "quad x pass: whole rows per thread group");
+    const int xq = 4 * (tid % NQ);  // this thread's quad of tile columns
+    Acc nx4[4];
+#pragma unroll
+    for (int o = 0; o < 4; ++o)
+        nx4[o] = (kQuad && x0 + xq + o < d.nx) ? op.nrm(0, x0 + xq + o) : Acc(0);
     int yk[CY];
     bool own[CY];
     Acc nyv[CY];
@@ -237,12 +290,15 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
         // plane on every plane, which is what the Carry exists to avoid
         __shared__ volatile unsigned s_sink;
         unsigned h = fold_bits(nxv);
+        if constexpr (kQuad) h ^= fold_bits(nx4);
 #pragma unroll
         for (int k = 0; k < CY; ++k) h ^= fold_bits(nyv[k]);
         if constexpr (!std::is_empty<typename Op::Prol>::value) h ^= pr.bits();
         if (DFM_SINK && h == 0x9e3779b9u) s_sink = h;  // any consumer will do; almost never runs
     }
     typename Op::Carry carry[CY] = {};
+#pragma unroll
+    for (int r = 0; r < CY; ++r) carry_init(op, carry[r], r, 0);
 
     // register ring of the last K xy-filtered planes per owned row; it shifts
     // by register moves (C*(K-1) MOVs per plane and row) rather than unrolling
@@ -335,6 +391,17 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
                     for (int j = 0; j < K; ++j) a += op.wgt(0, j) * src[j];
                     sx[(c * HI + row) * TX + tx] = a * nxv;
                 }
+            }
+        } else if constexpr (kQuad) {
+            const unsigned char* st = stages + ((zi - q0) % S) * SB;
+#pragma unroll
+            for (int row = tid / NQ; row < HI; row += NTh / NQ) {
+                Acc v[C][4];
+                op.xpass4(st, row, xq, nx4, v);
+#pragma unroll
+                for (int c = 0; c < C; ++c)
+                    *reinterpret_cast<float4*>(sx + (c * HI + row) * TX + xq) =
+                        make_float4(v[c][0], v[c][1], v[c][2], v[c][3]);
             }
         } else {
             const unsigned char* st = stages + ((zi - q0) % S) * SB;
@@ -624,7 +691,8 @@ struct LnccBwd2 {
     using Prol = NoProl;
     using Carry = NoCarry;
     static constexpr int R = R_, C = 4, BACK = 0, AHEAD = 0, S = DFM_S_BWD, TYv = TY_;
-    static constexpr int kMinB = DFM_MINB_BWD, kCY = DFM_CY_BWD;
+    // fp32 sums: two consecutive rows per thread (-20 us/iteration at 160x192x224)
+    static constexpr int kMinB = DFM_MINB_BWD, kCY = sizeof(Acc) == 4 ? DFM_CY_BWD : 1;
     static constexpr bool kStaged = false, kSum = false, kMax = false;
     static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TYv + 2 * R;
     static constexpr int kBytes = BX * BY * int(sizeof(T));
@@ -652,6 +720,24 @@ struct LnccBwd2 {
     __device__ Acc wgt(int, int) const { return 1.0; }
     __device__ Acc nrm(int, int) const { return 1.0; }
     __device__ Prol prologue() const { return {}; }
+    static constexpr bool kXQuad = sizeof(Acc) == 4 && sizeof(T) == 4;
+    __device__ void xpass4(const unsigned char* st_, int row, int col, const Acc*,
+                           Acc v[4][4]) const {
+        constexpr int NCH = (XA + R + 4 + 3) / 4;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            float wv[4 * NCH];
+            load_row4<NCH>(reinterpret_cast<const float*>(st_) + c * (kBox / 4) + row * BX + col,
+                           wv);
+#pragma unroll
+            for (int o = 0; o < 4; ++o) {
+                Acc a = Acc(0);
+#pragma unroll
+                for (int j = 0; j < 2 * R + 1; ++j) a += static_cast<Acc>(wv[o + (XA - R) + j]);
+                v[c][o] = a;
+            }
+        }
+    }
     __device__ void xpass(const unsigned char* st_, int row, int col, Acc, Acc v[4]) const {
         const T* p = reinterpret_cast<const T*>(st_) + row * BX + col + (XA - R);
 #pragma unroll
@@ -756,6 +842,27 @@ struct SmoothAdam2 {
         p.ic2 = static_cast<T>(1.0 / corr2[t]);
         p.slot = st ? st->slot : 0;
         return p;
+    }
+    static constexpr bool kXQuad = sizeof(T) == 4 && (CY_ == 1 ? DFM_SA_QUAD1 : DFM_SA_QUAD2);
+    __device__ void xpass4(const unsigned char* st_, int row, int col, const Acc nx[4],
+                           Acc v[3][4]) const {
+        constexpr int NCH = (XA + R + 4 + 3) / 4;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            float wv[4 * NCH];
+            load_row4<NCH>(reinterpret_cast<const float*>(st_) + c * (kBox / 4) + row * BX + col,
+                           wv);
+#pragma unroll
+            for (int o = 0; o < 4; ++o) {  // the arithmetic of xpass, per column
+                const float* q = wv + o + (XA - R);
+                T a0 = T(0), a1 = T(0);
+#pragma unroll
+                for (int j = 0; j < 2 * R + 1; j += 2) a0 += w.taps[0][j] * q[j];
+#pragma unroll
+                for (int j = 1; j < 2 * R + 1; j += 2) a1 += w.taps[0][j] * q[j];
+                v[c][o] = (a0 + a1) * nx[o];
+            }
+        }
     }
     __device__ void xpass(const unsigned char* st_, int row, int col, Acc nx, Acc v[3]) const {
         const T* p = reinterpret_cast<const T*>(st_) + row * BX + col + (XA - R);
@@ -1052,7 +1159,7 @@ struct ComposeS2 {
     using Center = NoCenter;
     using Prol = NoProl;
     static constexpr int R = R_, C = 3, BACK = 0, AHEAD = 0, S = DFM_S_SA, TYv = TY_;
-    static constexpr int kMinB = DFM_MINB_CS, kCY = 1;
+    static constexpr int kMinB = DFM_MINB_CS, kCY = DFM_CY_CS;
     static constexpr bool kStaged = false, kSum = false, kMax = false;
     static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TYv + 2 * R;
     static constexpr int kBytes = BX * BY * int(sizeof(T));
@@ -1074,13 +1181,15 @@ struct ComposeS2 {
         int i;
         WG3<T> w;
     };
-    static constexpr int NTH = TX * TYv;
+    static constexpr int NTH = TX * TYv / kCY;
     // the 8 corners of the carried M gather land here (cp.async), two slots
     static constexpr bool kAsync = ASYNC_;
-    static constexpr int kExtraBytes = kAsync ? 2 * 8 * NTH * int(sizeof(T)) : 0;
+    // slots 2r, 2r+1 belong to the thread's row r
+    static constexpr int kExtraBytes = kAsync ? 2 * kCY * 8 * NTH * int(sizeof(T)) : 0;
     __device__ static T* gather_buf(int slot) {
         return reinterpret_cast<T*>(zm2_extra<ComposeS2>()) + (slot * 8) * NTH + threadIdx.x;
     }
+    __device__ void init_carry(Carry& c, int r) const { c.slot = 2 * r; }
 
     __device__ bool skip() const {
         if (!st) return false;
@@ -1103,6 +1212,25 @@ struct ComposeS2 {
     __device__ Acc wgt(int a, int j) const { return w.taps[a][j]; }
     __device__ Acc nrm(int a, int i) const { return __ldg(w.norm[a] + i); }
     __device__ Prol prologue() const { return {}; }
+    static constexpr bool kXQuad = sizeof(T) == 4;
+    __device__ void xpass4(const unsigned char* st_, int row, int col, const Acc nx[4],
+                           Acc v[3][4]) const {
+        constexpr int NCH = (XA + R + 4 + 3) / 4;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            float wv[4 * NCH];
+            load_row4<NCH>(reinterpret_cast<const float*>(st_) + c * (kBox / 4) + row * BX + col,
+                           wv);
+#pragma unroll
+            for (int o = 0; o < 4; ++o) {
+                const float* q = wv + o + (XA - R);
+                T a = T(0);
+#pragma unroll
+                for (int j = 0; j < 2 * R + 1; ++j) a += w.taps[0][j] * q[j];
+                v[c][o] = a * nx[o];
+            }
+        }
+    }
     __device__ void xpass(const unsigned char* st_, int row, int col, Acc nx, Acc v[3]) const {
         const T* p = reinterpret_cast<const T*>(st_) + row * BX + col + (XA - R);
 #pragma unroll
@@ -1405,7 +1533,7 @@ int launch_smooth_adam_tma(const Launch& L, int R, const GaussW<T>& w, const T* 
         // at R = 5 it spills, 504 vs ~160 us)
         if constexpr (RR <= 3) {
             if (sizeof(T) == 4 && d.n >= kSaCoarsenVoxels)
-                return go(SmoothAdam2<T, RR, 16, 2, 3>{});
+                return go(SmoothAdam2<T, RR, 16, 2, DFM_MINB_SA2>{});
         }
         return go(SmoothAdam2<T, RR>{});
     });
