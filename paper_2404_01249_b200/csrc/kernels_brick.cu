@@ -201,10 +201,10 @@ template <class Op>
 __global__ void __launch_bounds__(NTB, 2) k_brick(const __grid_constant__ Op op, const BG g) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double s_red[32];
-    pdl_trigger();
     pdl_wait();
     if (op.skip()) return;
     brick_body<Op, NTB>(op, g, blockIdx.x, smem, s_red);
+    pdl_trigger();  // the successor may launch while the last bricks finish
     if constexpr (Op::kSum) {
         if (op.mon.st)
             monitor_tail<NTB>(op.mon, op.partials, gridDim.x,

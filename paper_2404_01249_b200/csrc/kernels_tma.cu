@@ -58,6 +58,9 @@ constexpr int64_t kSaCoarsenVoxels = 2000000;
 #ifndef DFM_CS_ASYNC
 #define DFM_CS_ASYNC 1
 #endif
+#ifndef DFM_FWD_QUAD
+#define DFM_FWD_QUAD 1
+#endif
 #ifndef DFM_SA_QUAD1
 #define DFM_SA_QUAD1 1
 #endif
@@ -238,8 +241,7 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
     __shared__ __align__(8) uint64_t bars[S];
     __shared__ double s_red[32];
 
-    pdl_trigger();  // successor CTAs may be scheduled into our tail
-    pdl_wait();     // predecessor's outputs (and LoopState) are visible from here
+    pdl_wait();  // predecessor's outputs (and LoopState) are visible from here
     if (op.skip()) return;
     const Dims& d = g.d;
     const int tid = threadIdx.x;
@@ -399,9 +401,15 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
                 Acc v[C][4];
                 op.xpass4(st, row, xq, nx4, v);
 #pragma unroll
-                for (int c = 0; c < C; ++c)
-                    *reinterpret_cast<float4*>(sx + (c * HI + row) * TX + xq) =
-                        make_float4(v[c][0], v[c][1], v[c][2], v[c][3]);
+                for (int c = 0; c < C; ++c) {
+                    Acc* o = sx + (c * HI + row) * TX + xq;
+                    if constexpr (sizeof(Acc) == 4) {
+                        *reinterpret_cast<float4*>(o) = make_float4(v[c][0], v[c][1], v[c][2], v[c][3]);
+                    } else {
+                        reinterpret_cast<double2*>(o)[0] = make_double2(v[c][0], v[c][1]);
+                        reinterpret_cast<double2*>(o)[1] = make_double2(v[c][2], v[c][3]);
+                    }
+                }
             }
         } else {
             const unsigned char* st = stages + ((zi - q0) % S) * SB;
@@ -457,6 +465,7 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
         }
         buf ^= 1;
     }
+    pdl_trigger();  // the successor may launch into our tail (PDL mode)
 #pragma unroll
     for (int r = 0; r < CY; ++r) op.flush(carry[r]);
     if constexpr (Op::kSum || Op::kMax) {
@@ -646,6 +655,46 @@ struct LnccFwd3 {
     __device__ Acc wgt(int, int) const { return 1.0; }
     __device__ Acc nrm(int, int) const { return 1.0; }
     __device__ Prol prologue() const { return {}; }
+    // four columns per thread: each element is widened and its W^2, FW
+    // products formed once for the 4 windows that contain it
+    static constexpr bool kXQuad = sizeof(T) == 4 && DFM_FWD_QUAD;
+    __device__ void xpass4(const unsigned char* st_, int row, int col, const Acc*,
+                           Acc v[3][4]) const {
+        constexpr int NCH = (XA + R + 4 + 3) / 4, LO = XA - R, NE = 4 + 2 * R;
+        float wf[4 * NCH], ff[4 * NCH];
+        const float* base = reinterpret_cast<const float*>(st_) + row * BX + col;
+        load_row4<NCH>(base + kBox / 4, wf);
+        load_row4<NCH>(base, ff);
+        double e[NE];
+#pragma unroll
+        for (int k = 0; k < NE; ++k) e[k] = static_cast<double>(wf[LO + k]);
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+            double a = 0;
+#pragma unroll
+            for (int j = 0; j < 2 * R + 1; ++j) a += e[o + j];
+            v[0][o] = a;
+        }
+        double p[NE];
+#pragma unroll
+        for (int k = 0; k < NE; ++k) p[k] = __dmul_rn(e[k], e[k]);
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+            double a = 0;
+#pragma unroll
+            for (int j = 0; j < 2 * R + 1; ++j) a += p[o + j];
+            v[1][o] = a;
+        }
+#pragma unroll
+        for (int k = 0; k < NE; ++k) p[k] = __dmul_rn(static_cast<double>(ff[LO + k]), e[k]);
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+            double a = 0;
+#pragma unroll
+            for (int j = 0; j < 2 * R + 1; ++j) a += p[o + j];
+            v[2][o] = a;
+        }
+    }
     __device__ void xpass(const unsigned char* st_, int row, int col, Acc, Acc v[3]) const {
         const T* F = reinterpret_cast<const T*>(st_) + row * BX + col + (XA - R);
         const T* W = F + kBox / int(sizeof(T));
