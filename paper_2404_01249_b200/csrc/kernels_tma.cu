@@ -321,10 +321,15 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
         if constexpr (Op::kStaged && R == 0) {
             // pointwise staged op (e.g. the radius-0 compose of the split
             // update): the staged value is the output, no filter passes
-            while (waited < zi + Op::AHEAD) {
-                ++waited;
-                const int k = waited - q0;
-                mbar_wait(&bars[k % S], (k / S) & 1);
+            if constexpr (Op::AHEAD == 0) {  // exactly plane zi (ring position >= 0)
+                const unsigned k = static_cast<unsigned>(zi - q0);
+                mbar_wait(&bars[k % S], (k / S) & 1u);
+            } else {
+                while (waited < zi + Op::AHEAD) {
+                    ++waited;
+                    const unsigned k = static_cast<unsigned>(waited - q0);
+                    mbar_wait(&bars[k % S], (k / S) & 1u);
+                }
             }
             const typename Op::PlaneCtx pc = op.plane_ctx(stages, q0, zi);
             const bool fast = op.interior(x0, y0, zi);  // CTA-uniform
@@ -345,7 +350,7 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
             if (tid == 0) {
                 const int qf = zi - Op::BACK + S;
                 if (qf < qend) {
-                    const int k = qf - q0;
+                    const unsigned k = static_cast<unsigned>(qf - q0);
                     op.issue(stages + (k % S) * SB, &bars[k % S], x0, y0, qf);
                 }
             }
@@ -357,10 +362,15 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
 #pragma unroll
         for (int r = 0; r < CY; ++r)
             if (zo >= z0 && own[r]) op.load_center(x, yk[r], zo, cen[r]);
-        while (waited < zi + Op::AHEAD) {
-            ++waited;
-            const int k = waited - q0;
-            mbar_wait(&bars[k % S], (k / S) & 1);
+        if constexpr (Op::AHEAD == 0) {  // exactly plane zi (ring position >= 0)
+            const unsigned k = static_cast<unsigned>(zi - q0);
+            mbar_wait(&bars[k % S], (k / S) & 1u);
+        } else {
+            while (waited < zi + Op::AHEAD) {
+                ++waited;
+                const unsigned k = static_cast<unsigned>(waited - q0);
+                mbar_wait(&bars[k % S], (k / S) & 1u);
+            }
         }
         Acc* sx = s_x + buf * (C * HI * TX);
         if constexpr (Op::kStaged) {
@@ -395,7 +405,7 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
                 }
             }
         } else if constexpr (kQuad) {
-            const unsigned char* st = stages + ((zi - q0) % S) * SB;
+            const unsigned char* st = stages + (static_cast<unsigned>(zi - q0) % S) * SB;
 #pragma unroll
             for (int row = tid / NQ; row < HI; row += NTh / NQ) {
                 Acc v[C][4];
@@ -412,7 +422,7 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
                 }
             }
         } else {
-            const unsigned char* st = stages + ((zi - q0) % S) * SB;
+            const unsigned char* st = stages + (static_cast<unsigned>(zi - q0) % S) * SB;
 #pragma unroll
             for (int row = ty; row < HI; row += TYt) {
                 Acc v[C];
@@ -425,7 +435,7 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
         if (tid == 0) {
             const int qf = zi - Op::BACK + S;
             if (qf < qend) {
-                const int k = qf - q0;
+                const unsigned k = static_cast<unsigned>(qf - q0);
                 op.issue(stages + (k % S) * SB, &bars[k % S], x0, y0, qf);
             }
         }
@@ -1059,11 +1069,12 @@ struct Compose2 {
     };
     __device__ PlaneCtx plane_ctx(const unsigned char* stages, int q0, int zi) const {
         PlaneCtx pc;
-        pc.step = reinterpret_cast<const T*>(stages + ((zi - q0) % S) * kStageBytes);
+        pc.step = reinterpret_cast<const T*>(stages + (unsigned(zi - q0) % S) * kStageBytes);
 #pragma unroll
         for (int k = 0; k < 2 * CAPH + 1; ++k) {
             const int q = zi - CAPH + k;
-            pc.u[k] = reinterpret_cast<const T*>(stages + ((q - q0) % S) * kStageBytes + 3 * kBoxS);
+            pc.u[k] = reinterpret_cast<const T*>(stages + (unsigned(q - q0) % S) * kStageBytes +
+                                                 3 * kBoxS);
         }
         return pc;
     }
