@@ -103,6 +103,17 @@ template <class A>
 struct GaussW {
     A taps[3][2 * kRMax + 1];
     const A* norm[3];
+    // positions ra <= i < n - ra see the whole window: their norm is the one
+    // value norm_int (computed like the array's entries), no load needed
+    A norm_int[3];
+    int ra[3];
+#ifdef __CUDACC__
+    __device__ __forceinline__ A nrm(int a, int i, int n) const {
+        return static_cast<unsigned>(i - ra[a]) < static_cast<unsigned>(max(n - 2 * ra[a], 0))
+                   ? norm_int[a]
+                   : __ldg(norm[a] + i);
+    }
+#endif
 };
 
 // -------- conversions / staging

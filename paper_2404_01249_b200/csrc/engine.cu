@@ -291,6 +291,12 @@ GaussW<T> upload_gauss(dfm_ctx* ctx, const HostGauss& h, const Dims& d, const st
                 w.taps[a][j + h.R] = static_cast<T>(h.taps[a][j + h.Ra[a]]);
         for (int i = 0; i < n[a]; ++i) host[off + i] = static_cast<T>(h.norm[a][i]);
         off += n[a];
+        // the interior entry of make_gauss (same summation order)
+        double ws = 0.0;
+        for (int j = 0; j < 2 * h.Ra[a] + 1; ++j) ws += h.taps[a][j];
+        const bool active = h.Ra[a] > 0;
+        w.norm_int[a] = static_cast<T>(active ? 1.0 / ws : 1.0);
+        w.ra[a] = h.Ra[a];
     }
     T* dev = ctx->arr<T>("gauss_norm_" + key, static_cast<int64_t>(host.size()));
     CK(cudaMemcpyAsync(dev, host.data(), host.size() * sizeof(T), cudaMemcpyHostToDevice,

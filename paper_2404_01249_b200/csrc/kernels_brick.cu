@@ -431,7 +431,9 @@ struct SmoothAdamB {
     }
     __device__ void xpass(const T* p, int cs, T v[3]) const { gauss_xpass<T, R>(w, p, cs, v); }
     __device__ T wgt(int a, int j) const { return w.taps[a][j]; }
-    __device__ T nrm(int a, int i) const { return __ldg(w.norm[a] + i); }
+    __device__ T nrm(int a, int i) const {
+        return w.nrm(a, i, a == 0 ? d.nx : (a == 1 ? d.ny : d.gz()));
+    }
     __device__ Prol prologue() const {
         Prol p;
         const long long t = st ? st->t : 1;
@@ -517,7 +519,9 @@ struct ComposeB {
     }
     __device__ void xpass(const T* p, int cs, T v[3]) const { gauss_xpass<T, R>(w, p, cs, v); }
     __device__ T wgt(int a, int j) const { return w.taps[a][j]; }
-    __device__ T nrm(int a, int i) const { return __ldg(w.norm[a] + i); }
+    __device__ T nrm(int a, int i) const {
+        return w.nrm(a, i, a == 0 ? d.nx : (a == 1 ? d.ny : d.gz()));
+    }
     __device__ Prol prologue() const { return {}; }
     __device__ Red2 emit(int x, int y, int z, const T s[3], const Prol&) const {
         const int i = d.idx32(x, y, z);
@@ -580,7 +584,9 @@ struct ComposeSB {
     }
     __device__ void xpass(const T* p, int cs, T v[3]) const { gauss_xpass<T, R>(w, p, cs, v); }
     __device__ T wgt(int a, int j) const { return w.taps[a][j]; }
-    __device__ T nrm(int a, int i) const { return __ldg(w.norm[a] + i); }
+    __device__ T nrm(int a, int i) const {
+        return w.nrm(a, i, a == 0 ? d.nx : (a == 1 ? d.ny : d.gz()));
+    }
     __device__ Prol prologue() const { return {}; }
     __device__ Red2 emit(int x, int y, int z, const T s[3], const Prol&) const {
         const int i = d.idx32(x, y, z);

@@ -893,7 +893,9 @@ struct SmoothAdam2 {
         for (int k = 0; k < 3; ++k) tma_load_4d(dst + k * kBox, &mG, bar, x0 - XA, y0 - R, q, k);
     }
     __device__ Acc wgt(int a, int j) const { return w.taps[a][j]; }
-    __device__ Acc nrm(int a, int i) const { return __ldg(w.norm[a] + i); }
+    __device__ Acc nrm(int a, int i) const {
+        return w.nrm(a, i, a == 0 ? d.nx : (a == 1 ? d.ny : d.gz()));
+    }
     __device__ Prol prologue() const {
         Prol p;
         const long long t = st ? st->t : 1;
@@ -1021,11 +1023,11 @@ struct Compose2 {
     static constexpr int PS = kBoxS / int(sizeof(T)), PU = kBoxU / int(sizeof(T));
     CUtensorMap mS, mU;
     GaussW<T> w;
-    T* uout;  // 3 planes
+    T* uout[3];  // per-component plane pointers (3-D only: the launcher)
     const T* M;
     Dims dm;
     T* W;     // nullptr: do not produce W/G
-    T* G;     // 3 planes
+    T* G[3];
     LoopState* st;
     int count_update;  // 0 for all but one slab of an emulated decomposition
     Dims d;
@@ -1060,7 +1062,9 @@ struct Compose2 {
             tma_load_4d(dst + 3 * kBoxS + k * kBoxU, &mU, bar, x0 - XAU, y0 - HU, q, k);
     }
     __device__ Acc wgt(int a, int j) const { return w.taps[a][j]; }
-    __device__ Acc nrm(int a, int i) const { return __ldg(w.norm[a] + i); }
+    __device__ Acc nrm(int a, int i) const {
+        return w.nrm(a, i, a == 0 ? d.nx : (a == 1 ? d.ny : d.gz()));
+    }
     __device__ Prol prologue() const { return {}; }
     // stage pointers of the planes one composed plane needs (zi-CAPH .. zi+CAPH)
     struct PlaneCtx {
@@ -1182,16 +1186,16 @@ struct Compose2 {
         W[c.i] = wg3_value(c.w);
         T gr[3];
         wg3_grad(c.w, gr);
-        G[c.i] = gr[0];
-        G[d.n + c.i] = gr[1];
-        G[2 * d.n + c.i] = gr[2];
+        G[0][c.i] = gr[0];
+        G[1][c.i] = gr[1];
+        G[2][c.i] = gr[2];
     }
     __device__ Red2 emit(int x, int y, int z, const T u[3], const Center&, const Prol&,
                          Carry& cr) const {
-        const int64_t i = d.idx32(x, y, z);
-        uout[i] = u[0];
-        uout[d.n + i] = u[1];
-        uout[2 * d.n + i] = d.ndim == 3 ? u[2] : T(0);
+        const int i = d.idx32(x, y, z);
+        uout[0][i] = u[0];
+        uout[1][i] = u[1];
+        uout[2][i] = u[2];
         if (W) {  // similarity.cpp:25-45 for the next loss evaluation (3-D only: launcher)
             if (cr.valid) finish_wg(cr);
             wg3_fetch<T>(M, dm, x, y, z + d.zoff, u[0], u[1], u[2], cr.w);
@@ -1270,7 +1274,9 @@ struct ComposeS2 {
         for (int k = 0; k < 3; ++k) tma_load_4d(dst + k * kBox, &mC, bar, x0 - XA, y0 - R, q, k);
     }
     __device__ Acc wgt(int a, int j) const { return w.taps[a][j]; }
-    __device__ Acc nrm(int a, int i) const { return __ldg(w.norm[a] + i); }
+    __device__ Acc nrm(int a, int i) const {
+        return w.nrm(a, i, a == 0 ? d.nx : (a == 1 ? d.ny : d.gz()));
+    }
     __device__ Prol prologue() const { return {}; }
     static constexpr bool kXQuad = sizeof(T) == 4;
     __device__ void xpass4(const unsigned char* st_, int row, int col, const Acc nx[4],
@@ -1604,8 +1610,7 @@ int launch_compose_tma(const Launch& L, int R, double cap, const GaussW<T>& w, c
                        const T* uin, T* uout, const T* M, Dims dm, Dims d, T* W, T* G,
                        LoopState* st, bool count_update) {
     const int caph = cap <= 0.5 ? 1 : (cap <= 1.5 ? 2 : 0);
-    if (caph == 0) return -2;
-    if (W && d.ndim != 3) return -2;  // the fused M gather is the 3-D fast form
+    if (caph == 0 || d.ndim != 3) return -2;  // 3-D plane pointers, fast M gather
     return with_r<0, 4>(R, [&](auto rc) {
         constexpr int RR = decltype(rc)::value;
         auto go = [&](auto ch) {
@@ -1616,11 +1621,13 @@ int launch_compose_tma(const Launch& L, int R, double cap, const GaussW<T>& w, c
                 !make_map<T>(&op.mU, uin, d, 3, Op::BXU, Op::BYU))
                 return -1;
             op.w = w;
-            op.uout = uout;
+            for (int k = 0; k < 3; ++k) {
+                op.uout[k] = uout + k * d.n;
+                op.G[k] = G ? G + k * d.n : nullptr;
+            }
             op.M = M;
             op.dm = dm;
             op.W = W;
-            op.G = G;
             op.st = st;
             op.count_update = count_update ? 1 : 0;
             op.d = d;

@@ -132,8 +132,10 @@ __device__ __forceinline__ double window_inv(int x, int y, int z, const Dims& d)
     constexpr double K = 2 * R + 1;
     const int gz = d.gz(), zg = z + d.zoff;
     const bool three = gz > 1;
-    if (x >= R && x < d.nx - R && y >= R && y < d.ny - R &&
-        (!three || (zg >= R && zg < gz - R)))
+    // R <= i < n - R as one unsigned compare per axis (bounds are loop-invariant)
+    if (static_cast<unsigned>(x - R) < static_cast<unsigned>(max(d.nx - 2 * R, 0)) &&
+        static_cast<unsigned>(y - R) < static_cast<unsigned>(max(d.ny - 2 * R, 0)) &&
+        (!three || static_cast<unsigned>(zg - R) < static_cast<unsigned>(max(gz - 2 * R, 0))))
         return three ? 1.0 / (K * K * K) : 1.0 / (K * K);
     const double n = static_cast<double>(box_len(x, d.nx, R) * box_len(y, d.ny, R) *
                                          (three ? box_len(zg, gz, R) : 1));
