@@ -58,6 +58,9 @@ constexpr int64_t kSaCoarsenVoxels = 2000000;
 #ifndef DFM_CS_ASYNC
 #define DFM_CS_ASYNC 1
 #endif
+#ifndef DFM_SA_CTMA
+#define DFM_SA_CTMA 0
+#endif
 #ifndef DFM_FWD_QUAD
 #define DFM_FWD_QUAD 1
 #endif
@@ -202,6 +205,17 @@ __device__ __forceinline__ void load_row4(const float* p, float w[4 * NCH]) {
         w[4 * k + 3] = t.w;
     }
 }
+
+// the op's centre operands of plane zo = q - R arrive by TMA with stage q
+// (Op::kCenterTMA; read with Op::load_center_st): no per-voxel global loads
+template <class Op, class = void>
+struct CenterTMA {
+    static constexpr bool value = false;
+};
+template <class Op>
+struct CenterTMA<Op, std::void_t<decltype(Op::kCenterTMA)>> {
+    static constexpr bool value = Op::kCenterTMA;
+};
 
 // optional per-row carry initialisation (Op::init_carry(carry, row))
 template <class Op, class C>
@@ -358,10 +372,13 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
         }
         constexpr int kk = K - 1;
         const int zo = zi - R;
+        constexpr bool kCT = CenterTMA<Op>::value;
         typename Op::Center cen[CY];
+        if constexpr (!kCT) {
 #pragma unroll
-        for (int r = 0; r < CY; ++r)
-            if (zo >= z0 && own[r]) op.load_center(x, yk[r], zo, cen[r]);
+            for (int r = 0; r < CY; ++r)
+                if (zo >= z0 && own[r]) op.load_center(x, yk[r], zo, cen[r]);
+        }
         if constexpr (Op::AHEAD == 0) {  // exactly plane zi (ring position >= 0)
             const unsigned k = static_cast<unsigned>(zi - q0);
             mbar_wait(&bars[k % S], (k / S) & 1u);
@@ -433,8 +450,11 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
         }
         __syncthreads();
         if (tid == 0) {
-            const int qf = zi - Op::BACK + S;
-            if (qf < qend) {
+            // the slot of plane zi - BACK is free once every thread passed the
+            // x pass; with centre operands in the stage it is still read by
+            // this plane's emit, so the previous plane's slot is refilled
+            const int qf = kCT ? zi - 1 + S : zi - Op::BACK + S;
+            if (qf < qend && (!kCT || zi > q0)) {
                 const unsigned k = static_cast<unsigned>(qf - q0);
                 op.issue(stages + (k % S) * SB, &bars[k % S], x0, y0, qf);
             }
@@ -458,6 +478,9 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
 #pragma unroll
         for (int r = 0; r < CY; ++r) {
             if (zo >= z0 && own[r]) {
+                if constexpr (kCT)
+                    op.load_center_st(stages + (static_cast<unsigned>(zi - q0) % S) * SB,
+                                      ty * CY + r, tx, cen[r]);
                 // oldest plane (zo - R) sits in slot 0 (slot (kk + 1) % K)
                 const Acc nz = op.nrm(2, zo + d.zoff);
                 Acc sv[C];
@@ -858,8 +881,13 @@ struct SmoothAdam2 {
     static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TYv + 2 * R;
     static constexpr int kBytes = BX * BY * int(sizeof(T));
     static constexpr int kBox = align128(kBytes);
-    static constexpr int kStageBytes = 3 * kBox;
+    // stage q: 3 gradient boxes of plane q, then m and nu tiles of plane q - R
+    static constexpr bool kCenterTMA = DFM_SA_CTMA != 0;
+    static constexpr int kCBytes = TX * TYv * int(sizeof(T));
+    static constexpr int kCBox = align128(kCBytes);
+    static constexpr int kStageBytes = 3 * kBox + (kCenterTMA ? 6 * kCBox : 0);
     CUtensorMap mG;
+    CUtensorMap mM, mN;
     GaussW<T> w;
     // per-component plane pointers (3-D only: the TMA family): one 32-bit
     // index per voxel, no 64-bit component offsets
@@ -886,11 +914,32 @@ struct SmoothAdam2 {
     };
 
     __device__ bool skip() const { return st && st->done; }
-    __device__ void prefetch_maps() const { prefetch_tmap(&mG); }
+    __device__ void prefetch_maps() const {
+        prefetch_tmap(&mG);
+        if constexpr (kCenterTMA) {
+            prefetch_tmap(&mM);
+            prefetch_tmap(&mN);
+        }
+    }
     __device__ void issue(unsigned char* dst, uint64_t* bar, int x0, int y0, int q) const {
-        mbar_expect_tx(bar, 3 * kBytes);
+        mbar_expect_tx(bar, 3 * kBytes + (kCenterTMA ? 6 * kCBytes : 0));
 #pragma unroll
         for (int k = 0; k < 3; ++k) tma_load_4d(dst + k * kBox, &mG, bar, x0 - XA, y0 - R, q, k);
+        if constexpr (kCenterTMA) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                tma_load_4d(dst + 3 * kBox + k * kCBox, &mM, bar, x0, y0, q - R, k);
+                tma_load_4d(dst + 3 * kBox + (3 + k) * kCBox, &mN, bar, x0, y0, q - R, k);
+            }
+        }
+    }
+    __device__ void load_center_st(const unsigned char* st, int row, int col, Center& c) const {
+        const T* p = reinterpret_cast<const T*>(st + 3 * kBox) + row * TX + col;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            c.m[k] = p[k * (kCBox / int(sizeof(T)))];
+            c.nu[k] = p[(3 + k) * (kCBox / int(sizeof(T)))];
+        }
     }
     __device__ Acc wgt(int a, int j) const { return w.taps[a][j]; }
     __device__ Acc nrm(int a, int i) const {
@@ -1579,6 +1628,9 @@ int launch_smooth_adam_tma(const Launch& L, int R, const GaussW<T>& w, const T* 
         auto go = [&](auto op) {
             using Op = decltype(op);
             if (!make_map<T>(&op.mG, grad, d, 3, Op::BX, Op::BY)) return -1;
+            if (Op::kCenterTMA && (!make_map<T>(&op.mM, m, d, 3, TX, Op::TYv) ||
+                                   !make_map<T>(&op.mN, nu, d, 3, TX, Op::TYv)))
+                return -1;
             op.w = w;
             for (int k = 0; k < 3; ++k) {
                 op.m[k] = m + k * d.n;
@@ -1649,6 +1701,9 @@ int launch_smooth_adam_compose_tma(const Launch& L, int R, const GaussW<T>& w, c
         auto go = [&](auto op) {
             using Op = decltype(op);
             if (!make_map<T>(&op.mG, grad, d, 3, Op::BX, Op::BY)) return -1;
+            if (Op::kCenterTMA && (!make_map<T>(&op.mM, m, d, 3, TX, Op::TYv) ||
+                                   !make_map<T>(&op.mN, nu, d, 3, TX, Op::TYv)))
+                return -1;
             op.w = w;
             for (int k = 0; k < 3; ++k) {
                 op.m[k] = m + k * d.n;
