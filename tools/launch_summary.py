@@ -1,6 +1,6 @@
-"""Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv): runs
-of consecutive launches of the same kernel and grid, in launch order, with
-count, total, per-launch time and share of the whole.
+"""Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv): the
+launches of each (kernel, grid) in order of first launch, with count, total,
+per-launch time and share of the whole.
     python tools/launch_summary.py launches.csv [title]"""
 import csv
 import re
@@ -19,13 +19,12 @@ for r in rd:
     name = re.sub(r"\(.*$", "", r["Kernel Name"]).replace("dfm::", "").replace("<unnamed>::", "")
     rows.append((name, r["Grid Size"], us))
 total = sum(r[2] for r in rows)
-runs = []
+runs = {}  # (kernel, grid) in order of first launch
 for name, grid, us in rows:
-    if runs and runs[-1][0] == name and runs[-1][1] == grid:
-        runs[-1][2] += 1
-        runs[-1][3] += us
-    else:
-        runs.append([name, grid, 1, us])
+    r = runs.setdefault((name, grid), [name, grid, 0, 0.0])
+    r[2] += 1
+    r[3] += us
+runs = list(runs.values())
 title = sys.argv[2] if len(sys.argv) > 2 else ""
 print(f"{title}total {total / 1e3:.2f} ms over {len(rows)} launches")
 for name, grid, n, us in runs:
