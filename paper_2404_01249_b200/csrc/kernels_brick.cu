@@ -70,6 +70,20 @@ struct BrickLayout {
     static constexpr size_t bytes = bX + (bS > bY ? bS : bY);
 };
 
+// ops with centre operands (Op::Center, Op::load_center) have them loaded
+// before the stage, so their latency hides behind the stage round trip
+struct NoCenterB {};
+template <class Op, class = void>
+struct CenterOfB {
+    using type = NoCenterB;
+    static constexpr bool value = false;
+};
+template <class Op>
+struct CenterOfB<Op, std::void_t<typename Op::Center>> {
+    using type = typename Op::Center;
+    static constexpr bool value = true;
+};
+
 // One brick of one op: stage, x, y, z passes, per-voxel epilogue and the
 // CTA reduction; op.finish(b, ...) records brick b's partial.  Ends with the
 // CTA's threads synchronised (smem reusable).
@@ -94,6 +108,20 @@ __device__ __forceinline__ void brick_body(const Op& op, const BG& g, int b, uns
     const int y0 = (b % g.nby) * BY;
     const int z0 = (b / g.nby) * BZ;
 
+    // 0. centre operands of this thread's output voxels
+    constexpr int IZ = BZ * BY * BX / NTB;
+    static_assert(IZ * NTB == BZ * BY * BX, "brick must be a multiple of the CTA size");
+    using Cen = CenterOfB<Op>;
+    typename Cen::type cen[IZ];
+    if constexpr (Cen::value) {
+#pragma unroll
+        for (int k = 0; k < IZ; ++k) {
+            const int e = tid + k * NTB;
+            const int xl = e % BX, t = e / BX, yl = t % BY, zl = t / BY;
+            const int gx = x0 + xl, gy = y0 + yl, gz = z0 + zl;
+            if (gx < d.nx && gy < d.ny && gz < d.nz) op.load_center(gx, gy, gz, cen[k]);
+        }
+    }
     // 1. stage: the loads of a batch of elements are all issued before any is
     // stored (one L2 round trip per batch instead of one per element)
     const bool inner = x0 - R >= 0 && x0 + BX + R <= d.nx && y0 - R >= 0 &&
@@ -164,8 +192,6 @@ __device__ __forceinline__ void brick_body(const Op& op, const BG& g, int b, uns
     // 4. z pass + per-voxel epilogue (both voxels of a thread in flight together)
     const typename Op::Prol pr = op.prologue();
     double rsum = 0.0, rmax = 0.0;
-    constexpr int IZ = BZ * BY * BX / NTB;
-    static_assert(IZ * NTB == BZ * BY * BX, "brick must be a multiple of the CTA size");
 #pragma unroll
     for (int k = 0; k < IZ; ++k) {
         const int e = tid + k * NTB;
@@ -182,7 +208,11 @@ __device__ __forceinline__ void brick_body(const Op& op, const BG& g, int b, uns
                 for (int j = 0; j < K; ++j) a += op.wgt(2, j) * src[c * nY + j * (BY * BX)];
                 sv[c] = a * nzv;
             }
-            const Red2 r = op.emit(gx, gy, gz, sv, pr);
+            Red2 r;
+            if constexpr (Cen::value)
+                r = op.emit(gx, gy, gz, sv, pr, cen[k]);
+            else
+                r = op.emit(gx, gy, gz, sv, pr);
             rsum += r.sum;
             rmax = fmax(rmax, r.mx);
         }
@@ -273,12 +303,23 @@ struct LnccFwdB {
     __device__ double wgt(int, int) const { return 1.0; }
     __device__ double nrm(int, int) const { return 1.0; }
     __device__ Prol prologue() const { return {}; }
-    __device__ Red2 emit(int x, int y, int z, const double s[C], const Prol&) const {
+    struct Center {
+        double muF, vF;
+    };
+    __device__ void load_center(int x, int y, int z, Center& c) const {
+        if constexpr (FS) {
+            const int i = d.idx32(x, y, z);
+            c.muF = __ldg(fstat + i);
+            c.vF = __ldg(fstat + d.n + i);
+        }
+    }
+    __device__ Red2 emit(int x, int y, int z, const double s[C], const Prol&,
+                         const Center& c) const {
         const double inv_n = window_inv<R>(x, y, z, d);
         const int i = d.idx32(x, y, z);
         LnccCoef k;
         if constexpr (FS)
-            k = lncc_coef_f(__ldg(fstat + i), __ldg(fstat + d.n + i), s[0], s[1], s[2], inv_n);
+            k = lncc_coef_f(c.muF, c.vF, s[0], s[1], s[2], inv_n);
         else
             k = lncc_coef(s, inv_n);
         if (coef) {
@@ -369,15 +410,26 @@ struct LnccBwdB {
     __device__ Acc wgt(int, int) const { return Acc(1); }
     __device__ Acc nrm(int, int) const { return Acc(1); }
     __device__ Prol prologue() const { return {}; }
-    __device__ Red2 emit(int x, int y, int z, const Acc sa[4], const Prol&) const {
+    struct Center {
+        T f, w, g[3];
+    };
+    __device__ void load_center(int x, int y, int z, Center& c) const {
+        const int i = d.idx32(x, y, z);
+        c.f = __ldg(F + i);
+        c.w = W[i];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) c.g[k] = G[k * d.n + i];
+    }
+    __device__ Red2 emit(int x, int y, int z, const Acc sa[4], const Prol&,
+                         const Center& c) const {
         const double s[4] = {static_cast<double>(sa[0]), static_cast<double>(sa[1]),
                              static_cast<double>(sa[2]), static_cast<double>(sa[3])};
         const int i = d.idx32(x, y, z);
-        const double f = static_cast<double>(__ldg(F + i)), w = static_cast<double>(W[i]);
+        const double f = static_cast<double>(c.f), w = static_cast<double>(c.w);
         const double dW = lncc_dw(m2n, f, w, s);
-        grad[i] = static_cast<T>(dW * static_cast<double>(G[i]));
-        grad[d.n + i] = static_cast<T>(dW * static_cast<double>(G[d.n + i]));
-        grad[2 * d.n + i] = static_cast<T>(dW * static_cast<double>(G[2 * d.n + i]));
+        grad[i] = static_cast<T>(dW * static_cast<double>(c.g[0]));
+        grad[d.n + i] = static_cast<T>(dW * static_cast<double>(c.g[1]));
+        grad[2 * d.n + i] = static_cast<T>(dW * static_cast<double>(c.g[2]));
         return {0.0, 0.0};
     }
     __device__ void finish(int, double, double, const Prol&) const {}
@@ -442,14 +494,26 @@ struct SmoothAdamB {
         p.slot = st ? st->slot : 0;
         return p;
     }
-    __device__ Red2 emit(int x, int y, int z, const T s[3], const Prol& p) const {
+    struct Center {
+        T m[3], nu[3];
+    };
+    __device__ void load_center(int x, int y, int z, Center& c) const {
+        const int i = d.idx32(x, y, z);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            c.m[k] = m[k * d.n + i];
+            c.nu[k] = nu[k * d.n + i];
+        }
+    }
+    __device__ Red2 emit(int x, int y, int z, const T s[3], const Prol& p,
+                         const Center& c) const {
         const int i = d.idx32(x, y, z);
         T mx = T(0);
         bool bad = false;
-#pragma unroll
         T cl[3];
+#pragma unroll
         for (int k = 0; k < 3; ++k) {
-            T mm = m[k * d.n + i], nn = nu[k * d.n + i];
+            T mm = c.m[k], nn = c.nu[k];
             cl[k] = adam_component(ak, s[k], mm, nn, p.ic1, p.ic2, bad);
             m[k * d.n + i] = mm;
             nu[k * d.n + i] = nn;
