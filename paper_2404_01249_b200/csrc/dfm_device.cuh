@@ -403,6 +403,32 @@ __device__ __forceinline__ void jacobian_at(CPlanes3<T> u, const Dims& d, int x,
     }
 }
 
+// the same for a 3-D grid with compile-time indices (J stays in registers)
+template <class T>
+__device__ __forceinline__ void jacobian_at3(CPlanes3<T> u, const Dims& d, int x, int y, int z,
+                                             T J[9]) {
+    const int pos[3] = {x, y, z + d.zoff};
+    const int n[3] = {d.nx, d.ny, d.gz()};
+    const int64_t stride[3] = {1, d.nx, static_cast<int64_t>(d.nx) * d.ny};
+    const int64_t i = d.idx(x, y, z);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        int64_t lo = i - stride[a], hi = i + stride[a];
+        T scale = T(0.5);
+        if (pos[a] == 0) {
+            lo = i;
+            scale = T(1);
+        } else if (pos[a] == n[a] - 1) {
+            hi = i;
+            scale = T(1);
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            J[c * 3 + a] =
+                (__ldg(u.c[c] + hi) - __ldg(u.c[c] + lo)) * scale + (c == a ? T(1) : T(0));
+    }
+}
+
 template <class T>
 __device__ __forceinline__ T det_of(const T* j, int nd) {
     if (nd == 2) return j[0] * j[3] - j[1] * j[2];

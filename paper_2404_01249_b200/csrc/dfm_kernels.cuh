@@ -196,6 +196,10 @@ template <class T>
 void launch_compose_smooth(const Launch& L, int R, const GaussW<T>& w, CPlanes3<T> step,
                            CPlanes3<T> u_in, Planes3<T> u_out, Dims d, LoopState* st);
 // plain fused Gaussian (gaussian_smooth / gaussian_smooth_field), ncomp 1..3
+// one-component Gaussian on the TMA z-march (3-D; < 0: not eligible)
+template <class T>
+int launch_gauss_tma(const Launch& L, int R, const GaussW<T>& w, const T* in, T* out, Dims d);
+
 template <class T>
 void launch_gauss_fused(const Launch& L, int R, const GaussW<T>& w, CPlanes3<T> in,
                         Planes3<T> out, int ncomp, Dims d);

@@ -452,8 +452,9 @@ struct Impl {
             const HostGauss h = make_gauss(d, sigma);
             const GaussW<T> w = upload_gauss<T>(ctx, h, d, "down_" + key);
             T* b0 = ctx->arr<T>("down_tmp0", d.n);
-            launch_gauss_fused<T>(L, h.R, w, CPlanes3<T>{{img, nullptr, nullptr}},
-                                  Planes3<T>{{b0, nullptr, nullptr}}, 1, d);
+            if (h.R < 1 || launch_gauss_tma<T>(L, h.R, w, img, b0, d) < 0)
+                launch_gauss_fused<T>(L, h.R, w, CPlanes3<T>{{img, nullptr, nullptr}},
+                                      Planes3<T>{{b0, nullptr, nullptr}}, 1, d);
             src = b0;
         } else if (blur) {
             const HostGauss h = make_gauss(d, sigma);
@@ -2114,24 +2115,38 @@ struct Registrar {
         cur = 1 - cur;
     }
 
-    // upsample_field + upsample_state (pipeline.cpp:150-153, optim.cpp:59-85)
+    // upsample_field + upsample_state (pipeline.cpp:150-153, optim.cpp:59-85):
+    // the field and both Adam moments in one resampling pass (one cell
+    // location per voxel for 3 x ndim components)
     void upsample_state(const Dims& from, const Dims& to) {
-        upsample_field_only(from, to);
-        double mm[3] = {1.0, 1.0, 1.0}, mn[3] = {1.0, 1.0, 1.0};
+        relayout(u[1 - cur], to.n);
+        relayout(grad, to.n);
+        relayout(step, to.n);
+        double mu[3] = {1.0, 1.0, 1.0}, mm[3] = {1.0, 1.0, 1.0}, mn[3] = {1.0, 1.0, 1.0};
         const int nn[3] = {to.nx, to.ny, to.nz}, no[3] = {from.nx, from.ny, from.nz};
         for (int a = 0; a < to.ndim; ++a) {
             const double r = static_cast<double>(nn[a] - 1) / static_cast<double>(no[a] - 1);
+            mu[a] = r;
             mm[a] = r;
             mn[a] = r * r;
         }
-        relayout(grad, to.n);
-        relayout(step, to.n);
-        const T* sm[3] = {m.p[0], m.p[1], m.p[2]};
-        T* dm[3] = {grad.p[0], grad.p[1], grad.p[2]};
-        launch_resample<T>(ctx->L(), sm, from, dm, to, to.ndim, mm);
-        const T* sn[3] = {nu.p[0], nu.p[1], nu.p[2]};
-        T* dn[3] = {step.p[0], step.p[1], step.p[2]};
-        launch_resample<T>(ctx->L(), sn, from, dn, to, to.ndim, mn);
+        const int nd = to.ndim;
+        const T* src[9];
+        T* dst[9];
+        double mult[9];
+        for (int a = 0; a < nd; ++a) {
+            src[a] = u[cur].p[a];
+            dst[a] = u[1 - cur].p[a];
+            mult[a] = mu[a];
+            src[nd + a] = m.p[a];
+            dst[nd + a] = grad.p[a];
+            mult[nd + a] = mm[a];
+            src[2 * nd + a] = nu.p[a];
+            dst[2 * nd + a] = step.p[a];
+            mult[2 * nd + a] = mn[a];
+        }
+        launch_resample<T>(ctx->L(), src, from, dst, to, 3 * nd, mult);
+        cur = 1 - cur;
         std::swap(m, grad);
         std::swap(nu, step);
     }

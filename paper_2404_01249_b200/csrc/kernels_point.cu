@@ -20,6 +20,16 @@ inline int grid_for(int64_t n, int cap = 0x7fffffff) {  // callers with a cap gr
     return static_cast<int>(b < cap ? b : cap);
 }
 
+// per-voxel kernels over (x, row) with 32 x 8 blocks: x from the block's x
+// index, rows (y, z) grid-strided over blockIdx.y — one 32-bit division per
+// row instead of two 64-bit ones per voxel, and whole warps on one row
+constexpr int kRX = 32, kRY = 8;
+inline dim3 rows_grid(int nx, int64_t rows) {
+    const int64_t by = (rows + kRY - 1) / kRY;
+    return dim3(static_cast<unsigned>((nx + kRX - 1) / kRX),
+                static_cast<unsigned>(by < 65535 ? (by < 1 ? 1 : by) : 65535));
+}
+
 __device__ __forceinline__ void voxel_xyz(const Dims& d, int64_t i, int& x, int& y, int& z) {
     x = static_cast<int>(i % d.nx);
     const int64_t r = i / d.nx;
@@ -193,28 +203,39 @@ void launch_compose(const Launch& L, CPlanes3<T> phi, CPlanes3<T> psi, Dims d, P
 template <class T>
 __global__ void k_jacobian_det(CPlanes3<T> u, Dims d, T* det, unsigned long long* nonpos) {
     // only the produced planes [zb, ze) of a slab view are evaluated
-    const int64_t plane = static_cast<int64_t>(d.nx) * d.ny;
-    const int64_t i = d.out_begin() * plane + blockIdx.x * (int64_t)kNT + threadIdx.x;
-    int bad = 0;
-    if (i < d.out_end() * plane) {
-        int x, y, z;
-        voxel_xyz(d, i, x, y, z);
-        T J[9];
-        jacobian_at(u, d, x, y, z, J);
-        const T v = det_of(J, d.ndim);
-        if (det) det[i] = v;
-        bad = (v <= T(0));
-    }
-    if (nonpos) {
-        const unsigned m = __ballot_sync(0xffffffffu, bad);
-        if ((threadIdx.x & 31) == 0 && m) atomicAdd(nonpos, (unsigned long long)__popc(m));
+    const int x = blockIdx.x * kRX + threadIdx.x;
+    const int zb = d.out_begin();
+    const int rows = (d.out_end() - zb) * d.ny;
+    // rows are uniform per warp (threadIdx.y): the ballot below sees whole warps
+    for (int row0 = blockIdx.y * kRY; row0 < rows; row0 += gridDim.y * kRY) {
+        const int row = row0 + threadIdx.y;
+        int bad = 0;
+        if (x < d.nx && row < rows) {
+            const int y = row % d.ny, z = zb + row / d.ny;
+            T J[9];
+            T v;
+            if (d.ndim == 3) {
+                jacobian_at3(u, d, x, y, z, J);
+                v = det_of(J, 3);
+            } else {
+                jacobian_at(u, d, x, y, z, J);
+                v = det_of(J, d.ndim);
+            }
+            if (det) det[d.idx(x, y, z)] = v;
+            bad = (v <= T(0));
+        }
+        if (nonpos) {
+            const unsigned m = __ballot_sync(0xffffffffu, bad);
+            if ((threadIdx.x & 31) == 0 && m) atomicAdd(nonpos, (unsigned long long)__popc(m));
+        }
     }
 }
 
 template <class T>
 void launch_jacobian_det(const Launch& L, CPlanes3<T> u, Dims d, T* det,
                          unsigned long long* nonpos) {
-    k_jacobian_det<T><<<grid_for(d.n), kNT, 0, L.stream>>>(u, d, det, nonpos);
+    const int64_t rows = static_cast<int64_t>(d.out_end() - d.out_begin()) * d.ny;
+    k_jacobian_det<T><<<rows_grid(d.nx, rows), dim3(kRX, kRY), 0, L.stream>>>(u, d, det, nonpos);
     L.bump();
 }
 
@@ -298,10 +319,10 @@ void launch_clamp_step(const Launch& L, CPlanes3<T> v, Planes3<T> step, Dims d, 
 // The sample position is formed in double like the reference, the cell is
 // decided in double, only the fraction is rounded to T.
 template <class T>
-struct ResampleArgs {
-    const T* src[3];
-    T* dst[3];
-    double mult[3];
+struct ResampleArgs {  // up to 9 components (field + both Adam moments in one pass)
+    const T* src[9];
+    T* dst[9];
+    double mult[9];
     double step[3];
 };
 
@@ -321,28 +342,34 @@ __device__ __forceinline__ void locate_point(double p, int n, int& i0, double& f
 
 template <class T>
 __global__ void k_resample(ResampleArgs<T> a, Dims ds, Dims dd, int ncomp) {
-    const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
-    if (i >= dd.n) return;
-    int x, y, z;
-    voxel_xyz(dd, i, x, y, z);
-    int ix, iy, iz;
-    double fx, fy, fz;
+    const int x = blockIdx.x * kRX + threadIdx.x;
+    if (x >= dd.nx) return;
+    const int rows = dd.ny * dd.nz;
+    int ix;
+    double fx;
     locate_point(x * a.step[0], ds.nx, ix, fx);
-    locate_point(y * a.step[1], ds.ny, iy, fy);
-    locate_point((z + dd.zoff) * a.step[2], ds.nz, iz, fz);  // dd may be a z-slab view
-    Cell3<T> c;
-    c.base = ds.idx(ix, iy, iz);
-    c.sx = ds.nx > 1 ? 1 : 0;
-    c.sy = ds.ny > 1 ? ds.nx : 0;
-    c.three = ds.nz > 1;
-    c.sz = c.three ? static_cast<int64_t>(ds.nx) * ds.ny : 0;
-    c.fx = static_cast<T>(fx);
-    c.fy = static_cast<T>(fy);
-    c.fz = static_cast<T>(fz);
-    c.clx = c.cly = c.clz = false;
-    for (int k = 0; k < ncomp; ++k) {
-        const T v = lerp_value(c, fetch_corners<T>(a.src[k], c));
-        a.dst[k][i] = a.mult[k] == 1.0 ? v : static_cast<T>(v * a.mult[k]);
+    for (int row = blockIdx.y * kRY + threadIdx.y; row < rows; row += gridDim.y * kRY) {
+        const int y = row % dd.ny, z = row / dd.ny;
+        int iy, iz;
+        double fy, fz;
+        locate_point(y * a.step[1], ds.ny, iy, fy);
+        locate_point((z + dd.zoff) * a.step[2], ds.nz, iz, fz);  // dd may be a z-slab view
+        Cell3<T> c;
+        c.base = ds.idx(ix, iy, iz);
+        c.sx = ds.nx > 1 ? 1 : 0;
+        c.sy = ds.ny > 1 ? ds.nx : 0;
+        c.three = ds.nz > 1;
+        c.sz = c.three ? static_cast<int64_t>(ds.nx) * ds.ny : 0;
+        c.fx = static_cast<T>(fx);
+        c.fy = static_cast<T>(fy);
+        c.fz = static_cast<T>(fz);
+        c.clx = c.cly = c.clz = false;
+        const int64_t i = dd.idx(x, y, z);
+#pragma unroll 3
+        for (int k = 0; k < ncomp; ++k) {
+            const T v = lerp_value(c, fetch_corners<T>(a.src[k], c));
+            a.dst[k][i] = a.mult[k] == 1.0 ? v : static_cast<T>(v * a.mult[k]);
+        }
     }
 }
 
@@ -351,13 +378,15 @@ void launch_resample(const Launch& L, const T* const* src, Dims ds, T* const* ds
                      int ncomp, const double* mult) {
     ResampleArgs<T> a;
     const int ns[3] = {ds.nx, ds.ny, ds.nz}, nd[3] = {dd.nx, dd.ny, dd.gz()};
-    for (int k = 0; k < 3; ++k) {
+    for (int k = 0; k < 9; ++k) {
         a.src[k] = k < ncomp ? src[k] : nullptr;
         a.dst[k] = k < ncomp ? dst[k] : nullptr;
-        a.mult[k] = mult ? mult[k] : 1.0;
-        a.step[k] = nd[k] > 1 ? static_cast<double>(ns[k] - 1) / (nd[k] - 1) : 0.0;
+        a.mult[k] = mult && k < ncomp ? mult[k] : 1.0;
     }
-    k_resample<T><<<grid_for(dd.n), kNT, 0, L.stream>>>(a, ds, dd, ncomp);
+    for (int k = 0; k < 3; ++k)
+        a.step[k] = nd[k] > 1 ? static_cast<double>(ns[k] - 1) / (nd[k] - 1) : 0.0;
+    k_resample<T><<<rows_grid(dd.nx, static_cast<int64_t>(dd.ny) * dd.nz), dim3(kRX, kRY), 0,
+                    L.stream>>>(a, ds, dd, ncomp);
     L.bump();
 }
 

@@ -1407,25 +1407,91 @@ struct ComposeS2 {
     }
 };
 
+// interp.cpp:110-151 — one-component Gaussian smoothing (the pyramid's
+// pre-blur before downsampling), same arithmetic as the generic z-march
+// GaussOp of kernels_stencil.cu with TMA-fed planes and the quad x filter
+template <class T, int R_, int TY_ = 8>
+struct Gauss2 {
+    using Acc = T;
+    using Center = NoCenter;
+    using Prol = NoProl;
+    using Carry = NoCarry;
+    static constexpr int R = R_, C = 1, BACK = 0, AHEAD = 0, S = 4, TYv = TY_;
+    static constexpr int kMinB = 3, kCY = 1;
+    static constexpr bool kStaged = false, kSum = false, kMax = false;
+    static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TYv + 2 * R;
+    static constexpr int kBytes = BX * BY * int(sizeof(T));
+    static constexpr int kBox = align128(kBytes);
+    static constexpr int kStageBytes = kBox;
+    CUtensorMap mI;
+    GaussW<T> w;
+    T* out;
+    Dims d;
+
+    __device__ bool skip() const { return false; }
+    __device__ void prefetch_maps() const { prefetch_tmap(&mI); }
+    __device__ void issue(unsigned char* dst, uint64_t* bar, int x0, int y0, int q) const {
+        mbar_expect_tx(bar, kBytes);
+        tma_load_4d(dst, &mI, bar, x0 - XA, y0 - R, q, 0);
+    }
+    __device__ Acc wgt(int a, int j) const { return w.taps[a][j]; }
+    __device__ Acc nrm(int a, int i) const {
+        return w.nrm(a, i, a == 0 ? d.nx : (a == 1 ? d.ny : d.gz()));
+    }
+    __device__ Prol prologue() const { return {}; }
+    static constexpr bool kXQuad = sizeof(T) == 4;
+    __device__ void xpass4(const unsigned char* st_, int row, int col, const Acc nx[4],
+                           Acc v[1][4]) const {
+        constexpr int NCH = (XA + R + 4 + 3) / 4;
+        float wv[4 * NCH];
+        load_row4<NCH>(reinterpret_cast<const float*>(st_) + row * BX + col, wv);
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+            T a = T(0);
+#pragma unroll
+            for (int j = 0; j < 2 * R + 1; ++j) a += w.taps[0][j] * wv[o + (XA - R) + j];
+            v[0][o] = a * nx[o];
+        }
+    }
+    __device__ void xpass(const unsigned char* st_, int row, int col, Acc nx, Acc v[1]) const {
+        const T* q = reinterpret_cast<const T*>(st_) + row * BX + col + (XA - R);
+        T a = T(0);
+#pragma unroll
+        for (int j = 0; j < 2 * R + 1; ++j) a += w.taps[0][j] * q[j];
+        v[0] = a * nx;
+    }
+    __device__ void load_center(int, int, int, Center&) const {}
+    __device__ Red2 emit(int x, int y, int z, const T s[1], const Center&, const Prol&,
+                         Carry&) const {
+        out[d.idx32(x, y, z)] = s[0];
+        return {0.0, 0.0};
+    }
+    __device__ void flush(Carry&) const {}
+    __device__ void finish(int, double, double, const Prol&) const {}
+};
+
 // W = M(x+u), G = grad M(x+u) (similarity.cpp:25-45) at scale start / epilogue
 template <class T>
 __global__ void k_warpgrad(const T* __restrict__ M, Dims dm, CPlanes3<T> u, Dims d,
                            T* __restrict__ W, T* __restrict__ G) {
-    const int64_t i = blockIdx.x * 256ll + threadIdx.x;
-    if (i >= d.n) return;
-    const int x = static_cast<int>(i % d.nx);
-    const int64_t r = i / d.nx;
-    const int y = static_cast<int>(r % d.ny), z = static_cast<int>(r / d.ny);
-    const Cell3<T> c = locate3<T>(dm, x, y, z + d.zoff, __ldg(u.c[0] + i), __ldg(u.c[1] + i),
-                                  d.ndim == 3 ? __ldg(u.c[2] + i) : T(0));
-    const Corners<T> k = fetch_corners<T>(M, c);
-    W[i] = lerp_value(c, k);
-    if (G) {
-        T gr[3];
-        lerp_grad(c, k, d.ndim, gr);
-        G[i] = gr[0];
-        G[d.n + i] = gr[1];
-        G[2 * d.n + i] = gr[2];
+    // (x, row) mapping, 32 x 8 blocks: no 64-bit index division per voxel
+    const int x = blockIdx.x * 32 + threadIdx.x;
+    if (x >= d.nx) return;
+    const int rows = d.ny * d.nz;
+    for (int row = blockIdx.y * 8 + threadIdx.y; row < rows; row += gridDim.y * 8) {
+        const int y = row % d.ny, z = row / d.ny;
+        const int64_t i = d.idx(x, y, z);
+        const Cell3<T> c = locate3<T>(dm, x, y, z + d.zoff, __ldg(u.c[0] + i),
+                                      __ldg(u.c[1] + i), d.ndim == 3 ? __ldg(u.c[2] + i) : T(0));
+        const Corners<T> k = fetch_corners<T>(M, c);
+        W[i] = lerp_value(c, k);
+        if (G) {
+            T gr[3];
+            lerp_grad(c, k, d.ndim, gr);
+            G[i] = gr[0];
+            G[d.n + i] = gr[1];
+            G[2 * d.n + i] = gr[2];
+        }
     }
 }
 
@@ -1805,8 +1871,25 @@ int go_compose_smooth(const Launch& L, const GaussW<T>& w, const T* c, T* uout, 
 }
 
 template <class T>
+int launch_gauss_tma(const Launch& L, int R, const GaussW<T>& w, const T* in, T* out, Dims d) {
+    if (d.ndim != 3) return -2;
+    return with_r<1, 6>(R, [&](auto rc) {
+        constexpr int RR = decltype(rc)::value;
+        using Op = Gauss2<T, RR>;
+        Op op;
+        if (!make_map<T>(&op.mI, in, d, 1, Op::BX, Op::BY)) return -1;
+        op.w = w;
+        op.out = out;
+        op.d = d;
+        return run_zm2(L, op, d);
+    });
+}
+
+template <class T>
 void launch_warpgrad(const Launch& L, const T* M, Dims dm, CPlanes3<T> u, Dims d, T* W, T* G) {
-    k_warpgrad<T><<<static_cast<unsigned>((d.n + 255) / 256), 256, 0, L.stream>>>(M, dm, u, d, W, G);
+    const int64_t by = (static_cast<int64_t>(d.ny) * d.nz + 7) / 8;
+    const dim3 grid((d.nx + 31) / 32, static_cast<unsigned>(by < 65535 ? by : 65535));
+    k_warpgrad<T><<<grid, dim3(32, 8), 0, L.stream>>>(M, dm, u, d, W, G);
     L.bump();
 }
 
@@ -1826,6 +1909,7 @@ void launch_warpgrad(const Launch& L, const T* M, Dims dm, CPlanes3<T> u, Dims d
                                        const T*, T*, const T*, Dims, Dims, T*, T*,             \
                                        LoopState*, bool);                                      \
     template void launch_warpgrad<T>(const Launch&, const T*, Dims, CPlanes3<T>, Dims, T*, T*); \
+    template int launch_gauss_tma<T>(const Launch&, int, const GaussW<T>&, const T*, T*, Dims); \
     template int launch_smooth_adam_compose_tma<T>(const Launch&, int, const GaussW<T>&,        \
                                                    const T*, T*, T*, const T*, T*, double,     \
                                                    Dims, AdamParams, LoopState*,               \
