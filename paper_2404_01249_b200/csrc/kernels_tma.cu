@@ -1481,6 +1481,20 @@ __global__ void k_warpgrad(const T* __restrict__ M, Dims dm, CPlanes3<T> u, Dims
     for (int row = blockIdx.y * 8 + threadIdx.y; row < rows; row += gridDim.y * 8) {
         const int y = row % d.ny, z = row / d.ny;
         const int64_t i = d.idx(x, y, z);
+        if (d.ndim == 3 && dm.nx > 1 && dm.ny > 1 && dm.nz > 1 && dm.n < (int64_t(1) << 31)) {
+            WG3<T> w;
+            wg3_fetch<T>(M, dm, x, y, z + d.zoff, __ldg(u.c[0] + i), __ldg(u.c[1] + i),
+                         __ldg(u.c[2] + i), w);
+            W[i] = wg3_value(w);
+            if (G) {
+                T gr[3];
+                wg3_grad(w, gr);
+                G[i] = gr[0];
+                G[d.n + i] = gr[1];
+                G[2 * d.n + i] = gr[2];
+            }
+            continue;
+        }
         const Cell3<T> c = locate3<T>(dm, x, y, z + d.zoff, __ldg(u.c[0] + i),
                                       __ldg(u.c[1] + i), d.ndim == 3 ? __ldg(u.c[2] + i) : T(0));
         const Corners<T> k = fetch_corners<T>(M, c);
