@@ -2242,18 +2242,36 @@ struct Registrar {
             launch_stamp(ctx->L(), stamp + T_si);
             ev_collect(d);
         } else {
-            // capture the two ping-pong variants of one iteration as CUDA graphs
-            cudaGraphExec_t exec[2] = {nullptr, nullptr};
+            // capture the two ping-pong variants of one iteration as CUDA graphs,
+            // and G consecutive iterations (G even, alternating variants) as one
+            // graph: one graph launch per G iterations (the gap between graph
+            // launches exceeds the gap between kernels inside a graph)
+            static const int G = [] {
+                const char* e = getenv("DFM_GRAPH_ITERS");
+                const int g = e ? atoi(e) : 8;
+                return g >= 2 ? g & ~1 : 0;
+            }();
+            cudaGraphExec_t exec[2] = {nullptr, nullptr}, exec_g = nullptr;
             int64_t nodes_per = 0;
-            for (int v = 0; v < 2; ++v) {
+            for (int v = 0; v < 3; ++v) {
+                if (v == 2 && (G == 0 || T_si < G)) break;
                 const int64_t before = ctx->launches;
                 cudaGraph_t graph;
                 CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
-                enqueue_iteration(d, (start + v) % 2, Rg, Rw, wg, ww, pbg, pbw);
+                if (v < 2) {
+                    enqueue_iteration(d, (start + v) % 2, Rg, Rw, wg, ww, pbg, pbw);
+                } else {
+                    for (int k = 0; k < G; ++k)
+                        enqueue_iteration(d, (start + k) % 2, Rg, Rw, wg, ww, pbg, pbw);
+                }
                 CK(cudaStreamEndCapture(ctx->stream, &graph));
-                exec[v] = ctx->graph_exec(2 * si + v, graph);
+                if (v < 2) {
+                    exec[v] = ctx->graph_exec(2 * si + v, graph);
+                    nodes_per = ctx->launches - before;
+                } else {
+                    exec_g = ctx->graph_exec(1000 + si, graph);
+                }
                 CK(cudaGraphDestroy(graph));
-                nodes_per = ctx->launches - before;
                 ctx->launches = before;
             }
             // Launch in chunks, keeping at most two chunks in flight, and stop
@@ -2269,9 +2287,16 @@ struct Registrar {
                     if (hst[w].done) break;
                 }
                 const int jend = j + chunk < T_si ? j + chunk : T_si;
-                for (; j < jend; ++j) {
-                    CK(cudaGraphLaunch(exec[j % 2], ctx->stream));
-                    ctx->launches += nodes_per;
+                while (j < jend) {
+                    if (exec_g && j % 2 == 0 && j + G <= T_si) {  // G even: parity kept
+                        CK(cudaGraphLaunch(exec_g, ctx->stream));
+                        ctx->launches += G * nodes_per;
+                        j += G;
+                    } else {
+                        CK(cudaGraphLaunch(exec[j % 2], ctx->stream));
+                        ctx->launches += nodes_per;
+                        ++j;
+                    }
                 }
                 const int w = nchunk % 2;
                 CK(cudaMemcpyAsync(&hst[w], st, sizeof(LoopState), cudaMemcpyDeviceToHost,
