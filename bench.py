@@ -80,19 +80,56 @@ def voxel_iters(pair) -> int:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region: NVML in a
+    thread (every 10 ms, plus one sample when the region starts and one when it
+    ends, so even a short region is covered); nvidia-smi if NVML is missing."""
 
     Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits
+    BITS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+            "sw_power_cap": 0x4}
 
     def __init__(self, device: int):
         self.device = device
         self.rows = []
         self.proc = None
         self.thread = None
+        self.nvml = None
+        self.stop_evt = threading.Event()
+
+    def _nvml_sample(self):
+        nv, h = self.nvml
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        try:
+            rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except AttributeError:
+            rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        self.rows.append((float(sm), float(mx), int(rs)))
+
+    def _nvml_loop(self):
+        while not self.stop_evt.wait(0.01):
+            try:
+                self._nvml_sample()
+            except Exception:  # noqa: BLE001 - sampling must never break the bench
+                return
 
     def start(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            vis = [v.strip() for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")]
+            dev = (int(vis[self.device]) if len(vis) > self.device and
+                   all(v.isdigit() for v in vis) else self.device)
+            self.nvml = (nv, nv.nvmlDeviceGetHandleByIndex(dev))
+            self._nvml_sample()
+            self.thread = threading.Thread(target=self._nvml_loop, daemon=True)
+            self.thread.start()
+            return
+        except Exception:  # noqa: BLE001
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
@@ -109,6 +146,20 @@ class ClockSampler:
             self.rows.append([x.strip() for x in line.split(",")])
 
     def stop(self):
+        if self.nvml:
+            self.stop_evt.set()
+            if self.thread:
+                self.thread.join(timeout=2)
+            try:
+                self._nvml_sample()
+            except Exception:  # noqa: BLE001
+                pass
+            sm = [r[0] for r in self.rows]
+            reasons = sorted({nm for r in self.rows for nm, bit in self.BITS.items()
+                              if r[2] & bit})
+            return {"sm_mhz": float(np.median(sm)) if sm else None,
+                    "sm_max_mhz": max(r[1] for r in self.rows) if self.rows else None,
+                    "reasons": reasons, "samples": len(sm), "source": "nvml"}
         if self.proc:
             self.proc.terminate()
             try:
@@ -128,7 +179,7 @@ class ClockSampler:
                         reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvidia-smi"}
 
 
 def hbm_peak():
