@@ -41,10 +41,10 @@ namespace dfm {
 namespace {
 
 #ifndef DFM_BRICK_BY
-#define DFM_BRICK_BY 8
+#define DFM_BRICK_BY 4
 #endif
 #ifndef DFM_BRICK_NTB
-#define DFM_BRICK_NTB 512
+#define DFM_BRICK_NTB 256
 #endif
 constexpr int NTB = DFM_BRICK_NTB;
 constexpr int BX = 8, BY = DFM_BRICK_BY, BZ = 8;
