@@ -58,6 +58,9 @@ constexpr int64_t kSaCoarsenVoxels = 2000000;
 #ifndef DFM_CS_ASYNC
 #define DFM_CS_ASYNC 1
 #endif
+#ifndef DFM_SA_CASYNC
+#define DFM_SA_CASYNC 0
+#endif
 #ifndef DFM_SA_CTMA
 #define DFM_SA_CTMA 0
 #endif
@@ -217,6 +220,18 @@ struct CenterTMA<Op, std::void_t<decltype(Op::kCenterTMA)>> {
     static constexpr bool value = Op::kCenterTMA;
 };
 
+// the op's centre operands of plane zo + 1 are requested with cp.async during
+// plane zo's epilogue (Op::kCenterAsync: center_async / load_center_async):
+// a whole plane of latency hiding, no register scoreboard across the loop
+template <class Op, class = void>
+struct CenterAsync {
+    static constexpr bool value = false;
+};
+template <class Op>
+struct CenterAsync<Op, std::void_t<decltype(Op::kCenterAsync)>> {
+    static constexpr bool value = Op::kCenterAsync;
+};
+
 // optional per-row carry initialisation (Op::init_carry(carry, row))
 template <class Op, class C>
 __device__ __forceinline__ auto carry_init(const Op& op, C& c, int r, int)
@@ -315,6 +330,14 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
     typename Op::Carry carry[CY] = {};
 #pragma unroll
     for (int r = 0; r < CY; ++r) carry_init(op, carry[r], r, 0);
+    if constexpr (CenterAsync<Op>::value) {  // the first emitted plane's centre operands
+        if (z0 < z1) {
+#pragma unroll
+            for (int r = 0; r < CY; ++r)
+                if (own[r]) op.center_async(x, yk[r], z0, r, 0);
+        }
+        cp_async_commit();
+    }
 
     // register ring of the last K xy-filtered planes per owned row; it shifts
     // by register moves (C*(K-1) MOVs per plane and row) rather than unrolling
@@ -373,8 +396,9 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
         constexpr int kk = K - 1;
         const int zo = zi - R;
         constexpr bool kCT = CenterTMA<Op>::value;
+        constexpr bool kCA = CenterAsync<Op>::value;
         typename Op::Center cen[CY];
-        if constexpr (!kCT) {
+        if constexpr (!kCT && !kCA) {
 #pragma unroll
             for (int r = 0; r < CY; ++r)
                 if (zo >= z0 && own[r]) op.load_center(x, yk[r], zo, cen[r]);
@@ -473,6 +497,20 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
 #pragma unroll
                 for (int k = 0; k < K - 1; ++k) ring[r][c][k] = ring[r][c][k + 1];
                 ring[r][c][kk] = a * nyv[r];
+            }
+        }
+        if constexpr (kCA) {
+            if (zo >= z0) {  // request plane zo + 1, then wait for plane zo
+                if (zo + 1 < z1) {
+#pragma unroll
+                    for (int r = 0; r < CY; ++r)
+                        if (own[r]) op.center_async(x, yk[r], zo + 1, r, (zo + 1 - z0) & 1);
+                }
+                cp_async_commit();
+                cp_async_wait_group<1>();
+#pragma unroll
+                for (int r = 0; r < CY; ++r)
+                    if (own[r]) op.load_center_async(r, (zo - z0) & 1, cen[r]);
             }
         }
 #pragma unroll
@@ -873,9 +911,36 @@ struct SmoothAdam2 {
     static constexpr int kMinB = MINB_, kCY = CY_;
     static constexpr int NTH = TX * TY_ / CY_;
     // two slots of the 24 gathered corners per thread: [slot][corner][thread]
-    static constexpr int kExtraBytes = kAsync ? 2 * 24 * NTH * int(sizeof(T)) : 0;
+    static constexpr int kGatherBytes = kAsync ? 2 * 24 * NTH * int(sizeof(T)) : 0;
+    // m, nu of the next plane by cp.async (composing variant: its carried
+    // gather already needs the registers): [slot][row][6][thread]
+    static constexpr bool kCenterAsync = CAPH_ > 0 && DFM_SA_CASYNC != 0;
+    static constexpr int kCenterBytes = kCenterAsync ? 2 * CY_ * 6 * NTH * int(sizeof(T)) : 0;
+    static constexpr int kExtraBytes = kGatherBytes + kCenterBytes;
     __device__ static T* gather_buf(int slot) {
         return reinterpret_cast<T*>(zm2_extra<SmoothAdam2>()) + (slot * 24) * NTH + threadIdx.x;
+    }
+    __device__ static T* center_buf(int slot, int r) {
+        return reinterpret_cast<T*>(zm2_extra<SmoothAdam2>() + kGatherBytes) +
+               ((slot * CY_ + r) * 6) * NTH + threadIdx.x;
+    }
+    __device__ void center_async(int x, int y, int z, int r, int slot) const {
+        const int i = d.idx32(x, y, z);
+        T* b = center_buf(slot, r);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            cp_async<int(sizeof(T))>(b + k * NTH, m[k] + i);
+            cp_async<int(sizeof(T))>(b + (3 + k) * NTH, nu[k] + i);
+        }
+    }
+    template <class CC>  // CC = Center (declared below)
+    __device__ void load_center_async(int r, int slot, CC& c) const {
+        const T* b = center_buf(slot, r);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            c.m[k] = b[k * NTH];
+            c.nu[k] = b[(3 + k) * NTH];
+        }
     }
     static constexpr bool kStaged = false, kSum = false, kMax = true;
     static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TYv + 2 * R;
