@@ -8,6 +8,7 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2404_01249_b200 import _abi as A, synth
+from paper_2404_01249_b200 import engine
 from paper_2404_01249_b200.engine import Context, OPT_BRICK_MAX, OPT_PERSIST
 
 nx, ny, nz = (int(v) for v in sys.argv[1:4])
@@ -20,6 +21,9 @@ for fam, bm in [("stream", 0), ("brick", 1 << 40)][:int(os.environ.get("KT_FAMS"
     ctx = Context(0, prec)
     ctx.set_option(OPT_BRICK_MAX, bm)
     ctx.set_option(OPT_PERSIST, 0)
+    for kv in filter(None, os.environ.get("KT_OPTS", "").split(",")):  # e.g. SPLIT_FOLD_MAX=0
+        k, v = kv.split("=")
+        ctx.set_option(getattr(engine, "OPT_" + k), int(float(v)))
     ctx.set_profiling(True)
     try:
         ctx.register_images(p.grid, p.fixed, p.moving, cfg, sched)
