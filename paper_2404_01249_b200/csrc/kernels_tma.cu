@@ -31,7 +31,7 @@ namespace dfm {
 
 namespace {
 
-constexpr int TX = kTX, TY = kTY;
+constexpr int TX = kTX;
 constexpr int64_t kSaCoarsenVoxels = 2000000;
 
 // TMA ring depths (planes in flight per CTA); overridable for tuning builds
