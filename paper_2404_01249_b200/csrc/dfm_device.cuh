@@ -68,9 +68,11 @@ struct AxisCell {
     bool clamped;
 };
 
+// kFlat = false: the caller guarantees n >= 2 (no flat-axis branch)
+template <bool kFlat = true>
 __device__ __forceinline__ AxisCell<double> locate_axis(int xi, double u, int n) {
     AxisCell<double> c;
-    if (n == 1) {
+    if (kFlat && n == 1) {
         c.i0 = 0;
         c.f = 0.0;
         c.clamped = false;
@@ -88,9 +90,10 @@ __device__ __forceinline__ AxisCell<double> locate_axis(int xi, double u, int n)
     return c;
 }
 
+template <bool kFlat = true>
 __device__ __forceinline__ AxisCell<float> locate_axis(int xi, float u, int n) {
     AxisCell<float> c;
-    if (n == 1) {
+    if (kFlat && n == 1) {
         c.i0 = 0;
         c.f = 0.f;
         c.clamped = false;
@@ -263,13 +266,13 @@ __device__ __forceinline__ void wg3_fetch(const T* __restrict__ M, const Dims& m
 
 // the same gather issued as cp.async copies of the 8 corners into s[k * ss]
 // (shared memory); wg3_load pulls them into w.v once cp_async_wait_all() ran
-template <class T>
+template <class T, bool kFlat = true>
 __device__ __forceinline__ void wg3_fetch_async(const T* __restrict__ M, const Dims& m, int x,
                                                 int y, int z, T ux, T uy, T uz, WG3<T>& w,
                                                 T* s, int ss) {
-    const AxisCell<T> ax = locate_axis(x, ux, m.nx);
-    const AxisCell<T> ay = locate_axis(y, uy, m.ny);
-    const AxisCell<T> az = locate_axis(z, uz, m.nz);
+    const AxisCell<T> ax = locate_axis<kFlat>(x, ux, m.nx);
+    const AxisCell<T> ay = locate_axis<kFlat>(y, uy, m.ny);
+    const AxisCell<T> az = locate_axis<kFlat>(z, uz, m.nz);
     w.fx = ax.f;
     w.fy = ay.f;
     w.fz = az.f;

@@ -1331,7 +1331,7 @@ struct Compose2 {
 // fused W = M(x+u'), G = grad M(x+u') epilogue (3-D fast gather, carried one
 // plane).  With the pointwise compose in the Adam kernel this replaces
 // Compose2, which recomposed every halo element of its tile (1.7x work).
-template <class T, int R_, int TY_ = DFM_TY_CS, bool ASYNC_ = DFM_CS_ASYNC>
+template <class T, int R_, int TY_ = DFM_TY_CS, bool ASYNC_ = DFM_CS_ASYNC, bool FLAT_ = true>
 struct ComposeS2 {
     using Acc = T;
     using Center = NoCenter;
@@ -1451,7 +1451,7 @@ struct ComposeS2 {
                 finish_wg(cr);
             }
             cr.slot ^= 1;
-            wg3_fetch_async<T>(M, dm, x, y, z + d.zoff, u[0], u[1], u[2], cr.w,
+            wg3_fetch_async<T, FLAT_>(M, dm, x, y, z + d.zoff, u[0], u[1], u[2], cr.w,
                                gather_buf(cr.slot), NTH);
             cr.i = i;
             cr.valid = true;
@@ -1922,9 +1922,13 @@ int launch_compose_smooth_tma(const Launch& L, int R, const GaussW<T>& w, const 
         constexpr int RR = decltype(rc)::value;
         // the cp.async carried gather pays on large levels (-10 us/iteration at
         // 160x192x224), the register carry on mid ones (-1.6 us at 80x96x112)
-        if (d.n >= kSaCoarsenVoxels)
+        if (d.n >= kSaCoarsenVoxels) {
+            if (dm.nx > 1 && dm.ny > 1 && dm.nz > 1)  // no flat axis: no per-voxel check
+                return go_compose_smooth<ComposeS2<T, RR, DFM_TY_CS, DFM_CS_ASYNC != 0, false>>(
+                    L, w, c, uout, M, dm, d, W, G, st, count_update);
             return go_compose_smooth<ComposeS2<T, RR, DFM_TY_CS, DFM_CS_ASYNC != 0>>(
                 L, w, c, uout, M, dm, d, W, G, st, count_update);
+        }
         return go_compose_smooth<ComposeS2<T, RR, DFM_TY_CS, false>>(L, w, c, uout, M, dm, d, W,
                                                                       G, st, count_update);
     });
