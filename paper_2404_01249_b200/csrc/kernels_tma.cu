@@ -369,16 +369,12 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
                 }
             }
             const typename Op::PlaneCtx pc = op.plane_ctx(stages, q0, zi);
-            const bool fast = op.interior(x0, y0, zi);  // CTA-uniform
             typename Op::Center cen{};
 #pragma unroll
             for (int r = 0; r < CY; ++r) {
                 if (!own[r]) continue;
                 Acc v[C];
-                if (fast)
-                    op.stage_fast(pc, x0, y0, zi, ty * CY + r, tx, v);
-                else
-                    op.stage(pc, x0, y0, zi, ty * CY + r, tx, v);
+                op.stage_point(pc, x0, y0, zi, ty * CY + r, tx, v);
                 const Red2 rr = op.emit(x, yk[r], zi, v, cen, pr, carry[r]);
                 rsum += rr.sum;
                 rmax = fmax(rmax, rr.mx);
@@ -1229,6 +1225,41 @@ struct Compose2 {
         const T wx0 = T(1) - fx, wy0 = T(1) - fy, wz0 = T(1) - fz;
         const T w00 = wx0 * wy0, w10 = fx * wy0, w01 = wx0 * fy, w11 = fx * fy;
         const int dz = iz - zi;
+        const T* u0 = pc.u[CAPH];
+        const T* u1 = pc.u[CAPH];
+#pragma unroll
+        for (int k = 0; k < 2 * CAPH; ++k)
+            if (dz == k - CAPH) {
+                u0 = pc.u[k];
+                u1 = pc.u[k + 1];
+            }
+        const T s[3] = {s0, s1, s2};
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const T* a = u0 + k * PU + o;
+            const T* b = u1 + k * PU + o;
+            const T lo = bilerp4(w00, w10, w01, w11, a[0], a[1], a[BXU], a[BXU + 1]);
+            const T hi = bilerp4(w00, w10, w01, w11, b[0], b[1], b[BXU], b[BXU + 1]);
+            v[k] = s[k] + zlerp(wz0, lo, fz, hi);
+        }
+    }
+    // the pointwise (radius-0) form for any voxel of the tile: the clamped cell
+    // search of stage() (identical to stage_fast's cell where nothing clamps),
+    // without its halo bounds and 2-D branches — border tiles no longer take
+    // the general path (their clamped corners stay inside the staged tiles)
+    __device__ void stage_point(const PlaneCtx& pc, int x0, int y0, int zi, int row, int col,
+                                T v[3]) const {
+        const int gx = x0 + col, gy = y0 + row, zg = zi + d.zoff;
+        const int so = row * BXS + col + (XAS - R);
+        const T s0 = pc.step[so], s1 = pc.step[PS + so], s2 = pc.step[2 * PS + so];
+        const AxisCell<T> ax = locate_axis(gx, s0, d.nx);
+        const AxisCell<T> ay = locate_axis(gy, s1, d.ny);
+        const AxisCell<T> az = locate_axis(zg, s2, d.gz());
+        const int o = (ay.i0 - (y0 - HU)) * BXU + (ax.i0 - (x0 - XAU));
+        const T fx = ax.f, fy = ay.f, fz = az.f;
+        const T wx0 = T(1) - fx, wy0 = T(1) - fy, wz0 = T(1) - fz;
+        const T w00 = wx0 * wy0, w10 = fx * wy0, w01 = wx0 * fy, w11 = fx * fy;
+        const int dz = az.i0 - zg;
         const T* u0 = pc.u[CAPH];
         const T* u1 = pc.u[CAPH];
 #pragma unroll
