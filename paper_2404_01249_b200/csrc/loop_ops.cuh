@@ -189,24 +189,8 @@ __device__ __forceinline__ T adam_component(const AdamK<T>& k, T g, T& m, T& nu,
 // compose at one voxel (interp.cpp:269-289 with psi = step): the composed
 // value step + u(x + step), u read from global memory (3 packed planes of the
 // volume view d; zg = global z of the voxel).  Same arithmetic as the staged
-// compose of kernels_tma.cu (Compose2::stage / stage_fast) so both give
+// compose of kernels_tma.cu (Compose2::stage / stage_point) so both give
 // bit-identical values; CAPH bounds |step| (cap <= CAPH - 0.5).
-template <class T>
-__device__ __forceinline__ void cell_exact(int g, T s, int& i0, T& f);
-template <>
-__device__ __forceinline__ void cell_exact<float>(int g, float s, int& i0, float& f) {
-    const float fl = floorf(s);
-    f = s - fl;
-    i0 = g + static_cast<int>(fl);
-}
-template <>
-__device__ __forceinline__ void cell_exact<double>(int g, double s, int& i0, double& f) {
-    const double p = static_cast<double>(g) + s;  // the reference's formulation
-    const double fl = floor(p);
-    f = p - fl;
-    i0 = static_cast<int>(fl);
-}
-
 // the 8 corner values of each component and the weights, fetched at one
 // plane and combined at the next (the gathers' latency hides behind a plane)
 template <class T>
@@ -224,23 +208,15 @@ __device__ __forceinline__ void compose_fetch(const T* __restrict__ u, const Dim
                                               ComposeCarry<T>& c) {
     const int64_t n = d.n;
     const int gz = d.gz();
-    int ix, iy, iz;
-    if (x >= CAPH && x < d.nx - CAPH && y >= CAPH && y < d.ny - CAPH && zg >= CAPH &&
-        zg < gz - CAPH) {
-        cell_exact<T>(x, s[0], ix, c.fx);
-        cell_exact<T>(y, s[1], iy, c.fy);
-        cell_exact<T>(zg, s[2], iz, c.fz);
-    } else {
-        const AxisCell<T> ax = locate_axis(x, s[0], d.nx);
-        const AxisCell<T> ay = locate_axis(y, s[1], d.ny);
-        const AxisCell<T> az = locate_axis(zg, s[2], gz);
-        ix = ax.i0;
-        iy = ay.i0;
-        iz = az.i0;
-        c.fx = ax.f;
-        c.fy = ay.f;
-        c.fz = az.f;
-    }
+    // one clamped cell search for every voxel (equal to the unclamped one
+    // where nothing clamps): no divergent interior/border split in a warp
+    const AxisCell<T> ax = locate_axis(x, s[0], d.nx);
+    const AxisCell<T> ay = locate_axis(y, s[1], d.ny);
+    const AxisCell<T> az = locate_axis(zg, s[2], gz);
+    const int ix = ax.i0, iy = ay.i0, iz = az.i0;
+    c.fx = ax.f;
+    c.fy = ay.f;
+    c.fz = az.f;
     const int sy = d.nx;
     const int64_t sz = static_cast<int64_t>(d.nx) * d.ny;
     const int64_t base = (static_cast<int64_t>(iz - d.zoff) * d.ny + iy) * d.nx + ix;
@@ -306,23 +282,15 @@ __device__ __forceinline__ void compose_fetch_async(const T* const* u, const Dim
                                                     int y, int zg, const T s[3], int64_t i,
                                                     ComposeCarryA<T>& c, T* buf, int ss) {
     const int gz = d.gz();
-    int ix, iy, iz;
-    if (x >= CAPH && x < d.nx - CAPH && y >= CAPH && y < d.ny - CAPH && zg >= CAPH &&
-        zg < gz - CAPH) {
-        cell_exact<T>(x, s[0], ix, c.fx);
-        cell_exact<T>(y, s[1], iy, c.fy);
-        cell_exact<T>(zg, s[2], iz, c.fz);
-    } else {
-        const AxisCell<T> ax = locate_axis(x, s[0], d.nx);
-        const AxisCell<T> ay = locate_axis(y, s[1], d.ny);
-        const AxisCell<T> az = locate_axis(zg, s[2], gz);
-        ix = ax.i0;
-        iy = ay.i0;
-        iz = az.i0;
-        c.fx = ax.f;
-        c.fy = ay.f;
-        c.fz = az.f;
-    }
+    // one clamped cell search for every voxel (equal to the unclamped one
+    // where nothing clamps): no divergent interior/border split in a warp
+    const AxisCell<T> ax = locate_axis(x, s[0], d.nx);
+    const AxisCell<T> ay = locate_axis(y, s[1], d.ny);
+    const AxisCell<T> az = locate_axis(zg, s[2], gz);
+    const int ix = ax.i0, iy = ay.i0, iz = az.i0;
+    c.fx = ax.f;
+    c.fy = ay.f;
+    c.fz = az.f;
     const int sy = d.nx;
     const int64_t sz = static_cast<int64_t>(d.nx) * d.ny;
     const int64_t base = (static_cast<int64_t>(iz - d.zoff) * d.ny + iy) * d.nx + ix;
