@@ -241,12 +241,12 @@ struct WG3 {
     T v[8];          // corners in (cz, cy, cx) order
 };
 
-template <class T, bool NC = true>
+template <class T, bool NC = true, bool kFlat = true>
 __device__ __forceinline__ void wg3_fetch(const T* __restrict__ M, const Dims& m, int x, int y,
                                           int z, T ux, T uy, T uz, WG3<T>& w) {
-    const AxisCell<T> ax = locate_axis(x, ux, m.nx);
-    const AxisCell<T> ay = locate_axis(y, uy, m.ny);
-    const AxisCell<T> az = locate_axis(z, uz, m.nz);
+    const AxisCell<T> ax = locate_axis<kFlat>(x, ux, m.nx);
+    const AxisCell<T> ay = locate_axis<kFlat>(y, uy, m.ny);
+    const AxisCell<T> az = locate_axis<kFlat>(z, uz, m.nz);
     w.fx = ax.f;
     w.fy = ay.f;
     w.fz = az.f;

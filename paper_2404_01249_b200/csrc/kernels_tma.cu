@@ -1471,7 +1471,7 @@ struct ComposeS2 {
         if (W) {
             if constexpr (!kAsync) {
                 if (cr.valid) finish_wg(cr);
-                wg3_fetch<T>(M, dm, x, y, z + d.zoff, u[0], u[1], u[2], cr.w);
+                wg3_fetch<T, true, FLAT_>(M, dm, x, y, z + d.zoff, u[0], u[1], u[2], cr.w);
                 cr.i = i;
                 cr.valid = true;
                 return {0.0, 0.0};
@@ -1960,6 +1960,9 @@ int launch_compose_smooth_tma(const Launch& L, int R, const GaussW<T>& w, const 
             return go_compose_smooth<ComposeS2<T, RR, DFM_TY_CS, DFM_CS_ASYNC != 0>>(
                 L, w, c, uout, M, dm, d, W, G, st, count_update);
         }
+        if (dm.nx > 1 && dm.ny > 1 && dm.nz > 1)
+            return go_compose_smooth<ComposeS2<T, RR, DFM_TY_CS, false, false>>(
+                L, w, c, uout, M, dm, d, W, G, st, count_update);
         return go_compose_smooth<ComposeS2<T, RR, DFM_TY_CS, false>>(L, w, c, uout, M, dm, d, W,
                                                                       G, st, count_update);
     });
