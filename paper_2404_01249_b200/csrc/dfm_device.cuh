@@ -281,8 +281,10 @@ __device__ __forceinline__ void wg3_fetch_async(const T* __restrict__ M, const D
     w.base = (az.i0 * m.ny + ay.i0) * m.nx + ax.i0;
     const T* p = M + w.base;
     const int off[8] = {0, 1, sy, sy + 1, sz, sz + 1, sz + sy, sz + sy + 1};
+    const uint32_t sa = smem_u32(s);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) cp_async<int(sizeof(T))>(s + k * ss, p + off[k]);
+    for (int k = 0; k < 8; ++k)  // one generic->shared conversion for the 8 copies
+        cp_async_u32<int(sizeof(T))>(sa + k * ss * int(sizeof(T)), p + off[k]);
     cp_async_commit();
 }
 

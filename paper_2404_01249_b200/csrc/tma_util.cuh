@@ -79,6 +79,11 @@ __device__ __forceinline__ void cp_async(void* s, const void* g) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(s)), "l"(g), "n"(B)
                  : "memory");
 }
+template <int B>
+__device__ __forceinline__ void cp_async_u32(uint32_t saddr, const void* g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(saddr), "l"(g), "n"(B)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() {
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
