@@ -692,7 +692,9 @@ struct LnccFwd3 {
     using Prol = NoProl;
     using Carry = NoCarry;
     static constexpr int R = R_, C = 3, BACK = 0, AHEAD = 0, S = DFM_S_FWD, TYv = TY_;
-    static constexpr int kMinB = DFM_MINB_FWD3, kCY = 1;
+    // radius >= 3 (LNCC window 7+) or fp64 needs more than the 80 registers of
+    // 3 CTAs per SM: 2 CTAs, no spills
+    static constexpr int kMinB = (R_ >= 3 || sizeof(T) == 8) ? 2 : DFM_MINB_FWD3, kCY = 1;
     static constexpr bool kStaged = false, kSum = true, kMax = false;
     static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TYv + 2 * R;
     static constexpr int kBytes = BX * BY * int(sizeof(T));
@@ -1829,6 +1831,9 @@ int launch_smooth_adam_tma(const Launch& L, int R, const GaussW<T>& w, const T* 
             if (sizeof(T) == 4 && d.n >= kSaCoarsenVoxels)
                 return go(SmoothAdam2<T, RR, 16, 2, DFM_MINB_SA2>{});
         }
+        // 512-thread CTAs (TY 16) get 64 registers at 2 CTAs per SM: the
+        // gradient ring of radius >= 4 and every fp64 variant spill there
+        if constexpr (RR >= 4 || sizeof(T) == 8) return go(SmoothAdam2<T, RR, 8>{});
         return go(SmoothAdam2<T, RR>{});
     });
 }
