@@ -58,6 +58,9 @@ constexpr int64_t kSaCoarsenVoxels = 2000000;
 #ifndef DFM_CS_ASYNC
 #define DFM_CS_ASYNC 1
 #endif
+#ifndef DFM_FWD3_WIDE_R
+#define DFM_FWD3_WIDE_R 3
+#endif
 #ifndef DFM_SA_CASYNC
 #define DFM_SA_CASYNC 0
 #endif
@@ -694,7 +697,8 @@ struct LnccFwd3 {
     static constexpr int R = R_, C = 3, BACK = 0, AHEAD = 0, S = DFM_S_FWD, TYv = TY_;
     // radius >= 3 (LNCC window 7+) or fp64 needs more than the 80 registers of
     // 3 CTAs per SM: 2 CTAs, no spills
-    static constexpr int kMinB = (R_ >= 3 || sizeof(T) == 8) ? 2 : DFM_MINB_FWD3, kCY = 1;
+    static constexpr int kMinB = (R_ >= DFM_FWD3_WIDE_R || sizeof(T) == 8) ? 2 : DFM_MINB_FWD3,
+                         kCY = 1;
     static constexpr bool kStaged = false, kSum = true, kMax = false;
     static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TYv + 2 * R;
     static constexpr int kBytes = BX * BY * int(sizeof(T));
