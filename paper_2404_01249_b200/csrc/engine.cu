@@ -1853,8 +1853,21 @@ struct Registrar {
         launch_exp_map<T>(L, u[src].p[0], d, M, svf_levels, st);
         const T* ph = svf_levels + 3 * n * M;
         const CPlanes3<T> phi{{ph, ph + n, ph + 2 * n}};
-        const int np = loss_kind_launch_fwd<T>(ctx, loss_kind, cfg->lncc_radius, Fs, Ms, d, d,
-                                               phi, coef, grad.w(), partials, st);
+        // LNCC at phi = exp(v) through the plane-streaming kernels where they
+        // apply: W, G = M(x + phi), then the moment/coefficient and the dW pass
+        const bool tma = loss_kind == DFM_LOSS_LNCC && d.ndim == 3 && !ctx->force_legacy &&
+                         cfg->lncc_radius >= 1 && cfg->lncc_radius <= 5 &&
+                         tma_supported(d, sizeof(T));
+        int np = -1;
+        if (tma) {
+            launch_warpgrad<T>(L, Ms, d, phi, d, Wb, Gb);
+            np = launch_lncc_fwd_tma<T>(L, cfg->lncc_radius, Fs, Wb, d, coef[0], partials, st,
+                                        nullptr);
+        }
+        const bool tma_fwd = np >= 0;
+        if (!tma_fwd)
+            np = loss_kind_launch_fwd<T>(ctx, loss_kind, cfg->lncc_radius, Fs, Ms, d, d, phi,
+                                         coef, grad.w(), partials, st);
         ev_end();
         ev_begin(KC_MON);
         launch_monitor(L, monitor_kind(loss_kind), partials, np, static_cast<double>(n), st,
@@ -1863,7 +1876,10 @@ struct Registrar {
         if (loss_kind == DFM_LOSS_LNCC) {
             const T* cc[4] = {coef[0], coef[1], coef[2], coef[3]};
             ev_begin(KC_BWD);
-            launch_lncc_bwd<T>(L, cfg->lncc_radius, Fs, Ms, d, d, phi, cc, grad.w(), st);
+            if (!tma_fwd ||
+                launch_lncc_bwd_tma<T>(L, cfg->lncc_radius, coef[0], Fs, Wb, Gb, d, grad.p[0],
+                                       st) < 0)
+                launch_lncc_bwd<T>(L, cfg->lncc_radius, Fs, Ms, d, d, phi, cc, grad.w(), st);
             ev_end();
         }
         ev_begin(KC_ADAM);
@@ -1874,8 +1890,11 @@ struct Registrar {
                 axis_smooth_plane<T>(ctx, d, *big_g, svf_g + c * n, svf_g + c * n, step.p[c], st);
         AdamParams ap{cfg->beta1, cfg->beta2, cfg->eps_adam, cfg->eta, cfg->step_cap,
                       corr1, corr2, 0};
-        launch_smooth_adam<T>(L, big_g ? 0 : Rg, wg, g, u[src].r(), m.w(), nu.w(), step.w(), d,
-                              ap, st, maxstep);
+        if (!tma || big_g ||
+            launch_smooth_adam_tma<T>(L, Rg, wg, svf_g, m.p[0], nu.p[0], step.p[0], d, ap, st,
+                                      maxstep) < 0)
+            launch_smooth_adam<T>(L, big_g ? 0 : Rg, wg, g, u[src].r(), m.w(), nu.w(), step.w(),
+                                  d, ap, st, maxstep);
         ev_end();
         ev_begin(KC_COMPOSE);
         launch_svf_update<T>(L, big_w ? 0 : Rw, ww, u[src].r(), step.r(), u[1 - src].w(), d, st);
