@@ -336,6 +336,7 @@ struct SvfWork {
     int32_t* keys[2];   // 8n each
     int32_t* vals[2];   // 8n each
     int32_t* start;     // n+1
+    T* wts;             // 8n: lerp weight of pair 8i+k (written with the keys)
     void* temp;
     size_t temp_bytes;  // >= svf_sort_temp_bytes(n)
 };

@@ -1202,6 +1202,7 @@ dfm_status dfm_svf_pullback(dfm_ctx* ctx, const dfm_grid* g, const double* v,
                 ws.vals[k] = kv + (2 * k + 1) * 8 * d.n;
             }
             ws.start = ctx->arr<int32_t>("api_svf_start", d.n + 1);
+            ws.wts = ctx->arr<T>("api_svf_wts", 8 * d.n);
             ws.temp_bytes = svf_sort_temp_bytes(d.n);
             ws.temp = ctx->get("api_svf_temp", ws.temp_bytes);
             launch_svf_pullback<T>(ctx->L(), lev, d, M, b.p[0], o.p[0], ws);
@@ -1628,6 +1629,7 @@ struct Registrar {
                 svf.vals[k] = kv + (2 * k + 1) * 8 * n;
             }
             svf.start = ctx->arr<int32_t>("svf_start", n + 1);
+            svf.wts = ctx->arr<T>("svf_wts", 8 * n);
             svf.temp_bytes = svf_sort_temp_bytes(n);
             svf.temp = ctx->get("svf_temp", svf.temp_bytes);
         }

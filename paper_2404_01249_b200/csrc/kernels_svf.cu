@@ -59,7 +59,7 @@ __device__ __forceinline__ T corner_wt(const Cell3<T>& c, int k) {
 template <class T>
 __global__ void k_svf_jt(const T* __restrict__ uk, const T* __restrict__ w, Dims d,
                          T* __restrict__ wn, int32_t* __restrict__ keys,
-                         int32_t* __restrict__ vals, const LoopState* st) {
+                         int32_t* __restrict__ vals, T* __restrict__ wts, const LoopState* st) {
     if (st && st->done) return;
     const int64_t i = blockIdx.x * static_cast<int64_t>(kNS) + threadIdx.x;
     if (i >= d.n) return;
@@ -93,16 +93,31 @@ __global__ void k_svf_jt(const T* __restrict__ uk, const T* __restrict__ w, Dims
         wn[a * n + i] = wi[a] + acc;
     }
     const int ncorner = three ? 8 : 4;
+    // pair 8i+k: (node, pair id) for the sort, and the corner's lerp weight for
+    // the gather (the same corner_wt the gather would recompute), 16 B stores
+    int32_t kk[8], vv[8];
+    T ww[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
         int32_t node = static_cast<int32_t>(n);  // sentinel: sorts after every node
+        T wt = T(0);
         if (k < ncorner) {
             const int cx = k & 1, cy = (k >> 1) & 1, cz = k >> 2;
             node = static_cast<int32_t>(c.base + cx * c.sx + cy * c.sy + cz * c.sz);
+            wt = corner_wt(c, k);
         }
-        keys[8 * i + k] = node;
-        vals[8 * i + k] = static_cast<int32_t>(8 * i + k);
+        kk[k] = node;
+        vv[k] = static_cast<int32_t>(8 * i + k);
+        ww[k] = wt;
     }
+    int4* k4 = reinterpret_cast<int4*>(keys + 8 * i);
+    int4* v4 = reinterpret_cast<int4*>(vals + 8 * i);
+    k4[0] = make_int4(kk[0], kk[1], kk[2], kk[3]);
+    k4[1] = make_int4(kk[4], kk[5], kk[6], kk[7]);
+    v4[0] = make_int4(vv[0], vv[1], vv[2], vv[3]);
+    v4[1] = make_int4(vv[4], vv[5], vv[6], vv[7]);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) wts[8 * i + k] = ww[k];
 }
 
 // segment start of every node q in [0, n]: start[q] = first j with key[j] >= q
@@ -120,8 +135,8 @@ __global__ void k_svf_offsets(const int32_t* __restrict__ keys, int64_t m, int32
 
 // term (c) as a gather: node q adds wt * w[i] of its contributors in voxel order
 template <class T>
-__global__ void k_svf_gather(const T* __restrict__ uk, const T* __restrict__ w, Dims d,
-                             const int32_t* __restrict__ vals, const int32_t* __restrict__ start,
+__global__ void k_svf_gather(const T* __restrict__ w, Dims d, const int32_t* __restrict__ vals,
+                             const T* __restrict__ wts, const int32_t* __restrict__ start,
                              T* __restrict__ wn, const LoopState* st) {
     if (st && st->done) return;
     const int64_t q = blockIdx.x * static_cast<int64_t>(kNS) + threadIdx.x;
@@ -133,11 +148,7 @@ __global__ void k_svf_gather(const T* __restrict__ uk, const T* __restrict__ w, 
     for (int32_t j = j0; j < j1; ++j) {
         const int32_t v = vals[j];
         const int64_t i = v >> 3;
-        int x, y, z;
-        voxel_of(d, i, x, y, z);
-        const Cell3<T> c =
-            locate3<T>(d, x, y, z, uk[i], uk[n + i], three ? uk[2 * n + i] : T(0));
-        const T wt = corner_wt(c, v & 7);
+        const T wt = wts[v];      // corner_wt of pair v, stored by k_svf_jt
         if (wt == T(0)) continue;  // diffeo.cpp:147-148
         acc[0] += wt * w[i];
         acc[1] += wt * w[n + i];
@@ -190,7 +201,8 @@ void launch_svf_pullback(const Launch& L, const T* levels, Dims d, int M, const 
     for (int k = M - 1; k >= 0; --k) {
         const T* uk = levels + k * n3;
         T* wn = bufs[k & 1];
-        k_svf_jt<T><<<grid_n(n), kNS, 0, L.stream>>>(uk, w, d, wn, ws.keys[0], ws.vals[0], st);
+        k_svf_jt<T><<<grid_n(n), kNS, 0, L.stream>>>(uk, w, d, wn, ws.keys[0], ws.vals[0], ws.wts,
+                                                    st);
         L.bump();
         size_t tb = ws.temp_bytes;
         cub::DeviceRadixSort::SortPairs(ws.temp, tb, ws.keys[0], ws.keys[1], ws.vals[0],
@@ -199,7 +211,8 @@ void launch_svf_pullback(const Launch& L, const T* levels, Dims d, int M, const 
         k_svf_offsets<<<grid_n(m), kNS, 0, L.stream>>>(ws.keys[1], m, static_cast<int32_t>(n),
                                                        ws.start, st);
         L.bump();
-        k_svf_gather<T><<<grid_n(n), kNS, 0, L.stream>>>(uk, w, d, ws.vals[1], ws.start, wn, st);
+        k_svf_gather<T><<<grid_n(n), kNS, 0, L.stream>>>(w, d, ws.vals[1], ws.wts, ws.start, wn,
+                                                        st);
         L.bump();
         w = wn;
     }
