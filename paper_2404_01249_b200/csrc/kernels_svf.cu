@@ -9,11 +9,14 @@
 // where the scatter spreads w at voxel i onto the 8 corners of the cell its
 // sample x_i + u_k(x_i) fell in.  A float-atomic scatter would make the result
 // depend on thread timing; here the scatter is a deterministic GATHER instead:
-//   1. k_svf_jt writes, per voxel and corner, the pair (node, 8*i + corner);
-//   2. a stable radix sort by node (CUB) keeps each node's contributions in
-//      increasing voxel order, i.e. the reference's serial order;
-//   3. k_svf_offsets turns the sorted keys into per-node segment starts;
-//   4. k_svf_gather walks each node's segment in order and accumulates.
+//   1. k_svf_jt writes, per voxel, the pair (cell base node, voxel) and the
+//      lerp weights of its 8 corners;
+//   2. a stable radix sort by base (CUB) keeps each base's voxels in
+//      increasing order (n pairs, not 8n: the corners are base + fixed offsets);
+//   3. k_svf_offsets turns the sorted keys into per-base segment starts;
+//   4. k_svf_gather, for node q, merges the segments of the 8 bases q - off_k
+//      by voxel index (ties: corner order) — the reference's serial order —
+//      and accumulates.
 // Results are bit-stable run to run and the per-node summation order is the
 // reference's own.
 #include <cmath>
@@ -93,31 +96,11 @@ __global__ void k_svf_jt(const T* __restrict__ uk, const T* __restrict__ w, Dims
         wn[a * n + i] = wi[a] + acc;
     }
     const int ncorner = three ? 8 : 4;
-    // pair 8i+k: (node, pair id) for the sort, and the corner's lerp weight for
-    // the gather (the same corner_wt the gather would recompute), 16 B stores
-    int32_t kk[8], vv[8];
-    T ww[8];
+    // (cell base, voxel) for the sort; the corners' lerp weights for the gather
+    keys[i] = static_cast<int32_t>(c.base);
+    vals[i] = static_cast<int32_t>(i);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        int32_t node = static_cast<int32_t>(n);  // sentinel: sorts after every node
-        T wt = T(0);
-        if (k < ncorner) {
-            const int cx = k & 1, cy = (k >> 1) & 1, cz = k >> 2;
-            node = static_cast<int32_t>(c.base + cx * c.sx + cy * c.sy + cz * c.sz);
-            wt = corner_wt(c, k);
-        }
-        kk[k] = node;
-        vv[k] = static_cast<int32_t>(8 * i + k);
-        ww[k] = wt;
-    }
-    int4* k4 = reinterpret_cast<int4*>(keys + 8 * i);
-    int4* v4 = reinterpret_cast<int4*>(vals + 8 * i);
-    k4[0] = make_int4(kk[0], kk[1], kk[2], kk[3]);
-    k4[1] = make_int4(kk[4], kk[5], kk[6], kk[7]);
-    v4[0] = make_int4(vv[0], vv[1], vv[2], vv[3]);
-    v4[1] = make_int4(vv[4], vv[5], vv[6], vv[7]);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) wts[8 * i + k] = ww[k];
+    for (int k = 0; k < 8; ++k) wts[8 * i + k] = k < ncorner ? corner_wt(c, k) : T(0);
 }
 
 // segment start of every node q in [0, n]: start[q] = first j with key[j] >= q
@@ -133,7 +116,12 @@ __global__ void k_svf_offsets(const int32_t* __restrict__ keys, int64_t m, int32
         for (int32_t q = key + 1; q <= n; ++q) start[q] = static_cast<int32_t>(m);
 }
 
-// term (c) as a gather: node q adds wt * w[i] of its contributors in voxel order
+// term (c) as a gather: node q adds wt * w[i] of its contributors in voxel
+// order.  Voxel i contributes to q through corner k when its cell base is
+// q - off_k; the voxels of each base are consecutive in the sorted pairs, in
+// increasing order, so node q merges the (usually one-element) segments of its
+// 8 candidate bases by voxel index, ties in corner order (flat axes make
+// corners coincide) — exactly the order of the serial scatter.
 template <class T>
 __global__ void k_svf_gather(const T* __restrict__ w, Dims d, const int32_t* __restrict__ vals,
                              const T* __restrict__ wts, const int32_t* __restrict__ start,
@@ -143,12 +131,38 @@ __global__ void k_svf_gather(const T* __restrict__ w, Dims d, const int32_t* __r
     if (q >= d.n) return;
     const int64_t n = d.n;
     const bool three = d.ndim == 3;
+    const int sx = d.nx > 1 ? 1 : 0, sy = d.ny > 1 ? d.nx : 0;
+    const int sz = three ? d.nx * d.ny : 0;
+    const int ncorner = three ? 8 : 4;
+    int lo[8], hi[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int cx = k & 1, cy = (k >> 1) & 1, cz = k >> 2;
+        const int64_t b = q - (cx * sx + cy * sy + cz * sz);
+        lo[k] = hi[k] = 0;
+        if (k < ncorner && b >= 0) {
+            lo[k] = start[b];
+            hi[k] = start[b + 1];
+        }
+    }
     T acc[3] = {wn[q], wn[n + q], three ? wn[2 * n + q] : T(0)};
-    const int32_t j0 = start[q], j1 = start[q + 1];
-    for (int32_t j = j0; j < j1; ++j) {
-        const int32_t v = vals[j];
-        const int64_t i = v >> 3;
-        const T wt = wts[v];      // corner_wt of pair v, stored by k_svf_jt
+    for (;;) {
+        int bk = -1;
+        int32_t best = 0x7fffffff;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (lo[k] < hi[k]) {
+                const int32_t vi = vals[lo[k]];
+                if (vi < best) {  // strict: ties keep the lower corner
+                    best = vi;
+                    bk = k;
+                }
+            }
+        if (bk < 0) break;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) lo[k] += (k == bk);
+        const int64_t i = best;
+        const T wt = wts[8 * i + bk];
         if (wt == T(0)) continue;  // diffeo.cpp:147-148
         acc[0] += wt * w[i];
         acc[1] += wt * w[n + i];
@@ -195,7 +209,7 @@ void launch_exp_map(const Launch& L, const T* v, Dims d, int M, T* levels, const
 template <class T>
 void launch_svf_pullback(const Launch& L, const T* levels, Dims d, int M, const T* grad_phi,
                          T* out, const SvfWork<T>& ws, const LoopState* st) {
-    const int64_t n = d.n, n3 = 3 * n, m = 8 * n;
+    const int64_t n = d.n, n3 = 3 * n, m = n;  // one (base, voxel) pair per voxel
     const T* w = grad_phi;
     T* bufs[2] = {ws.wa, ws.wb};
     for (int k = M - 1; k >= 0; --k) {
