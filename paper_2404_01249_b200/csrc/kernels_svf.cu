@@ -112,8 +112,15 @@ __global__ void k_svf_offsets(const int32_t* __restrict__ keys, int64_t m, int32
     const int32_t key = keys[j];
     const int32_t prev = j == 0 ? -1 : keys[j - 1];
     for (int32_t q = prev + 1; q <= key && q <= n; ++q) start[q] = static_cast<int32_t>(j);
-    if (j == m - 1)
-        for (int32_t q = key + 1; q <= n; ++q) start[q] = static_cast<int32_t>(m);
+    // nodes past the last key keep the value k_svf_fill set (m): the tail after
+    // the last cell base spans a whole plane, too long for one thread
+}
+
+__global__ void k_svf_fill(int32_t* __restrict__ start, int64_t count, int32_t v,
+                           const LoopState* st) {
+    if (st && st->done) return;
+    const int64_t q = blockIdx.x * static_cast<int64_t>(kNS) + threadIdx.x;
+    if (q < count) start[q] = v;
 }
 
 // term (c) as a gather: node q adds wt * w[i] of its contributors in voxel
@@ -222,6 +229,9 @@ void launch_svf_pullback(const Launch& L, const T* levels, Dims d, int M, const 
         cub::DeviceRadixSort::SortPairs(ws.temp, tb, ws.keys[0], ws.keys[1], ws.vals[0],
                                         ws.vals[1], static_cast<int>(m), 0, key_bits(n),
                                         L.stream);  // library kernels: not counted
+        k_svf_fill<<<grid_n(n + 1), kNS, 0, L.stream>>>(ws.start, n + 1,
+                                                        static_cast<int32_t>(m), st);
+        L.bump();
         k_svf_offsets<<<grid_n(m), kNS, 0, L.stream>>>(ws.keys[1], m, static_cast<int32_t>(n),
                                                        ws.start, st);
         L.bump();
