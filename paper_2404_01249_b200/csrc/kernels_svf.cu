@@ -204,12 +204,19 @@ void launch_exp_map(const Launch& L, const T* v, Dims d, int M, T* levels, const
     const T s = static_cast<T>(std::ldexp(1.0, -M));
     k_scale3<T><<<grid_n(n3), kNS, 0, L.stream>>>(v, levels, n3, s, st);
     L.bump();
+    // self-composition u <- u + u(x + u); 3-D grids without flat axes take the
+    // loop's pointwise compose (one clamped cell search, 24 gathers, fma form)
+    const bool fast3 = d.ndim == 3 && d.nx > 1 && d.ny > 1 && d.nz > 1 && d.zoff == 0 &&
+                       d.gnz == 0;
     for (int k = 0; k < M; ++k) {
         const T* a = levels + k * n3;
         T* b = levels + (k + 1) * n3;
-        launch_compose<T>(L, CPlanes3<T>{{a, a + d.n, a + 2 * d.n}},
-                          CPlanes3<T>{{a, a + d.n, a + 2 * d.n}}, d,
-                          Planes3<T>{{b, b + d.n, b + 2 * d.n}});
+        if (fast3)
+            launch_compose_pointwise<T>(L, a, a, 1e30, d, b, nullptr);
+        else
+            launch_compose<T>(L, CPlanes3<T>{{a, a + d.n, a + 2 * d.n}},
+                              CPlanes3<T>{{a, a + d.n, a + 2 * d.n}}, d,
+                              Planes3<T>{{b, b + d.n, b + 2 * d.n}});
     }
 }
 
