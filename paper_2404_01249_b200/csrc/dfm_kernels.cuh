@@ -196,6 +196,11 @@ template <class T>
 void launch_compose_smooth(const Launch& L, int R, const GaussW<T>& w, CPlanes3<T> step,
                            CPlanes3<T> u_in, Planes3<T> u_out, Dims d, LoopState* st);
 // plain fused Gaussian (gaussian_smooth / gaussian_smooth_field), ncomp 1..3
+// SVF update v' = G * (v + step) on the TMA z-march (3-D; < 0: not eligible)
+template <class T>
+int launch_svf_update_tma(const Launch& L, int R, const GaussW<T>& w, const T* v, const T* step,
+                          T* out, Dims d, LoopState* st);
+
 // one-component Gaussian on the TMA z-march (3-D; < 0: not eligible)
 template <class T>
 int launch_gauss_tma(const Launch& L, int R, const GaussW<T>& w, const T* in, T* out, Dims d);

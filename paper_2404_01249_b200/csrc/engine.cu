@@ -1899,7 +1899,10 @@ struct Registrar {
                                   d, ap, st, maxstep);
         ev_end();
         ev_begin(KC_COMPOSE);
-        launch_svf_update<T>(L, big_w ? 0 : Rw, ww, u[src].r(), step.r(), u[1 - src].w(), d, st);
+        if (!tma || big_w ||
+            launch_svf_update_tma<T>(L, Rw, ww, u[src].p[0], step.p[0], u[1 - src].p[0], d, st) < 0)
+            launch_svf_update<T>(L, big_w ? 0 : Rw, ww, u[src].r(), step.r(), u[1 - src].w(), d,
+                                 st);
         if (big_w)
             for (int c = 0; c < 3; ++c)
                 axis_smooth_plane<T>(ctx, d, *big_w, u[1 - src].p[c], u[1 - src].p[c], grad.p[c],

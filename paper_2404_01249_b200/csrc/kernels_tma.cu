@@ -1572,6 +1572,72 @@ struct Gauss2 {
     __device__ void finish(int, double, double, const Prol&) const {}
 };
 
+// pipeline.cpp:199-205 — the SVF update v' = G_sigma_warp * (v + step) (the
+// generic z-march SvfUpdateOp's arithmetic: sum per element, then the three
+// normalised passes) with TMA-fed planes; one counted update per launch
+template <class T, int R_, int TY_ = 8>
+struct SvfUpdate2 {
+    using Acc = T;
+    using Center = NoCenter;
+    using Prol = NoProl;
+    using Carry = NoCarry;
+    static constexpr int R = R_, C = 3, BACK = 0, AHEAD = 0, S = 4, TYv = TY_;
+    static constexpr int kMinB = 2, kCY = 1;
+    static constexpr bool kStaged = false, kSum = false, kMax = false;
+    static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TYv + 2 * R;
+    static constexpr int kBytes = BX * BY * int(sizeof(T));
+    static constexpr int kBox = align128(kBytes);
+    static constexpr int kStageBytes = 6 * kBox;  // v (3 components), step (3)
+    CUtensorMap mV, mS;
+    GaussW<T> w;
+    T* out[3];
+    LoopState* st;
+    Dims d;
+
+    __device__ bool skip() const { return st && st->done; }
+    __device__ void prefetch_maps() const {
+        prefetch_tmap(&mV);
+        prefetch_tmap(&mS);
+    }
+    __device__ void issue(unsigned char* dst, uint64_t* bar, int x0, int y0, int q) const {
+        mbar_expect_tx(bar, 6 * kBytes);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            tma_load_4d(dst + k * kBox, &mV, bar, x0 - XA, y0 - R, q, k);
+            tma_load_4d(dst + (3 + k) * kBox, &mS, bar, x0 - XA, y0 - R, q, k);
+        }
+    }
+    __device__ Acc wgt(int a, int j) const { return w.taps[a][j]; }
+    __device__ Acc nrm(int a, int i) const {
+        return w.nrm(a, i, a == 0 ? d.nx : (a == 1 ? d.ny : d.gz()));
+    }
+    __device__ Prol prologue() const { return {}; }
+    __device__ void xpass(const unsigned char* st_, int row, int col, Acc nx, Acc v[3]) const {
+        const T* p = reinterpret_cast<const T*>(st_) + row * BX + col + (XA - R);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const T* pv = p + c * (kBox / int(sizeof(T)));
+            const T* ps = p + (3 + c) * (kBox / int(sizeof(T)));
+            T a = T(0);
+#pragma unroll
+            for (int j = 0; j < 2 * R + 1; ++j) a += w.taps[0][j] * (pv[j] + ps[j]);
+            v[c] = a * nx;
+        }
+    }
+    __device__ void load_center(int, int, int, Center&) const {}
+    __device__ Red2 emit(int x, int y, int z, const T s[3], const Center&, const Prol&,
+                         Carry&) const {
+        const int i = d.idx32(x, y, z);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) out[c][i] = s[c];
+        return {0.0, 0.0};
+    }
+    __device__ void flush(Carry&) const {}
+    __device__ void finish(int, double, double, const Prol&) const {
+        if (st) st->nupdates += 1;
+    }
+};
+
 // W = M(x+u), G = grad M(x+u) (similarity.cpp:25-45) at scale start / epilogue
 template <class T>
 __global__ void k_warpgrad(const T* __restrict__ M, Dims dm, CPlanes3<T> u, Dims d,
@@ -1997,6 +2063,25 @@ int go_compose_smooth(const Launch& L, const GaussW<T>& w, const T* c, T* uout, 
 }
 
 template <class T>
+int launch_svf_update_tma(const Launch& L, int R, const GaussW<T>& w, const T* v, const T* step,
+                          T* out, Dims d, LoopState* st) {
+    if (d.ndim != 3) return -2;
+    return with_r<0, 4>(R, [&](auto rc) {
+        constexpr int RR = decltype(rc)::value;
+        using Op = SvfUpdate2<T, RR>;
+        Op op;
+        if (!make_map<T>(&op.mV, v, d, 3, Op::BX, Op::BY) ||
+            !make_map<T>(&op.mS, step, d, 3, Op::BX, Op::BY))
+            return -1;
+        op.w = w;
+        for (int k = 0; k < 3; ++k) op.out[k] = out + k * d.n;
+        op.st = st;
+        op.d = d;
+        return run_zm2(L, op, d);
+    });
+}
+
+template <class T>
 int launch_gauss_tma(const Launch& L, int R, const GaussW<T>& w, const T* in, T* out, Dims d) {
     if (d.ndim != 3) return -2;
     return with_r<1, 6>(R, [&](auto rc) {
@@ -2036,6 +2121,8 @@ void launch_warpgrad(const Launch& L, const T* M, Dims dm, CPlanes3<T> u, Dims d
                                        LoopState*, bool);                                      \
     template void launch_warpgrad<T>(const Launch&, const T*, Dims, CPlanes3<T>, Dims, T*, T*); \
     template int launch_gauss_tma<T>(const Launch&, int, const GaussW<T>&, const T*, T*, Dims); \
+    template int launch_svf_update_tma<T>(const Launch&, int, const GaussW<T>&, const T*,       \
+                                          const T*, T*, Dims, LoopState*);                      \
     template int launch_smooth_adam_compose_tma<T>(const Launch&, int, const GaussW<T>&,        \
                                                    const T*, T*, T*, const T*, T*, double,     \
                                                    Dims, AdamParams, LoopState*,               \
