@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--config", type=int, default=1, choices=[0, 1, 3])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-f64", action="store_true",
+                    help="skip the fp64 (parity-mode) sub-record")
     ap.add_argument("--pairs-per-gpu", type=int, default=1,
                     help="config-2 style batch: K concurrent pairs per GPU, one context "
                          "(stream) and host thread each; value = aggregate voxel-iter/s")
@@ -190,9 +192,31 @@ def hbm_peak():
         return FALLBACK_HBM, "fallback"
 
 
-def cpu_leg(pair, kind_pref="reference", sample_iters=(8, 4, 2)):
-    """Times the reference CPU path (oracle/_ref, else the C restatement) on a
-    bounded sample of the same workload; returns the cpu_baseline dict."""
+def cpu_model_name() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return "unknown"
+
+
+SAMPLE_ITERS = (8, 4, 2)
+
+
+def cpu_leg(pair, kind_pref="reference", sample_iters=SAMPLE_ITERS):
+    """The reference CPU path (oracle/_ref, else the C restatement) on all host
+    cores, reported for the SAME schedule as the GPU line: one bounded sample
+    registration (same pair, same scales, `sample_iters` iterations) gives
+    per-level per-iteration times (the reference's own IterationRecord.wall_ms,
+    pipeline.cpp:159-209, median per level) and the one-off work (pyramid,
+    level transitions, final full-resolution loss + fold check: RunLog.total_ms
+    minus the iterations, pipeline.cpp:140-153, 213-223); the full-schedule
+    time is one-offs + sum over levels of iterations x per-iteration time.
+    tools/cpu_model_check.py validates this model against real full-schedule
+    runs (profiles/r2_cpu_model_check_*.json)."""
     ncores = os.cpu_count() or 1
     os.environ["DIFFORM_THREADS"] = str(ncores)
     from oracle import pyoracle
@@ -200,47 +224,75 @@ def cpu_leg(pair, kind_pref="reference", sample_iters=(8, 4, 2)):
                                  pyoracle.reference_available()) else pyoracle.port()
     from paper_2404_01249_b200 import _abi as A
     sched = A.PyramidSchedule(pair.schedule.scales, sample_iters)
-    cfg = pair.config
     t0 = time.perf_counter()
-    o.register_images(pair.grid, pair.fixed, pair.moving, cfg, sched)
+    _, log = o.register_images(pair.grid, pair.fixed, pair.moving, pair.config, sched)
     dt = time.perf_counter() - t0
-
-    class _P:
-        pass
-    pp = _P()
-    pp.grid, pp.schedule = pair.grid, sched
-    vi = voxel_iters(pp)
-    return {"value": vi / dt, "unit": "voxel-iter/s",
+    per_level = []
+    for si in range(len(sched.scales)):
+        w = [r.wall_ms for r in log.iterations if r.scale_index == si]
+        per_level.append(float(np.median(w)) if w else 0.0)
+    oneoff_ms = log.total_ms - sum(r.wall_ms for r in log.iterations)
+    model_ms = oneoff_ms + sum(n * t for n, t in zip(pair.schedule.iterations, per_level))
+    vi = voxel_iters(pair)
+    return {"value": vi / (model_ms / 1e3), "unit": "voxel-iter/s",
             "cores": ncores if o.kind == "reference" else 1, "kind": o.kind,
-            "sample": (f"{pair.name}: one registration with the same scales and "
-                       f"{'/'.join(map(str, sample_iters))} iterations (incl. pyramid and "
-                       f"final full-res loss + fold check), {dt:.1f} s"),
-            "seconds": dt}
+            "cpu_model": cpu_model_name(),
+            "s_per_pair": model_ms / 1e3,
+            "per_level_iter_ms": per_level, "oneoff_ms": oneoff_ms,
+            "schedule": list(pair.schedule.iterations),
+            "sample": (f"{pair.name}: same-schedule model from one registration with the same "
+                       f"scales and {'/'.join(map(str, sample_iters))} iterations ({dt:.1f} s): "
+                       f"one-offs {oneoff_ms / 1e3:.2f} s + "
+                       + " + ".join(f"{n} x {t:.1f} ms" for n, t in
+                                    zip(pair.schedule.iterations, per_level))
+                       + f" = {model_ms / 1e3:.1f} s per pair"),
+            "sample_seconds": dt}
+
+
+def workload_config(pair, world):
+    """The `config` object both arms print (same workload, same keys)."""
+    from paper_2404_01249_b200 import _abi as A
+    cfg = pair.config
+    return {"workload": pair.name, "shape_xyz": list(pair.grid.dims),
+            "scales": list(pair.schedule.scales), "iterations": list(pair.schedule.iterations),
+            "loss": f"lncc r={cfg.lncc_radius}" if cfg.loss == A.LOSS_LNCC else "ssd",
+            "sigma_grad": cfg.sigma_grad, "sigma_warp": cfg.sigma_warp, "eta": cfg.eta,
+            "early_stop": "off (conv_window > max iterations)",
+            "pairs_per_step": world, "voxel_iters_per_pair": voxel_iters(pair),
+            "l2": "working set ~0.7 GB per pair >> 126 MB L2 (no flush needed)"}
 
 
 def run_reference_arm(args, rank, world):
+    """The reference's own CPU implementation (oracle/_ref: the unmodified
+    sources compiled in place) on rank 0 with every host core; other ranks
+    exit without work.  Each step = one bounded sample registration; value =
+    the same-schedule (200/100/50) rate of cpu_leg's model."""
     if rank != 0:
         return
     from paper_2404_01249_b200 import synth
     pair = synth.make_pair(args.config, seed=0)
-    vals = []
+    vals, secs, pairs_s = [], [], []
     cb = None
     for k in range(args.warmup + args.steps):
-        cb = cpu_leg(pair, "reference", (4, 2, 1) if k < args.warmup else (8, 4, 2))
+        t0 = time.perf_counter()
+        cb = cpu_leg(pair, "reference", (4, 2, 1) if k < args.warmup else SAMPLE_ITERS)
         if k >= args.warmup:
+            secs.append(time.perf_counter() - t0)
             vals.append(cb["value"])
+            pairs_s.append(cb["s_per_pair"])
     v = float(np.mean(vals))
     cb["value"] = v
-    s_pair_est = voxel_iters(pair) / v
+    cb["s_per_pair"] = float(np.mean(pairs_s))
     line = {"impl": "reference", "metric": "voxel-iterations/sec", "value": v,
-            "unit": "voxel-iter/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": s_pair_est * 1e3,
+            "unit": "voxel-iter/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": float(np.mean(secs)) * 1e3,
+            "s_per_pair": cb["s_per_pair"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (BASELINE config recipe, seeded)",
-            "config": {"workload": pair.name, "shape_xyz": list(pair.grid.dims),
-                       "schedule": list(pair.schedule.iterations),
-                       "note": "each step times a bounded sample (8/4/2 iterations); "
-                               "ms_per_step = full-schedule estimate at that rate"},
+            "config": workload_config(pair, world),
+            "note": ("each timed step is one bounded sample registration "
+                     f"({'/'.join(map(str, SAMPLE_ITERS))} iterations, ms_per_step is its wall "
+                     "time); value and s_per_pair are the same-schedule model (cpu_baseline)"),
             "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "voxel-iter/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -323,19 +375,41 @@ def run_batch(args, rank, world, local):
         print(json.dumps(line), flush=True)
 
 
+def spawn_ranks(args) -> int:
+    """`--gpus N` without a launcher: start N ranks (one per GPU) through
+    torch.distributed.run on 127.0.0.1 and return their exit code."""
+    if args.impl == "ours":
+        import torch
+        n = torch.cuda.device_count()
+        if n < args.gpus:
+            print(f"bench.py --gpus {args.gpus}: only {n} CUDA device(s) visible",
+                  file=sys.stderr)
+            return 2
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     rank, world, local = dist_env()
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
+    if args.impl == "reference":
+        # the reference is a CPU library: rank 0 alone runs, the others exit
+        run_reference_arm(args, rank, world)
+        return
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
-    if args.impl == "reference":
-        run_reference_arm(args, rank, world)
-        if world > 1:
-            import torch.distributed as dist
-            dist.barrier()
-            dist.destroy_process_group()
-        return
+        dist.init_process_group("nccl")
 
     import torch
     torch.cuda.set_device(local)
@@ -471,12 +545,52 @@ def main():
             except (OSError, ValueError):
                 pass
 
+    # ---- parity-mode (fp64 context) time of the same pair, device-timed
+    f64 = None
+    if args.precision == "f32" and not args.no_f64:
+        ctx64 = Context(local, "f64")
+        F64, M64 = F.double(), M.double()
+        o64 = torch.empty((3,) + g.shape, dtype=torch.float64, device=f"cuda:{local}")
+        s64 = torch.cuda.ExternalStream(ctx64.stream_ptr, device=f"cuda:{local}")
+
+        def step64():
+            return ctx64.register_device(g, F64.data_ptr(), M64.data_ptr(), cfg, sched,
+                                         o64.data_ptr())
+        step64()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n64 = max(1, min(args.steps, 5))
+        a.record(s64)
+        for _ in range(n64):
+            log64 = step64()
+        b.record(s64)
+        torch.cuda.synchronize()
+        ms64 = a.elapsed_time(b) / n64
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([ms64], device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms64 = float(t.item())
+        f64 = {"value": world * vi / (ms64 / 1e3), "unit": "voxel-iter/s", "ms_per_step": ms64,
+               "steps": n64, "dtype": "f64", "final_loss": log64.final_loss,
+               "note": "fp64 context (parity mode), same pair and schedule, device-resident"}
+        ctx64.close()
+
+    # ---- CPU reference beside it (rank 0; the other ranks wait on a gloo
+    # barrier, which sleeps in a socket read instead of spinning a core)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    cpu_group = None
+    if world > 1:
+        import torch.distributed as dist
+        cpu_group = dist.new_group(backend="gloo")
+    if rank == 0 and not args.no_cpu_baseline:
         try:
             cpu = cpu_leg(pair)
         except Exception as e:  # keep the GPU line even if the checker is missing
             cpu = {"error": str(e)}
+    if cpu_group is not None:
+        import torch.distributed as dist
+        dist.barrier(group=cpu_group)
 
     if rank == 0:
         line = {"metric": "voxel-iterations/sec", "value": value, "unit": "voxel-iter/s",
@@ -485,15 +599,10 @@ def main():
                 "scaling": "weak", "vs_baseline": None,
                 "dtype": "f32" if args.precision == "f32" else "f64",
                 "data": "synthetic (BASELINE config recipe, seeded per pair)",
-                "config": {"workload": pair.name, "shape_xyz": list(g.dims),
-                           "scales": list(sched.scales), "iterations": list(sched.iterations),
-                           "loss": "lncc r=2" if cfg.loss == A.LOSS_LNCC else "ssd",
-                           "early_stop": "off (conv_window > max iterations)",
-                           "pairs_per_step": world, "voxel_iters_per_pair": vi,
-                           "l2": "working set ~0.7 GB per pair >> 126 MB L2 (no flush needed)"},
+                "config": workload_config(pair, world),
                 "gpu_launches": launches,
                 "final_loss": log.final_loss,
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk}
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "f64": f64}
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:

@@ -185,6 +185,12 @@ DFM_API dfm_status dfm_downsample_image(dfm_ctx* ctx, const dfm_grid* g, const d
 DFM_API dfm_status dfm_sample_linear_points(dfm_ctx* ctx, const dfm_grid* g, const double* img,
                                     int64_t npts, const double* points, double* values,
                                     double* grads);
+/* sample_field + sample_field_jacobian (interp.hpp:18-24, interp.cpp:188-227)
+ * of an AoS field at npts points (xyz triples): values 3 per point (ndim
+ * used), jac 9 per point row-major J[c][a] = d f_c / d x_a (may be NULL). */
+DFM_API dfm_status dfm_sample_field_points(dfm_ctx* ctx, const dfm_grid* g, const double* field,
+                                           int64_t npts, const double* points, double* values,
+                                           double* jac);
 /* warp_image (interp.hpp:28) */
 DFM_API dfm_status dfm_warp_image(dfm_ctx* ctx, const dfm_grid* g, const double* img,
                           const double* phi, double* out);
@@ -224,6 +230,9 @@ DFM_API dfm_status dfm_exp_map(dfm_ctx* ctx, const dfm_grid* g, const double* v,
  * bit-stable across runs.  Needs 8 * voxels < 2^31. */
 DFM_API dfm_status dfm_svf_pullback(dfm_ctx* ctx, const dfm_grid* g, const double* v,
                                     const double* grad_phi, int M, double* out);
+/* jacobian (interp.hpp:49, interp.cpp:291-328): per-voxel J = I + central
+ * differences, ndim*ndim row-major doubles per voxel. */
+DFM_API dfm_status dfm_jacobian(dfm_ctx* ctx, const dfm_grid* g, const double* phi, double* out);
 /* jacobian_det (interp.hpp:50) */
 DFM_API dfm_status dfm_jacobian_det(dfm_ctx* ctx, const dfm_grid* g, const double* phi, double* out);
 /* gaussian_smooth / gaussian_smooth_field (interp.hpp:54-57) */
@@ -235,6 +244,10 @@ DFM_API dfm_status dfm_gaussian_smooth_field(dfm_ctx* ctx, const dfm_grid* g, co
  * (interp.hpp:65-75) */
 DFM_API dfm_status dfm_upsample_field(dfm_ctx* ctx, const dfm_grid* g, const double* phi,
                               const dfm_grid* new_grid, double* out);
+/* upsample_field with UpsampleMethod::cubic (interp.hpp:65-67,
+ * interp.cpp:59-101): Catmull-Rom, the reference's folding demonstration. */
+DFM_API dfm_status dfm_upsample_field_cubic(dfm_ctx* ctx, const dfm_grid* g, const double* phi,
+                                            const dfm_grid* new_grid, double* out);
 DFM_API dfm_status dfm_resample_field_linear(dfm_ctx* ctx, const dfm_grid* g, const double* f,
                                      const dfm_grid* new_grid, double* out);
 DFM_API dfm_status dfm_resample_displacement(dfm_ctx* ctx, const dfm_grid* g, const double* phi,
@@ -259,6 +272,10 @@ DFM_API dfm_status dfm_dice_eval(dfm_ctx* ctx, const dfm_grid* fixed_grid, const
 DFM_API dfm_status dfm_adam_step(dfm_ctx* ctx, const dfm_grid* g, double* m, double* nu,
                          int64_t* t, double beta1, double beta2, double eps,
                          const double* v, double* dir);
+/* sgd_step (optim.hpp:27-29, optim.cpp:44-57): momentum 0 returns v and
+ * leaves mu; otherwise mu <- momentum*mu + v (in place) and out = mu. */
+DFM_API dfm_status dfm_sgd_step(dfm_ctx* ctx, const dfm_grid* g, double* mu, const double* v,
+                                double momentum, double* out);
 /* upsample_state (optim.hpp:31) */
 DFM_API dfm_status dfm_upsample_state(dfm_ctx* ctx, const dfm_grid* g, const double* m,
                               const double* nu, const dfm_grid* new_grid, double* m_out,
@@ -279,6 +296,11 @@ DFM_API dfm_status dfm_singularity_fraction(dfm_ctx* ctx, const dfm_grid* g, con
                                     double* fraction);
 
 /* ---- pipeline.hpp ------------------------------------------------------ */
+/* validate_config / validate_schedule (pipeline.hpp:21,43, pipeline.cpp:83-119):
+ * DFM_E_INVALID with the reference's message. */
+DFM_API dfm_status dfm_validate_config(const dfm_config* cfg);
+DFM_API dfm_status dfm_validate_schedule(const double* scales, const int32_t* iterations,
+                                         int32_t nscales);
 /* register_images, direct mode (pipeline.hpp:70-73, pipeline.cpp:121-224).
  * fixed/moving: host arrays of `image_dtype` (dfm_host_dtype) on grid g.
  * out_field: host AoS array of `field_dtype` (voxel_count*ndim) or NULL.
@@ -462,7 +484,24 @@ DFM_API dfm_status dfm_ctx_kernel_times(const dfm_ctx* ctx, double* ms, int64_t*
  * 2000000).  Both give bit-identical fields.  Env DFM_SPLIT, DFM_SPLIT_FOLD_MAX. */
 #define DFM_OPT_SPLIT 5
 #define DFM_OPT_SPLIT_FOLD_MAX 6
+/* DFM_OPT_LARGE_MIN: pyramid levels with at least this many voxels run the
+ * large-level kernel variants (fp32 two-row smooth+Adam, compose-smooth with
+ * the cp.async-carried W/G gather); default 2000000.  Lowering it lets the
+ * parity tests run those variants at sizes the oracle finishes quickly. */
+#define DFM_OPT_LARGE_MIN 7
 DFM_API dfm_status dfm_ctx_set_option(dfm_ctx* ctx, int key, int64_t value);
+
+/* White-box read of a named device workspace buffer of the context after a
+ * call (the parity tests compare the hot loop's per-kernel intermediates —
+ * Adam moments, capped step, composed field, W/G — with the oracle at the
+ * benchmarked size; no reference counterpart).  Copies `bytes` bytes from
+ * byte `offset` of buffer `name` into `host`; DFM_E_INVALID when the buffer
+ * does not exist or is smaller.  Buffers of register_images after a
+ * single-scale run: "reg_u0"/"reg_u1" (ping-pong displacement, 3 planes),
+ * "reg_m", "reg_nu", "reg_step", "reg_grad" (holds the composed c of the
+ * split update), "reg_W", "reg_G" (3 planes), in the context precision. */
+DFM_API dfm_status dfm_ctx_debug_read(dfm_ctx* ctx, const char* name, size_t offset,
+                                      size_t bytes, void* host);
 
 #ifdef __cplusplus
 }

@@ -26,13 +26,14 @@ from paper_2404_01249_b200 import _abi as A
 HERE = os.path.dirname(os.path.abspath(__file__))
 PORT_SO = os.path.join(HERE, "_build", "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libdifform_ref.so")
+REF_FMA_SO = os.path.join(HERE, "_ref", "libdifform_ref_fma.so")
 
 
 def build(ref: bool = True) -> None:
     """Builds the restatement and, when /root/reference exists, the reference."""
     targets = ["port"]
     if ref and os.path.isdir("/root/reference/proj/src"):
-        targets.append("ref")
+        targets += ["ref", "ref-fma"]
     subprocess.check_call(["make", "-s", "-C", HERE] + targets)
 
 
@@ -108,6 +109,17 @@ def reference() -> Oracle:
             raise FileNotFoundError(f"{REF_SO} not built (needs /root/reference at build time)")
         _cache["ref"] = Oracle(REF_SO, "dfmref_", "reference")
     return _cache["ref"]
+
+
+def reference_fma() -> Oracle:
+    """The same unmodified reference built with FMA contraction: a rounding
+    change of the reference itself (its divergence from reference() is the
+    conditioning envelope of the chaotic LNCC loop)."""
+    if "ref_fma" not in _cache:
+        if not os.path.exists(REF_FMA_SO):
+            raise FileNotFoundError(f"{REF_FMA_SO} not built (make -C oracle ref-fma)")
+        _cache["ref_fma"] = Oracle(REF_FMA_SO, "dfmref_", "reference-fma")
+    return _cache["ref_fma"]
 
 
 def best() -> Oracle:

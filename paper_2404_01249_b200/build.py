@@ -21,6 +21,9 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "libdifform_cuda.so")
+CPP_LIB = os.path.join(PKG, "libdifform_b200.so")
+CPP_SRC = os.path.join(PKG, "cpp", "difform_b200.cpp")
+REF_INCLUDE = "/root/reference/proj/include"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden",
@@ -59,7 +62,32 @@ def build(force: bool = False, verbose: bool = True) -> str:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     if verbose:
         print(f"built {LIB}", file=sys.stderr)
+    build_cpp(force, verbose)
     return LIB
+
+
+def build_cpp(force: bool = False, verbose: bool = True) -> None:
+    """The C++ drop-in (cpp/difform_b200.cpp -> libdifform_b200.so): the
+    reference's API compiled against the reference's own headers, so it is
+    built where /root/reference exists (this container); the built .so
+    travels with the repo like libdifform_cuda.so."""
+    if not os.path.isdir(REF_INCLUDE):
+        if verbose:
+            print(f"{REF_INCLUDE} absent: keeping the prebuilt {CPP_LIB}", file=sys.stderr)
+        return
+    deps = [CPP_SRC, LIB, os.path.join(ROOT, "include", "difform_b200.hpp"),
+            os.path.join(ROOT, "include", "difform_gpu.h")]
+    if (not force and os.path.exists(CPP_LIB)
+            and os.path.getmtime(CPP_LIB) >= max(map(os.path.getmtime, deps))):
+        return
+    cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra", "-include",
+           "algorithm", "-I" + REF_INCLUDE, "-I" + os.path.join(ROOT, "include"), CPP_SRC,
+           "-o", CPP_LIB, "-L" + PKG, "-ldifform_cuda", "-Wl,-rpath,$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"g++ failed for {CPP_SRC}:\n{r.stdout}\n{r.stderr}")
+    if verbose:
+        print(f"built {CPP_LIB}", file=sys.stderr)
 
 
 if __name__ == "__main__":

@@ -74,6 +74,10 @@ struct Launch {
     int64_t* counter;  // incremented per kernel launch (host side)
     int num_sms;
     bool pdl = false;  // launch the loop kernels with programmatic dependent launch
+    // levels with at least this many voxels take the large-level kernel variants
+    // (two-row fp32 smooth+Adam, cp.async-carried compose-smooth gather);
+    // DFM_OPT_LARGE_MIN lowers it so the tests reach those variants at any size
+    int64_t large_min = 2000000;
     void bump() const {
         if (counter) ++*counter;
     }
@@ -137,6 +141,13 @@ void launch_warp_labels(const Launch& L, const int32_t* lab, CPlanes3<T> u, Dims
                         int32_t* out);
 template <class T>
 void launch_compose(const Launch& L, CPlanes3<T> phi, CPlanes3<T> psi, Dims d, Planes3<T> out);
+template <class T>
+void launch_jacobian_full(const Launch& L, CPlanes3<T> u, Dims d, T* out);
+template <class T>
+void launch_upsample_cubic(const Launch& L, CPlanes3<T> f, Dims ds, Planes3<T> out, Dims dd,
+                           const double step[3], const double rescale[3]);
+template <class T>
+void launch_sgd(const Launch& L, Planes3<T> mu, CPlanes3<T> v, Dims d, double momentum);
 template <class T>
 void launch_jacobian_det(const Launch& L, CPlanes3<T> u, Dims d, T* det,
                          unsigned long long* nonpos);

@@ -118,7 +118,9 @@ struct dfm_ctx {
     // ones run it as its own radius-0 streaming kernel
     int64_t split_fold_max = getenv("DFM_SPLIT_FOLD_MAX") ? atoll(getenv("DFM_SPLIT_FOLD_MAX"))
                                                           : 2000000;
-    Launch L() { return Launch{stream, &launches, num_sms, pdl}; }
+    // large-level kernel variants from this many voxels (DFM_OPT_LARGE_MIN)
+    int64_t large_min = 2000000;
+    Launch L() { return Launch{stream, &launches, num_sms, pdl, large_min}; }
 
     LoopState* pinned_state() {
         if (!hstate) {
@@ -658,9 +660,27 @@ dfm_status dfm_ctx_set_option(dfm_ctx* ctx, int key, int64_t value) {
         } else if (key == DFM_OPT_SPLIT_FOLD_MAX) {
             if (value < 0) fail(DFM_E_INVALID, "split_fold_max must be >= 0");
             ctx->split_fold_max = value;
+        } else if (key == DFM_OPT_LARGE_MIN) {
+            if (value < 0) fail(DFM_E_INVALID, "large_min must be >= 0");
+            ctx->large_min = value;
         } else {
             fail(DFM_E_INVALID, "unknown context option %d", key);
         }
+    });
+}
+
+dfm_status dfm_ctx_debug_read(dfm_ctx* ctx, const char* name, size_t offset, size_t bytes,
+                              void* host) {
+    return guarded([&] {
+        if (!ctx || !name || (!host && bytes)) fail(DFM_E_INVALID, "NULL argument");
+        auto it = ctx->bufs.find(name);
+        if (it == ctx->bufs.end()) fail(DFM_E_INVALID, "no workspace buffer '%s'", name);
+        if (offset + bytes > it->second.second)
+            fail(DFM_E_INVALID, "workspace buffer '%s' holds %zu bytes", name, it->second.second);
+        CK(cudaSetDevice(ctx->device));
+        ctx->sync();
+        CK(cudaMemcpy(host, static_cast<char*>(it->second.first) + offset, bytes,
+                      cudaMemcpyDeviceToHost));
     });
 }
 
@@ -679,6 +699,10 @@ dfm_status dfm_ctx_kernel_times(const dfm_ctx* ctx, double* ms, int64_t* launche
 dfm_status dfm_validate_grid(const dfm_grid* g) {
     return guarded([&] { validate_grid(g); });
 }
+
+dfm_status dfm_validate_config(const dfm_config* c);
+dfm_status dfm_validate_schedule(const double* scales, const int32_t* iterations,
+                                 int32_t nscales);
 
 dfm_status dfm_downsample_grid(const dfm_grid* g, const double factor[3], dfm_grid* out) {
     return guarded([&] { downsample_grid(g, factor, out); });
@@ -1223,6 +1247,115 @@ dfm_status dfm_jacobian_det(dfm_ctx* ctx, const dfm_grid* g, const double* phi, 
             launch_jacobian_det<T>(ctx->L(), a.r(), d, o, nullptr);
             download_image<T, double>(ctx, o, d.n, out);
             ctx->sync();
+        });
+    });
+}
+
+dfm_status dfm_jacobian(dfm_ctx* ctx, const dfm_grid* g, const double* phi, double* out) {
+    return guarded([&] {
+        validate_grid(g);
+        const Dims d = to_dims(g);
+        const int64_t nn = static_cast<int64_t>(d.ndim) * d.ndim;
+        DFM_DISPATCH(ctx, {
+            Field<T> a = dev_field<T>(ctx, "api_f0", d.n);
+            T* o = ctx->arr<T>("api_jac", nn * d.n);
+            upload_field<T>(ctx, phi, d.n, d.ndim, a);
+            launch_jacobian_full<T>(ctx->L(), a.r(), d, o);
+            download_image<T, double>(ctx, o, nn * d.n, out);
+            ctx->sync();
+        });
+    });
+}
+
+dfm_status dfm_upsample_field_cubic(dfm_ctx* ctx, const dfm_grid* g, const double* phi,
+                                    const dfm_grid* ng, double* out) {
+    return guarded([&] {
+        validate_grid(g);
+        validate_grid(ng);
+        if (ng->ndim != g->ndim) fail(DFM_E_INVALID, "upsample_field: dimensionality mismatch");
+        for (int a = 0; a < g->ndim; ++a)
+            if (ng->dims[a] < g->dims[a]) fail(DFM_E_INVALID, "upsample_field: shrinking not allowed");
+        const Dims d = to_dims(g), nd = to_dims(ng);
+        if (dims_equal(d, nd)) {
+            std::memmove(out, phi, sizeof(double) * d.n * d.ndim);
+            return;
+        }
+        double step[3] = {0.0, 0.0, 0.0}, rescale[3] = {1.0, 1.0, 1.0};
+        for (int a = 0; a < g->ndim; ++a) {
+            step[a] = static_cast<double>(g->dims[a] - 1) / static_cast<double>(ng->dims[a] - 1);
+            rescale[a] = static_cast<double>(ng->dims[a] - 1) / static_cast<double>(g->dims[a] - 1);
+        }
+        DFM_DISPATCH(ctx, {
+            Field<T> a = dev_field<T>(ctx, "api_f0", d.n);
+            Field<T> o = dev_field<T>(ctx, "api_f1", nd.n);
+            upload_field<T>(ctx, phi, d.n, d.ndim, a);
+            launch_upsample_cubic<T>(ctx->L(), a.r(), d, o.w(), nd, step, rescale);
+            download_field<T, double>(ctx, o.r(), nd.n, nd.ndim, out);
+            ctx->sync();
+        });
+    });
+}
+
+dfm_status dfm_sgd_step(dfm_ctx* ctx, const dfm_grid* g, double* mu, const double* v,
+                        double momentum, double* out) {
+    return guarded([&] {
+        validate_grid(g);
+        const Dims d = to_dims(g);
+        const size_t cnt = static_cast<size_t>(d.n) * d.ndim;
+        if (momentum == 0.0) {  // optim.cpp:45-46: v unchanged, mu untouched
+            std::memmove(out, v, sizeof(double) * cnt);
+            return;
+        }
+        DFM_DISPATCH(ctx, {
+            Field<T> a = dev_field<T>(ctx, "api_f0", d.n);
+            Field<T> b = dev_field<T>(ctx, "api_f1", d.n);
+            upload_field<T>(ctx, mu, d.n, d.ndim, a);
+            upload_field<T>(ctx, v, d.n, d.ndim, b);
+            launch_sgd<T>(ctx->L(), a.w(), b.r(), d, momentum);
+            download_field<T, double>(ctx, a.r(), d.n, d.ndim, mu);
+            ctx->sync();
+        });
+        std::memcpy(out, mu, sizeof(double) * cnt);
+    });
+}
+
+dfm_status dfm_sample_field_points(dfm_ctx* ctx, const dfm_grid* g, const double* field,
+                                   int64_t npts, const double* points, double* values,
+                                   double* jac) {
+    return guarded([&] {
+        validate_grid(g);
+        const Dims d = to_dims(g);
+        const int nd = d.ndim;
+        DFM_DISPATCH(ctx, {
+            Field<T> f = dev_field<T>(ctx, "api_f0", d.n);
+            upload_field<T>(ctx, field, d.n, nd, f);
+            double* pts = ctx->arr<double>("api_pts", 3 * npts + 1);
+            double* vals = ctx->arr<double>("api_vals", 3 * npts + 1);
+            double* grs = ctx->arr<double>("api_grads", 9 * npts + 1);
+            std::vector<double> hv(3 * static_cast<size_t>(npts)), hg(9 * static_cast<size_t>(npts));
+            if (npts > 0) {
+                CK(cudaMemcpyAsync(pts, points, sizeof(double) * 3 * npts, cudaMemcpyHostToDevice,
+                                   ctx->stream));
+                // sample_field / sample_field_jacobian (interp.cpp:188-227): the
+                // per-component lerp and its gradient
+                for (int c = 0; c < nd; ++c)
+                    launch_sample_points<T>(ctx->L(), f.p[c], d, pts, npts, vals + c * npts,
+                                            jac ? grs + 3 * c * npts : nullptr);
+                CK(cudaMemcpyAsync(hv.data(), vals, sizeof(double) * nd * npts,
+                                   cudaMemcpyDeviceToHost, ctx->stream));
+                if (jac)
+                    CK(cudaMemcpyAsync(hg.data(), grs, sizeof(double) * 3 * nd * npts,
+                                       cudaMemcpyDeviceToHost, ctx->stream));
+            }
+            ctx->sync();
+            for (int64_t i = 0; i < npts; ++i)
+                for (int c = 0; c < 3; ++c) {
+                    values[3 * i + c] = c < nd ? hv[c * npts + i] : 0.0;
+                    if (jac)
+                        for (int a = 0; a < 3; ++a)
+                            jac[9 * i + 3 * c + a] =
+                                (c < nd && a < nd) ? hg[3 * c * npts + 3 * i + a] : 0.0;
+                }
         });
     });
 }
@@ -2404,6 +2537,15 @@ void fill_log(const RegOut& o, dfm_iter_record* records, int64_t max_records, df
 }  // namespace
 
 extern "C" {
+
+dfm_status dfm_validate_config(const dfm_config* c) {
+    return guarded([&] { validate_config(c); });
+}
+
+dfm_status dfm_validate_schedule(const double* scales, const int32_t* iterations,
+                                 int32_t nscales) {
+    return guarded([&] { validate_schedule(scales, iterations, nscales); });
+}
 
 dfm_status dfm_register(dfm_ctx* ctx, const dfm_grid* g, const void* fixed, const void* moving,
                         int image_dtype, const dfm_config* cfg, const double* scales,

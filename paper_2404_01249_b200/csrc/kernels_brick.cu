@@ -377,8 +377,9 @@ struct FStatsB {
 // similarity.cpp:170-189 — box sums of the 4 coefficients, dW, grad = dW * G
 template <class T, int R_>
 struct LnccBwdB {
-    // fp32 context: coefficient box sums in fp32 (as LnccBwd2, DFM_BWD_ACC32)
-    using Acc = typename std::conditional<sizeof(T) == 4, float, double>::type;
+    // coefficient box sums in fp64 unless DFM_BWD_ACC32 (as LnccBwd2)
+    using Acc = typename std::conditional<(DFM_BWD_ACC32 != 0) && sizeof(T) == 4, float,
+                                          double>::type;
     using Raw = Acc;
     using Prol = NoProl;
     static constexpr int R = R_, C = 4, NR = 4, kStageBatch = 8;

@@ -677,6 +677,110 @@ void launch_stamp(const Launch& L, unsigned long long* slot) {
     L.bump();
 }
 
+// ---------------------------------------------------------------- C++ drop-in extras
+// jacobian (interp.cpp:291-328): J = I + central differences (one-sided at the
+// borders), ndim x ndim row-major per voxel (row = component), AoS
+template <class T>
+__global__ void k_jacobian_full(CPlanes3<T> u, Dims d, T* __restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
+    if (i >= d.n) return;
+    int x, y, z;
+    voxel_xyz(d, i, x, y, z);
+    T J[9];
+    jacobian_at(u, d, x, y, z, J);
+    const int nn = d.ndim * d.ndim;
+    for (int k = 0; k < nn; ++k) out[i * nn + k] = J[k];
+}
+
+template <class T>
+void launch_jacobian_full(const Launch& L, CPlanes3<T> u, Dims d, T* out) {
+    k_jacobian_full<T><<<grid_for(d.n), kNT, 0, L.stream>>>(u, d, out);
+    L.bump();
+}
+
+// Catmull-Rom weight (interp.cpp:59-67)
+__device__ __forceinline__ double cubic_weight(double t) {
+    t = fabs(t);
+    if (t <= 1.0) return __dadd_rn(__dmul_rn(__dmul_rn(__dsub_rn(__dmul_rn(1.5, t), 2.5), t), t), 1.0);
+    if (t < 2.0)
+        return __dadd_rn(
+            __dmul_rn(__dsub_rn(__dmul_rn(__dadd_rn(__dmul_rn(-0.5, t), 2.5), t), 4.0), t), 2.0);
+    return 0.0;
+}
+
+// upsample_field with UpsampleMethod::cubic (interp.cpp:69-101, 408-445):
+// corner-aligned Catmull-Rom resample of each component (clamped 4^d
+// neighbourhood), then the per-axis displacement rescale.  The reference keeps
+// it only for its folding demonstration; it is not on the registration path.
+template <class T>
+__global__ void k_upsample_cubic(CPlanes3<T> f, Dims ds, Planes3<T> out, Dims dd, double st0,
+                                 double st1, double st2, double r0, double r1, double r2) {
+    const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
+    if (i >= dd.n) return;
+    int x, y, z;
+    voxel_xyz(dd, i, x, y, z);
+    const double p[3] = {__dmul_rn(static_cast<double>(x), st0),
+                         __dmul_rn(static_cast<double>(y), st1),
+                         __dmul_rn(static_cast<double>(z), st2)};
+    const int dims[3] = {ds.nx, ds.ny, ds.nz};
+    int base[3];
+    double frac[3];
+    for (int a = 0; a < 3; ++a) {
+        if (a >= ds.ndim || dims[a] == 1) {
+            base[a] = 0;
+            frac[a] = 0.0;
+            continue;
+        }
+        const double q = fmin(fmax(p[a], 0.0), static_cast<double>(dims[a] - 1));
+        int b = static_cast<int>(floor(q));
+        b = min(max(b, 0), dims[a] - 2);
+        base[a] = b;
+        frac[a] = __dsub_rn(q, static_cast<double>(b));
+    }
+    const int na = (ds.ndim == 3 && ds.nz > 1) ? 4 : 1;
+    const double rs[3] = {r0, r1, r2};
+    for (int c = 0; c < ds.ndim; ++c) {
+        double acc = 0.0;
+        for (int kz = 0; kz < na; ++kz) {
+            const double wz = na == 4 ? cubic_weight(__dsub_rn(frac[2], double(kz - 1))) : 1.0;
+            const int zz = na == 4 ? min(max(base[2] + kz - 1, 0), ds.nz - 1) : 0;
+            for (int ky = 0; ky < 4; ++ky) {
+                const double wy = cubic_weight(__dsub_rn(frac[1], double(ky - 1)));
+                const int yy = min(max(base[1] + ky - 1, 0), ds.ny - 1);
+                for (int kx = 0; kx < 4; ++kx) {
+                    const double wx = cubic_weight(__dsub_rn(frac[0], double(kx - 1)));
+                    const int xx = min(max(base[0] + kx - 1, 0), ds.nx - 1);
+                    const double v = static_cast<double>(f.c[c][ds.idx(xx, yy, zz)]);
+                    acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(__dmul_rn(wz, wy), wx), v));
+                }
+            }
+        }
+        out.c[c][i] = static_cast<T>(__dmul_rn(acc, rs[c]));
+    }
+}
+
+template <class T>
+void launch_upsample_cubic(const Launch& L, CPlanes3<T> f, Dims ds, Planes3<T> out, Dims dd,
+                           const double step[3], const double rescale[3]) {
+    k_upsample_cubic<T><<<grid_for(dd.n), kNT, 0, L.stream>>>(
+        f, ds, out, dd, step[0], step[1], step[2], rescale[0], rescale[1], rescale[2]);
+    L.bump();
+}
+
+// sgd_step (optim.cpp:44-57): mu <- momentum * mu + v
+template <class T>
+__global__ void k_sgd(Planes3<T> mu, CPlanes3<T> v, Dims d, T momentum) {
+    const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
+    if (i >= d.n) return;
+    for (int c = 0; c < d.ndim; ++c) mu.c[c][i] = momentum * mu.c[c][i] + v.c[c][i];
+}
+
+template <class T>
+void launch_sgd(const Launch& L, Planes3<T> mu, CPlanes3<T> v, Dims d, double momentum) {
+    k_sgd<T><<<grid_for(d.n), kNT, 0, L.stream>>>(mu, v, d, T(momentum));
+    L.bump();
+}
+
 // ---------------------------------------------------------------- instantiations
 #define DFM_INST_T(T)                                                                          \
     template void launch_aos_to_soa<T, double>(const Launch&, const double*, Planes3<T>,       \
@@ -715,7 +819,11 @@ void launch_stamp(const Launch& L, unsigned long long* slot) {
                                      CPlanes3<T>, double*, const LoopState*);                  \
     template void launch_dice_grad<T>(const Launch&, const T*, const T*, Dims, Dims,           \
                                       CPlanes3<T>, Planes3<T>, const LoopState*, double,       \
-                                      double);
+                                      double);                                                 \
+    template void launch_jacobian_full<T>(const Launch&, CPlanes3<T>, Dims, T*);              \
+    template void launch_upsample_cubic<T>(const Launch&, CPlanes3<T>, Dims, Planes3<T>, Dims, \
+                                           const double*, const double*);                      \
+    template void launch_sgd<T>(const Launch&, Planes3<T>, CPlanes3<T>, Dims, double);
 
 DFM_INST_T(float)
 DFM_INST_T(double)

@@ -32,7 +32,6 @@ namespace dfm {
 namespace {
 
 constexpr int TX = kTX;
-constexpr int64_t kSaCoarsenVoxels = 2000000;
 
 // TMA ring depths (planes in flight per CTA); overridable for tuning builds
 #ifndef DFM_S_FWD
@@ -97,8 +96,11 @@ constexpr int64_t kSaCoarsenVoxels = 2000000;
 #ifndef DFM_MINB_CS
 #define DFM_MINB_CS 3
 #endif
-#ifndef DFM_BWD_ACC32
-#define DFM_BWD_ACC32 1
+#ifndef DFM_CY_BWD64
+#define DFM_CY_BWD64 2
+#endif
+#ifndef DFM_BWD_QUAD64
+#define DFM_BWD_QUAD64 1
 #endif
 #ifndef DFM_MINB_FWD3
 #define DFM_MINB_FWD3 3
@@ -806,15 +808,18 @@ struct LnccFwd3 {
 // similarity.cpp:170-189 — box sums of the coefficients, dW, grad = dW * G
 template <class T, int R_, int TY_ = DFM_TY_BWD>
 struct LnccBwd2 {
-    // fp32 context: the box sums of the (fp32-stored) coefficients may run in
-    // fp32 (DFM_BWD_ACC32); the dW combination stays fp64
+    // box sums of the (fp32-stored) coefficients in fp64 (DFM_BWD_ACC32 = 0,
+    // loop_ops.cuh): fp32 sums miss the per-kernel criterion at 160x192x224
     using Acc = typename std::conditional<(DFM_BWD_ACC32 != 0) && sizeof(T) == 4, float,
                                           double>::type;
     using Prol = NoProl;
     using Carry = NoCarry;
     static constexpr int R = R_, C = 4, BACK = 0, AHEAD = 0, S = DFM_S_BWD, TYv = TY_;
     // fp32 sums: two consecutive rows per thread (-20 us/iteration at 160x192x224)
-    static constexpr int kMinB = DFM_MINB_BWD, kCY = sizeof(Acc) == 4 ? DFM_CY_BWD : 1;
+    // fp64 sums at radius >= 3 need the 128-register budget of 2 CTAs per SM
+    static constexpr int kMinB = (sizeof(Acc) == 8 && R_ >= 3) ? 2 : DFM_MINB_BWD,
+                         kCY = sizeof(Acc) == 4 ? DFM_CY_BWD
+                                              : (sizeof(T) == 4 && R_ <= 2 ? DFM_CY_BWD64 : 1);
     static constexpr bool kStaged = false, kSum = false, kMax = false;
     static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TYv + 2 * R;
     static constexpr int kBytes = BX * BY * int(sizeof(T));
@@ -842,7 +847,7 @@ struct LnccBwd2 {
     __device__ Acc wgt(int, int) const { return 1.0; }
     __device__ Acc nrm(int, int) const { return 1.0; }
     __device__ Prol prologue() const { return {}; }
-    static constexpr bool kXQuad = sizeof(Acc) == 4 && sizeof(T) == 4;
+    static constexpr bool kXQuad = sizeof(T) == 4 && (sizeof(Acc) == 4 || (DFM_BWD_QUAD64 && R_ <= 2));
     __device__ void xpass4(const unsigned char* st_, int row, int col, const Acc*,
                            Acc v[4][4]) const {
         constexpr int NCH = (XA + R + 4 + 3) / 4;
@@ -1898,7 +1903,7 @@ int launch_smooth_adam_tma(const Launch& L, int R, const GaussW<T>& w, const T* 
         // (register ring of 2 x 3 x (2R+1): only for the BASELINE sigma_grad 1.0;
         // at R = 5 it spills, 504 vs ~160 us)
         if constexpr (RR <= 3) {
-            if (sizeof(T) == 4 && d.n >= kSaCoarsenVoxels)
+            if (sizeof(T) == 4 && d.n >= L.large_min)
                 return go(SmoothAdam2<T, RR, 16, 2, DFM_MINB_SA2>{});
         }
         // 512-thread CTAs (TY 16) get 64 registers at 2 CTAs per SM: the
@@ -2028,7 +2033,7 @@ int launch_compose_smooth_tma(const Launch& L, int R, const GaussW<T>& w, const 
         constexpr int RR = decltype(rc)::value;
         // the cp.async carried gather pays on large levels (-10 us/iteration at
         // 160x192x224), the register carry on mid ones (-1.6 us at 80x96x112)
-        if (d.n >= kSaCoarsenVoxels) {
+        if (d.n >= L.large_min) {
             if (dm.nx > 1 && dm.ny > 1 && dm.nz > 1)  // no flat axis: no per-voxel check
                 return go_compose_smooth<ComposeS2<T, RR, DFM_TY_CS, DFM_CS_ASYNC != 0, false>>(
                     L, w, c, uout, M, dm, d, W, G, st, count_update);

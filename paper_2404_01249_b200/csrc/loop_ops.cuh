@@ -142,6 +142,16 @@ __device__ __forceinline__ double window_inv(int x, int y, int z, const Dims& d)
     return 1.0 / n;
 }
 
+// Box sums of the 4 LNCC coefficients in the backward: fp64 (0, default) or
+// fp32 (1, fp32 context only; A/B builds).  fp32 sums cancel: dW combines
+// F*S[an] - S[amu] - W*S[bn] + S[bmu], and at 160x192x224 the fp32-summed
+// gradient misses the per-kernel criterion (1e-5 relative + 1e-6 of peak) by
+// up to 2.3x on 167 of 20.6M components; fp64 sums of the same fp32-stored
+// coefficients stay within 0.2 of it (tests/test_fullsize_parity_gpu.py).
+#ifndef DFM_BWD_ACC32
+#define DFM_BWD_ACC32 0
+#endif
+
 // dL/dW at one voxel from the box sums of the 4 coefficients (similarity.cpp:182)
 __device__ __forceinline__ double lncc_dw(double m2n, double f, double w, const double s[4]) {
     return m2n * (f * s[0] - s[1] - w * s[2] + s[3]);

@@ -38,7 +38,8 @@ EXPORTS = [
     "dfm_dev_overlap_report", "dfm_dev_warp_labels", "dfm_landmark_error", "dfm_sweep",
     "dfm_mhd_read_header", "dfm_mhd_write_image", "dfm_mhd_read_image", "dfm_mhd_write_labels",
     "dfm_mhd_read_labels", "dfm_mhd_write_field", "dfm_mhd_read_field", "dfm_dev_load_image_mhd",
-    "dfm_dev_save_field_mhd",
+    "dfm_dev_save_field_mhd", "dfm_ctx_debug_read", "dfm_sample_field_points", "dfm_jacobian",
+    "dfm_upsample_field_cubic", "dfm_sgd_step", "dfm_validate_config", "dfm_validate_schedule",
 ]
 
 OPT_BRICK_MAX = 1
@@ -47,6 +48,7 @@ OPT_PERSIST = 3
 OPT_PDL = 4
 OPT_SPLIT = 5
 OPT_SPLIT_FOLD_MAX = 6
+OPT_LARGE_MIN = 7
 
 _lib: Optional[C.CDLL] = None
 
@@ -96,6 +98,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         lib.dfm_ctx_kernel_times.argtypes = [C.c_void_p, C.POINTER(C.c_double),
                                              C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         lib.dfm_ctx_kernel_times.restype = C.c_int
+        lib.dfm_ctx_debug_read.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t, C.c_size_t,
+                                           C.c_void_p]
+        lib.dfm_ctx_debug_read.restype = C.c_int
         reg = [C.c_void_p, C.POINTER(A.dfm_grid), C.c_void_p, C.c_void_p]
         lib.dfm_register.argtypes = reg + [C.c_int, C.POINTER(A.dfm_config),
                                            C.POINTER(C.c_double), C.POINTER(C.c_int32),
@@ -170,6 +175,23 @@ class Context(A.HostAPI):
         """dfm_ctx_set_option: OPT_BRICK_MAX (voxels) / OPT_FORCE_LEGACY (0|1)."""
         self.t.check(self.lib.dfm_ctx_set_option(self.handle, int(key), int(value)),
                      "set_option")
+
+    def debug_read(self, name: str, count: int, offset: int = 0) -> np.ndarray:
+        """dfm_ctx_debug_read: `count` elements (context precision) of the named
+        workspace buffer from element `offset` (white-box parity tests)."""
+        dt = np.float64 if self.precision == "f64" else np.float32
+        out = np.empty(int(count), dtype=dt)
+        it = out.itemsize
+        self.t.check(self.lib.dfm_ctx_debug_read(self.handle, name.encode(), int(offset) * it,
+                                                 out.nbytes, out.ctypes.data), "debug_read")
+        return out
+
+    def debug_field(self, name: str, g: A.GridMeta) -> np.ndarray:
+        """A 3-plane SoA workspace field packed at g's voxel count -> AoS
+        (z, y, x, 3) float64, the host layout of the reference."""
+        n = g.voxel_count
+        soa = self.debug_read(name, 3 * n).astype(np.float64).reshape(3, n)
+        return np.ascontiguousarray(soa.T).reshape(g.field_shape)
 
     def kernel_times(self) -> dict:
         ms = (C.c_double * A.NUM_KCLASS)()
