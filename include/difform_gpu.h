@@ -227,7 +227,7 @@ DFM_API dfm_status dfm_exp_map(dfm_ctx* ctx, const dfm_grid* g, const double* v,
 /* svf_pullback (diffeo.hpp:22-26, diffeo.cpp:79-167): the discrete adjoint of
  * exp_map applied to the cotangent grad_phi.  The reference's serial scatter
  * is a stable-sorted gather on the device: same per-node summation order,
- * bit-stable across runs.  Needs 8 * voxels < 2^31. */
+ * bit-stable across runs. */
 DFM_API dfm_status dfm_svf_pullback(dfm_ctx* ctx, const dfm_grid* g, const double* v,
                                     const double* grad_phi, int M, double* out);
 /* jacobian (interp.hpp:49, interp.cpp:291-328): per-voxel J = I + central

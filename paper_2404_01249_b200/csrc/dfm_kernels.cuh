@@ -251,7 +251,7 @@ int launch_lncc_fwd3_tma(const Launch& L, int R, const T* F, const T* W, const d
 template <class T>
 int launch_smooth_adam_tma(const Launch& L, int R, const GaussW<T>& w, const T* grad, T* m,
                            T* nu, T* step, Dims d, AdamParams ap, LoopState* st,
-                           unsigned long long* maxstep);
+                           unsigned long long* maxstep, const T* ujac = nullptr);
 template <class T>
 int launch_compose_tma(const Launch& L, int R, double cap, const GaussW<T>& w, const T* step,
                        const T* uin, T* uout, const T* M, Dims dm, Dims d, T* W, T* G,

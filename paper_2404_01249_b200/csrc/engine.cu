@@ -1207,8 +1207,6 @@ dfm_status dfm_svf_pullback(dfm_ctx* ctx, const dfm_grid* g, const double* v,
         if (M < 0) fail(DFM_E_INVALID, "svf_pullback: M must be >= 0");
         validate_grid(g);
         const Dims d = to_dims(g);
-        if (8 * d.n >= (int64_t(1) << 31))
-            fail(DFM_E_INVALID, "svf_pullback: volume too large (8 * voxels must be < 2^31)");
         DFM_DISPATCH(ctx, {
             Field<T> a = dev_field<T>(ctx, "api_f0", d.n);
             Field<T> b = dev_field<T>(ctx, "api_f1", d.n);
@@ -1220,10 +1218,11 @@ dfm_status dfm_svf_pullback(dfm_ctx* ctx, const dfm_grid* g, const double* v,
             SvfWork<T> ws{};
             ws.wa = ctx->arr<T>("api_svf_wa", 3 * d.n);
             ws.wb = ctx->arr<T>("api_svf_wb", 3 * d.n);
-            int32_t* kv = ctx->arr<int32_t>("api_svf_kv", 4 * 8 * d.n);
+            // one (cell base, voxel) pair per voxel, double-buffered for the sort
+            int32_t* kv = ctx->arr<int32_t>("api_svf_kv", 4 * d.n);
             for (int k = 0; k < 2; ++k) {
-                ws.keys[k] = kv + (2 * k) * 8 * d.n;
-                ws.vals[k] = kv + (2 * k + 1) * 8 * d.n;
+                ws.keys[k] = kv + (2 * k) * d.n;
+                ws.vals[k] = kv + (2 * k + 1) * d.n;
             }
             ws.start = ctx->arr<int32_t>("api_svf_start", d.n + 1);
             ws.wts = ctx->arr<T>("api_svf_wts", 8 * d.n);
@@ -1749,17 +1748,15 @@ struct Registrar {
         Gb = ctx->arr<T>("reg_G", 3 * n);
         if (cfg->loss == DFM_LOSS_LNCC && ctx->fwd3) fstat = ctx->arr<double>("reg_fstat", 2 * n);
         if (cfg->mode == DFM_MODE_SVF) {
-            if (8 * n >= (int64_t(1) << 31))
-                fail(DFM_E_INVALID, "svf mode: volume too large (8 * voxels must be < 2^31)");
             const int M = cfg->svf_M;
             svf_levels = ctx->arr<T>("svf_levels", 3 * n * (M + 1));
             svf_g = ctx->arr<T>("svf_g", 3 * n);
             svf.wa = ctx->arr<T>("svf_wa", 3 * n);
             svf.wb = ctx->arr<T>("svf_wb", 3 * n);
-            int32_t* kv = ctx->arr<int32_t>("svf_kv", 4 * 8 * n);
+            int32_t* kv = ctx->arr<int32_t>("svf_kv", 4 * n);  // keys/vals x 2 (sort)
             for (int k = 0; k < 2; ++k) {
-                svf.keys[k] = kv + (2 * k) * 8 * n;
-                svf.vals[k] = kv + (2 * k + 1) * 8 * n;
+                svf.keys[k] = kv + (2 * k) * n;
+                svf.vals[k] = kv + (2 * k + 1) * n;
             }
             svf.start = ctx->arr<int32_t>("svf_start", n + 1);
             svf.wts = ctx->arr<T>("svf_wts", 8 * n);
@@ -1829,7 +1826,7 @@ struct Registrar {
 
     // can this scale run the plane-streaming (TMA) kernels?
     bool tma_eligible(const Dims& d, int Rg, int Rw, bool big) const {
-        return !big && !cfg->use_jac && cfg->step_cap <= 1.5 && Rg <= 6 && Rw <= 4 &&
+        return !big && cfg->step_cap <= 1.5 && Rg <= 6 && Rw <= 4 &&
                d.ndim == 3 &&  // Compose2's fused W/G gather is 3-D only
                (cfg->loss != DFM_LOSS_LNCC || cfg->lncc_radius <= 5) &&
                tma_supported(d, sizeof(T));
@@ -1895,7 +1892,7 @@ struct Registrar {
         // measured: the split wins on mid-size levels (80x96x112: 127 -> 115 us per
         // iteration) and loses on the full 160x192x224 level (610 -> 650 us)
         const bool split = !use_brick && ctx->split_compose && (mask & 4) && (mask & 8) &&
-                           d.ndim == 3 && d.n < ctx->split_fold_max;
+                           d.ndim == 3 && d.n < ctx->split_fold_max && !cfg->use_jac;
         if (use_brick && ctx->split_compose) {  // brick: compose once per voxel, not per halo
             ev_begin(KC_ADAM);
             const int r1 = launch_smooth_adam_compose_brick<T>(
@@ -1912,12 +1909,15 @@ struct Registrar {
         }
         // large levels: plain smooth+Adam, a pointwise compose kernel, then the
         // smoothing + W/G kernel (compose once per voxel, at full occupancy)
-        const bool split3 = !use_brick && ctx->split_compose && ctx->split3 && (mask & 4) &&
-                            (mask & 8) && d.ndim == 3 && d.n >= ctx->split_fold_max;
+        // use_jac (diffeo.cpp:25-39): J(u)^T in the plain smooth+Adam, so this path
+        const bool split3 = !use_brick && (mask & 4) && (mask & 8) && d.ndim == 3 &&
+                            ((ctx->split_compose && ctx->split3 && d.n >= ctx->split_fold_max) ||
+                             cfg->use_jac);
         if (split3) {
             ev_begin(KC_ADAM);
-            launch_smooth_adam_tma<T>(L, Rg, wg, grad.p[0], m.p[0], nu.p[0], step.p[0], d, ap, st,
-                                      maxstep);
+            if (launch_smooth_adam_tma<T>(L, Rg, wg, grad.p[0], m.p[0], nu.p[0], step.p[0], d, ap,
+                                          st, maxstep, cfg->use_jac ? u[src].p[0] : nullptr) < 0)
+                fail(DFM_E_CUDA, "smooth+Adam launch failed");
             ev_end();
             ev_begin(KC_COMPOSE);
             T* cbuf = grad.p[0];  // grad is dead after smooth+Adam: it holds c

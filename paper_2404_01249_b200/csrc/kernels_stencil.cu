@@ -459,7 +459,21 @@ struct SvfUpdateOp {
     LoopState* st;
     Dims d;
 
-    __device__ bool skip() const { return st && st->done; }
+    // diffeo-mode parity: a non-finite Adam step throws before the update
+    // (pipeline.cpp:198-203 clamps NaN into the field; the next loss throws) —
+    // here the update is skipped and the run fails with DFM_E_NUMERICAL
+    __device__ bool skip() const {
+        if (!st) return false;
+        if (st->done) return true;
+        if (st->bad_step) {
+            if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+                st->err = 2;
+                st->done = 1;
+            }
+            return true;
+        }
+        return false;
+    }
     __device__ Acc wgt(int a, int j) const { return w.taps[a][j]; }
     __device__ Acc nrm(int a, int i) const { return __ldg(w.norm[a] + i); }
     __device__ void load(int x, int y, int z, T s[3]) const {

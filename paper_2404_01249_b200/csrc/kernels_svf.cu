@@ -193,7 +193,7 @@ size_t svf_sort_temp_bytes(int64_t n) {
     cub::DeviceRadixSort::SortPairs(nullptr, bytes, static_cast<const int32_t*>(nullptr),
                                     static_cast<int32_t*>(nullptr),
                                     static_cast<const int32_t*>(nullptr),
-                                    static_cast<int32_t*>(nullptr), static_cast<int>(8 * n), 0,
+                                    static_cast<int32_t*>(nullptr), static_cast<int>(n), 0,
                                     key_bits(n));
     return bytes;
 }

@@ -903,8 +903,11 @@ struct LnccBwd2 {
 // pipeline.cpp:182-186 + optim.cpp:22-42 + diffeo.cpp:47-57
 // CAPH_ > 0: the emit also composes, writing c = step + u(x + step) (the
 // composed field ComposeS2 smooths) into `step` instead of the step itself
+// JAC_: eulerian_direction(use_jac = true) (diffeo.cpp:25-39): the smoothed
+// gradient is mapped by J(u)^T at the voxel before Adam (central differences of
+// the current field, one-sided at the borders)
 template <class T, int R_, int TY_ = DFM_TY_SA, int CY_ = DFM_CY_SA, int MINB_ = DFM_MINB_SA,
-          int CAPH_ = 0>
+          int CAPH_ = 0, bool JAC_ = false>
 struct SmoothAdam2 {
     using Acc = T;
     // the composing emit's gather: cp.async into shared memory (fp32, one row
@@ -968,6 +971,7 @@ struct SmoothAdam2 {
     T* step[3];
     const T* uin;  // CAPH_ > 0: the current field (3 planes)
     const T* uin3[3];
+    const T* ujac[3];  // JAC_: the current field u (3 planes) for J(u)^T
     AdamK<T> ak;
     const double* corr1;
     const double* corr2;
@@ -1087,10 +1091,22 @@ struct SmoothAdam2 {
         T mx = T(0);
         bool bad = false;
         T cl[3];
+        T g[3] = {s[0], s[1], s[2]};
+        if constexpr (JAC_) {  // diffeo.cpp:30-37: acc_a = sum_c J[c][a] g_c, v = -acc
+            T J[9];
+            jacobian_at3(CPlanes3<T>{{ujac[0], ujac[1], ujac[2]}}, d, x, y, z, J);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                T acc = T(0);
+#pragma unroll
+                for (int k = 0; k < 3; ++k) acc += J[k * 3 + a] * s[k];
+                g[a] = acc;
+            }
+        }
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             T mm = c.m[k], nn = c.nu[k];
-            cl[k] = adam_component(ak, s[k], mm, nn, p.ic1, p.ic2, bad);
+            cl[k] = adam_component(ak, g[k], mm, nn, p.ic1, p.ic2, bad);
             m[k][i] = mm;
             nu[k][i] = nn;
             mx = fmax(mx, fabs(cl[k]));
@@ -1599,7 +1615,21 @@ struct SvfUpdate2 {
     LoopState* st;
     Dims d;
 
-    __device__ bool skip() const { return st && st->done; }
+    // diffeo-mode parity: a non-finite Adam step throws before the update
+    // (pipeline.cpp:198-203 clamps NaN into the field; the next loss throws) —
+    // here the update is skipped and the run fails with DFM_E_NUMERICAL
+    __device__ bool skip() const {
+        if (!st) return false;
+        if (st->done) return true;
+        if (st->bad_step) {
+            if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+                st->err = 2;
+                st->done = 1;
+            }
+            return true;
+        }
+        return false;
+    }
     __device__ void prefetch_maps() const {
         prefetch_tmap(&mV);
         prefetch_tmap(&mS);
@@ -1874,8 +1904,9 @@ int launch_lncc_bwd_tma(const Launch& L, int R, const T* coef, const T* F, const
 template <class T>
 int launch_smooth_adam_tma(const Launch& L, int R, const GaussW<T>& w, const T* grad, T* m,
                            T* nu, T* step, Dims d, AdamParams ap, LoopState* st,
-                           unsigned long long* maxstep) {
+                           unsigned long long* maxstep, const T* ujac) {
     if (d.ndim != 3) return -2;
+    if (ap.use_jac && !ujac) return -2;
     return with_r<0, 6>(R, [&](auto rc) {
         constexpr int RR = decltype(rc)::value;
         auto go = [&](auto op) {
@@ -1890,6 +1921,7 @@ int launch_smooth_adam_tma(const Launch& L, int R, const GaussW<T>& w, const T* 
                 op.nu[k] = nu + k * d.n;
                 op.step[k] = step + k * d.n;
             }
+            for (int k = 0; k < 3; ++k) op.ujac[k] = ujac ? ujac + k * d.n : nullptr;
             op.ak = adam_k<T>(ap);
             op.corr1 = ap.corr1;
             op.corr2 = ap.corr2;
@@ -1898,6 +1930,7 @@ int launch_smooth_adam_tma(const Launch& L, int R, const GaussW<T>& w, const T* 
             op.d = d;
             return run_zm2(L, op, d);
         };
+        if (ap.use_jac) return go(SmoothAdam2<T, RR, 8, 1, DFM_MINB_SA, 0, true>{});
         // large levels: two rows per thread (measured -8% at 160x192x224,
         // +8% at 80x96x112); fp64 keeps one row (register budget)
         // (register ring of 2 x 3 x (2R+1): only for the BASELINE sigma_grad 1.0;
@@ -2120,7 +2153,7 @@ void launch_warpgrad(const Launch& L, const T* M, Dims dm, CPlanes3<T> u, Dims d
                                          const MonitorArgs*);                                  \
     template int launch_smooth_adam_tma<T>(const Launch&, int, const GaussW<T>&, const T*, T*, \
                                            T*, T*, Dims, AdamParams, LoopState*,               \
-                                           unsigned long long*);                               \
+                                           unsigned long long*, const T*);                     \
     template int launch_compose_tma<T>(const Launch&, int, double, const GaussW<T>&, const T*, \
                                        const T*, T*, const T*, Dims, Dims, T*, T*,             \
                                        LoopState*, bool);                                      \

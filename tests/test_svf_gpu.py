@@ -112,3 +112,18 @@ def test_svf_errors_map_to_reference_exceptions(ctx32):
     with pytest.raises(A.InvalidArgument):
         ctx32.register_images(p.grid, np.clip(p.fixed, 0, 1), np.clip(p.moving, 0, 1), cfg,
                               A.PyramidSchedule((1.0,), (2,)))
+
+
+@pytest.mark.parametrize("mode", [A.MODE_DIRECT, A.MODE_SVF])
+def test_nonfinite_step_raises_numerical(ctx32, mode):
+    """A gradient that overflows fp32 (intensities ~3e19: the fp64 loss stays
+    finite, (W - F) * grad M does not) makes the Adam step non-finite: both
+    modes must fail with NumericalError (diffeo.cpp:52-53) instead of
+    clamping NaN into the field and returning a corrupted result."""
+    g = A.GridMeta.make_3d(12, 12, 12)
+    rng = np.random.default_rng(3)
+    F = (rng.random(g.shape) * 3e19).astype(np.float32)
+    M = (rng.random(g.shape) * 3e19).astype(np.float32)
+    cfg = A.RegistrationConfig(loss=A.LOSS_SSD, mode=mode)
+    with pytest.raises(A.NumericalError):
+        ctx32.register_images(g, F, M, cfg, A.PyramidSchedule((1.0,), (4,)))
