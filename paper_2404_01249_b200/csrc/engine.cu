@@ -134,8 +134,19 @@ struct dfm_ctx {
     // per-(level, ping-pong variant) executable graphs kept across calls: a
     // re-capture is applied with cudaGraphExecUpdate (cheap) instead of a new
     // cudaGraphInstantiate (hundreds of us of host time the GPU waits for)
-    std::map<int, cudaGraphExec_t> graph_cache;
-    cudaGraphExec_t graph_exec(int key, cudaGraph_t graph) {
+    // keyed by a signature of everything that shapes the captured kernels
+    // (level dims, config, kernel family, options): an in-place update is only
+    // attempted between captures of the same structure.  (An update from a
+    // clustered plane-streaming launch of another level or config could
+    // report success yet keep stale launch attributes.)
+    std::map<uint64_t, cudaGraphExec_t> graph_cache;
+    void trim_graphs() {  // bounded cache: a long sweep of shapes/configs (between levels)
+        if (graph_cache.size() < 64) return;
+        CK(cudaStreamSynchronize(stream));
+        for (auto& kv : graph_cache) cudaGraphExecDestroy(kv.second);
+        graph_cache.clear();
+    }
+    cudaGraphExec_t graph_exec(uint64_t key, cudaGraph_t graph) {
         auto it = graph_cache.find(key);
         if (it != graph_cache.end()) {
             cudaGraphExecUpdateResultInfo info;
@@ -2412,7 +2423,27 @@ struct Registrar {
                 const int g = e ? atoi(e) : 8;
                 return g >= 2 ? g & ~1 : 0;
             }();
+            ctx->trim_graphs();
             cudaGraphExec_t exec[2] = {nullptr, nullptr}, exec_g = nullptr;
+            uint64_t sig = 1469598103934665603ull;  // FNV-1a over the level's structure
+            auto mix = [&sig](const void* p, size_t nbytes) {
+                const unsigned char* b = static_cast<const unsigned char*>(p);
+                for (size_t k = 0; k < nbytes; ++k) sig = (sig ^ b[k]) * 1099511628211ull;
+            };
+            {
+                const int64_t parts[] = {si, d.nx, d.ny, d.nz, d.ndim, Rg, Rw, use_brick, use_tma,
+                                         fstat_ready, pbg != nullptr, pbw != nullptr, G,
+                                         ctx->prec, ctx->brick_max, ctx->split_compose,
+                                         ctx->split3, ctx->split_fold_max, ctx->large_min,
+                                         ctx->pdl, ctx->tma_mask, ctx->fwd3,
+                                         ctx->force_legacy};
+                mix(parts, sizeof(parts));
+                // config fields that select kernels (scalars such as eta or the
+                // betas are kernel parameters: an update carries them)
+                const int64_t cparts[] = {cfg->loss, cfg->lncc_radius, cfg->use_jac, cfg->mode,
+                                          cfg->svf_M, cfg->step_cap <= 0.5 ? 1 : (cfg->step_cap <= 1.5 ? 2 : 3)};
+                mix(cparts, sizeof(cparts));
+            }
             int64_t nodes_per = 0;
             for (int v = 0; v < 3; ++v) {
                 if (v == 2 && (G == 0 || T_si < G)) break;
@@ -2427,10 +2458,10 @@ struct Registrar {
                 }
                 CK(cudaStreamEndCapture(ctx->stream, &graph));
                 if (v < 2) {
-                    exec[v] = ctx->graph_exec(2 * si + v, graph);
+                    exec[v] = ctx->graph_exec(sig * 4 + v, graph);
                     nodes_per = ctx->launches - before;
                 } else {
-                    exec_g = ctx->graph_exec(1000 + si, graph);
+                    exec_g = ctx->graph_exec(sig * 4 + 2, graph);
                 }
                 CK(cudaGraphDestroy(graph));
                 ctx->launches = before;

@@ -19,8 +19,10 @@
 #include <cudaTypedefs.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
+
 
 #include "dfm_device.cuh"
 #include "dfm_kernels.cuh"
