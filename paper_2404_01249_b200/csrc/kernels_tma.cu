@@ -101,6 +101,15 @@ constexpr int TX = kTX;
 #ifndef DFM_CY_BWD64
 #define DFM_CY_BWD64 2
 #endif
+// sliding box sums in the fp64 LNCC moment / coefficient passes: bit 0 the
+// x (quad) and y (row pairs) sums, bit 1 a running z sum (more registers)
+#ifndef DFM_SLIDE
+#define DFM_SLIDE 1
+#endif
+// rows per thread of the fp32 LNCC forward (radius <= 2)
+#ifndef DFM_CY_FWD3
+#define DFM_CY_FWD3 1
+#endif
 #ifndef DFM_BWD_QUAD64
 #define DFM_BWD_QUAD64 1
 #endif
@@ -203,6 +212,27 @@ struct XQuad<Op, std::void_t<decltype(Op::kXQuad)>> {
     static constexpr bool value = Op::kXQuad;
 };
 
+// four consecutive box sums of 2R+1 values (e[0 .. 2R+4)): the first direct,
+// the next three sliding (+ entering - leaving) when DFM_SLIDE
+template <int R, class A>
+__device__ __forceinline__ void box4(const A* e, A out[4]) {
+    A a = A(0);
+#pragma unroll
+    for (int j = 0; j < 2 * R + 1; ++j) a += e[j];
+    out[0] = a;
+#pragma unroll
+    for (int o = 1; o < 4; ++o) {
+        if constexpr ((DFM_SLIDE & 1) != 0) {
+            a = (a + e[o + 2 * R]) - e[o - 1];
+        } else {
+            a = A(0);
+#pragma unroll
+            for (int j = 0; j < 2 * R + 1; ++j) a += e[o + j];
+        }
+        out[o] = a;
+    }
+}
+
 // the float4 chunks [col, col + 4 * NCH) of a stage row, col % 4 == 0
 template <int NCH>
 __device__ __forceinline__ void load_row4(const float* p, float w[4 * NCH]) {
@@ -215,6 +245,19 @@ __device__ __forceinline__ void load_row4(const float* p, float w[4 * NCH]) {
         w[4 * k + 3] = t.w;
     }
 }
+
+// box-filter ops (unit taps, unit norms: the LNCC moments and coefficient
+// sums) may compute their window sums by sliding: y rows of a thread from the
+// previous row's sum (+ entering - leaving), z from a running sum of the ring
+// (Op::kSlide).  fp64 accumulation keeps the rounding drift ~1e-16 relative.
+template <class Op, class = void>
+struct BoxSlide {
+    static constexpr bool value = false;
+};
+template <class Op>
+struct BoxSlide<Op, std::void_t<decltype(Op::kSlide)>> {
+    static constexpr bool value = Op::kSlide;
+};
 
 // the op's centre operands of plane zo = q - R arrive by TMA with stage q
 // (Op::kCenterTMA; read with Op::load_center_st): no per-voxel global loads
@@ -356,6 +399,13 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
         for (int c = 0; c < C; ++c)
 #pragma unroll
             for (int k = 0; k < K; ++k) ring[r][c][k] = Acc(0);
+    constexpr bool kSlide = BoxSlide<Op>::value;
+    constexpr bool kSlideZ = kSlide && (DFM_SLIDE & 2);  // running z sum (+registers)
+    Acc zsum[kSlideZ ? CY : 1][kSlideZ ? C : 1];
+#pragma unroll
+    for (int r = 0; r < (kSlideZ ? CY : 1); ++r)
+#pragma unroll
+        for (int c = 0; c < (kSlideZ ? C : 1); ++c) zsum[r][c] = Acc(0);
     double rsum = 0.0, rmax = 0.0;
     int waited = q0 - 1;
     int buf = 0;
@@ -488,18 +538,44 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
         }
         // y pass of every owned row into ring slot kk (the newest plane) before
         // any emit: the rows' windows overlap and their loads are shared
+        if constexpr (kSlide) {
+            Acc yprev[C];
 #pragma unroll
-        for (int r = 0; r < CY; ++r) {
-            const int row = ty * CY + r;
+            for (int r = 0; r < CY; ++r) {
+                const int row = ty * CY + r;
 #pragma unroll
-            for (int c = 0; c < C; ++c) {
-                const Acc* src = sx + (c * HI + row) * TX + tx;
-                Acc a = Acc(0);
+                for (int c = 0; c < C; ++c) {
+                    const Acc* src = sx + (c * HI + row) * TX + tx;
+                    Acc a;
+                    if (r == 0) {
+                        a = Acc(0);
 #pragma unroll
-                for (int j = 0; j < K; ++j) a += op.wgt(1, j) * src[j * TX];
+                        for (int j = 0; j < K; ++j) a += src[j * TX];
+                    } else {  // the previous row's window, shifted by one row
+                        a = (yprev[c] + src[(K - 1) * TX]) - src[-TX];
+                    }
+                    yprev[c] = a;
+                    const Acc leaving = ring[r][c][0];
 #pragma unroll
-                for (int k = 0; k < K - 1; ++k) ring[r][c][k] = ring[r][c][k + 1];
-                ring[r][c][kk] = a * nyv[r];
+                    for (int k = 0; k < K - 1; ++k) ring[r][c][k] = ring[r][c][k + 1];
+                    ring[r][c][kk] = a;
+                    if constexpr (kSlideZ) zsum[r][c] = (zsum[r][c] + a) - leaving;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < CY; ++r) {
+                const int row = ty * CY + r;
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    const Acc* src = sx + (c * HI + row) * TX + tx;
+                    Acc a = Acc(0);
+#pragma unroll
+                    for (int j = 0; j < K; ++j) a += op.wgt(1, j) * src[j * TX];
+#pragma unroll
+                    for (int k = 0; k < K - 1; ++k) ring[r][c][k] = ring[r][c][k + 1];
+                    ring[r][c][kk] = a * nyv[r];
+                }
             }
         }
         if constexpr (kCA) {
@@ -527,10 +603,15 @@ __global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
                 Acc sv[C];
 #pragma unroll
                 for (int c = 0; c < C; ++c) {
-                    Acc a = Acc(0);
+                    if constexpr (kSlideZ) {
+                        sv[c] = zsum[r][c];
+                    } else {
+                        Acc a = Acc(0);
 #pragma unroll
-                    for (int j = 0; j < K; ++j) a += op.wgt(2, j) * ring[r][c][(kk + 1 + j) % K];
-                    sv[c] = a * nz;
+                        for (int j = 0; j < K; ++j)
+                            a += op.wgt(2, j) * ring[r][c][(kk + 1 + j) % K];
+                        sv[c] = a * nz;
+                    }
                 }
                 const Red2 rr = op.emit(x, yk[r], zo, sv, cen[r], pr, carry[r]);
                 rsum += rr.sum;
@@ -702,8 +783,9 @@ struct LnccFwd3 {
     // radius >= 3 (LNCC window 7+) or fp64 needs more than the 80 registers of
     // 3 CTAs per SM: 2 CTAs, no spills
     static constexpr int kMinB = (R_ >= DFM_FWD3_WIDE_R || sizeof(T) == 8) ? 2 : DFM_MINB_FWD3,
-                         kCY = 1;
+                         kCY = (sizeof(T) == 4 && R_ <= 2) ? DFM_CY_FWD3 : 1;
     static constexpr bool kStaged = false, kSum = true, kMax = false;
+    static constexpr bool kSlide = DFM_SLIDE != 0;  // box moments: sliding y/z sums
     static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TYv + 2 * R;
     static constexpr int kBytes = BX * BY * int(sizeof(T));
     static constexpr int kBox = align128(kBytes);
@@ -745,32 +827,14 @@ struct LnccFwd3 {
         double e[NE];
 #pragma unroll
         for (int k = 0; k < NE; ++k) e[k] = static_cast<double>(wf[LO + k]);
-#pragma unroll
-        for (int o = 0; o < 4; ++o) {
-            double a = 0;
-#pragma unroll
-            for (int j = 0; j < 2 * R + 1; ++j) a += e[o + j];
-            v[0][o] = a;
-        }
+        box4<R>(e, v[0]);
         double p[NE];
 #pragma unroll
         for (int k = 0; k < NE; ++k) p[k] = __dmul_rn(e[k], e[k]);
-#pragma unroll
-        for (int o = 0; o < 4; ++o) {
-            double a = 0;
-#pragma unroll
-            for (int j = 0; j < 2 * R + 1; ++j) a += p[o + j];
-            v[1][o] = a;
-        }
+        box4<R>(p, v[1]);
 #pragma unroll
         for (int k = 0; k < NE; ++k) p[k] = __dmul_rn(static_cast<double>(ff[LO + k]), e[k]);
-#pragma unroll
-        for (int o = 0; o < 4; ++o) {
-            double a = 0;
-#pragma unroll
-            for (int j = 0; j < 2 * R + 1; ++j) a += p[o + j];
-            v[2][o] = a;
-        }
+        box4<R>(p, v[2]);
     }
     __device__ void xpass(const unsigned char* st_, int row, int col, Acc, Acc v[3]) const {
         const T* F = reinterpret_cast<const T*>(st_) + row * BX + col + (XA - R);
@@ -823,6 +887,7 @@ struct LnccBwd2 {
                          kCY = sizeof(Acc) == 4 ? DFM_CY_BWD
                                               : (sizeof(T) == 4 && R_ <= 2 ? DFM_CY_BWD64 : 1);
     static constexpr bool kStaged = false, kSum = false, kMax = false;
+    static constexpr bool kSlide = DFM_SLIDE != 0 && sizeof(Acc) == 8;  // fp64 sliding sums
     static constexpr int XA = round_bx<T>(R), BX = round_bx<T>(TX + XA + R), BY = TYv + 2 * R;
     static constexpr int kBytes = BX * BY * int(sizeof(T));
     static constexpr int kBox = align128(kBytes);
@@ -858,12 +923,19 @@ struct LnccBwd2 {
             float wv[4 * NCH];
             load_row4<NCH>(reinterpret_cast<const float*>(st_) + c * (kBox / 4) + row * BX + col,
                            wv);
+            if constexpr (kSlide) {
+                double e[4 + 2 * R];
 #pragma unroll
-            for (int o = 0; o < 4; ++o) {
-                Acc a = Acc(0);
+                for (int k = 0; k < 4 + 2 * R; ++k) e[k] = static_cast<double>(wv[(XA - R) + k]);
+                box4<R>(e, v[c]);
+            } else {
 #pragma unroll
-                for (int j = 0; j < 2 * R + 1; ++j) a += static_cast<Acc>(wv[o + (XA - R) + j]);
-                v[c][o] = a;
+                for (int o = 0; o < 4; ++o) {
+                    Acc a = Acc(0);
+#pragma unroll
+                    for (int j = 0; j < 2 * R + 1; ++j) a += static_cast<Acc>(wv[o + (XA - R) + j]);
+                    v[c][o] = a;
+                }
             }
         }
     }
