@@ -688,8 +688,10 @@ template <class T, int R, int RG, int RW>
 struct PersistArgs {
     LnccFwdB<T, R> fwd;
     LnccBwdB<T, R> bwd;
-    SmoothAdamB<T, RG> sa;
-    ComposeB<T, RW> co;  // u -> uout in even iterations, swapped in odd ones
+    // the split update of the graph path: smooth+Adam composes c = step + u(x+step)
+    // once per voxel (u alternates between the two fields), then sigma_warp + W/G
+    SmoothAdamB<T, RG, 1> sa;
+    ComposeSB<T, RW> co;  // c -> uout; uout alternates with sa.uin
     int iters;
     LoopState* st;
     double* loss;
@@ -698,10 +700,10 @@ struct PersistArgs {
     double tol;
 };
 
-constexpr int NTP = 256;  // persistent solver: 2 CTAs of 256 threads per SM
+constexpr int NTP = 256;  // persistent solver: 3 CTAs of 256 threads per SM (one brick each)
 
 template <class T, int R, int RG, int RW>
-__global__ void __launch_bounds__(NTP, 2)
+__global__ void __launch_bounds__(NTP, 3)
     k_persist(const __grid_constant__ PersistArgs<T, R, RG, RW> a, const BG g, int nb) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
@@ -730,7 +732,13 @@ __global__ void __launch_bounds__(NTP, 2)
         if (stop) break;
         for (int b = blockIdx.x; b < nb; b += gridDim.x) brick_body<decltype(a.bwd), NTP>(a.bwd, g, b, smem, s_red);
         grid.sync();  // also publishes CTA 0's st->t / st->slot to the Adam prologue
-        for (int b = blockIdx.x; b < nb; b += gridDim.x) brick_body<decltype(a.sa), NTP>(a.sa, g, b, smem, s_red);
+        SmoothAdamB<T, RG, 1> sa = a.sa;
+        ComposeSB<T, RW> co = a.co;
+        if (it & 1) {  // ping-pong of the field
+            sa.uin = a.co.uout;
+            co.uout = const_cast<T*>(a.sa.uin);
+        }
+        for (int b = blockIdx.x; b < nb; b += gridDim.x) brick_body<decltype(sa), NTP>(sa, g, b, smem, s_red);
         grid.sync();
         if (*reinterpret_cast<volatile int*>(&st->bad_step)) {  // diffeo.cpp:52-53
             if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -738,11 +746,6 @@ __global__ void __launch_bounds__(NTP, 2)
                 st->done = 1;
             }
             break;
-        }
-        ComposeB<T, RW> co = a.co;
-        if (it & 1) {
-            co.u = a.co.uout;
-            co.uout = const_cast<T*>(a.co.u);
         }
         for (int b = blockIdx.x; b < nb; b += gridDim.x) brick_body<decltype(co), NTP>(co, g, b, smem, s_red);
         ++nupd;
@@ -960,15 +963,15 @@ int launch_persist_scale(const Launch& L, const PersistScale<T>& p) {
         a.sa.w = p.wg;
         a.sa.m = p.m;
         a.sa.nu = p.nu;
-        a.sa.step = p.step;
+        a.sa.step = p.step;  // receives c
+        a.sa.uin = p.u0;
         a.sa.ak = adam_k<T>(p.ap);
         a.sa.corr1 = p.ap.corr1;
         a.sa.corr2 = p.ap.corr2;
         a.sa.st = p.st;
         a.sa.maxstep = p.maxstep;
         a.sa.d = p.d;
-        a.co.step = p.step;
-        a.co.u = p.u0;
+        a.co.c = p.step;
         a.co.w = p.ww;
         a.co.uout = p.u1;
         a.co.M = p.M;
@@ -986,7 +989,7 @@ int launch_persist_scale(const Launch& L, const PersistScale<T>& p) {
         a.tol = p.tol;
         return run_persist(L, a, p.d);
     };
-    if (p.rg != 3 || p.rw != 2) return -2;
+    if (p.rg != 3 || p.rw != 2 || p.ap.cap > 0.5) return -2;
     switch (p.lncc_r) {
         case 1: return go(std::integral_constant<int, 1>{});
         case 2: return go(std::integral_constant<int, 2>{});
