@@ -450,6 +450,42 @@ DFM_API dfm_status dfm_dev_register_slab(dfm_ctx* ctx, const dfm_grid* g, const 
                                          int64_t* out_zhi, dfm_iter_record* records,
                                          int64_t max_records, dfm_runlog* log);
 
+/* A caller-provided transport for the slab exchange (no reference
+ * counterpart): the slab loop's three collective steps — halo exchange with
+ * the z neighbours, global sums/maxima for the loss and the convergence
+ * monitor, and the gather of owned blocks at scale changes — go through these
+ * host callbacks on host-staged (pinned) buffers.  It lets a slab
+ * decomposition run across processes without NCCL (e.g. two processes on one
+ * GPU, or a CPU-side messaging layer); the NCCL path keeps its device-side
+ * collectives inside the captured iteration graphs.  Each callback returns 0
+ * on success.  Every rank makes the same sequence of calls. */
+typedef struct dfm_slab_transport {
+    void* user;
+    /* send `send_bytes` to rank `peer` and receive `recv_bytes` from it */
+    int (*sendrecv)(void* user, int peer, const void* sendbuf, int64_t send_bytes,
+                    void* recvbuf, int64_t recv_bytes);
+    /* in-place element-wise sum over all ranks of n doubles */
+    int (*allreduce_sum_f64)(void* user, double* buf, int64_t n);
+    /* in-place element-wise maximum over all ranks of n unsigned 64-bit ints */
+    int (*allreduce_max_u64)(void* user, uint64_t* buf, int64_t n);
+    /* every rank's block (send_bytes; rank r contributes counts[r] bytes) into
+     * recvbuf, concatenated in rank order */
+    int (*allgather)(void* user, const void* sendbuf, int64_t send_bytes, void* recvbuf,
+                     const int64_t* counts);
+} dfm_slab_transport;
+
+/* dfm_dev_register_slab over a caller transport: the same plan, kernels and
+ * call sequence as the NCCL path (world > 1, this process = slab `rank`),
+ * with every collective host-staged through `tp`. */
+DFM_API dfm_status dfm_dev_register_slab_tp(dfm_ctx* ctx, const dfm_grid* g, const void* d_fixed,
+                                            const void* d_moving, const dfm_config* cfg,
+                                            const double* scales, const int32_t* iterations,
+                                            int32_t nscales, int rank, int world,
+                                            const dfm_slab_transport* tp, void* d_out_soa_field,
+                                            int64_t* out_zlo, int64_t* out_zhi,
+                                            dfm_iter_record* records, int64_t max_records,
+                                            dfm_runlog* log);
+
 /* Timing hook for benchmarks: per-kernel-class accumulated device time (ms)
  * and launch counts over the last dfm_register/dfm_dev_register call when
  * profiling is enabled with dfm_ctx_set_profiling(ctx, 1).  Class ids:

@@ -2740,13 +2740,76 @@ int slab_halo(const dfm_config* c) {
 }
 
 template <class T>
+struct SlabRun;
+
+// The slab loop's collective steps, behind one interface:
+//   exchange  halo planes of a buffer with the z neighbours;
+//   gather    every slab's owned planes of (u, m, nu) -> full volumes (scale
+//             changes: the next level is resampled from them);
+//   sum/max   global reductions of device scalars (loss partials, the
+//             non-finite-step flag, the max-step log, the fold count).
+// Three implementations: emulated slabs in one process (device copies),
+// NCCL between processes (device-side, inside the captured graphs), and a
+// caller transport (dfm_slab_transport: host-staged callbacks, eager loop).
+template <class T>
+struct SlabTransport {
+    virtual ~SlabTransport() = default;
+    virtual void exchange(SlabRun<T>& R, int which, int ncomp) = 0;
+    virtual void gather(SlabRun<T>& R, const Dims& ds) = 0;
+    virtual void sum_f64(SlabRun<T>& R, double* dev, int n) = 0;
+    virtual void sum_u64(SlabRun<T>& R, unsigned long long* dev, int n) = 0;
+    virtual void max_u64(SlabRun<T>& R, unsigned long long* dev, int n) = 0;
+    virtual void max_i32(SlabRun<T>& R, int* dev, int n) = 0;
+    virtual bool capturable() const = 0;  // may be recorded into a CUDA graph
+};
+
+template <class T>
+struct EmulatedTransport final : SlabTransport<T> {
+    void exchange(SlabRun<T>& R, int which, int ncomp) override;
+    void gather(SlabRun<T>& R, const Dims& ds) override;
+    void sum_f64(SlabRun<T>&, double*, int) override {}
+    void sum_u64(SlabRun<T>&, unsigned long long*, int) override {}
+    void max_u64(SlabRun<T>&, unsigned long long*, int) override {}
+    void max_i32(SlabRun<T>&, int*, int) override {}
+    bool capturable() const override { return true; }
+};
+
+template <class T>
+struct NcclTransport final : SlabTransport<T> {
+    const NcclApi* nc = nullptr;
+    ncclComm_t comm = nullptr;
+    void exchange(SlabRun<T>& R, int which, int ncomp) override;
+    void gather(SlabRun<T>& R, const Dims& ds) override;
+    void sum_f64(SlabRun<T>& R, double* dev, int n) override;
+    void sum_u64(SlabRun<T>& R, unsigned long long* dev, int n) override;
+    void max_u64(SlabRun<T>& R, unsigned long long* dev, int n) override;
+    void max_i32(SlabRun<T>& R, int* dev, int n) override;
+    bool capturable() const override { return true; }
+};
+
+template <class T>
+struct HostTransport final : SlabTransport<T> {
+    const dfm_slab_transport* tp = nullptr;
+    void exchange(SlabRun<T>& R, int which, int ncomp) override;
+    void gather(SlabRun<T>& R, const Dims& ds) override;
+    void sum_f64(SlabRun<T>& R, double* dev, int n) override;
+    void sum_u64(SlabRun<T>& R, unsigned long long* dev, int n) override;
+    void max_u64(SlabRun<T>& R, unsigned long long* dev, int n) override;
+    void max_i32(SlabRun<T>& R, int* dev, int n) override;
+    bool capturable() const override { return false; }
+    void ck(int rc, const char* what) const {
+        if (rc != 0) fail(DFM_E_CUDA, "slab transport: %s failed (%d)", what, rc);
+    }
+};
+
+template <class T>
 struct SlabRun {
     dfm_ctx* ctx;
     const dfm_grid* g;
     const dfm_config* cfg;
     Dims full;
-    int rank = 0, world = 1, E = 1;  // E local slabs (emulation) or 1 (NCCL)
-    ncclComm_t comm = nullptr;
+    int rank = 0, world = 1, E = 1;  // E local slabs (emulation) or 1 (one per process)
+    SlabTransport<T>* tp = nullptr;
     int H = 0;
 
     struct Part {
@@ -2761,6 +2824,7 @@ struct SlabRun {
         T* u(int k) const { return base[5 + k]; }
         T* m() const { return base[7]; }
         T* nu() const { return base[8]; }
+        double* fstat = nullptr;  // per-level muF, vF of the owned planes (FStats2)
     };
     std::vector<Part> parts;
     T* Fs = nullptr;
@@ -2771,11 +2835,9 @@ struct SlabRun {
            *red = nullptr;
     unsigned long long *maxstep = nullptr, *stamp = nullptr;
     int cur = 0;
-    const NcclApi* nc = nullptr;
 
     int nparts() const { return world > 1 ? world : E; }
     int part_id(int j) const { return world > 1 ? rank : j; }
-    bool is_nccl() const { return world > 1; }
     // plane size of the current slab views (the scale being processed)
     int64_t plane() const { return static_cast<int64_t>(parts.empty() ? full.nx * full.ny
                                                                        : parts[0].dl.nx * parts[0].dl.ny); }
@@ -2791,10 +2853,12 @@ struct SlabRun {
         const int64_t cap = pl * maxn;
         parts.resize(E);
         const int comps[9] = {1, 3, 4, 3, 3, 3, 3, 3, 3};
-        for (int j = 0; j < E; ++j)
+        for (int j = 0; j < E; ++j) {
             for (int k = 0; k < 9; ++k)
                 parts[j].base[k] = ctx->arr<T>("slab" + std::to_string(j) + "_" + std::to_string(k),
                                                comps[k] * cap);
+            parts[j].fstat = ctx->arr<double>("slab" + std::to_string(j) + "_fstat", 2 * cap);
+        }
         Fs = ctx->arr<T>("slab_Fs", full.n);
         Ms = ctx->arr<T>("slab_Ms", full.n);
         for (int k = 0; k < 3; ++k)  // u: also the final gathered field (full grid)
@@ -2838,90 +2902,8 @@ struct SlabRun {
         }
     }
 
-    // copy the owned planes of component buffers into halos of the neighbours
-    void exchange(int which, int ncomp) {
-        const int64_t pl = plane();
-        if (!is_nccl()) {
-            for (int j = 0; j < E; ++j) {
-                const Part& p = parts[j];
-                if (j > 0 && p.b.hlo > 0) {  // lower halo <- part j-1's top owned planes
-                    const Part& q = parts[j - 1];
-                    const int src_local = p.b.zlo - p.b.hlo - q.b.z0g();
-                    for (int c = 0; c < ncomp; ++c)
-                        CK(cudaMemcpyAsync(p.base[which] + c * p.dl.n,
-                                           q.base[which] + c * q.dl.n + src_local * pl,
-                                           sizeof(T) * pl * p.b.hlo, cudaMemcpyDeviceToDevice,
-                                           ctx->stream));
-                }
-                if (j + 1 < E && p.b.hhi > 0) {  // upper halo <- part j+1's bottom owned planes
-                    const Part& q = parts[j + 1];
-                    const int src_local = p.b.zhi - q.b.z0g();
-                    const int dst_local = p.b.hlo + p.b.owned();
-                    for (int c = 0; c < ncomp; ++c)
-                        CK(cudaMemcpyAsync(p.base[which] + c * p.dl.n + dst_local * pl,
-                                           q.base[which] + c * q.dl.n + src_local * pl,
-                                           sizeof(T) * pl * p.b.hhi, cudaMemcpyDeviceToDevice,
-                                           ctx->stream));
-                }
-            }
-            return;
-        }
-        const Part& p = parts[0];
-        const ncclDataType_t dt = sizeof(T) == 4 ? ncclFloat32 : ncclFloat64;
-        nc->ck(nc->GroupStart(), "group");
-        for (int c = 0; c < ncomp; ++c) {
-            T* buf = p.base[which] + c * p.dl.n;
-            if (rank > 0) {  // exchange with the lower neighbour: H planes each way
-                nc->ck(nc->Send(buf + p.b.hlo * pl, pl * p.b.hlo, dt, rank - 1, comm, ctx->stream), "send");
-                nc->ck(nc->Recv(buf, pl * p.b.hlo, dt, rank - 1, comm, ctx->stream), "recv");
-            }
-            if (rank + 1 < world) {
-                const int top = p.b.hlo + p.b.owned();
-                nc->ck(nc->Send(buf + (top - p.b.hhi) * pl, pl * p.b.hhi, dt, rank + 1, comm,
-                                ctx->stream), "send");
-                nc->ck(nc->Recv(buf + top * pl, pl * p.b.hhi, dt, rank + 1, comm, ctx->stream), "recv");
-            }
-        }
-        nc->ck(nc->GroupEnd(), "group");
-    }
-
-    // owned planes of (u[cur], m, nu) of every slab -> full volumes at grid ds
-    void gather(const Dims& ds) {
-        const int64_t pl = static_cast<int64_t>(ds.nx) * ds.ny;
-        T* srcs[3];
-        for (int j = 0; j < E; ++j) {
-            const Part& p = parts[j];
-            srcs[0] = p.u(cur);
-            srcs[1] = p.m();
-            srcs[2] = p.nu();
-            for (int f = 0; f < 3; ++f)
-                for (int c = 0; c < 3; ++c) {
-                    if (!is_nccl())
-                        CK(cudaMemcpyAsync(gath[f] + c * ds.n + static_cast<int64_t>(p.b.zlo) * pl,
-                                           srcs[f] + c * p.dl.n + p.b.hlo * pl,
-                                           sizeof(T) * pl * p.b.owned(), cudaMemcpyDeviceToDevice,
-                                           ctx->stream));
-                }
-        }
-        if (is_nccl()) {  // every rank broadcasts its owned block to all
-            const Part& p = parts[0];
-            srcs[0] = p.u(cur);
-            srcs[1] = p.m();
-            srcs[2] = p.nu();
-            const ncclDataType_t dt = sizeof(T) == 4 ? ncclFloat32 : ncclFloat64;
-            nc->ck(nc->GroupStart(), "group");
-            for (int r = 0; r < world; ++r) {
-                const SlabBounds b = slab_bounds(ds.nz, r, world, H);
-                for (int f = 0; f < 3; ++f)
-                    for (int c = 0; c < 3; ++c)
-                        nc->ck(nc->Broadcast(srcs[f] + c * p.dl.n + p.b.hlo * pl,
-                                             gath[f] + c * ds.n + static_cast<int64_t>(b.zlo) * pl,
-                                             pl * b.owned(), dt, r, comm, ctx->stream),
-                               "broadcast");
-            }
-            nc->ck(nc->GroupEnd(), "group");
-        }
-    }
+    void exchange(int which, int ncomp) { tp->exchange(*this, which, ncomp); }
+    void gather(const Dims& ds) { tp->gather(*this, ds); }
 
     // full volumes at grid from -> every slab's local planes at grid to
     void scatter_resample(const Dims& from, const Dims& to, bool with_state) {
@@ -2955,30 +2937,34 @@ struct SlabRun {
     double global_sum(const double* part_sums, int np) {
         // fixed-order device reduction, then (NCCL) a sum over ranks
         launch_reduce_value(ctx->L(), 0, part_sums, np, 1.0, red);
-        if (is_nccl())
-            nc->ck(nc->AllReduce(red, red, 1, ncclFloat64, ncclSum, comm, ctx->stream), "allreduce");
+        if (world > 1) tp->sum_f64(*this, red, 1);
         double h[3];
         CK(cudaMemcpyAsync(h, red, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
         ctx->sync();
         return h[0];
     }
 
+    // one iteration on every local slab: the monolithic loop's large-level
+    // kernels (3-moment LNCC forward on the level's F statistics, backward,
+    // smooth+Adam, radius-0 compose, compose-smooth + W/G) with the halo of
+    // each produced buffer exchanged before its consumer
     void enqueue_iteration(const Dims& ds, int src, int Rg, int Rw, const GaussW<T>& wg,
-                           const GaussW<T>& ww) {
+                           const GaussW<T>& ww, const GaussW<T>& wid) {
         Launch L = ctx->L();
         const int64_t pl = static_cast<int64_t>(ds.nx) * ds.ny;
         const double N = static_cast<double>(ds.n);
         int off = 0;
         for (int j = 0; j < E; ++j) {
             Part& p = parts[j];
-            const int np = launch_lncc_fwd_tma<T>(L, cfg->lncc_radius, Fs + p.b.z0g() * pl, p.W(),
-                                                  p.dl, p.coef(), partials + off, st);
+            const int np = launch_lncc_fwd3_tma<T>(L, cfg->lncc_radius, Fs + p.b.z0g() * pl,
+                                                   p.W(), p.fstat, p.dl, p.coef(), partials + off,
+                                                   st, nullptr);
             if (np < 0) fail(DFM_E_CUDA, "slab: lncc forward launch failed");
             off += np;
         }
-        if (is_nccl()) {
+        if (world > 1) {
             launch_reduce_value(L, 0, partials, off, 1.0, red);
-            nc->ck(nc->AllReduce(red, red, 1, ncclFloat64, ncclSum, comm, ctx->stream), "allreduce");
+            tp->sum_f64(*this, red, 1);
             launch_monitor(L, 1, red, 1, N, st, loss, stamp, cfg->conv_window, cfg->conv_tol);
         } else {
             launch_monitor(L, 1, partials, off, N, st, loss, stamp, cfg->conv_window, cfg->conv_tol);
@@ -2991,16 +2977,22 @@ struct SlabRun {
         AdamParams ap{cfg->beta1, cfg->beta2, cfg->eps_adam, cfg->eta, cfg->step_cap,
                       corr1, corr2, cfg->use_jac};
         for (Part& p : parts)
-            launch_smooth_adam_tma<T>(L, Rg, wg, p.grad(), p.m(), p.nu(), p.step(), p.dl, ap, st,
-                                      maxstep);
-        if (is_nccl())  // a non-finite step anywhere aborts everywhere
-            nc->ck(nc->AllReduce(&st->bad_step, &st->bad_step, 1, ncclInt32, ncclMax, comm,
-                                 ctx->stream), "allreduce");
-        exchange(4, 3);  // step
+            if (launch_smooth_adam_tma<T>(L, Rg, wg, p.grad(), p.m(), p.nu(), p.step(), p.dl, ap,
+                                          st, maxstep) < 0)
+                fail(DFM_E_CUDA, "slab: smooth+Adam launch failed");
+        if (world > 1) tp->max_i32(*this, &st->bad_step, 1);  // a non-finite step aborts everywhere
+        // c = step + u(x + step) on the owned planes (the u halo covers the
+        // gather reach), into the dead gradient buffer
+        for (Part& p : parts)
+            if (launch_compose_tma<T>(L, 0, cfg->step_cap, wid, p.step(), p.u(src), p.grad(), Ms, ds,
+                                      p.dl, nullptr, nullptr, st, false) < 0)
+                fail(DFM_E_CUDA, "slab: compose launch failed");
+        exchange(3, 3);  // c
         for (int j = 0; j < E; ++j) {
             Part& p = parts[j];
-            launch_compose_tma<T>(L, Rw, cfg->step_cap, ww, p.step(), p.u(src), p.u(1 - src), Ms,
-                                  ds, p.dl, p.W(), p.G(), st, j == 0);
+            if (launch_compose_smooth_tma<T>(L, Rw, ww, p.grad(), p.u(1 - src), Ms, ds, p.dl, p.W(),
+                                             p.G(), st, j == 0) < 0)
+                fail(DFM_E_CUDA, "slab: compose-smooth launch failed");
         }
         exchange(6 - src, 3);  // u (the buffer just written)
         exchange(0, 1);        // W
@@ -3011,6 +3003,8 @@ struct SlabRun {
         const double t0 = now_ms();
         if (cfg->loss != DFM_LOSS_LNCC || cfg->use_jac || cfg->mode != DFM_MODE_DIRECT)
             fail(DFM_E_INVALID, "slab decomposition: direct mode, LNCC loss, use_jac off only");
+        if (cfg->step_cap > 1.5)
+            fail(DFM_E_INVALID, "slab decomposition: step_cap <= 1.5 only");
         if (!tma_supported(full, sizeof(T)))
             fail(DFM_E_INVALID, "slab decomposition: x extent must be a multiple of 16 bytes");
         if (full.ndim != 3) fail(DFM_E_INVALID, "slab decomposition: 3-D volumes only");
@@ -3062,10 +3056,15 @@ struct SlabRun {
             prev = ds;
             const int T_si = iters[si];
             if (T_si == 0) continue;
-            for (Part& p : parts)
+            for (Part& p : parts) {
                 launch_warpgrad<T>(ctx->L(), Ms, ds, CPlanes3<T>{{p.u(cur), p.u(cur) + p.dl.n,
                                                                   p.u(cur) + 2 * p.dl.n}},
                                    [&] { Dims a = p.dl; a.zb = a.ze = 0; return a; }(), p.W(), p.G());
+                // the level's F window statistics of the owned planes
+                if (launch_fstats_tma<T>(ctx->L(), cfg->lncc_radius, Fs + p.b.z0g() * plane(),
+                                         p.dl, p.fstat) < 0)
+                    fail(DFM_E_CUDA, "slab: F statistics launch failed");
+            }
             CK(cudaMemsetAsync(st, 0, offsetof(LoopState, t), ctx->stream));
             CK(cudaMemsetAsync(maxstep, 0, sizeof(unsigned long long) * (T_si + 1), ctx->stream));
             const double sg[3] = {cfg->sigma_grad, cfg->sigma_grad, cfg->sigma_grad};
@@ -3075,38 +3074,52 @@ struct SlabRun {
                 fail(DFM_E_INVALID, "slab decomposition: sigma_grad <= 2, sigma_warp <= 1.33 only");
             const GaussW<T> wg = upload_gauss<T>(ctx, hg, ds, "slab_g");
             const GaussW<T> ww = upload_gauss<T>(ctx, hw, ds, "slab_w");
+            const double zero[3] = {0, 0, 0};
+            const GaussW<T> wid = upload_gauss<T>(ctx, make_gauss(ds, zero), ds, "slab_id");
             const int start = cur;
-            cudaGraphExec_t exec[2] = {nullptr, nullptr};
-            for (int v = 0; v < 2; ++v) {
-                cudaGraph_t graph;
-                CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
-                enqueue_iteration(ds, (start + v) % 2, hg.R, hw.R, wg, ww);
-                CK(cudaStreamEndCapture(ctx->stream, &graph));
-                CK(cudaGraphInstantiate(&exec[v], graph, 0));
-                CK(cudaGraphDestroy(graph));
-            }
-            // every rank launches the same number of graphs (global decisions)
             LoopState* hst = ctx->pinned_state();
-            int nchunk = 0;
-            for (int j = 0; j < T_si;) {
-                if (nchunk >= 2) {
-                    const int w = (nchunk - 2) % 2;
-                    CK(cudaEventSynchronize(ctx->chunk_ev[w]));
-                    if (hst[w].done) break;
+            if (tp->capturable()) {
+                cudaGraphExec_t exec[2] = {nullptr, nullptr};
+                for (int v = 0; v < 2; ++v) {
+                    cudaGraph_t graph;
+                    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
+                    enqueue_iteration(ds, (start + v) % 2, hg.R, hw.R, wg, ww, wid);
+                    CK(cudaStreamEndCapture(ctx->stream, &graph));
+                    CK(cudaGraphInstantiate(&exec[v], graph, 0));
+                    CK(cudaGraphDestroy(graph));
                 }
-                const int jend = std::min(j + 16, T_si);
-                for (; j < jend; ++j) CK(cudaGraphLaunch(exec[j % 2], ctx->stream));
-                const int w = nchunk % 2;
-                CK(cudaMemcpyAsync(&hst[w], st, sizeof(LoopState), cudaMemcpyDeviceToHost, ctx->stream));
-                CK(cudaEventRecord(ctx->chunk_ev[w], ctx->stream));
-                ++nchunk;
+                // every rank launches the same number of graphs (global decisions)
+                int nchunk = 0;
+                for (int j = 0; j < T_si;) {
+                    if (nchunk >= 2) {
+                        const int w = (nchunk - 2) % 2;
+                        CK(cudaEventSynchronize(ctx->chunk_ev[w]));
+                        if (hst[w].done) break;
+                    }
+                    const int jend = std::min(j + 16, T_si);
+                    for (; j < jend; ++j) CK(cudaGraphLaunch(exec[j % 2], ctx->stream));
+                    const int w = nchunk % 2;
+                    CK(cudaMemcpyAsync(&hst[w], st, sizeof(LoopState), cudaMemcpyDeviceToHost,
+                                       ctx->stream));
+                    CK(cudaEventRecord(ctx->chunk_ev[w], ctx->stream));
+                    ++nchunk;
+                }
+                ctx->sync();
+                for (int v = 0; v < 2; ++v) CK(cudaGraphExecDestroy(exec[v]));
+            } else {
+                // host-staged transport: eager iterations (its collectives
+                // synchronise); the global monitor decides on every rank alike
+                for (int j = 0; j < T_si; ++j) {
+                    enqueue_iteration(ds, (start + j) % 2, hg.R, hw.R, wg, ww, wid);
+                    CK(cudaMemcpyAsync(&hst[0], st, sizeof(LoopState), cudaMemcpyDeviceToHost,
+                                       ctx->stream));
+                    ctx->sync();
+                    if (hst[0].done) break;
+                }
             }
             launch_stamp(ctx->L(), stamp + T_si);
-            if (is_nccl())  // max |step| of the log over ranks
-                nc->ck(nc->AllReduce(maxstep, maxstep, T_si, ncclUint64, ncclMax, comm, ctx->stream),
-                       "allreduce");
+            if (world > 1) tp->max_u64(*this, maxstep, T_si);  // max |step| of the log over ranks
             ctx->sync();
-            for (int v = 0; v < 2; ++v) CK(cudaGraphExecDestroy(exec[v]));
             LoopState hs;
             std::vector<double> hl(T_si + 1);
             std::vector<unsigned long long> hm(T_si + 1), ht(T_si + 1);
@@ -3166,8 +3179,7 @@ struct SlabRun {
             launch_jacobian_det<T>(ctx->L(), CPlanes3<T>{{p.u(cur), p.u(cur) + p.dl.n,
                                                           p.u(cur) + 2 * p.dl.n}},
                                    p.dl, nullptr, cnt);
-        if (is_nccl())
-            nc->ck(nc->AllReduce(cnt, cnt, 1, ncclUint64, ncclSum, comm, ctx->stream), "allreduce");
+        if (world > 1) tp->sum_u64(*this, cnt, 1);
         unsigned long long hc = 0;
         CK(cudaMemcpyAsync(&hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream));
         // result planes
@@ -3187,6 +3199,221 @@ struct SlabRun {
         if (ozhi) *ozhi = zhi;
     }
 };
+
+// ---- emulated slabs: device copies between the parts of one process
+template <class T>
+void EmulatedTransport<T>::exchange(SlabRun<T>& R, int which, int ncomp) {
+    const int64_t pl = R.plane();
+    for (int j = 0; j < R.E; ++j) {
+        auto& p = R.parts[j];
+        if (j > 0 && p.b.hlo > 0) {  // lower halo <- part j-1's top owned planes
+            const auto& q = R.parts[j - 1];
+            const int src_local = p.b.zlo - p.b.hlo - q.b.z0g();
+            for (int c = 0; c < ncomp; ++c)
+                CK(cudaMemcpyAsync(p.base[which] + c * p.dl.n,
+                                   q.base[which] + c * q.dl.n + src_local * pl,
+                                   sizeof(T) * pl * p.b.hlo, cudaMemcpyDeviceToDevice,
+                                   R.ctx->stream));
+        }
+        if (j + 1 < R.E && p.b.hhi > 0) {  // upper halo <- part j+1's bottom owned planes
+            const auto& q = R.parts[j + 1];
+            const int src_local = p.b.zhi - q.b.z0g();
+            const int dst_local = p.b.hlo + p.b.owned();
+            for (int c = 0; c < ncomp; ++c)
+                CK(cudaMemcpyAsync(p.base[which] + c * p.dl.n + dst_local * pl,
+                                   q.base[which] + c * q.dl.n + src_local * pl,
+                                   sizeof(T) * pl * p.b.hhi, cudaMemcpyDeviceToDevice,
+                                   R.ctx->stream));
+        }
+    }
+}
+
+template <class T>
+void EmulatedTransport<T>::gather(SlabRun<T>& R, const Dims& ds) {
+    const int64_t pl = static_cast<int64_t>(ds.nx) * ds.ny;
+    for (int j = 0; j < R.E; ++j) {
+        const auto& p = R.parts[j];
+        const T* srcs[3] = {p.u(R.cur), p.m(), p.nu()};
+        for (int f = 0; f < 3; ++f)
+            for (int c = 0; c < 3; ++c)
+                CK(cudaMemcpyAsync(R.gath[f] + c * ds.n + static_cast<int64_t>(p.b.zlo) * pl,
+                                   srcs[f] + c * p.dl.n + p.b.hlo * pl,
+                                   sizeof(T) * pl * p.b.owned(), cudaMemcpyDeviceToDevice,
+                                   R.ctx->stream));
+    }
+}
+
+// ---- NCCL between processes (device-side, capturable)
+template <class T>
+void NcclTransport<T>::exchange(SlabRun<T>& R, int which, int ncomp) {
+    const int64_t pl = R.plane();
+    const auto& p = R.parts[0];
+    const ncclDataType_t dt = sizeof(T) == 4 ? ncclFloat32 : ncclFloat64;
+    nc->ck(nc->GroupStart(), "group");
+    for (int c = 0; c < ncomp; ++c) {
+        T* buf = p.base[which] + c * p.dl.n;
+        if (R.rank > 0) {  // exchange with the lower neighbour: H planes each way
+            nc->ck(nc->Send(buf + p.b.hlo * pl, pl * p.b.hlo, dt, R.rank - 1, comm, R.ctx->stream),
+                   "send");
+            nc->ck(nc->Recv(buf, pl * p.b.hlo, dt, R.rank - 1, comm, R.ctx->stream), "recv");
+        }
+        if (R.rank + 1 < R.world) {
+            const int top = p.b.hlo + p.b.owned();
+            nc->ck(nc->Send(buf + (top - p.b.hhi) * pl, pl * p.b.hhi, dt, R.rank + 1, comm,
+                            R.ctx->stream), "send");
+            nc->ck(nc->Recv(buf + top * pl, pl * p.b.hhi, dt, R.rank + 1, comm, R.ctx->stream),
+                   "recv");
+        }
+    }
+    nc->ck(nc->GroupEnd(), "group");
+}
+
+template <class T>
+void NcclTransport<T>::gather(SlabRun<T>& R, const Dims& ds) {
+    const int64_t pl = static_cast<int64_t>(ds.nx) * ds.ny;
+    const auto& p = R.parts[0];
+    const T* srcs[3] = {p.u(R.cur), p.m(), p.nu()};
+    const ncclDataType_t dt = sizeof(T) == 4 ? ncclFloat32 : ncclFloat64;
+    nc->ck(nc->GroupStart(), "group");
+    for (int r = 0; r < R.world; ++r) {  // every rank broadcasts its owned block to all
+        const SlabBounds b = slab_bounds(ds.nz, r, R.world, R.H);
+        for (int f = 0; f < 3; ++f)
+            for (int c = 0; c < 3; ++c)
+                nc->ck(nc->Broadcast(srcs[f] + c * p.dl.n + p.b.hlo * pl,
+                                     R.gath[f] + c * ds.n + static_cast<int64_t>(b.zlo) * pl,
+                                     pl * b.owned(), dt, r, comm, R.ctx->stream),
+                       "broadcast");
+    }
+    nc->ck(nc->GroupEnd(), "group");
+}
+
+template <class T>
+void NcclTransport<T>::sum_f64(SlabRun<T>& R, double* dev, int n) {
+    nc->ck(nc->AllReduce(dev, dev, n, ncclFloat64, ncclSum, comm, R.ctx->stream), "allreduce");
+}
+template <class T>
+void NcclTransport<T>::sum_u64(SlabRun<T>& R, unsigned long long* dev, int n) {
+    nc->ck(nc->AllReduce(dev, dev, n, ncclUint64, ncclSum, comm, R.ctx->stream), "allreduce");
+}
+template <class T>
+void NcclTransport<T>::max_u64(SlabRun<T>& R, unsigned long long* dev, int n) {
+    nc->ck(nc->AllReduce(dev, dev, n, ncclUint64, ncclMax, comm, R.ctx->stream), "allreduce");
+}
+template <class T>
+void NcclTransport<T>::max_i32(SlabRun<T>& R, int* dev, int n) {
+    nc->ck(nc->AllReduce(dev, dev, n, ncclInt32, ncclMax, comm, R.ctx->stream), "allreduce");
+}
+
+// ---- caller transport: host-staged through pinned buffers (eager loop)
+template <class T>
+void HostTransport<T>::exchange(SlabRun<T>& R, int which, int ncomp) {
+    const int64_t pl = R.plane();
+    const auto& p = R.parts[0];
+    const int top = p.b.hlo + p.b.owned();
+    struct Side {
+        int peer, n;       // neighbour rank, planes each way
+        int send0, recv0;  // first local plane sent / received
+        const char* name;
+    };
+    Side sides[2] = {{R.rank - 1, p.b.hlo, p.b.hlo, 0, "lo"},
+                     {R.rank + 1, p.b.hhi, top - p.b.hhi, top, "hi"}};
+    for (const Side& sd : sides) {
+        if (sd.peer < 0 || sd.peer >= R.world || sd.n == 0) continue;
+        const int64_t blk = pl * sd.n;  // elements per component
+        const int64_t bytes = static_cast<int64_t>(sizeof(T)) * blk * ncomp;
+        T* hs = static_cast<T*>(R.ctx->get_pinned(std::string("slab_tx_") + sd.name, bytes));
+        T* hr = static_cast<T*>(R.ctx->get_pinned(std::string("slab_rx_") + sd.name, bytes));
+        for (int c = 0; c < ncomp; ++c)
+            CK(cudaMemcpyAsync(hs + c * blk, p.base[which] + c * p.dl.n + sd.send0 * pl,
+                               sizeof(T) * blk, cudaMemcpyDeviceToHost, R.ctx->stream));
+        R.ctx->sync();
+        ck(tp->sendrecv(tp->user, sd.peer, hs, bytes, hr, bytes), "sendrecv");
+        for (int c = 0; c < ncomp; ++c)
+            CK(cudaMemcpyAsync(p.base[which] + c * p.dl.n + sd.recv0 * pl, hr + c * blk,
+                               sizeof(T) * blk, cudaMemcpyHostToDevice, R.ctx->stream));
+        R.ctx->sync();  // the staging buffers are reused by the next exchange
+    }
+}
+
+template <class T>
+void HostTransport<T>::gather(SlabRun<T>& R, const Dims& ds) {
+    const int64_t pl = static_cast<int64_t>(ds.nx) * ds.ny;
+    const auto& p = R.parts[0];
+    const T* srcs[3] = {p.u(R.cur), p.m(), p.nu()};
+    std::vector<int64_t> counts(R.world);
+    int64_t total = 0;
+    for (int r = 0; r < R.world; ++r) {
+        counts[r] = static_cast<int64_t>(sizeof(T)) * 9 * pl * slab_bounds(ds.nz, r, R.world, R.H).owned();
+        total += counts[r];
+    }
+    const int64_t mine = pl * p.b.owned();
+    T* hs = static_cast<T*>(R.ctx->get_pinned("slab_gather_tx", counts[R.rank]));
+    T* hr = static_cast<T*>(R.ctx->get_pinned("slab_gather_rx", total));
+    for (int f = 0; f < 3; ++f)
+        for (int c = 0; c < 3; ++c)
+            CK(cudaMemcpyAsync(hs + (f * 3 + c) * mine, srcs[f] + c * p.dl.n + p.b.hlo * pl,
+                               sizeof(T) * mine, cudaMemcpyDeviceToHost, R.ctx->stream));
+    R.ctx->sync();
+    ck(tp->allgather(tp->user, hs, counts[R.rank], hr, counts.data()), "allgather");
+    const T* q = hr;
+    for (int r = 0; r < R.world; ++r) {
+        const SlabBounds b = slab_bounds(ds.nz, r, R.world, R.H);
+        const int64_t own = pl * b.owned();
+        for (int f = 0; f < 3; ++f)
+            for (int c = 0; c < 3; ++c)
+                CK(cudaMemcpyAsync(R.gath[f] + c * ds.n + static_cast<int64_t>(b.zlo) * pl,
+                                   q + (f * 3 + c) * own, sizeof(T) * own, cudaMemcpyHostToDevice,
+                                   R.ctx->stream));
+        q += 9 * own;
+    }
+    R.ctx->sync();
+}
+
+template <class T>
+void HostTransport<T>::sum_f64(SlabRun<T>& R, double* dev, int n) {
+    std::vector<double> h(n);
+    CK(cudaMemcpyAsync(h.data(), dev, sizeof(double) * n, cudaMemcpyDeviceToHost, R.ctx->stream));
+    R.ctx->sync();
+    ck(tp->allreduce_sum_f64(tp->user, h.data(), n), "allreduce_sum_f64");
+    CK(cudaMemcpyAsync(dev, h.data(), sizeof(double) * n, cudaMemcpyHostToDevice, R.ctx->stream));
+    R.ctx->sync();
+}
+
+template <class T>
+void HostTransport<T>::max_u64(SlabRun<T>& R, unsigned long long* dev, int n) {
+    std::vector<uint64_t> h(n);
+    CK(cudaMemcpyAsync(h.data(), dev, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, R.ctx->stream));
+    R.ctx->sync();
+    ck(tp->allreduce_max_u64(tp->user, h.data(), n), "allreduce_max_u64");
+    CK(cudaMemcpyAsync(dev, h.data(), sizeof(uint64_t) * n, cudaMemcpyHostToDevice, R.ctx->stream));
+    R.ctx->sync();
+}
+
+template <class T>
+void HostTransport<T>::sum_u64(SlabRun<T>& R, unsigned long long* dev, int n) {
+    // counts (far below 2^53): summed exactly as doubles
+    std::vector<uint64_t> h(n);
+    CK(cudaMemcpyAsync(h.data(), dev, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, R.ctx->stream));
+    R.ctx->sync();
+    std::vector<double> d(h.begin(), h.end());
+    ck(tp->allreduce_sum_f64(tp->user, d.data(), n), "allreduce_sum_f64");
+    for (int k = 0; k < n; ++k) h[k] = static_cast<uint64_t>(d[k]);
+    CK(cudaMemcpyAsync(dev, h.data(), sizeof(uint64_t) * n, cudaMemcpyHostToDevice, R.ctx->stream));
+    R.ctx->sync();
+}
+
+template <class T>
+void HostTransport<T>::max_i32(SlabRun<T>& R, int* dev, int n) {
+    std::vector<int> h(n);
+    CK(cudaMemcpyAsync(h.data(), dev, sizeof(int) * n, cudaMemcpyDeviceToHost, R.ctx->stream));
+    R.ctx->sync();
+    std::vector<uint64_t> u(n);
+    for (int k = 0; k < n; ++k) u[k] = static_cast<uint64_t>(static_cast<int64_t>(h[k]) + (int64_t(1) << 31));
+    ck(tp->allreduce_max_u64(tp->user, u.data(), n), "allreduce_max_u64");
+    for (int k = 0; k < n; ++k) h[k] = static_cast<int>(static_cast<int64_t>(u[k]) - (int64_t(1) << 31));
+    CK(cudaMemcpyAsync(dev, h.data(), sizeof(int) * n, cudaMemcpyHostToDevice, R.ctx->stream));
+    R.ctx->sync();
+}
 
 }  // namespace
 
@@ -3216,13 +3443,17 @@ dfm_status dfm_slab_unique_id(unsigned char id[128]) {
     });
 }
 
-dfm_status dfm_dev_register_slab(dfm_ctx* ctx, const dfm_grid* g, const void* d_fixed,
-                                 const void* d_moving, const dfm_config* cfg,
-                                 const double* scales, const int32_t* iterations,
-                                 int32_t nscales, int rank, int world,
-                                 const unsigned char* nccl_id, int emulate,
-                                 void* d_out_soa_field, int64_t* out_zlo, int64_t* out_zhi,
-                                 dfm_iter_record* records, int64_t max_records, dfm_runlog* log) {
+}  // extern "C"
+
+namespace {
+
+dfm_status register_slab_impl(dfm_ctx* ctx, const dfm_grid* g, const void* d_fixed,
+                              const void* d_moving, const dfm_config* cfg, const double* scales,
+                              const int32_t* iterations, int32_t nscales, int rank, int world,
+                              const unsigned char* nccl_id, int emulate,
+                              const dfm_slab_transport* tp, void* d_out_soa_field,
+                              int64_t* out_zlo, int64_t* out_zhi, dfm_iter_record* records,
+                              int64_t max_records, dfm_runlog* log) {
     return guarded([&] {
         validate_grid(g);
         validate_config(cfg);
@@ -3240,28 +3471,68 @@ dfm_status dfm_dev_register_slab(dfm_ctx* ctx, const dfm_grid* g, const void* d_
             R.rank = rank;
             R.world = world;
             R.E = world > 1 ? 1 : std::max(1, emulate);
-            if (world > 1) {
+            EmulatedTransport<T> emu;
+            NcclTransport<T> ncx;
+            HostTransport<T> host;
+            if (tp) {
+                host.tp = tp;
+                R.tp = &host;
+            } else if (world > 1) {
                 if (!nccl_id) fail(DFM_E_INVALID, "slab: nccl_id required when world > 1");
                 NcclApi& api = nccl_api();
                 api.load();
                 ncclUniqueId u;
                 std::memcpy(u.internal, nccl_id, 128);
-                api.ck(api.CommInitRank(&R.comm, world, u, rank), "comm init");
-                R.nc = &api;
+                api.ck(api.CommInitRank(&ncx.comm, world, u, rank), "comm init");
+                ncx.nc = &api;
+                R.tp = &ncx;
+            } else {
+                R.tp = &emu;
             }
             try {
                 R.run(static_cast<const T*>(d_fixed), static_cast<const T*>(d_moving), scales,
                       iterations, nscales, o, static_cast<T*>(d_out_soa_field), out_zlo, out_zhi);
             } catch (...) {
-                if (R.comm) R.nc->CommDestroy(R.comm);
+                if (ncx.comm) ncx.nc->CommDestroy(ncx.comm);
                 throw;
             }
-            if (R.comm) R.nc->CommDestroy(R.comm);
+            if (ncx.comm) ncx.nc->CommDestroy(ncx.comm);
         });
         fill_log(o, records, max_records, log);
         if (o.sing > 0.0)
             fail(DFM_E_NUMERICAL, "register_images: folded warp (det J <= 0 somewhere)");
     });
+}
+
+}  // namespace
+
+extern "C" {
+
+dfm_status dfm_dev_register_slab(dfm_ctx* ctx, const dfm_grid* g, const void* d_fixed,
+                                 const void* d_moving, const dfm_config* cfg,
+                                 const double* scales, const int32_t* iterations,
+                                 int32_t nscales, int rank, int world,
+                                 const unsigned char* nccl_id, int emulate,
+                                 void* d_out_soa_field, int64_t* out_zlo, int64_t* out_zhi,
+                                 dfm_iter_record* records, int64_t max_records, dfm_runlog* log) {
+    return register_slab_impl(ctx, g, d_fixed, d_moving, cfg, scales, iterations, nscales, rank,
+                              world, nccl_id, emulate, nullptr, d_out_soa_field, out_zlo, out_zhi,
+                              records, max_records, log);
+}
+
+dfm_status dfm_dev_register_slab_tp(dfm_ctx* ctx, const dfm_grid* g, const void* d_fixed,
+                                    const void* d_moving, const dfm_config* cfg,
+                                    const double* scales, const int32_t* iterations,
+                                    int32_t nscales, int rank, int world,
+                                    const dfm_slab_transport* tp, void* d_out_soa_field,
+                                    int64_t* out_zlo, int64_t* out_zhi, dfm_iter_record* records,
+                                    int64_t max_records, dfm_runlog* log) {
+    if (!tp || !tp->sendrecv || !tp->allreduce_sum_f64 || !tp->allreduce_max_u64 ||
+        !tp->allgather)
+        return dfm_internal_set_error(DFM_E_INVALID, "slab transport: missing callback");
+    return register_slab_impl(ctx, g, d_fixed, d_moving, cfg, scales, iterations, nscales, rank,
+                              world, nullptr, 1, tp, d_out_soa_field, out_zlo, out_zhi, records,
+                              max_records, log);
 }
 
 }  // extern "C"

@@ -40,6 +40,7 @@ EXPORTS = [
     "dfm_mhd_read_labels", "dfm_mhd_write_field", "dfm_mhd_read_field", "dfm_dev_load_image_mhd",
     "dfm_dev_save_field_mhd", "dfm_ctx_debug_read", "dfm_sample_field_points", "dfm_jacobian",
     "dfm_upsample_field_cubic", "dfm_sgd_step", "dfm_validate_config", "dfm_validate_schedule",
+    "dfm_dev_register_slab_tp",
 ]
 
 OPT_BRICK_MAX = 1
@@ -51,6 +52,19 @@ OPT_SPLIT_FOLD_MAX = 6
 OPT_LARGE_MIN = 7
 
 _lib: Optional[C.CDLL] = None
+
+# dfm_slab_transport (difform_gpu.h): host callbacks of a caller transport
+_SENDRECV = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p,
+                        C.c_int64)
+_SUM_F64 = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int64)
+_MAX_U64 = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint64), C.c_int64)
+_ALLGATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                         C.POINTER(C.c_int64))
+
+
+class SlabTransportC(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("sendrecv", _SENDRECV), ("allreduce_sum_f64", _SUM_F64),
+                ("allreduce_max_u64", _MAX_U64), ("allgather", _ALLGATHER)]
 
 
 def load_library(path: str = LIB_PATH) -> C.CDLL:
@@ -126,6 +140,12 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
             C.POINTER(C.c_int64), C.POINTER(A.dfm_iter_record), C.c_int64,
             C.POINTER(A.dfm_runlog)]
         lib.dfm_dev_register_slab.restype = C.c_int
+        lib.dfm_dev_register_slab_tp.argtypes = reg + [
+            C.POINTER(A.dfm_config), C.POINTER(C.c_double), C.POINTER(C.c_int32), C.c_int32,
+            C.c_int, C.c_int, C.POINTER(SlabTransportC), C.c_void_p, C.POINTER(C.c_int64),
+            C.POINTER(C.c_int64), C.POINTER(A.dfm_iter_record), C.c_int64,
+            C.POINTER(A.dfm_runlog)]
+        lib.dfm_dev_register_slab_tp.restype = C.c_int
         _lib = lib
     return _lib
 
@@ -287,6 +307,96 @@ def register_slab(ctx: "Context", g: A.GridMeta, d_fixed: int, d_moving: int,
         emulate, C.c_void_p(d_out) if d_out else None, C.byref(zlo), C.byref(zhi), recs, cap,
         C.byref(rl))
     ctx.t.check(rc, "register_slab")
+    return zlo.value, zhi.value, A.records_to_log(recs, rl)
+
+
+class TorchDistTransport:
+    """dfm_slab_transport over torch.distributed (any backend with CPU tensors,
+    e.g. gloo): the host-staged collectives of a slab decomposition between
+    processes — no NCCL needed, so two ranks may share one GPU."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+
+        def _bytes(ptr, n):
+            import torch
+            a = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_uint8)), shape=(int(n),))
+            return torch.from_numpy(a)
+
+        def sendrecv(_, peer, sbuf, sbytes, rbuf, rbytes):
+            try:
+                s = _bytes(sbuf, sbytes)
+                r = _bytes(rbuf, rbytes)
+                reqs = [dist.isend(s, peer, group=group), dist.irecv(r, peer, group=group)]
+                for q in reqs:
+                    q.wait()
+                return 0
+            except Exception:  # noqa: BLE001 - reported as a status code
+                return 1
+
+        def sum_f64(_, buf, n):
+            try:
+                import torch
+                t = torch.from_numpy(np.ctypeslib.as_array(buf, shape=(int(n),)))
+                dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        def max_u64(_, buf, n):
+            try:
+                import torch
+                a = np.ctypeslib.as_array(buf, shape=(int(n),))
+                t = torch.from_numpy(a.view(np.int64))  # < 2^63 here: same order
+                dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        def allgather(_, sbuf, sbytes, rbuf, counts):
+            try:
+                import torch
+                world = dist.get_world_size(group)
+                cnt = [int(counts[r]) for r in range(world)]
+                mx = max(cnt)
+                s = torch.zeros(mx, dtype=torch.uint8)
+                s[:int(sbytes)] = _bytes(sbuf, sbytes)
+                outs = [torch.empty(mx, dtype=torch.uint8) for _ in range(world)]
+                dist.all_gather(outs, s, group=group)
+                r = _bytes(rbuf, sum(cnt))
+                off = 0
+                for k in range(world):
+                    r[off:off + cnt[k]] = outs[k][:cnt[k]]
+                    off += cnt[k]
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        # keep the ctypes callbacks alive as long as the transport
+        self._cb = (_SENDRECV(sendrecv), _SUM_F64(sum_f64), _MAX_U64(max_u64),
+                    _ALLGATHER(allgather))
+        self.c = SlabTransportC(None, *self._cb)
+
+
+def register_slab_tp(ctx: "Context", g: A.GridMeta, d_fixed: int, d_moving: int,
+                     cfg: A.RegistrationConfig, sched: A.PyramidSchedule, rank: int, world: int,
+                     transport: TorchDistTransport, d_out: int = 0):
+    """dfm_dev_register_slab_tp: this process = slab `rank` of `world`, every
+    collective through `transport` -> (zlo, zhi, RunLog)."""
+    s, it = A.schedule_arrays(sched)
+    cap = int(it.sum()) + 1
+    recs = (A.dfm_iter_record * cap)()
+    rl = A.dfm_runlog()
+    cc = cfg.c()
+    zlo, zhi = C.c_int64(), C.c_int64()
+    rc = ctx.lib.dfm_dev_register_slab_tp(
+        ctx.handle, C.byref(g.c()), C.c_void_p(d_fixed), C.c_void_p(d_moving), C.byref(cc),
+        A._dptr(s), it.ctypes.data_as(C.POINTER(C.c_int32)), len(s), rank, world,
+        C.byref(transport.c), C.c_void_p(d_out) if d_out else None, C.byref(zlo), C.byref(zhi),
+        recs, cap, C.byref(rl))
+    ctx.t.check(rc, "register_slab_tp")
     return zlo.value, zhi.value, A.records_to_log(recs, rl)
 
 
