@@ -525,6 +525,11 @@ DFM_API dfm_status dfm_ctx_kernel_times(const dfm_ctx* ctx, double* ms, int64_t*
  * the cp.async-carried W/G gather); default 2000000.  Lowering it lets the
  * parity tests run those variants at sizes the oracle finishes quickly. */
 #define DFM_OPT_LARGE_MIN 7
+/* DFM_OPT_SLAB_REPL_MAX: in a z-slab registration, the coarse pyramid levels
+ * with at most this many voxels run whole on every rank (no halo exchange,
+ * no collective; each rank computes the same level) and only the finer levels
+ * are decomposed; 0 = decompose every level.  Default 4000000. */
+#define DFM_OPT_SLAB_REPL_MAX 9
 DFM_API dfm_status dfm_ctx_set_option(dfm_ctx* ctx, int key, int64_t value);
 
 /* White-box read of a named device workspace buffer of the context after a

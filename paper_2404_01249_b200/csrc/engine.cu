@@ -120,6 +120,9 @@ struct dfm_ctx {
                                                           : 2000000;
     // large-level kernel variants from this many voxels (DFM_OPT_LARGE_MIN)
     int64_t large_min = 2000000;
+    // z-slab runs: pyramid levels up to this many voxels are replicated on every
+    // rank instead of decomposed (DFM_OPT_SLAB_REPL_MAX)
+    int64_t slab_repl_max = 4000000;
     Launch L() { return Launch{stream, &launches, num_sms, pdl, large_min}; }
 
     LoopState* pinned_state() {
@@ -671,6 +674,9 @@ dfm_status dfm_ctx_set_option(dfm_ctx* ctx, int key, int64_t value) {
         } else if (key == DFM_OPT_SPLIT_FOLD_MAX) {
             if (value < 0) fail(DFM_E_INVALID, "split_fold_max must be >= 0");
             ctx->split_fold_max = value;
+        } else if (key == DFM_OPT_SLAB_REPL_MAX) {
+            if (value < 0) fail(DFM_E_INVALID, "slab_repl_max must be >= 0");
+            ctx->slab_repl_max = value;
         } else if (key == DFM_OPT_LARGE_MIN) {
             if (value < 0) fail(DFM_E_INVALID, "large_min must be >= 0");
             ctx->large_min = value;
@@ -2811,6 +2817,13 @@ struct SlabRun {
     int rank = 0, world = 1, E = 1;  // E local slabs (emulation) or 1 (one per process)
     SlabTransport<T>* tp = nullptr;
     int H = 0;
+    // replicated levels: a small (coarse) level runs whole on every rank — one
+    // local part, no halo exchange, no collective — until the first level with
+    // more than repl_max voxels; from there on the levels are decomposed
+    int64_t repl_max = 0;
+    bool repl = false;
+    int Ea = 1;  // active local parts (E, or 1 on a replicated level)
+    int64_t cap = 0;  // elements per component buffer of a part
 
     struct Part {
         SlabBounds b;
@@ -2836,8 +2849,16 @@ struct SlabRun {
     unsigned long long *maxstep = nullptr, *stamp = nullptr;
     int cur = 0;
 
-    int nparts() const { return world > 1 ? world : E; }
-    int part_id(int j) const { return world > 1 ? rank : j; }
+    int nparts() const { return repl ? 1 : (world > 1 ? world : E); }
+    int part_id(int j) const { return repl ? 0 : (world > 1 ? rank : j); }
+    bool collective() const { return world > 1 && !repl; }
+    struct Active {  // the active parts, for range-for
+        Part* b;
+        Part* e;
+        Part* begin() const { return b; }
+        Part* end() const { return e; }
+    };
+    Active active() { return {parts.data(), parts.data() + Ea}; }
     // plane size of the current slab views (the scale being processed)
     int64_t plane() const { return static_cast<int64_t>(parts.empty() ? full.nx * full.ny
                                                                        : parts[0].dl.nx * parts[0].dl.ny); }
@@ -2850,7 +2871,7 @@ struct SlabRun {
             const SlabBounds b = slab_bounds(full.nz, part_id(j), nparts(), H);
             maxn = std::max(maxn, b.nzl());
         }
-        const int64_t cap = pl * maxn;
+        cap = pl * maxn;
         parts.resize(E);
         const int comps[9] = {1, 3, 4, 3, 3, 3, 3, 3, 3};
         for (int j = 0; j < E; ++j) {
@@ -2885,7 +2906,8 @@ struct SlabRun {
 
     // slab views of every part at scale grid ds
     void layout(const Dims& ds) {
-        for (int j = 0; j < E; ++j) {
+        Ea = repl ? 1 : E;
+        for (int j = 0; j < Ea; ++j) {
             Part& p = parts[j];
             p.b = slab_bounds(ds.nz, part_id(j), nparts(), H);
             if (p.b.owned() < H && nparts() > 1)
@@ -2902,8 +2924,16 @@ struct SlabRun {
         }
     }
 
-    void exchange(int which, int ncomp) { tp->exchange(*this, which, ncomp); }
-    void gather(const Dims& ds) { tp->gather(*this, ds); }
+    void exchange(int which, int ncomp) {
+        if (!repl) tp->exchange(*this, which, ncomp);
+    }
+    void gather(const Dims& ds) {
+        if (repl) {  // every rank holds the whole level
+            EmulatedTransport<T>().gather(*this, ds);
+            return;
+        }
+        tp->gather(*this, ds);
+    }
 
     // full volumes at grid from -> every slab's local planes at grid to
     void scatter_resample(const Dims& from, const Dims& to, bool with_state) {
@@ -2913,7 +2943,7 @@ struct SlabRun {
             mult[a] = static_cast<double>(nn[a] - 1) / static_cast<double>(no[a] - 1);
             sq[a] = mult[a] * mult[a];
         }
-        for (int j = 0; j < E; ++j) {
+        for (int j = 0; j < Ea; ++j) {
             Part& p = parts[j];
             Dims dall = p.dl;  // every local plane, halos included
             dall.zb = 0;
@@ -2937,7 +2967,7 @@ struct SlabRun {
     double global_sum(const double* part_sums, int np) {
         // fixed-order device reduction, then (NCCL) a sum over ranks
         launch_reduce_value(ctx->L(), 0, part_sums, np, 1.0, red);
-        if (world > 1) tp->sum_f64(*this, red, 1);
+        if (collective()) tp->sum_f64(*this, red, 1);
         double h[3];
         CK(cudaMemcpyAsync(h, red, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
         ctx->sync();
@@ -2954,7 +2984,7 @@ struct SlabRun {
         const int64_t pl = static_cast<int64_t>(ds.nx) * ds.ny;
         const double N = static_cast<double>(ds.n);
         int off = 0;
-        for (int j = 0; j < E; ++j) {
+        for (int j = 0; j < Ea; ++j) {
             Part& p = parts[j];
             const int np = launch_lncc_fwd3_tma<T>(L, cfg->lncc_radius, Fs + p.b.z0g() * pl,
                                                    p.W(), p.fstat, p.dl, p.coef(), partials + off,
@@ -2962,7 +2992,7 @@ struct SlabRun {
             if (np < 0) fail(DFM_E_CUDA, "slab: lncc forward launch failed");
             off += np;
         }
-        if (world > 1) {
+        if (collective()) {
             launch_reduce_value(L, 0, partials, off, 1.0, red);
             tp->sum_f64(*this, red, 1);
             launch_monitor(L, 1, red, 1, N, st, loss, stamp, cfg->conv_window, cfg->conv_tol);
@@ -2970,25 +3000,25 @@ struct SlabRun {
             launch_monitor(L, 1, partials, off, N, st, loss, stamp, cfg->conv_window, cfg->conv_tol);
         }
         exchange(2, 4);  // coefficients
-        for (Part& p : parts)
+        for (Part& p : active())
             launch_lncc_bwd_tma<T>(L, cfg->lncc_radius, p.coef(), Fs + p.b.z0g() * pl, p.W(), p.G(),
                                    p.dl, p.grad(), st);
         exchange(3, 3);  // gradient
         AdamParams ap{cfg->beta1, cfg->beta2, cfg->eps_adam, cfg->eta, cfg->step_cap,
                       corr1, corr2, cfg->use_jac};
-        for (Part& p : parts)
+        for (Part& p : active())
             if (launch_smooth_adam_tma<T>(L, Rg, wg, p.grad(), p.m(), p.nu(), p.step(), p.dl, ap,
                                           st, maxstep) < 0)
                 fail(DFM_E_CUDA, "slab: smooth+Adam launch failed");
-        if (world > 1) tp->max_i32(*this, &st->bad_step, 1);  // a non-finite step aborts everywhere
+        if (collective()) tp->max_i32(*this, &st->bad_step, 1);  // a non-finite step aborts everywhere
         // c = step + u(x + step) on the owned planes (the u halo covers the
         // gather reach), into the dead gradient buffer
-        for (Part& p : parts)
+        for (Part& p : active())
             if (launch_compose_tma<T>(L, 0, cfg->step_cap, wid, p.step(), p.u(src), p.grad(), Ms, ds,
                                       p.dl, nullptr, nullptr, st, false) < 0)
                 fail(DFM_E_CUDA, "slab: compose launch failed");
         exchange(3, 3);  // c
-        for (int j = 0; j < E; ++j) {
+        for (int j = 0; j < Ea; ++j) {
             Part& p = parts[j];
             if (launch_compose_smooth_tma<T>(L, Rw, ww, p.grad(), p.u(1 - src), Ms, ds, p.dl, p.W(),
                                              p.G(), st, j == 0) < 0)
@@ -3028,6 +3058,7 @@ struct SlabRun {
         alloc(total, prev_n);
         Dims prev{};
         bool have = false;
+        bool may_repl = true;  // replicated levels only precede the decomposed ones
         int64_t global = 0;
         const int64_t pl = static_cast<int64_t>(full.nx) * full.ny;  // epilogue (full grid)
         for (int si = 0; si < ns; ++si) {
@@ -3041,22 +3072,26 @@ struct SlabRun {
                 fail(DFM_E_INVALID, "lncc_eval: window larger than image");
             Impl<T>{ctx}.downsample_dev(full, F, fac, ds, Fs, "spyr");
             Impl<T>{ctx}.downsample_dev(full, M, fac, ds, Ms, "spyr");
+            const bool want_repl = may_repl && ds.n <= repl_max && ds.n <= cap;
+            may_repl = want_repl;
             if (!have) {
+                repl = want_repl;
                 layout(ds);
-                for (Part& p : parts)
+                for (Part& p : active())
                     for (int k : {5, 6, 7, 8})
                         CK(cudaMemsetAsync(p.base[k], 0, sizeof(T) * 3 * p.dl.n, ctx->stream));
                 cur = 0;
                 have = true;
             } else if (!dims_equal(prev, ds)) {
-                gather(prev);
+                gather(prev);  // in the previous level's mode
+                repl = want_repl;
                 layout(ds);
                 scatter_resample(prev, ds, true);
             }
             prev = ds;
             const int T_si = iters[si];
             if (T_si == 0) continue;
-            for (Part& p : parts) {
+            for (Part& p : active()) {
                 launch_warpgrad<T>(ctx->L(), Ms, ds, CPlanes3<T>{{p.u(cur), p.u(cur) + p.dl.n,
                                                                   p.u(cur) + 2 * p.dl.n}},
                                    [&] { Dims a = p.dl; a.zb = a.ze = 0; return a; }(), p.W(), p.G());
@@ -3118,7 +3153,7 @@ struct SlabRun {
                 }
             }
             launch_stamp(ctx->L(), stamp + T_si);
-            if (world > 1) tp->max_u64(*this, maxstep, T_si);  // max |step| of the log over ranks
+            if (collective()) tp->max_u64(*this, maxstep, T_si);  // max |step| of the log over ranks
             ctx->sync();
             LoopState hs;
             std::vector<double> hl(T_si + 1);
@@ -3157,11 +3192,12 @@ struct SlabRun {
         // epilogue at full resolution (pipeline.cpp:213-223)
         if (!dims_equal(prev, full)) {
             gather(prev);
+            repl = may_repl && full.n <= repl_max && full.n <= cap;
             layout(full);
             scatter_resample(prev, full, false);
         }
         int off = 0;
-        for (Part& p : parts) {
+        for (Part& p : active()) {
             Dims dall = p.dl;
             dall.zb = dall.ze = 0;
             launch_warpgrad<T>(ctx->L(), M, full,
@@ -3175,18 +3211,18 @@ struct SlabRun {
         out.final_loss = -S / static_cast<double>(full.n);
         auto* cnt = ctx->arr<unsigned long long>("slab_count", 1);
         CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), ctx->stream));
-        for (Part& p : parts)
+        for (Part& p : active())
             launch_jacobian_det<T>(ctx->L(), CPlanes3<T>{{p.u(cur), p.u(cur) + p.dl.n,
                                                           p.u(cur) + 2 * p.dl.n}},
                                    p.dl, nullptr, cnt);
-        if (world > 1) tp->sum_u64(*this, cnt, 1);
+        if (collective()) tp->sum_u64(*this, cnt, 1);
         unsigned long long hc = 0;
         CK(cudaMemcpyAsync(&hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream));
         // result planes
-        int64_t zlo = parts.front().b.zlo, zhi = parts.back().b.zhi;
+        int64_t zlo = parts[0].b.zlo, zhi = parts[Ea - 1].b.zhi;
         const int64_t nout = (zhi - zlo) * pl;
         if (d_out)
-            for (Part& p : parts)
+            for (Part& p : active())
                 for (int c = 0; c < 3; ++c)
                     CK(cudaMemcpyAsync(d_out + c * nout + (p.b.zlo - zlo) * pl,
                                        p.u(cur) + c * p.dl.n + p.b.hlo * pl,
@@ -3204,7 +3240,7 @@ struct SlabRun {
 template <class T>
 void EmulatedTransport<T>::exchange(SlabRun<T>& R, int which, int ncomp) {
     const int64_t pl = R.plane();
-    for (int j = 0; j < R.E; ++j) {
+    for (int j = 0; j < R.Ea; ++j) {
         auto& p = R.parts[j];
         if (j > 0 && p.b.hlo > 0) {  // lower halo <- part j-1's top owned planes
             const auto& q = R.parts[j - 1];
@@ -3215,7 +3251,7 @@ void EmulatedTransport<T>::exchange(SlabRun<T>& R, int which, int ncomp) {
                                    sizeof(T) * pl * p.b.hlo, cudaMemcpyDeviceToDevice,
                                    R.ctx->stream));
         }
-        if (j + 1 < R.E && p.b.hhi > 0) {  // upper halo <- part j+1's bottom owned planes
+        if (j + 1 < R.Ea && p.b.hhi > 0) {  // upper halo <- part j+1's bottom owned planes
             const auto& q = R.parts[j + 1];
             const int src_local = p.b.zhi - q.b.z0g();
             const int dst_local = p.b.hlo + p.b.owned();
@@ -3231,7 +3267,7 @@ void EmulatedTransport<T>::exchange(SlabRun<T>& R, int which, int ncomp) {
 template <class T>
 void EmulatedTransport<T>::gather(SlabRun<T>& R, const Dims& ds) {
     const int64_t pl = static_cast<int64_t>(ds.nx) * ds.ny;
-    for (int j = 0; j < R.E; ++j) {
+    for (int j = 0; j < R.Ea; ++j) {
         const auto& p = R.parts[j];
         const T* srcs[3] = {p.u(R.cur), p.m(), p.nu()};
         for (int f = 0; f < 3; ++f)
@@ -3471,6 +3507,7 @@ dfm_status register_slab_impl(dfm_ctx* ctx, const dfm_grid* g, const void* d_fix
             R.rank = rank;
             R.world = world;
             R.E = world > 1 ? 1 : std::max(1, emulate);
+            R.repl_max = ctx->slab_repl_max;
             EmulatedTransport<T> emu;
             NcclTransport<T> ncx;
             HostTransport<T> host;

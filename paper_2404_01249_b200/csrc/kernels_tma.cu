@@ -113,6 +113,9 @@ constexpr int TX = kTX;
 #ifndef DFM_BWD_QUAD64
 #define DFM_BWD_QUAD64 1
 #endif
+#ifndef DFM_BWD_QUAD64_RMAX
+#define DFM_BWD_QUAD64_RMAX 3
+#endif
 #ifndef DFM_MINB_FWD3
 #define DFM_MINB_FWD3 3
 #endif
@@ -914,7 +917,7 @@ struct LnccBwd2 {
     __device__ Acc wgt(int, int) const { return 1.0; }
     __device__ Acc nrm(int, int) const { return 1.0; }
     __device__ Prol prologue() const { return {}; }
-    static constexpr bool kXQuad = sizeof(T) == 4 && (sizeof(Acc) == 4 || (DFM_BWD_QUAD64 && R_ <= 2));
+    static constexpr bool kXQuad = sizeof(T) == 4 && (sizeof(Acc) == 4 || (DFM_BWD_QUAD64 && R_ <= DFM_BWD_QUAD64_RMAX));
     __device__ void xpass4(const unsigned char* st_, int row, int col, const Acc*,
                            Acc v[4][4]) const {
         constexpr int NCH = (XA + R + 4 + 3) / 4;

@@ -4,7 +4,7 @@ loop with rank-local slab views and offsets, its collectives host-staged over
 torch.distributed gloo (dfm_dev_register_slab_tp) — kernels never wait on
 another process, the hosts exchange between launches.
 
-    python tests/slab_worker.py RANK WORLD PORT OUTDIR PREC
+    python tests/slab_worker.py RANK WORLD PORT OUTDIR PREC [REPL_MAX]
 """
 import os
 import sys
@@ -24,16 +24,18 @@ def case():
     return p, sched, cfg
 
 
-def main(rank, world, port, outdir, prec):
+def main(rank, world, port, outdir, prec, repl_max=0):
     import torch
     import torch.distributed as dist
-    from paper_2404_01249_b200.engine import Context, TorchDistTransport, register_slab_tp
+    from paper_2404_01249_b200.engine import (Context, OPT_SLAB_REPL_MAX, TorchDistTransport,
+                                              register_slab_tp)
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
     p, sched, cfg = case()
     g = p.grid
     dt = torch.float32 if prec == "f32" else torch.float64
     ctx = Context(0, prec)
+    ctx.set_option(OPT_SLAB_REPL_MAX, repl_max)
     F = torch.from_numpy(p.fixed).cuda().to(dt)
     M = torch.from_numpy(p.moving).cuda().to(dt)
     out = torch.zeros((3,) + g.shape, dtype=dt, device="cuda")
@@ -51,4 +53,5 @@ def main(rank, world, port, outdir, prec):
 
 
 if __name__ == "__main__":
-    main(int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), sys.argv[4], sys.argv[5])
+    main(int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), sys.argv[4], sys.argv[5],
+         int(sys.argv[6]) if len(sys.argv) > 6 else 0)

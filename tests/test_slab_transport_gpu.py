@@ -24,15 +24,15 @@ def _port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("prec", ["f32", "f64"])
-def test_two_processes_match_monolithic(tmp_path, prec):
+@pytest.mark.parametrize("prec,repl", [("f32", 0), ("f64", 0), ("f32", 20000)])
+def test_two_processes_match_monolithic(tmp_path, prec, repl):
     import torch
     sys.path.insert(0, HERE)
     import slab_worker
     from paper_2404_01249_b200.engine import Context, OPT_BRICK_MAX
     world, port = 2, _port()
     procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "slab_worker.py"), str(r),
-                               str(world), str(port), str(tmp_path), prec],
+                               str(world), str(port), str(tmp_path), prec, str(repl)],
                               stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
              for r in range(world)]
     outs = [q.communicate(timeout=600)[0] for q in procs]
