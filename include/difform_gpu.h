@@ -530,6 +530,12 @@ DFM_API dfm_status dfm_ctx_kernel_times(const dfm_ctx* ctx, double* ms, int64_t*
  * no collective; each rank computes the same level) and only the finer levels
  * are decomposed; 0 = decompose every level.  Default 4000000. */
 #define DFM_OPT_SLAB_REPL_MAX 9
+/* DFM_OPT_SLAB_OVERLAP: in a z-slab registration, each stage first computes
+ * the planes its neighbours need, then exchanges them on a second stream
+ * while the interior planes are computed (results unchanged, bit for bit).
+ * -1 (default) = on for the multi-process NCCL path, off for emulated slabs
+ * (one GPU: the copies compete with the compute for HBM); 0 off; 1 on. */
+#define DFM_OPT_SLAB_OVERLAP 10
 DFM_API dfm_status dfm_ctx_set_option(dfm_ctx* ctx, int key, int64_t value);
 
 /* White-box read of a named device workspace buffer of the context after a

@@ -123,6 +123,9 @@ struct dfm_ctx {
     // z-slab runs: pyramid levels up to this many voxels are replicated on every
     // rank instead of decomposed (DFM_OPT_SLAB_REPL_MAX)
     int64_t slab_repl_max = 4000000;
+    // z-slab runs: overlap each stage's halo exchange with its interior planes
+    // (-1 auto = multi-process NCCL only, 0 off, 1 on; DFM_OPT_SLAB_OVERLAP)
+    int slab_overlap = -1;
     Launch L() { return Launch{stream, &launches, num_sms, pdl, large_min}; }
 
     LoopState* pinned_state() {
@@ -674,6 +677,9 @@ dfm_status dfm_ctx_set_option(dfm_ctx* ctx, int key, int64_t value) {
         } else if (key == DFM_OPT_SPLIT_FOLD_MAX) {
             if (value < 0) fail(DFM_E_INVALID, "split_fold_max must be >= 0");
             ctx->split_fold_max = value;
+        } else if (key == DFM_OPT_SLAB_OVERLAP) {
+            if (value < -1 || value > 1) fail(DFM_E_INVALID, "slab_overlap must be -1, 0 or 1");
+            ctx->slab_overlap = static_cast<int>(value);
         } else if (key == DFM_OPT_SLAB_REPL_MAX) {
             if (value < 0) fail(DFM_E_INVALID, "slab_repl_max must be >= 0");
             ctx->slab_repl_max = value;
@@ -2760,7 +2766,8 @@ struct SlabRun;
 template <class T>
 struct SlabTransport {
     virtual ~SlabTransport() = default;
-    virtual void exchange(SlabRun<T>& R, int which, int ncomp) = 0;
+    // on stream s (the exchange stream: it overlaps the interior planes)
+    virtual void exchange(SlabRun<T>& R, int which, int ncomp, cudaStream_t s) = 0;
     virtual void gather(SlabRun<T>& R, const Dims& ds) = 0;
     virtual void sum_f64(SlabRun<T>& R, double* dev, int n) = 0;
     virtual void sum_u64(SlabRun<T>& R, unsigned long long* dev, int n) = 0;
@@ -2771,7 +2778,7 @@ struct SlabTransport {
 
 template <class T>
 struct EmulatedTransport final : SlabTransport<T> {
-    void exchange(SlabRun<T>& R, int which, int ncomp) override;
+    void exchange(SlabRun<T>& R, int which, int ncomp, cudaStream_t s) override;
     void gather(SlabRun<T>& R, const Dims& ds) override;
     void sum_f64(SlabRun<T>&, double*, int) override {}
     void sum_u64(SlabRun<T>&, unsigned long long*, int) override {}
@@ -2784,7 +2791,7 @@ template <class T>
 struct NcclTransport final : SlabTransport<T> {
     const NcclApi* nc = nullptr;
     ncclComm_t comm = nullptr;
-    void exchange(SlabRun<T>& R, int which, int ncomp) override;
+    void exchange(SlabRun<T>& R, int which, int ncomp, cudaStream_t s) override;
     void gather(SlabRun<T>& R, const Dims& ds) override;
     void sum_f64(SlabRun<T>& R, double* dev, int n) override;
     void sum_u64(SlabRun<T>& R, unsigned long long* dev, int n) override;
@@ -2796,7 +2803,7 @@ struct NcclTransport final : SlabTransport<T> {
 template <class T>
 struct HostTransport final : SlabTransport<T> {
     const dfm_slab_transport* tp = nullptr;
-    void exchange(SlabRun<T>& R, int which, int ncomp) override;
+    void exchange(SlabRun<T>& R, int which, int ncomp, cudaStream_t s) override;
     void gather(SlabRun<T>& R, const Dims& ds) override;
     void sum_f64(SlabRun<T>& R, double* dev, int n) override;
     void sum_u64(SlabRun<T>& R, unsigned long long* dev, int n) override;
@@ -2848,6 +2855,12 @@ struct SlabRun {
            *red = nullptr;
     unsigned long long *maxstep = nullptr, *stamp = nullptr;
     int cur = 0;
+
+    ~SlabRun() {
+        if (xs) cudaStreamDestroy(xs);
+        for (auto e : xev)
+            if (e) cudaEventDestroy(e);
+    }
 
     int nparts() const { return repl ? 1 : (world > 1 ? world : E); }
     int part_id(int j) const { return repl ? 0 : (world > 1 ? rank : j); }
@@ -2925,7 +2938,61 @@ struct SlabRun {
     }
 
     void exchange(int which, int ncomp) {
-        if (!repl) tp->exchange(*this, which, ncomp);
+        if (!repl) tp->exchange(*this, which, ncomp, ctx->stream);
+    }
+
+    // Halo-overlapped stage: `fn(part, j, view)` launches the stage's kernel on
+    // a z sub-range of a part.  The planes the neighbours need (H next to each
+    // internal face) go first; the exchange of `exch` (buffer index, component
+    // count pairs) then runs on the exchange stream while the interior planes
+    // are computed; the main stream joins it before the next stage.  Every
+    // output plane's arithmetic is independent of the launch split.
+    cudaStream_t xs = nullptr;
+    cudaEvent_t xev[2] = {nullptr, nullptr};
+    bool overlap = false;
+    template <class Fn>
+    void stage(Fn&& fn, std::initializer_list<std::pair<int, int>> exch) {
+        const bool ov = overlap && !repl && tp->capturable() && xs != nullptr;
+        int ib[64], ie[64];
+        for (int j = 0; j < Ea; ++j) {
+            Part& p = parts[j];
+            const int lo = p.b.hlo, top = p.b.hlo + p.b.owned();
+            ib[j] = lo;
+            ie[j] = top;
+            if (!ov) continue;
+            if (p.b.hlo > 0) {  // a neighbour below reads our first H owned planes
+                Dims d = p.dl;
+                d.zb = lo;
+                d.ze = std::min(lo + H, top);
+                fn(p, j, d);
+                ib[j] = d.ze;
+            }
+            if (p.b.hhi > 0 && ib[j] < top) {  // ... and one above our last H
+                Dims d = p.dl;
+                d.zb = std::max(top - H, ib[j]);
+                d.ze = top;
+                fn(p, j, d);
+                ie[j] = d.zb;
+            }
+        }
+        if (ov) {
+            CK(cudaEventRecord(xev[0], ctx->stream));
+            CK(cudaStreamWaitEvent(xs, xev[0], 0));
+            for (const auto& e : exch) tp->exchange(*this, e.first, e.second, xs);
+            CK(cudaEventRecord(xev[1], xs));
+        }
+        for (int j = 0; j < Ea; ++j) {
+            if (ib[j] >= ie[j]) continue;
+            Dims d = parts[j].dl;
+            d.zb = ib[j];
+            d.ze = ie[j];
+            fn(parts[j], j, d);
+        }
+        if (ov) {
+            CK(cudaStreamWaitEvent(ctx->stream, xev[1], 0));
+        } else {
+            for (const auto& e : exch) exchange(e.first, e.second);
+        }
     }
     void gather(const Dims& ds) {
         if (repl) {  // every rank holds the whole level
@@ -2984,14 +3051,13 @@ struct SlabRun {
         const int64_t pl = static_cast<int64_t>(ds.nx) * ds.ny;
         const double N = static_cast<double>(ds.n);
         int off = 0;
-        for (int j = 0; j < Ea; ++j) {
-            Part& p = parts[j];
-            const int np = launch_lncc_fwd3_tma<T>(L, cfg->lncc_radius, Fs + p.b.z0g() * pl,
-                                                   p.W(), p.fstat, p.dl, p.coef(), partials + off,
-                                                   st, nullptr);
+        stage([&](Part& p, int, const Dims& dv) {
+            const int np = launch_lncc_fwd3_tma<T>(L, cfg->lncc_radius, Fs + p.b.z0g() * pl, p.W(),
+                                                   p.fstat, dv, p.coef(), partials + off, st,
+                                                   nullptr);
             if (np < 0) fail(DFM_E_CUDA, "slab: lncc forward launch failed");
             off += np;
-        }
+        }, {{2, 4}});  // coefficients
         if (collective()) {
             launch_reduce_value(L, 0, partials, off, 1.0, red);
             tp->sum_f64(*this, red, 1);
@@ -2999,11 +3065,11 @@ struct SlabRun {
         } else {
             launch_monitor(L, 1, partials, off, N, st, loss, stamp, cfg->conv_window, cfg->conv_tol);
         }
-        exchange(2, 4);  // coefficients
-        for (Part& p : active())
-            launch_lncc_bwd_tma<T>(L, cfg->lncc_radius, p.coef(), Fs + p.b.z0g() * pl, p.W(), p.G(),
-                                   p.dl, p.grad(), st);
-        exchange(3, 3);  // gradient
+        stage([&](Part& p, int, const Dims& dv) {
+            if (launch_lncc_bwd_tma<T>(L, cfg->lncc_radius, p.coef(), Fs + p.b.z0g() * pl, p.W(),
+                                       p.G(), dv, p.grad(), st) < 0)
+                fail(DFM_E_CUDA, "slab: lncc backward launch failed");
+        }, {{3, 3}});  // gradient
         AdamParams ap{cfg->beta1, cfg->beta2, cfg->eps_adam, cfg->eta, cfg->step_cap,
                       corr1, corr2, cfg->use_jac};
         for (Part& p : active())
@@ -3013,19 +3079,18 @@ struct SlabRun {
         if (collective()) tp->max_i32(*this, &st->bad_step, 1);  // a non-finite step aborts everywhere
         // c = step + u(x + step) on the owned planes (the u halo covers the
         // gather reach), into the dead gradient buffer
-        for (Part& p : active())
+        stage([&](Part& p, int, const Dims& dv) {
             if (launch_compose_tma<T>(L, 0, cfg->step_cap, wid, p.step(), p.u(src), p.grad(), Ms, ds,
-                                      p.dl, nullptr, nullptr, st, false) < 0)
+                                      dv, nullptr, nullptr, st, false) < 0)
                 fail(DFM_E_CUDA, "slab: compose launch failed");
-        exchange(3, 3);  // c
-        for (int j = 0; j < Ea; ++j) {
-            Part& p = parts[j];
-            if (launch_compose_smooth_tma<T>(L, Rw, ww, p.grad(), p.u(1 - src), Ms, ds, p.dl, p.W(),
-                                             p.G(), st, j == 0) < 0)
+        }, {{3, 3}});  // c
+        bool counted = false;  // one counted update per iteration (emulated parts, split launches)
+        stage([&](Part& p, int, const Dims& dv) {
+            if (launch_compose_smooth_tma<T>(L, Rw, ww, p.grad(), p.u(1 - src), Ms, ds, dv, p.W(),
+                                             p.G(), st, !counted) < 0)
                 fail(DFM_E_CUDA, "slab: compose-smooth launch failed");
-        }
-        exchange(6 - src, 3);  // u (the buffer just written)
-        exchange(0, 1);        // W
+            counted = true;
+        }, {{6 - src, 3}, {0, 1}});  // u (the buffer just written), W
     }
 
     void run(const T* F, const T* M, const double* scales, const int32_t* iters, int ns,
@@ -3039,6 +3104,10 @@ struct SlabRun {
             fail(DFM_E_INVALID, "slab decomposition: x extent must be a multiple of 16 bytes");
         if (full.ndim != 3) fail(DFM_E_INVALID, "slab decomposition: 3-D volumes only");
         H = slab_halo(cfg);
+        if (overlap && tp->capturable() && !xs) {
+            CK(cudaStreamCreateWithFlags(&xs, cudaStreamNonBlocking));
+            for (auto& e : xev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
         int64_t total = 0;
         for (int i = 0; i < ns; ++i) total += iters[i];
         // m and nu are gathered only when leaving a level that is not the full
@@ -3238,7 +3307,7 @@ struct SlabRun {
 
 // ---- emulated slabs: device copies between the parts of one process
 template <class T>
-void EmulatedTransport<T>::exchange(SlabRun<T>& R, int which, int ncomp) {
+void EmulatedTransport<T>::exchange(SlabRun<T>& R, int which, int ncomp, cudaStream_t s) {
     const int64_t pl = R.plane();
     for (int j = 0; j < R.Ea; ++j) {
         auto& p = R.parts[j];
@@ -3249,7 +3318,7 @@ void EmulatedTransport<T>::exchange(SlabRun<T>& R, int which, int ncomp) {
                 CK(cudaMemcpyAsync(p.base[which] + c * p.dl.n,
                                    q.base[which] + c * q.dl.n + src_local * pl,
                                    sizeof(T) * pl * p.b.hlo, cudaMemcpyDeviceToDevice,
-                                   R.ctx->stream));
+                                   s));
         }
         if (j + 1 < R.Ea && p.b.hhi > 0) {  // upper halo <- part j+1's bottom owned planes
             const auto& q = R.parts[j + 1];
@@ -3259,7 +3328,7 @@ void EmulatedTransport<T>::exchange(SlabRun<T>& R, int which, int ncomp) {
                 CK(cudaMemcpyAsync(p.base[which] + c * p.dl.n + dst_local * pl,
                                    q.base[which] + c * q.dl.n + src_local * pl,
                                    sizeof(T) * pl * p.b.hhi, cudaMemcpyDeviceToDevice,
-                                   R.ctx->stream));
+                                   s));
         }
     }
 }
@@ -3281,7 +3350,7 @@ void EmulatedTransport<T>::gather(SlabRun<T>& R, const Dims& ds) {
 
 // ---- NCCL between processes (device-side, capturable)
 template <class T>
-void NcclTransport<T>::exchange(SlabRun<T>& R, int which, int ncomp) {
+void NcclTransport<T>::exchange(SlabRun<T>& R, int which, int ncomp, cudaStream_t s) {
     const int64_t pl = R.plane();
     const auto& p = R.parts[0];
     const ncclDataType_t dt = sizeof(T) == 4 ? ncclFloat32 : ncclFloat64;
@@ -3289,15 +3358,15 @@ void NcclTransport<T>::exchange(SlabRun<T>& R, int which, int ncomp) {
     for (int c = 0; c < ncomp; ++c) {
         T* buf = p.base[which] + c * p.dl.n;
         if (R.rank > 0) {  // exchange with the lower neighbour: H planes each way
-            nc->ck(nc->Send(buf + p.b.hlo * pl, pl * p.b.hlo, dt, R.rank - 1, comm, R.ctx->stream),
+            nc->ck(nc->Send(buf + p.b.hlo * pl, pl * p.b.hlo, dt, R.rank - 1, comm, s),
                    "send");
-            nc->ck(nc->Recv(buf, pl * p.b.hlo, dt, R.rank - 1, comm, R.ctx->stream), "recv");
+            nc->ck(nc->Recv(buf, pl * p.b.hlo, dt, R.rank - 1, comm, s), "recv");
         }
         if (R.rank + 1 < R.world) {
             const int top = p.b.hlo + p.b.owned();
             nc->ck(nc->Send(buf + (top - p.b.hhi) * pl, pl * p.b.hhi, dt, R.rank + 1, comm,
-                            R.ctx->stream), "send");
-            nc->ck(nc->Recv(buf + top * pl, pl * p.b.hhi, dt, R.rank + 1, comm, R.ctx->stream),
+                            s), "send");
+            nc->ck(nc->Recv(buf + top * pl, pl * p.b.hhi, dt, R.rank + 1, comm, s),
                    "recv");
         }
     }
@@ -3342,7 +3411,7 @@ void NcclTransport<T>::max_i32(SlabRun<T>& R, int* dev, int n) {
 
 // ---- caller transport: host-staged through pinned buffers (eager loop)
 template <class T>
-void HostTransport<T>::exchange(SlabRun<T>& R, int which, int ncomp) {
+void HostTransport<T>::exchange(SlabRun<T>& R, int which, int ncomp, cudaStream_t) {
     const int64_t pl = R.plane();
     const auto& p = R.parts[0];
     const int top = p.b.hlo + p.b.owned();
@@ -3497,6 +3566,7 @@ dfm_status register_slab_impl(dfm_ctx* ctx, const dfm_grid* g, const void* d_fix
         if (g->ndim != 3) fail(DFM_E_INVALID, "slab decomposition needs a 3-D grid");
         if (world < 1 || rank < 0 || rank >= world) fail(DFM_E_INVALID, "slab: bad rank/world");
         if (world > 1 && emulate > 1) fail(DFM_E_INVALID, "slab: emulate needs world == 1");
+        if (emulate > 64) fail(DFM_E_INVALID, "slab: at most 64 emulated slabs");
         RegOut o;
         DFM_DISPATCH(ctx, {
             SlabRun<T> R;
@@ -3508,6 +3578,10 @@ dfm_status register_slab_impl(dfm_ctx* ctx, const dfm_grid* g, const void* d_fix
             R.world = world;
             R.E = world > 1 ? 1 : std::max(1, emulate);
             R.repl_max = ctx->slab_repl_max;
+            // halo/interior overlap: across GPUs the exchange rides NVLink while
+            // the interior planes compute; emulated slabs share one GPU's HBM
+            // (measured slower there: 3.23 -> 3.39 s on config 4), so auto = NCCL only
+            R.overlap = ctx->slab_overlap > 0 || (ctx->slab_overlap < 0 && world > 1 && !tp);
             EmulatedTransport<T> emu;
             NcclTransport<T> ncx;
             HostTransport<T> host;

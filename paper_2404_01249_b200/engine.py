@@ -51,6 +51,7 @@ OPT_SPLIT = 5
 OPT_SPLIT_FOLD_MAX = 6
 OPT_LARGE_MIN = 7
 OPT_SLAB_REPL_MAX = 9
+OPT_SLAB_OVERLAP = 10
 
 _lib: Optional[C.CDLL] = None
 

@@ -7,23 +7,26 @@ import numpy as np
 import pytest
 
 from paper_2404_01249_b200 import _abi as A, synth
-from paper_2404_01249_b200.engine import (Context, OPT_BRICK_MAX, OPT_SLAB_REPL_MAX,
-                                          register_slab)
+from paper_2404_01249_b200.engine import (Context, OPT_BRICK_MAX, OPT_SLAB_OVERLAP,
+                                          OPT_SLAB_REPL_MAX, register_slab)
 
 pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("prec", ["f32", "f64"])
-@pytest.mark.parametrize("slabs,repl", [(2, 0), (3, 0), (4, 0), (4, 20000)])
-def test_emulated_slabs_match_monolithic(prec, slabs, repl):
+@pytest.mark.parametrize("slabs,repl,overlap", [(2, 0, 0), (3, 0, 1), (4, 0, 0), (4, 20000, 1)])
+def test_emulated_slabs_match_monolithic(prec, slabs, repl, overlap):
     """repl 0: every level decomposed; repl 20000: the coarsest level (16 x 10
-    x 12) replicated, the finer ones decomposed (DFM_OPT_SLAB_REPL_MAX)."""
+    x 12) replicated, the finer ones decomposed (DFM_OPT_SLAB_REPL_MAX);
+    overlap 1: boundary planes first, exchange on a second stream beside the
+    interior planes (DFM_OPT_SLAB_OVERLAP)."""
     import torch
     # the slab path runs the plane-streaming kernels: so does the monolithic
     # reference run here (the brick family sums in another order)
     ctx = Context(0, prec)
     ctx.set_option(OPT_BRICK_MAX, 0)
     ctx.set_option(OPT_SLAB_REPL_MAX, repl)
+    ctx.set_option(OPT_SLAB_OVERLAP, overlap)
     p = synth.make_pair(0, seed=5, shape=(64, 40, 48))   # z, y, x
     g = p.grid
     sched = A.PyramidSchedule((4.0, 2.0, 1.0), (12, 8, 4))
