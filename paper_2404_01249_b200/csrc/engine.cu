@@ -21,6 +21,7 @@
 #include <cstddef>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/difform_gpu.h"
 #include "dfm_device.cuh"
@@ -76,6 +77,22 @@ dfm_status guarded(F&& fn) {
         return DFM_E_CUDA;
     }
 }
+
+// NVTX ranges (SURVEY §5 tracing): registration, pyramid level, level loop,
+// epilogue, slab level; header-only NVTX v3, inert unless a tool is attached
+struct Nvtx {
+    explicit Nvtx(const char* fmt, ...) {
+        char buf[160];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        nvtxRangePushA(buf);
+    }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx&) = delete;
+    Nvtx& operator=(const Nvtx&) = delete;
+};
 
 double now_ms() {
     using clk = std::chrono::steady_clock;
@@ -2119,6 +2136,8 @@ struct Registrar {
 
     void run(const T* F, const T* M, const double* scales, const int32_t* iters, int ns,
              const dfm_init* init, RegOut& out) {
+        Nvtx range("register_images %s %dx%dx%d, %d levels", sizeof(T) == 4 ? "f32" : "f64",
+                   full.nx, full.ny, full.nz, ns);
         const double t0 = now_ms();
         int64_t total = 0;
         for (int i = 0; i < ns; ++i) total += iters[i];
@@ -2132,6 +2151,8 @@ struct Registrar {
             dfm_grid wgd;
             downsample_grid(g, fac, &wgd);
             const Dims d = to_dims(&wgd);
+            Nvtx lrange("level %d (scale %g): %dx%dx%d, %d iterations", si, scales[si], d.nx, d.ny,
+                        d.nz, iters[si]);
             ev_begin(KC_PYR);
             bool blur = false;
             for (int a = 0; a < g->ndim; ++a) blur |= fac[a] > 1.0;
@@ -2161,6 +2182,7 @@ struct Registrar {
             run_scale(d, Fw, Mw, si, scales[si], T_si, global, out);
         }
         // epilogue (pipeline.cpp:213-223)
+        Nvtx erange("epilogue: full-resolution loss + fold check");
         ev_begin(KC_EPI);
         if (!dims_equal(cd, full)) {
             upsample_field_only(cd, full);
@@ -2337,6 +2359,7 @@ struct Registrar {
 
     void run_scale(const Dims& d, const T* Fw, const T* Mw, int si, double scale, int T_si,
                    int64_t& global, RegOut& out) {
+        Nvtx range("loop: %d iterations at %dx%dx%d", T_si, d.nx, d.ny, d.nz);
         Fs = const_cast<T*>(Fw);
         Ms = const_cast<T*>(Mw);
         // per-scale reset of the loop state (t is kept)
@@ -3095,6 +3118,8 @@ struct SlabRun {
 
     void run(const T* F, const T* M, const double* scales, const int32_t* iters, int ns,
              RegOut& out, T* d_out, int64_t* ozlo, int64_t* ozhi) {
+        Nvtx range("register_images slab %d/%d (%d local parts) %dx%dx%d", rank, world, E,
+                   full.nx, full.ny, full.nz);
         const double t0 = now_ms();
         if (cfg->loss != DFM_LOSS_LNCC || cfg->use_jac || cfg->mode != DFM_MODE_DIRECT)
             fail(DFM_E_INVALID, "slab decomposition: direct mode, LNCC loss, use_jac off only");
@@ -3141,6 +3166,8 @@ struct SlabRun {
                 fail(DFM_E_INVALID, "lncc_eval: window larger than image");
             Impl<T>{ctx}.downsample_dev(full, F, fac, ds, Fs, "spyr");
             Impl<T>{ctx}.downsample_dev(full, M, fac, ds, Ms, "spyr");
+            Nvtx lrange("slab level %d (scale %g): %dx%dx%d, %d iterations", si, scales[si], ds.nx,
+                        ds.ny, ds.nz, iters[si]);
             const bool want_repl = may_repl && ds.n <= repl_max && ds.n <= cap;
             may_repl = want_repl;
             if (!have) {
