@@ -99,3 +99,26 @@ def test_reference_acceptance_harness_passes_on_the_device():
     rr, cref = _run(ACC_REF)
     print(rr.stdout)
     assert cref == crit
+
+
+def _numbers(exe):
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    return {k: float(v) for k, v in (ln.split() for ln in r.stdout.splitlines() if ln.strip())}
+
+
+@pytest.mark.gpu
+def test_dropin_numbers_match_the_reference_objects():
+    """tests/cpp/dropin_numbers.cpp (reference headers only) linked against the
+    reference's objects and against the drop-in: per-operator results within
+    1e-10 relative (fp64 on both sides), the 30-iteration registration within
+    1e-6 (same record count)."""
+    ref = os.path.join(REFOUT, "dropin_numbers_ref")
+    b200 = os.path.join(REFOUT, "dropin_numbers_b200")
+    assert os.path.exists(ref) and os.path.exists(b200), "make -C oracle accept"
+    a, b = _numbers(ref), _numbers(b200)
+    assert a.keys() == b.keys()
+    print({k: (a[k], b[k]) for k in a})
+    for k in a:
+        tol = 1e-6 if k.startswith("register") else 1e-10
+        assert abs(a[k] - b[k]) <= tol * max(abs(a[k]), 1e-300), (k, a[k], b[k])
