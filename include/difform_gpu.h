@@ -536,6 +536,12 @@ DFM_API dfm_status dfm_ctx_kernel_times(const dfm_ctx* ctx, double* ms, int64_t*
  * -1 (default) = on for the multi-process NCCL path, off for emulated slabs
  * (one GPU: the copies compete with the compute for HBM); 0 off; 1 on. */
 #define DFM_OPT_SLAB_OVERLAP 10
+/* DFM_OPT_EXACT: 1 = register_images (direct mode, SSD/LNCC) evaluates the
+ * reference's arithmetic in the reference's order, one IEEE operation at a
+ * time (kernels_exact.cu, compiled without FMA contraction): bit-identical
+ * to the reference's result, for parity checks on chaotic inputs.  fp64
+ * contexts only; unfused, so far slower than the tuned loop.  Default 0. */
+#define DFM_OPT_EXACT 11
 DFM_API dfm_status dfm_ctx_set_option(dfm_ctx* ctx, int key, int64_t value);
 
 /* White-box read of a named device workspace buffer of the context after a

@@ -40,7 +40,9 @@ def _compile(src: str, force: bool) -> str:
     if (not force and os.path.exists(obj)
             and os.path.getmtime(obj) >= max(os.path.getmtime(src), _deps_mtime())):
         return obj
-    cmd = [NVCC] + ARCH + FLAGS + ["-Xptxas", "-v", "-c", src, "-o", obj]
+    # the exact parity mode: no mul+add contraction anywhere (reference order)
+    extra = ["-fmad=false"] if os.path.basename(src) == "kernels_exact.cu" else []
+    cmd = [NVCC] + ARCH + FLAGS + extra + ["-Xptxas", "-v", "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")

@@ -29,6 +29,16 @@
 
 using namespace dfm;
 
+namespace dfm {
+// kernels_exact.cu: register_images with the reference's arithmetic (DFM_OPT_EXACT)
+int exact_register_status(cudaStream_t stream, int64_t* launches, const dfm_grid* g,
+                          const double* F, const double* M, const dfm_config* cfg,
+                          const double* scales, const int32_t* iters, int ns,
+                          const dfm_init* init, double* d_field_aos,
+                          std::vector<dfm_iter_record>& recs, double* final_loss, double* sing,
+                          std::string& msg);
+}  // namespace dfm
+
 namespace {
 
 
@@ -143,6 +153,9 @@ struct dfm_ctx {
     // z-slab runs: overlap each stage's halo exchange with its interior planes
     // (-1 auto = multi-process NCCL only, 0 off, 1 on; DFM_OPT_SLAB_OVERLAP)
     int slab_overlap = -1;
+    // register_images with the reference's arithmetic, bit-identical (fp64
+    // contexts; DFM_OPT_EXACT)
+    bool exact = false;
     Launch L() { return Launch{stream, &launches, num_sms, pdl, large_min}; }
 
     LoopState* pinned_state() {
@@ -694,6 +707,10 @@ dfm_status dfm_ctx_set_option(dfm_ctx* ctx, int key, int64_t value) {
         } else if (key == DFM_OPT_SPLIT_FOLD_MAX) {
             if (value < 0) fail(DFM_E_INVALID, "split_fold_max must be >= 0");
             ctx->split_fold_max = value;
+        } else if (key == DFM_OPT_EXACT) {
+            if (value && ctx->prec != DFM_PREC_F64)
+                fail(DFM_E_INVALID, "exact mode needs an fp64 context");
+            ctx->exact = value != 0;
         } else if (key == DFM_OPT_SLAB_OVERLAP) {
             if (value < -1 || value > 1) fail(DFM_E_INVALID, "slab_overlap must be -1, 0 or 1");
             ctx->slab_overlap = static_cast<int>(value);
@@ -2587,6 +2604,28 @@ void register_dev(dfm_ctx* ctx, const dfm_grid* g, const T* F, const T* M, const
     if (result) *result = R.u[R.cur].r();
 }
 
+// DFM_OPT_EXACT: register_images through kernels_exact.cu; F, M full-resolution
+// device doubles; the AoS field stays in the context buffer "exact_field"
+double* run_exact(dfm_ctx* ctx, const dfm_grid* g, const double* F, const double* M,
+                  const dfm_config* cfg, const double* scales, const int32_t* iters, int ns,
+                  const dfm_init* init, RegOut& out) {
+    const double t0 = now_ms();
+    for (int i = 0; i < ns; ++i) {  // core.cpp:58-74 grid checks, as the tuned path
+        const double fac[3] = {scales[i], scales[i], scales[i]};
+        dfm_grid wgd;
+        downsample_grid(g, fac, &wgd);
+    }
+    const int64_t n = g->dims[0] * g->dims[1] * g->dims[2];
+    double* field = ctx->arr<double>("exact_field", n * g->ndim);
+    std::string msg;
+    const int rc = exact_register_status(ctx->stream, &ctx->launches, g, F, M, cfg, scales, iters,
+                                         ns, init, field, out.recs, &out.final_loss, &out.sing,
+                                         msg);
+    if (rc != DFM_OK) fail(rc, "%s", msg.c_str());
+    out.total_ms = now_ms() - t0;
+    return field;
+}
+
 void fill_log(const RegOut& o, dfm_iter_record* records, int64_t max_records, dfm_runlog* log) {
     const int64_t n = static_cast<int64_t>(o.recs.size());
     const int64_t k = n < max_records ? n : max_records;
@@ -2628,6 +2667,33 @@ dfm_status dfm_register(dfm_ctx* ctx, const dfm_grid* g, const void* fixed, cons
         const Dims d = to_dims(g);
         RegOut o;
         for (int k = 0; k < DFM_NUM_KCLASS; ++k) ctx->kt_ms[k] = 0, ctx->kt_n[k] = 0, ctx->kt_vox[k] = 0;
+        if (ctx && ctx->exact) {
+            CK(cudaSetDevice(ctx->device));
+            double* F = ctx->arr<double>("host_F", d.n);
+            double* M = ctx->arr<double>("host_M", d.n);
+            if (image_dtype == DFM_HOST_F32) {
+                upload_image<double, float>(ctx, static_cast<const float*>(fixed), d.n, F);
+                upload_image<double, float>(ctx, static_cast<const float*>(moving), d.n, M);
+            } else {
+                upload_image<double, double>(ctx, static_cast<const double*>(fixed), d.n, F);
+                upload_image<double, double>(ctx, static_cast<const double*>(moving), d.n, M);
+            }
+            double* fld = run_exact(ctx, g, F, M, cfg, scales, iterations, nscales, init, o);
+            if (out_field) {
+                if (field_dtype == DFM_HOST_F32)
+                    download_image<double, float>(ctx, fld, d.n * d.ndim,
+                                                  static_cast<float*>(out_field));
+                else
+                    download_image<double, double>(ctx, fld, d.n * d.ndim,
+                                                   static_cast<double*>(out_field));
+            }
+            ctx->sync();
+            o.total_ms = now_ms() - t0;
+            fill_log(o, records, max_records, log);
+            if (o.sing > 0.0)
+                fail(DFM_E_NUMERICAL, "register_images: folded warp (det J <= 0 somewhere)");
+            return;
+        }
         DFM_DISPATCH(ctx, {
             T* F = ctx->arr<T>("host_F", d.n);
             T* M = ctx->arr<T>("host_M", d.n);
@@ -2667,6 +2733,23 @@ dfm_status dfm_dev_register(dfm_ctx* ctx, const dfm_grid* g, const void* d_fixed
         const Dims d = to_dims(g);
         RegOut o;
         for (int k = 0; k < DFM_NUM_KCLASS; ++k) ctx->kt_ms[k] = 0, ctx->kt_n[k] = 0, ctx->kt_vox[k] = 0;
+        if (ctx && ctx->exact) {  // fp64 context: device doubles in, SoA doubles out
+            CK(cudaSetDevice(ctx->device));
+            double* fld = run_exact(ctx, g, static_cast<const double*>(d_fixed),
+                                    static_cast<const double*>(d_moving), cfg, scales, iterations,
+                                    nscales, nullptr, o);
+            if (d_out_soa_field) {
+                double* outp = static_cast<double*>(d_out_soa_field);
+                launch_aos_to_soa<double, double>(
+                    ctx->L(), fld, Planes3<double>{{outp, outp + d.n, outp + 2 * d.n}}, d.n,
+                    d.ndim);
+            }
+            ctx->sync();
+            fill_log(o, records, max_records, log);
+            if (o.sing > 0.0)
+                fail(DFM_E_NUMERICAL, "register_images: folded warp (det J <= 0 somewhere)");
+            return;
+        }
         DFM_DISPATCH(ctx, {
             CPlanes3<T> res;
             register_dev<T>(ctx, g, static_cast<const T*>(d_fixed), static_cast<const T*>(d_moving),

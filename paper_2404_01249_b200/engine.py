@@ -52,6 +52,7 @@ OPT_SPLIT_FOLD_MAX = 6
 OPT_LARGE_MIN = 7
 OPT_SLAB_REPL_MAX = 9
 OPT_SLAB_OVERLAP = 10
+OPT_EXACT = 11
 
 _lib: Optional[C.CDLL] = None
 
