@@ -19,6 +19,9 @@ namespace gpu {
 // the reference's arithmetic type) or DFM_PREC_F32 (the benchmarked mode).
 void set_precision(int precision);
 int precision();
+// register_images with the reference's arithmetic, bit-identical to it
+// (DFM_OPT_EXACT; fp64 only, unfused): parity checks on chaotic inputs.
+void set_exact(bool on);
 // Devices the sweep's workers are spread over (default {0}).
 void set_sweep_devices(const std::vector<int>& devices);
 // The calling thread's context (created on first use on device 0) and the

@@ -55,6 +55,11 @@ int& thread_precision() {
     return p;
 }
 
+bool& thread_exact() {
+    thread_local bool e = false;
+    return e;
+}
+
 struct CtxDeleter {
     void operator()(dfm_ctx* c) const { dfm_ctx_destroy(c); }
 };
@@ -77,11 +82,13 @@ void check(dfm_status s) {
 dfm_ctx* ctx() {
     thread_local std::unique_ptr<dfm_ctx, CtxDeleter> c;
     thread_local int made_for = -1;
-    if (!c || made_for != thread_precision()) {
+    const int want = thread_precision() * 2 + (thread_exact() ? 1 : 0);
+    if (!c || made_for != want) {
         dfm_ctx* raw = nullptr;
         check(dfm_ctx_create(0, thread_precision(), &raw));
         c.reset(raw);
-        made_for = thread_precision();
+        if (thread_exact()) check(dfm_ctx_set_option(raw, DFM_OPT_EXACT, 1));
+        made_for = want;
     }
     return c.get();
 }
@@ -92,6 +99,12 @@ void set_precision(int precision) {
     thread_precision() = precision;
 }
 int precision() { return thread_precision(); }
+
+void set_exact(bool on) {
+    if (on && thread_precision() != DFM_PREC_F64)
+        throw std::invalid_argument("set_exact: needs the fp64 precision");
+    thread_exact() = on;
+}
 
 void set_sweep_devices(const std::vector<int>& devices) {
     if (devices.empty()) throw std::invalid_argument("set_sweep_devices: no devices");
