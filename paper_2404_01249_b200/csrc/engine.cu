@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <limits>
 #include <map>
 #include <stdexcept>
@@ -232,6 +233,17 @@ struct dfm_ctx {
     }
     void sync() { CK(cudaStreamSynchronize(stream)); }
     void check_launch() { CK(cudaGetLastError()); }
+    // a second stream for copies that overlap the main stream's kernels (the
+    // result download beside the registration epilogue)
+    cudaStream_t side = nullptr;
+    cudaEvent_t side_ev = nullptr;
+    cudaStream_t side_stream() {
+        if (!side) {
+            CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&side_ev, cudaEventDisableTiming));
+        }
+        return side;
+    }
 };
 
 namespace {
@@ -652,6 +664,11 @@ void dfm_ctx_destroy(dfm_ctx* ctx) {
     for (auto& kv : ctx->bufs) cudaFree(kv.second.first);
     for (auto& kv : ctx->pinned) cudaFreeHost(kv.second.first);
     for (auto& kv : ctx->graph_cache) cudaGraphExecDestroy(kv.second);
+    if (ctx->side) {
+        cudaStreamSynchronize(ctx->side);
+        cudaStreamDestroy(ctx->side);
+        cudaEventDestroy(ctx->side_ev);
+    }
     if (ctx->hstate) cudaFreeHost(ctx->hstate);
     for (int k = 0; k < 2; ++k)
         if (ctx->chunk_ev[k]) cudaEventDestroy(ctx->chunk_ev[k]);
@@ -1755,6 +1772,10 @@ enum { KC_FWD = 0, KC_BWD = 1, KC_ADAM = 2, KC_COMPOSE = 3, KC_MON = 4, KC_PYR =
 
 template <class T>
 struct Registrar {
+    // called once the full-resolution result field is final, before the
+    // epilogue's loss and fold-check kernels (which only read it): the host
+    // entry point starts the result download there, beside the epilogue
+    std::function<void(CPlanes3<T>)> on_final;
     dfm_ctx* ctx;
     const dfm_grid* g;
     const dfm_config* cfg;
@@ -2212,6 +2233,7 @@ struct Registrar {
                                sizeof(T) * 3 * d.n, cudaMemcpyDeviceToDevice, ctx->stream));
             cur = 1 - cur;
         }
+        if (on_final) on_final(u[cur].r());
         T* coef0[4] = {nullptr, nullptr, nullptr, nullptr};
         check_loss_inputs(F, M, g);
         int np = -1;
@@ -2594,8 +2616,10 @@ struct Registrar {
 template <class T>
 void register_dev(dfm_ctx* ctx, const dfm_grid* g, const T* F, const T* M, const dfm_config* cfg,
                   const double* scales, const int32_t* iters, int ns, const dfm_init* init,
-                  RegOut& out, CPlanes3<T>* result) {
+                  RegOut& out, CPlanes3<T>* result,
+                  std::function<void(CPlanes3<T>)> on_final = {}) {
     Registrar<T> R{};
+    R.on_final = std::move(on_final);
     R.ctx = ctx;
     R.g = g;
     R.cfg = cfg;
@@ -2705,14 +2729,32 @@ dfm_status dfm_register(dfm_ctx* ctx, const dfm_grid* g, const void* fixed, cons
                 upload_image<T, double>(ctx, static_cast<const double*>(moving), d.n, M);
             }
             CPlanes3<T> res;
-            register_dev<T>(ctx, g, F, M, cfg, scales, iterations, nscales, init, o, &res);
-            if (out_field) {
-                if (field_dtype == DFM_HOST_F32)
-                    download_field<T, float>(ctx, res, d.n, d.ndim, static_cast<float*>(out_field));
-                else
-                    download_field<T, double>(ctx, res, d.n, d.ndim,
-                                              static_cast<double*>(out_field));
-            }
+            // the result leaves for the host on the side stream while the
+            // epilogue (full-resolution loss, fold check) runs
+            std::function<void(CPlanes3<T>)> hook;
+            if (out_field)
+                hook = [&](CPlanes3<T> r) {
+                    cudaStream_t s2 = ctx->side_stream();
+                    CK(cudaEventRecord(ctx->side_ev, ctx->stream));
+                    CK(cudaStreamWaitEvent(s2, ctx->side_ev, 0));
+                    cudaStream_t s1 = ctx->stream;
+                    ctx->stream = s2;  // download_field enqueues on ctx->stream
+                    if (field_dtype == DFM_HOST_F32)
+                        download_field<T, float>(ctx, r, d.n, d.ndim,
+                                                 static_cast<float*>(out_field));
+                    else
+                        download_field<T, double>(ctx, r, d.n, d.ndim,
+                                                  static_cast<double*>(out_field));
+                    ctx->stream = s1;
+                };
+            struct SideJoin {  // the download finishes before we return, error or not
+                dfm_ctx* c;
+                ~SideJoin() {
+                    if (c->side) cudaStreamSynchronize(c->side);
+                }
+            } join{ctx};
+            register_dev<T>(ctx, g, F, M, cfg, scales, iterations, nscales, init, o, &res, hook);
+            if (out_field) CK(cudaStreamSynchronize(ctx->side_stream()));
             ctx->sync();
         });
         o.total_ms = now_ms() - t0;
