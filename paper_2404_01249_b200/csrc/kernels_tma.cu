@@ -33,7 +33,12 @@ namespace dfm {
 
 namespace {
 
-constexpr int TX = kTX;
+#ifndef DFM_TMA_TX  // x width of a z-march tile (A/B builds; 32 = one warp per row)
+#define DFM_TMA_TX kTX
+#endif
+constexpr int TX = DFM_TMA_TX;
+// launch bounds keep the register budget of a 32-wide tile at any width
+constexpr int kMinBScale = TX < 32 ? 32 / TX : 1;
 
 // TMA ring depths (planes in flight per CTA); overridable for tuning builds
 #ifndef DFM_S_FWD
@@ -185,12 +190,12 @@ struct ExtraBytes<Op, std::void_t<decltype(Op::kExtraBytes)>> {
 template <class Op>
 __host__ __device__ constexpr int zm2_core_bytes() {
     using Acc = typename Op::Acc;
-    constexpr int HI = Op::TYv + 2 * Op::R, WI = kTX + 2 * Op::R;
+    constexpr int HI = Op::TYv + 2 * Op::R, WI = TX + 2 * Op::R;
     if constexpr (Op::kStaged && Op::R == 0)  // pointwise: no filter buffers
         return Op::S * Op::kStageBytes;
     return Op::S * Op::kStageBytes +
            (Op::kStaged ? int(sizeof(Acc)) * Op::C * HI * WI : 0) +
-           2 * int(sizeof(Acc)) * Op::C * HI * kTX;
+           2 * int(sizeof(Acc)) * Op::C * HI * TX;
 }
 __device__ __forceinline__ unsigned char* zm2_smem_base() {
     // TMA destinations need 128 B alignment; the dynamic window starts right
@@ -308,7 +313,7 @@ struct ZG2 {
 // Adam bias corrections) are computed once; Op::Carry lets an op defer work of
 // plane zo into plane zo+1 (latency hiding).
 template <class Op>
-__global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB)
+__global__ void __launch_bounds__(TX * Op::TYv / Op::kCY, Op::kMinB * kMinBScale)
     k_zm2(const __grid_constant__ Op op, const ZG2 g) {
     using Acc = typename Op::Acc;
     constexpr int TYv = Op::TYv, CY = Op::kCY, TYt = TYv / CY, NTh = TX * TYt;
