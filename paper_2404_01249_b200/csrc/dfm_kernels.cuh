@@ -3,11 +3,38 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <cuda_runtime.h>
 
 #include "dfm_device.cuh"
 
 namespace dfm {
+
+// One-time setup of a kernel on the current device: opt in to `smem` bytes of
+// dynamic shared memory and return its resident CTAs per SM (0 on failure).
+// Function attributes belong to the device's context, so a process driving
+// several GPUs (dfm_sweep over devices) configures each device once.
+inline int kernel_setup(const void* kern, int block, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, int> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_pair(dev, kern);
+    const auto it = done.find(key);
+    if (it != done.end()) return it->second;
+    int occ = 0;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem)) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, block, smem) != cudaSuccess) {
+        cudaGetLastError();
+        occ = 0;
+    }
+    done[key] = occ;
+    return occ;
+}
 
 constexpr int kRMax = 8;          // largest radius of the fused z-march kernels
 constexpr int kTX = 32, kTY = 8;  // z-march CTA tile (x, y)

@@ -766,16 +766,8 @@ int run_persist(const Launch& L, const PersistArgs<T, R, RG, RW>& a, const Dims&
     if constexpr (bytes > kBrickSmemMax) {
         return -2;
     } else {
-        static std::once_flag once;
-        static int per_sm = 0;
-        std::call_once(once, [] {
-            cudaFuncSetAttribute(k_persist<T, R, RG, RW>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(bytes));
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_persist<T, R, RG, RW>,
-                                                              NTP, bytes) != cudaSuccess)
-                per_sm = 0;
-        });
+        const int per_sm =
+            kernel_setup(reinterpret_cast<const void*>(k_persist<T, R, RG, RW>), NTP, bytes);
         if (per_sm < 1) return -3;
         BG g;
         g.d = d;
@@ -803,11 +795,7 @@ int run_brick(const Launch& L, const Op& op, const Dims& d) {
     if constexpr (Lay::bytes > kBrickSmemMax) {
         return -2;  // e.g. fp64 with a large Gaussian radius: caller falls back
     } else {
-    static std::once_flag once;
-    std::call_once(once, [] {
-        cudaFuncSetAttribute(k_brick<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(Lay::bytes));
-    });
+    kernel_setup(reinterpret_cast<const void*>(k_brick<Op>), NTB, Lay::bytes);
     BG g;
     g.d = d;
     g.nbx = (d.nx + BX - 1) / BX;

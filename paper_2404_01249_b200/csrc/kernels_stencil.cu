@@ -510,12 +510,7 @@ int run_zmarch(const Launch& L, const Op& op, Dims d) {
     const int nchunks = zmarch_blocks(d, R, L.num_sms, &g.zchunk, &tiles);
     g.tiles_x = (d.nx + kTX - 1) / kTX;
     const size_t smem = zmarch_smem<R, Op>();
-    static bool configured = false;  // per instantiation
-    if (!configured) {
-        cudaFuncSetAttribute(k_zmarch<R, Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
-        configured = true;
-    }
+    kernel_setup(reinterpret_cast<const void*>(k_zmarch<R, Op>), kNT, smem);
     dim3 grid(tiles, nchunks);
     k_zmarch<R, Op><<<grid, kNT, smem, L.stream>>>(op, g);
     L.bump();

@@ -1863,15 +1863,9 @@ int run_zm2(const Launch& L, const Op& op, Dims d) {
     ZG2 g;
     g.d = d;
     const size_t smem = zm2_smem<Op>();
-    static int occ = 0;  // resident CTAs per SM for this instantiation
-    if (occ == 0) {
-        cudaFuncSetAttribute(k_zm2<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_zm2<Op>, TX * Op::TYv / Op::kCY,
-                                                          smem) !=
-                cudaSuccess || occ < 1)
-            occ = 1;
-    }
+    int occ = kernel_setup(reinterpret_cast<const void*>(k_zm2<Op>), TX * Op::TYv / Op::kCY,
+                           smem);  // resident CTAs per SM
+    if (occ < 1) occ = 1;
     g.tiles_x = (d.nx + TX - 1) / TX;
     const int tiles = g.tiles_x * ((d.ny + Op::TYv - 1) / Op::TYv);
     // resident-CTA slots the chunking may plan for (DFM_SLOT_CAP caps CTAs per
