@@ -640,8 +640,6 @@ void exact_register(cudaStream_t stream, int64_t* launches, const dfm_grid* g, c
         return value;
     };
 
-    const double t0_unused = 0.0;
-    (void)t0_unused;
     Meta cur{};
     bool have = false;
     int64_t t_adam = 0, global = 0;
