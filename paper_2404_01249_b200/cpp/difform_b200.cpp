@@ -96,6 +96,8 @@ dfm_ctx* ctx() {
 void set_precision(int precision) {
     if (precision != DFM_PREC_F32 && precision != DFM_PREC_F64)
         throw std::invalid_argument("set_precision: DFM_PREC_F32 or DFM_PREC_F64");
+    if (precision != DFM_PREC_F64 && thread_exact())
+        throw std::invalid_argument("set_precision: the exact mode needs fp64 (set_exact(false) first)");
     thread_precision() = precision;
 }
 int precision() { return thread_precision(); }
