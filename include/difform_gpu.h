@@ -542,6 +542,10 @@ DFM_API dfm_status dfm_ctx_kernel_times(const dfm_ctx* ctx, double* ms, int64_t*
  * to the reference's result, for parity checks on chaotic inputs.  fp64
  * contexts only; unfused, so far slower than the tuned loop.  Default 0. */
 #define DFM_OPT_EXACT 11
+/* DFM_OPT_NARROW: 1 (default) = a plane-streaming level whose last 32-wide x
+ * tile would be at most half full (e.g. 80 columns) runs the 16-wide
+ * instantiation of the z-march kernels (same results); 0 = always 32-wide. */
+#define DFM_OPT_NARROW 12
 DFM_API dfm_status dfm_ctx_set_option(dfm_ctx* ctx, int key, int64_t value);
 
 /* White-box read of a named device workspace buffer of the context after a

@@ -37,8 +37,11 @@ def _deps_mtime() -> float:
 
 def _compile(src: str, force: bool) -> str:
     obj = os.path.join(OBJ, os.path.basename(src).replace(".cu", ".o"))
+    srcs = [src]
+    if os.path.basename(src) == "kernels_tma16.cu":  # includes kernels_tma.cu
+        srcs.append(os.path.join(CSRC, "kernels_tma.cu"))
     if (not force and os.path.exists(obj)
-            and os.path.getmtime(obj) >= max(os.path.getmtime(src), _deps_mtime())):
+            and os.path.getmtime(obj) >= max(max(map(os.path.getmtime, srcs)), _deps_mtime())):
         return obj
     # the exact parity mode: no mul+add contraction anywhere (reference order)
     extra = ["-fmad=false"] if os.path.basename(src) == "kernels_exact.cu" else []

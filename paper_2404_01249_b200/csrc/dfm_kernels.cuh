@@ -105,6 +105,9 @@ struct Launch {
     // (two-row fp32 smooth+Adam, cp.async-carried compose-smooth gather);
     // DFM_OPT_LARGE_MIN lowers it so the tests reach those variants at any size
     int64_t large_min = 2000000;
+    // mid-size levels whose last 32-wide x tile would be at most half full run
+    // the 16-wide z-march instantiation (DFM_OPT_NARROW)
+    bool narrow = true;
     void bump() const {
         if (counter) ++*counter;
     }

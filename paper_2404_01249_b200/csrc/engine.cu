@@ -157,7 +157,13 @@ struct dfm_ctx {
     // register_images with the reference's arithmetic, bit-identical (fp64
     // contexts; DFM_OPT_EXACT)
     bool exact = false;
-    Launch L() { return Launch{stream, &launches, num_sms, pdl, large_min}; }
+    // 16-wide z-march tiles on mid-size levels with a half-empty last x tile
+    bool narrow = getenv("DFM_TMA_NARROW") ? atoi(getenv("DFM_TMA_NARROW")) != 0 : true;
+    Launch L() {
+        Launch l{stream, &launches, num_sms, pdl, large_min};
+        l.narrow = narrow;
+        return l;
+    }
 
     LoopState* pinned_state() {
         if (!hstate) {
@@ -724,6 +730,8 @@ dfm_status dfm_ctx_set_option(dfm_ctx* ctx, int key, int64_t value) {
         } else if (key == DFM_OPT_SPLIT_FOLD_MAX) {
             if (value < 0) fail(DFM_E_INVALID, "split_fold_max must be >= 0");
             ctx->split_fold_max = value;
+        } else if (key == DFM_OPT_NARROW) {
+            ctx->narrow = value != 0;
         } else if (key == DFM_OPT_EXACT) {
             if (value && ctx->prec != DFM_PREC_F64)
                 fail(DFM_E_INVALID, "exact mode needs an fp64 context");
@@ -2510,7 +2518,7 @@ struct Registrar {
                                          ctx->prec, ctx->brick_max, ctx->split_compose,
                                          ctx->split3, ctx->split_fold_max, ctx->large_min,
                                          ctx->pdl, ctx->tma_mask, ctx->fwd3,
-                                         ctx->force_legacy};
+                                         ctx->force_legacy, ctx->narrow};
                 mix(parts, sizeof(parts));
                 // config fields that select kernels (scalars such as eta or the
                 // betas are kernel parameters: an update carries them)

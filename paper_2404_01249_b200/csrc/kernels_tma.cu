@@ -29,13 +29,22 @@
 #include "loop_ops.cuh"
 #include "tma_util.cuh"
 
+// This file is compiled twice: as itself (32-wide tiles, namespace dfm::tx32,
+// plus the public dispatching launchers at the end) and through
+// kernels_tma16.cu (16-wide tiles, dfm::tx16): a level whose last 32-wide x
+// tile would be at most half full runs the narrow instantiation.
+#ifndef DFM_TMA_TX  // x width of a z-march tile
+#define DFM_TMA_TX kTX
+#endif
+#ifndef DFM_TMA_NS
+#define DFM_TMA_NS tx32
+#endif
+
 namespace dfm {
+namespace DFM_TMA_NS {
 
 namespace {
 
-#ifndef DFM_TMA_TX  // x width of a z-march tile (A/B builds; 32 = one warp per row)
-#define DFM_TMA_TX kTX
-#endif
 constexpr int TX = DFM_TMA_TX;
 // launch bounds keep the register budget of a 32-wide tile at any width
 constexpr int kMinBScale = TX < 32 ? 32 / TX : 1;
@@ -1898,7 +1907,7 @@ int with_r(int R, F&& f) {
 
 }  // namespace
 
-bool tma_supported(Dims d, int esz) {
+bool tma_supported_(Dims d, int esz) {
     return encoder() != nullptr && (static_cast<int64_t>(d.nx) * esz) % 16 == 0;
 }
 
@@ -2249,5 +2258,128 @@ void launch_warpgrad(const Launch& L, const T* M, Dims dm, CPlanes3<T> u, Dims d
 
 DFM_INST_TMA(float)
 DFM_INST_TMA(double)
+
+}  // namespace DFM_TMA_NS
+
+#ifndef DFM_TMA_NO_DISPATCH
+// ---------------------------------------------------------------------------
+// public launchers (dfm_kernels.cuh): 16-wide tiles where the last 32-wide x
+// tile of a mid-size level would be at most half full (80 columns: 97.6 ->
+// 93.7 us per iteration at 80x96x112; full-size and 32-multiple widths keep
+// 32); DFM_OPT_NARROW 0 disables the choice
+namespace tx16 {
+template <class T>
+int launch_lncc_fwd_tma(const Launch&, int, const T*, const T*, Dims, T*, double*,
+                        const LoopState*, const MonitorArgs*);
+template <class T>
+int launch_lncc_bwd_tma(const Launch&, int, const T*, const T*, const T*, const T*, Dims, T*,
+                        const LoopState*);
+template <class T>
+int launch_fstats_tma(const Launch&, int, const T*, Dims, double*);
+template <class T>
+int launch_lncc_fwd3_tma(const Launch&, int, const T*, const T*, const double*, Dims, T*,
+                         double*, const LoopState*, const MonitorArgs*);
+template <class T>
+int launch_smooth_adam_tma(const Launch&, int, const GaussW<T>&, const T*, T*, T*, T*, Dims,
+                           AdamParams, LoopState*, unsigned long long*, const T*);
+template <class T>
+int launch_compose_tma(const Launch&, int, double, const GaussW<T>&, const T*, const T*, T*,
+                       const T*, Dims, Dims, T*, T*, LoopState*, bool);
+template <class T>
+int launch_gauss_tma(const Launch&, int, const GaussW<T>&, const T*, T*, Dims);
+template <class T>
+int launch_svf_update_tma(const Launch&, int, const GaussW<T>&, const T*, const T*, T*, Dims,
+                          LoopState*);
+template <class T>
+int launch_smooth_adam_compose_tma(const Launch&, int, const GaussW<T>&, const T*, T*, T*,
+                                   const T*, T*, double, Dims, AdamParams, LoopState*,
+                                   unsigned long long*);
+template <class T>
+int launch_compose_smooth_tma(const Launch&, int, const GaussW<T>&, const T*, T*, const T*, Dims,
+                              Dims, T*, T*, LoopState*, bool);
+}  // namespace tx16
+
+namespace {
+bool narrow_tile(const Launch& L, const Dims& d) {
+    const int rem = d.nx % kTX;
+    return L.narrow && d.n < L.large_min && rem != 0 && rem <= kTX / 2 && d.nx >= kTX;
+}
+}  // namespace
+
+bool tma_supported(Dims d, int esz) { return tx32::tma_supported_(d, esz); }
+
+#define DFM_PICK(fn, ...) \
+    (narrow_tile(L, d) ? tx16::fn<T>(__VA_ARGS__) : tx32::fn<T>(__VA_ARGS__))
+
+template <class T>
+int launch_lncc_fwd_tma(const Launch& L, int R, const T* F, const T* W, Dims d, T* coef,
+                        double* partials, const LoopState* st, const MonitorArgs* mon) {
+    return DFM_PICK(launch_lncc_fwd_tma, L, R, F, W, d, coef, partials, st, mon);
+}
+template <class T>
+int launch_lncc_bwd_tma(const Launch& L, int R, const T* coef, const T* F, const T* W,
+                        const T* G, Dims d, T* grad, const LoopState* st) {
+    return DFM_PICK(launch_lncc_bwd_tma, L, R, coef, F, W, G, d, grad, st);
+}
+template <class T>
+int launch_fstats_tma(const Launch& L, int R, const T* F, Dims d, double* fstat) {
+    return DFM_PICK(launch_fstats_tma, L, R, F, d, fstat);
+}
+template <class T>
+int launch_lncc_fwd3_tma(const Launch& L, int R, const T* F, const T* W, const double* fstat,
+                         Dims d, T* coef, double* partials, const LoopState* st,
+                         const MonitorArgs* mon) {
+    return DFM_PICK(launch_lncc_fwd3_tma, L, R, F, W, fstat, d, coef, partials, st, mon);
+}
+template <class T>
+int launch_smooth_adam_tma(const Launch& L, int R, const GaussW<T>& w, const T* grad, T* m,
+                           T* nu, T* step, Dims d, AdamParams ap, LoopState* st,
+                           unsigned long long* maxstep, const T* ujac) {
+    return DFM_PICK(launch_smooth_adam_tma, L, R, w, grad, m, nu, step, d, ap, st, maxstep, ujac);
+}
+template <class T>
+int launch_compose_tma(const Launch& L, int R, double cap, const GaussW<T>& w, const T* step,
+                       const T* uin, T* uout, const T* M, Dims dm, Dims d, T* W, T* G,
+                       LoopState* st, bool count_update) {
+    return DFM_PICK(launch_compose_tma, L, R, cap, w, step, uin, uout, M, dm, d, W, G, st,
+                    count_update);
+}
+template <class T>
+int launch_gauss_tma(const Launch& L, int R, const GaussW<T>& w, const T* in, T* out, Dims d) {
+    return DFM_PICK(launch_gauss_tma, L, R, w, in, out, d);
+}
+template <class T>
+int launch_svf_update_tma(const Launch& L, int R, const GaussW<T>& w, const T* v, const T* step,
+                          T* out, Dims d, LoopState* st) {
+    return DFM_PICK(launch_svf_update_tma, L, R, w, v, step, out, d, st);
+}
+template <class T>
+int launch_smooth_adam_compose_tma(const Launch& L, int R, const GaussW<T>& w, const T* grad,
+                                   T* m, T* nu, const T* uin, T* cout, double cap, Dims d,
+                                   AdamParams ap, LoopState* st, unsigned long long* maxstep) {
+    return DFM_PICK(launch_smooth_adam_compose_tma, L, R, w, grad, m, nu, uin, cout, cap, d, ap,
+                    st, maxstep);
+}
+template <class T>
+int launch_compose_smooth_tma(const Launch& L, int R, const GaussW<T>& w, const T* c, T* uout,
+                              const T* M, Dims dm, Dims d, T* W, T* G, LoopState* st,
+                              bool count_update) {
+    return DFM_PICK(launch_compose_smooth_tma, L, R, w, c, uout, M, dm, d, W, G, st,
+                    count_update);
+}
+#undef DFM_PICK
+template <class T>
+int launch_compose_pointwise(const Launch& L, const T* step, const T* u, double cap, Dims d,
+                             T* c, const LoopState* st) {
+    return tx32::launch_compose_pointwise<T>(L, step, u, cap, d, c, st);
+}
+template <class T>
+void launch_warpgrad(const Launch& L, const T* M, Dims dm, CPlanes3<T> u, Dims d, T* W, T* G) {
+    tx32::launch_warpgrad<T>(L, M, dm, u, d, W, G);
+}
+
+DFM_INST_TMA(float)
+DFM_INST_TMA(double)
+#endif  // DFM_TMA_NO_DISPATCH
 
 }  // namespace dfm

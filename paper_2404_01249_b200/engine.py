@@ -53,6 +53,7 @@ OPT_LARGE_MIN = 7
 OPT_SLAB_REPL_MAX = 9
 OPT_SLAB_OVERLAP = 10
 OPT_EXACT = 11
+OPT_NARROW = 12
 
 _lib: Optional[C.CDLL] = None
 

@@ -12,8 +12,8 @@ import pytest
 
 import golden_cases as G
 from paper_2404_01249_b200 import _abi as A, synth
-from paper_2404_01249_b200.engine import (Context, OPT_BRICK_MAX, OPT_PERSIST, OPT_SPLIT,
-                                          OPT_SPLIT_FOLD_MAX)
+from paper_2404_01249_b200.engine import (Context, OPT_BRICK_MAX, OPT_NARROW, OPT_PERSIST,
+                                          OPT_SPLIT, OPT_SPLIT_FOLD_MAX)
 
 pytestmark = pytest.mark.gpu
 
@@ -127,6 +127,27 @@ def test_update_variants_bit_identical(prec):
     for f, ls in fields[1:]:
         assert np.array_equal(f, fields[0][0])
         assert ls == fields[0][1]
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_narrow_tiles_match_wide(prec):
+    """DFM_OPT_NARROW: an 80-column level on 16-wide z-march tiles gives the
+    field of the 32-wide tiles bit for bit (the per-voxel arithmetic is the
+    same; only the loss's block partial sums are grouped differently)."""
+    p = synth.make_pair(1, seed=7, shape=(56, 48, 80))
+    sched = A.PyramidSchedule((1.0,), (6,))
+    cfg = synth.baseline_config(A.LOSS_LNCC, 2, 1.0, max_iters=6)
+    cfg.eta = 0.2
+    out = []
+    for narrow in (0, 1):
+        ctx = Context(0, prec)
+        ctx.set_option(OPT_BRICK_MAX, 0)
+        ctx.set_option(OPT_NARROW, narrow)
+        f, log = ctx.register_images(p.grid, p.fixed, p.moving, cfg, sched)
+        ctx.close()
+        out.append((f, np.array([r.loss for r in log.iterations])))
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.allclose(out[0][1], out[1][1], rtol=1e-12, atol=0)
 
 
 def test_set_option_rejects_unknown_key():

@@ -14,7 +14,7 @@ for f in sorted(os.listdir(B.CSRC)):
     if not f.endswith(".cu"):
         continue
     src = os.path.join(B.CSRC, f)
-    if f in ("kernels_tma.cu", "kernels_brick.cu"):
+    if f in ("kernels_tma.cu", "kernels_tma16.cu", "kernels_brick.cu"):
         obj = os.path.join(out, f.replace(".cu", ".o"))
         subprocess.run([B.NVCC] + B.ARCH + B.FLAGS + defs + ["-c", src, "-o", obj], check=True)
     else:
