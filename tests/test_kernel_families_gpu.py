@@ -129,11 +129,13 @@ def test_update_variants_bit_identical(prec):
         assert ls == fields[0][1]
 
 
-@pytest.mark.parametrize("prec", ["f32", "f64"])
-def test_narrow_tiles_match_wide(prec):
+@pytest.mark.parametrize("prec,split,fold_max", [("f32", 1, 1 << 40), ("f64", 1, 1 << 40),
+                                                 ("f32", 1, 0), ("f32", 0, 0)])
+def test_narrow_tiles_match_wide(prec, split, fold_max):
     """DFM_OPT_NARROW: an 80-column level on 16-wide z-march tiles gives the
     field of the 32-wide tiles bit for bit (the per-voxel arithmetic is the
-    same; only the loss's block partial sums are grouped differently)."""
+    same; only the loss's block partial sums are grouped differently), with the
+    folded, separate (radius-0 staged) and fused compose forms."""
     p = synth.make_pair(1, seed=7, shape=(56, 48, 80))
     sched = A.PyramidSchedule((1.0,), (6,))
     cfg = synth.baseline_config(A.LOSS_LNCC, 2, 1.0, max_iters=6)
@@ -142,6 +144,8 @@ def test_narrow_tiles_match_wide(prec):
     for narrow in (0, 1):
         ctx = Context(0, prec)
         ctx.set_option(OPT_BRICK_MAX, 0)
+        ctx.set_option(OPT_SPLIT, split)
+        ctx.set_option(OPT_SPLIT_FOLD_MAX, fold_max)
         ctx.set_option(OPT_NARROW, narrow)
         f, log = ctx.register_images(p.grid, p.fixed, p.moving, cfg, sched)
         ctx.close()
