@@ -5,7 +5,10 @@ import os, subprocess, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2404_01249_b200 import build as B
 
-name, defs = sys.argv[1], sys.argv[2:]
+name, args = sys.argv[1], sys.argv[2:]
+# "16:-DX=1" applies to the 16-wide instantiation only (kernels_tma16.cu)
+defs = [a for a in args if not a.startswith("16:")]
+defs16 = defs + [a[3:] for a in args if a.startswith("16:")]
 out = os.path.join(B.ROOT, "build", "variants", name)
 os.makedirs(out, exist_ok=True)
 B.build(verbose=False)
@@ -16,7 +19,8 @@ for f in sorted(os.listdir(B.CSRC)):
     src = os.path.join(B.CSRC, f)
     if f in ("kernels_tma.cu", "kernels_tma16.cu", "kernels_brick.cu"):
         obj = os.path.join(out, f.replace(".cu", ".o"))
-        subprocess.run([B.NVCC] + B.ARCH + B.FLAGS + defs + ["-c", src, "-o", obj], check=True)
+        extra = defs16 if f == "kernels_tma16.cu" else defs
+        subprocess.run([B.NVCC] + B.ARCH + B.FLAGS + extra + ["-c", src, "-o", obj], check=True)
     else:
         obj = os.path.join(B.OBJ, f.replace(".cu", ".o"))
     objs.append(obj)
