@@ -425,6 +425,10 @@ void launch_monitor(const Launch& L, int kind, const double* partials, int np, d
 void launch_reduce_value(const Launch& L, int kind, const double* partials, int np, double nvox,
                          double* out);
 void launch_stamp(const Launch& L, unsigned long long* slot);
+// copy src -> dst (ncomp planes of n) when (T_si - st->nupdates) is odd
+template <class T>
+void launch_parity_fix(const Launch& L, const LoopState* st, int T_si, CPlanes3<T> src,
+                       Planes3<T> dst, int64_t n, int ncomp);
 
 int zmarch_blocks(Dims d, int R, int num_sms, int* zchunk, int* tiles);
 

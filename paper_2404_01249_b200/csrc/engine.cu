@@ -219,6 +219,25 @@ struct dfm_ctx {
         return p;
     }
 
+    // small host -> device uploads staged through pinned memory: from pageable
+    // memory cudaMemcpyAsync first waits for the stream to drain, which would
+    // stall the host (and then idle the GPU) at every pyramid level
+    std::map<std::string, cudaEvent_t> up_ev;
+    void upload(void* dev, const void* src, size_t bytes, const std::string& key) {
+        auto it = up_ev.find(key);
+        if (it == up_ev.end()) {
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            it = up_ev.emplace(key, e).first;
+        } else {
+            CK(cudaEventSynchronize(it->second));  // the previous copy out of it is done
+        }
+        void* h = get_pinned("@up:" + key, bytes);
+        std::memcpy(h, src, bytes);
+        CK(cudaMemcpyAsync(dev, h, bytes, cudaMemcpyHostToDevice, stream));
+        CK(cudaEventRecord(it->second, stream));
+    }
+
     void* get(const std::string& name, size_t bytes) {
         if (bytes == 0) bytes = 16;
         auto it = bufs.find(name);
@@ -366,8 +385,7 @@ GaussW<T> upload_gauss(dfm_ctx* ctx, const HostGauss& h, const Dims& d, const st
         w.ra[a] = h.Ra[a];
     }
     T* dev = ctx->arr<T>("gauss_norm_" + key, static_cast<int64_t>(host.size()));
-    CK(cudaMemcpyAsync(dev, host.data(), host.size() * sizeof(T), cudaMemcpyHostToDevice,
-                       ctx->stream));
+    ctx->upload(dev, host.data(), host.size() * sizeof(T), "gauss_norm_" + key);
     w.norm[0] = dev;
     w.norm[1] = dev + n[0];
     w.norm[2] = dev + n[0] + n[1];
@@ -394,8 +412,7 @@ DevAxisGauss upload_axis_gauss(dfm_ctx* ctx, const HostGauss& h, const Dims& d,
         host.insert(host.end(), h.norm[a].begin(), h.norm[a].end());
     }
     double* dev = ctx->arr<double>("axis_gauss_" + key, static_cast<int64_t>(host.size()));
-    CK(cudaMemcpyAsync(dev, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice,
-                       ctx->stream));
+    ctx->upload(dev, host.data(), host.size() * sizeof(double), "axis_gauss_" + key);
     for (int a = 0; a < 3; ++a) {
         g.Ra[a] = h.Ra[a];
         g.taps[a] = dev + offs[2 * a];
@@ -668,6 +685,7 @@ void dfm_ctx_destroy(dfm_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     for (auto& kv : ctx->bufs) cudaFree(kv.second.first);
+    for (auto& kv : ctx->up_ev) cudaEventDestroy(kv.second);
     for (auto& kv : ctx->pinned) cudaFreeHost(kv.second.first);
     for (auto& kv : ctx->graph_cache) cudaGraphExecDestroy(kv.second);
     if (ctx->side) {
@@ -1862,13 +1880,9 @@ struct Registrar {
             h1[t] = 1.0 - std::pow(cfg->beta1, static_cast<double>(t));
             h2[t] = 1.0 - std::pow(cfg->beta2, static_cast<double>(t));
         }
-        CK(cudaMemcpyAsync(corr1, h1.data(), sizeof(double) * cap, cudaMemcpyHostToDevice,
-                           ctx->stream));
-        CK(cudaMemcpyAsync(corr2, h2.data(), sizeof(double) * cap, cudaMemcpyHostToDevice,
-                           ctx->stream));
+        ctx->upload(corr1, h1.data(), sizeof(double) * cap, "reg_corr1");
+        ctx->upload(corr2, h2.data(), sizeof(double) * cap, "reg_corr2");
         CK(cudaMemsetAsync(st, 0, sizeof(LoopState), ctx->stream));
-        // corr tables are host vectors: make sure the copies finished before they die
-        ctx->sync();
     }
 
     void zero_field(Field<T>& f, int64_t n) {
@@ -2270,6 +2284,7 @@ struct Registrar {
         CK(cudaMemcpyAsync(&hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream));
         ctx->sync();
         ev_collect(full);
+        consume_logs(global, out);
         out.final_loss = hv[0];
         out.sing = static_cast<double>(hc) / static_cast<double>(d.n);
         out.total_ms = now_ms() - t0;
@@ -2484,10 +2499,7 @@ struct Registrar {
             ps.tol = cfg->conv_tol;
             ps.iters = T_si;
             persisted = launch_persist_scale<T>(ctx->L(), ps) >= 0;
-            if (persisted) {
-                launch_stamp(ctx->L(), stamp + T_si);
-                ctx->sync();
-            }
+            if (persisted) launch_stamp(ctx->L(), stamp + T_si);
         }
         if (persisted) {
         } else if (ctx->profiling) {
@@ -2579,45 +2591,86 @@ struct Registrar {
                 ++nchunk;
             }
             launch_stamp(ctx->L(), stamp + T_si);
-            ctx->sync();  // the execs stay in ctx->graph_cache for the next call
+            // no sync: the execs stay in ctx->graph_cache for the next call, the
+            // scale's log leaves through pinned copies below
         }
-        // read back the scale's log (one readback per scale)
-        LoopState hs;
-        std::vector<double> hl(T_si + 1);
-        std::vector<unsigned long long> hm(T_si + 1), ht(T_si + 1);
-        CK(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
-        CK(cudaMemcpyAsync(hl.data(), loss, sizeof(double) * T_si, cudaMemcpyDeviceToHost,
+        // the scale's log leaves through stream-ordered copies into pinned
+        // per-level buffers and is read after the registration's last sync: no
+        // host round trip between levels (the host prepares the next level while
+        // the device finishes this one).  The field's buffer parity after an
+        // early stop is settled on the device.
+        LevelLog lg;
+        lg.si = si;
+        lg.scale = scale;
+        lg.T_si = T_si;
+        const std::string key = "lvl" + std::to_string(si) + "_";
+        lg.hs = static_cast<LoopState*>(ctx->get_pinned(key + "st", sizeof(LoopState)));
+        lg.hl = static_cast<double*>(ctx->get_pinned(key + "loss", sizeof(double) * (T_si + 1)));
+        lg.hm = static_cast<unsigned long long*>(
+            ctx->get_pinned(key + "max", sizeof(unsigned long long) * (T_si + 1)));
+        lg.ht = static_cast<unsigned long long*>(
+            ctx->get_pinned(key + "stamp", sizeof(unsigned long long) * (T_si + 1)));
+        CK(cudaMemcpyAsync(lg.hs, st, sizeof(LoopState), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(lg.hl, loss, sizeof(double) * T_si, cudaMemcpyDeviceToHost,
                            ctx->stream));
-        CK(cudaMemcpyAsync(hm.data(), maxstep, sizeof(unsigned long long) * T_si,
+        CK(cudaMemcpyAsync(lg.hm, maxstep, sizeof(unsigned long long) * T_si,
                            cudaMemcpyDeviceToHost, ctx->stream));
-        CK(cudaMemcpyAsync(ht.data(), stamp, sizeof(unsigned long long) * (T_si + 1),
+        CK(cudaMemcpyAsync(lg.ht, stamp, sizeof(unsigned long long) * (T_si + 1),
                            cudaMemcpyDeviceToHost, ctx->stream));
-        ctx->sync();
-        const int nrec = hs.it;
-        for (int j = 0; j < nrec; ++j) {
-            dfm_iter_record r{};
-            r.scale_index = si;
-            r.scale = scale;
-            r.iter = j;
-            r.global_iter = global++;
-            r.loss = hl[j];
-            const bool conv_rec = hs.converged && j == nrec - 1;
-            double ms;
-            std::memcpy(&ms, &hm[j], sizeof(double));
-            r.max_step = conv_rec ? 0.0 : ms;
-            const unsigned long long tn = (j + 1 < nrec) ? ht[j + 1] : ht[T_si];
-            r.wall_ms = tn > ht[j] ? static_cast<double>(tn - ht[j]) * 1e-6 : 0.0;
-            if (hs.err && j == nrec - 1 && !std::isfinite(hl[j])) break;  // not recorded
-            out.recs.push_back(r);
+        pending.push_back(lg);
+        const int assumed = (start + T_si) % 2;  // no early stop: T_si updates
+        launch_parity_fix<T>(ctx->L(), st, T_si, u[1 - assumed].r(), u[assumed].w(), d.n,
+                             d.ndim);
+        cur = assumed;
+        if (ctx->profiling) {  // per-kernel timing: keep the scale's records in step
+            ctx->sync();
+            consume_logs(global, out);
         }
-        if (hs.err) {
-            if (nrec > 0 && !std::isfinite(hl[nrec - 1]))
-                fail(DFM_E_NUMERICAL,
-                     "register_images: non-finite loss at scale %f, iteration %d", scale,
-                     nrec - 1);
-            fail(DFM_E_NUMERICAL, "apply_update: non-finite step");
+    }
+
+    struct LevelLog {
+        int si;
+        double scale;
+        int T_si;
+        LoopState* hs;
+        double* hl;
+        unsigned long long* hm;
+        unsigned long long* ht;
+    };
+    std::vector<LevelLog> pending;
+
+    // records of the finished levels, in order (after a sync); a level's
+    // numerical failure raises here, with the reference's messages
+    void consume_logs(int64_t& global, RegOut& out) {
+        std::vector<LevelLog> logs;
+        logs.swap(pending);
+        for (const LevelLog& lg : logs) {
+            const LoopState& hs = *lg.hs;
+            const int nrec = hs.it;
+            for (int j = 0; j < nrec; ++j) {
+                dfm_iter_record r{};
+                r.scale_index = lg.si;
+                r.scale = lg.scale;
+                r.iter = j;
+                r.global_iter = global++;
+                r.loss = lg.hl[j];
+                const bool conv_rec = hs.converged && j == nrec - 1;
+                double ms;
+                std::memcpy(&ms, &lg.hm[j], sizeof(double));
+                r.max_step = conv_rec ? 0.0 : ms;
+                const unsigned long long tn = (j + 1 < nrec) ? lg.ht[j + 1] : lg.ht[lg.T_si];
+                r.wall_ms = tn > lg.ht[j] ? static_cast<double>(tn - lg.ht[j]) * 1e-6 : 0.0;
+                if (hs.err && j == nrec - 1 && !std::isfinite(lg.hl[j])) break;  // not recorded
+                out.recs.push_back(r);
+            }
+            if (hs.err) {
+                if (nrec > 0 && !std::isfinite(lg.hl[nrec - 1]))
+                    fail(DFM_E_NUMERICAL,
+                         "register_images: non-finite loss at scale %f, iteration %d", lg.scale,
+                         nrec - 1);
+                fail(DFM_E_NUMERICAL, "apply_update: non-finite step");
+            }
         }
-        cur = (start + hs.nupdates) % 2;
     }
 };
 

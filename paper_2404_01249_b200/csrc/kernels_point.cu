@@ -781,6 +781,27 @@ void launch_sgd(const Launch& L, Planes3<T> mu, CPlanes3<T> v, Dims d, double mo
     L.bump();
 }
 
+// the level loop alternates the field between two buffers; with an early stop
+// the result may sit in the other one.  Without a host round trip the next
+// level reads `dst`: copy src -> dst when (T_si - nupdates) is odd.
+template <class T>
+__global__ void k_parity_fix(const LoopState* __restrict__ st, int T_si, CPlanes3<T> src,
+                             Planes3<T> dst, int64_t n, int ncomp) {
+    if (((T_si - st->nupdates) & 1) == 0) return;
+    for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * kNT)
+        for (int c = 0; c < ncomp; ++c) dst.c[c][i] = src.c[c][i];
+}
+
+template <class T>
+void launch_parity_fix(const Launch& L, const LoopState* st, int T_si, CPlanes3<T> src,
+                       Planes3<T> dst, int64_t n, int ncomp) {
+    const int64_t b = (n + kNT - 1) / kNT;
+    k_parity_fix<T><<<static_cast<unsigned>(b < 4096 ? b : 4096), kNT, 0, L.stream>>>(
+        st, T_si, src, dst, n, ncomp);
+    L.bump();
+}
+
 // ---------------------------------------------------------------- instantiations
 #define DFM_INST_T(T)                                                                          \
     template void launch_aos_to_soa<T, double>(const Launch&, const double*, Planes3<T>,       \
@@ -823,7 +844,9 @@ void launch_sgd(const Launch& L, Planes3<T> mu, CPlanes3<T> v, Dims d, double mo
     template void launch_jacobian_full<T>(const Launch&, CPlanes3<T>, Dims, T*);              \
     template void launch_upsample_cubic<T>(const Launch&, CPlanes3<T>, Dims, Planes3<T>, Dims, \
                                            const double*, const double*);                      \
-    template void launch_sgd<T>(const Launch&, Planes3<T>, CPlanes3<T>, Dims, double);
+    template void launch_sgd<T>(const Launch&, Planes3<T>, CPlanes3<T>, Dims, double);      \
+    template void launch_parity_fix<T>(const Launch&, const LoopState*, int, CPlanes3<T>,      \
+                                       Planes3<T>, int64_t, int);
 
 DFM_INST_T(float)
 DFM_INST_T(double)
