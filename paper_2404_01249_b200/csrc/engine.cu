@@ -1824,6 +1824,10 @@ struct Registrar {
     GaussW<T> w_id{};          // identity (sigma 0) weights of the current level
     double* fstat = nullptr;   // per-level muF, vF (2 planes) for the 3-moment forward
     bool fstat_ready = false;  // this level's F statistics are current
+    // the loop kept W = M(x+u) current for the field it ends with (and fstat
+    // for the level's F), on a level of dims w_dims
+    bool w_final = false;
+    Dims w_dims{};
     T* Wb = nullptr;  // W = M(x+u) for the current u (TMA path)
     T* Gb = nullptr;  // grad M(x+u), 3 planes
     bool use_tma = false;    // fused W/G-carrying loop (plane-streaming and/or brick kernels)
@@ -2259,7 +2263,16 @@ struct Registrar {
         T* coef0[4] = {nullptr, nullptr, nullptr, nullptr};
         check_loss_inputs(F, M, g);
         int np = -1;
-        if (cfg->loss == DFM_LOSS_LNCC && cfg->lncc_radius <= 5 && d.ndim == 3 &&
+        if (w_final && dims_equal(w_dims, full) && dims_equal(cd, full) && d.ndim == 3 &&
+            !use_brick && tma_supported(d, sizeof(T))) {
+            // the last level ran at full resolution on the streaming loop: its W is
+            // M(x+u) for the final field and fstat holds F's window statistics, so
+            // the value is one 3-moment forward (same coefficients as the 5-moment
+            // form, loop_ops.cuh)
+            np = launch_lncc_fwd3_tma<T>(L, cfg->lncc_radius, F, Wb, fstat, d, coef[0], partials,
+                                         nullptr, nullptr);
+        }
+        if (np < 0 && cfg->loss == DFM_LOSS_LNCC && cfg->lncc_radius <= 5 && d.ndim == 3 &&
             tma_supported(d, sizeof(T))) {
             // value only through the plane-streaming forward: W = M(x+u), then moments
             launch_warpgrad<T>(L, M, d, u[cur].r(), d, Wb, nullptr);
@@ -2618,6 +2631,9 @@ struct Registrar {
         CK(cudaMemcpyAsync(lg.ht, stamp, sizeof(unsigned long long) * (T_si + 1),
                            cudaMemcpyDeviceToHost, ctx->stream));
         pending.push_back(lg);
+        w_final = use_tma && cfg->mode == DFM_MODE_DIRECT && cfg->loss == DFM_LOSS_LNCC &&
+                  fstat_ready;
+        w_dims = d;
         const int assumed = (start + T_si) % 2;  // no early stop: T_si updates
         launch_parity_fix<T>(ctx->L(), st, T_si, u[1 - assumed].r(), u[assumed].w(), d.n,
                              d.ndim);
