@@ -368,9 +368,14 @@ struct PersistScale {
     int window;
     double tol;
     int iters;
+    const double* fstat;  // neighbour-synchronised solver: the level's F statistics
+    unsigned* sync;       // and its zeroed sync words (persist_nb_sync_words)
 };
 template <class T>
 int launch_persist_scale(const Launch& L, const PersistScale<T>& p);
+template <class T>
+int launch_persist_nb_scale(const Launch& L, const PersistScale<T>& p);
+int persist_nb_sync_words(Dims d, int iters);
 
 // -------- SVF mode (kernels_svf.cu): exp_map and the deterministic
 // svf_pullback (stable-sorted gather in place of the reference's serial

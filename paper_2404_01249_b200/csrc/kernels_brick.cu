@@ -87,9 +87,16 @@ struct CenterOfB<Op, std::void_t<typename Op::Center>> {
 // One brick of one op: stage, x, y, z passes, per-voxel epilogue and the
 // CTA reduction; op.finish(b, ...) records brick b's partial.  Ends with the
 // CTA's threads synchronised (smem reusable).
-template <class Op, int NTB>
-__device__ __forceinline__ void brick_body(const Op& op, const BG& g, int b, unsigned char* smem,
-                                           double* s_red) {
+struct NoPreStage {
+    __device__ bool operator()() const { return true; }
+};
+
+// pre(): called by every thread after the centre loads are issued and before
+// the stage (the persistent solver waits for its neighbours there, so the
+// own-brick centre loads overlap the wait); false -> return false at once
+template <class Op, int NTB, class Pre = NoPreStage>
+__device__ __forceinline__ bool brick_body(const Op& op, const BG& g, int b, unsigned char* smem,
+                                           double* s_red, const Pre& pre = Pre{}) {
     using Lay = BrickLayout<Op>;
     using A = typename Op::Acc;
     using S = typename Op::Raw;
@@ -122,6 +129,7 @@ __device__ __forceinline__ void brick_body(const Op& op, const BG& g, int b, uns
             if (gx < d.nx && gy < d.ny && gz < d.nz) op.load_center(gx, gy, gz, cen[k]);
         }
     }
+    if (!pre()) return false;
     // 1. stage: the loads of a batch of elements are all issued before any is
     // stored (one L2 round trip per batch instead of one per element)
     const bool inner = x0 - R >= 0 && x0 + BX + R <= d.nx && y0 - R >= 0 &&
@@ -225,6 +233,7 @@ __device__ __forceinline__ void brick_body(const Op& op, const BG& g, int b, uns
         if (tid == 0 && bid == 0) op.finish(0, 0.0, 0.0, pr);
         __syncthreads();
     }
+    return true;
 }
 
 template <class Op>
@@ -754,6 +763,320 @@ __global__ void __launch_bounds__(NTP, 3)
     if (blockIdx.x == 0 && threadIdx.x == 0) st->nupdates += nupd;
 }
 
+// ---------------------------------------------------------------------------
+// Neighbour-synchronised persistent solver.  Same phases and per-voxel
+// arithmetic as k_persist, but no grid-wide barrier: a brick's phase p only
+// reads (within its halo) what its 26 neighbour bricks wrote in phase p-1 or
+// earlier, so before phase p each brick waits for its neighbours' phase
+// counters to reach p-1 and publishes its own counter after the phase
+// (release / acquire at gpu scope).  CTAs drift against each other and the
+// fill/drain of a grid barrier (or of a kernel boundary) disappears.
+//
+// Hazards: a brick is at most one phase ahead of any neighbour, and no phase
+// writes a buffer its predecessor phase reads (F: coef / B: grad / A: m, nu,
+// c / C: u', W, G; u ping-pongs), so halo reads always see the intended
+// version.  Halo reach: LNCC r, sigma_grad radius, sigma_warp radius and the
+// compose gather (cap <= 1.5 -> 2 voxels) all stay within one brick
+// (8 x BY x 8, BY >= 4) of the own brick.
+//
+// Loss and monitor (pipeline.cpp:157-179): the last brick to finish the
+// forward of iteration i sums the iteration's partials (fixed order) and
+// commits the record; nobody waits for it unless iteration i could stop the
+// level (slot >= window), in which case every brick waits for the commit
+// before its update.  Adam's step counter and record slot are t0 + i + 1 and
+// it0 + i, exactly the values the monitor would have produced.  A non-finite
+// loss, a non-finite step or convergence raises `abort`, which every wait
+// polls; a wait that outlives kNbTimeoutNs raises err 4 instead of hanging.
+struct NbSync {
+    unsigned* flags;  // [2 nb] per brick: neighbour completions by phase parity (push)
+                      // or the brick's own completed phases (poll)
+    unsigned* fdone;  // [iters] bricks past the forward of iteration i
+    unsigned* mseq;   // iterations whose record is committed
+    unsigned* abort_;
+};
+constexpr unsigned long long kNbTimeoutNs = 4000000000ull;
+
+// polls are relaxed (no L1 invalidation per poll: the other CTAs of the SM
+// keep their cached halo lines); one acq_rel fence after a successful wait
+// and one before a publication make the pattern an acquire / a release
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u32(unsigned* p, unsigned v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() {
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+
+// raise abort (and err 4 on a stall); returns false
+__device__ bool nb_fail(const NbSync& s, LoopState* st, bool stalled) {
+    if (stalled && atomicCAS(&st->err, 0, 4) == 0) st->done = 1;
+    atomicExch(s.abort_, 1u);
+    return false;
+}
+
+#ifndef DFM_NB_PUSH
+#define DFM_NB_PUSH 1
+#endif
+// existing neighbour l (0..26, 13 = self excluded) of brick b, or -1
+__device__ __forceinline__ int nb_neighbour(const BG& g, int nbz, int b, int l) {
+    if (l >= 27 || l == 13) return -1;
+    const int bx = b % g.nbx, t = b / g.nbx, by = t % g.nby, bz = t / g.nby;
+    const int nx = bx + l % 3 - 1, ny = by + (l / 3) % 3 - 1, nz = bz + l / 9 - 1;
+    if (nx < 0 || nx >= g.nbx || ny < 0 || ny >= g.nby || nz < 0 || nz >= nbz) return -1;
+    return (nz * g.nby + ny) * g.nbx + nx;
+}
+
+// spin until *f >= target (or abort / stall); false when the level was aborted
+__device__ bool nb_spin(const NbSync& s, LoopState* st, const unsigned* f, unsigned target) {
+    if (ld_relaxed_u32(f) >= target) return true;
+    const unsigned long long t0 = dfm_global_ns();
+    while (ld_relaxed_u32(f) < target) {
+        if (ld_relaxed_u32(s.abort_)) return false;
+        if (dfm_global_ns() - t0 > kNbTimeoutNs) return nb_fail(s, st, true);
+    }
+    return true;
+}
+
+// wait until every existing neighbour of brick b has completed phase `target`.
+// Push form (DFM_NB_PUSH): neighbours add to b's counter of their completed
+// phases of b's parity class; a neighbour is at most one phase ahead of b, so
+// counter[target & 1] == nneigh * ((target + 1) / 2) exactly when all of them
+// completed `target` (one thread polls one word).  Poll form: warp 0 polls
+// the 26 neighbours' own phase counters.
+__device__ bool nb_wait(const NbSync& s, LoopState* st, const BG& g, int nbz, int b,
+                        unsigned target, int* s_flag) {
+    if (threadIdx.x < 32) {
+        const int l = threadIdx.x;
+        bool ok = true;
+        if (target > 0) {
+#if DFM_NB_PUSH
+            const unsigned nn = __popc(__ballot_sync(0xffffffffu, nb_neighbour(g, nbz, b, l) >= 0));
+            if (l == 0)
+                ok = nb_spin(s, st, s.flags + 2 * b + (target & 1u), nn * ((target + 1u) / 2u));
+#else
+            const int n = nb_neighbour(g, nbz, b, l);
+            if (n >= 0) ok = nb_spin(s, st, s.flags + n, target);
+#endif
+        }
+        ok = __all_sync(0xffffffffu, ok);
+        if (l == 0) {
+            fence_acq_rel_gpu();  // acquire: the neighbours' phase outputs
+            *s_flag = ok;
+        }
+    }
+    __syncthreads();
+    return *s_flag != 0;
+}
+
+// publish: brick b completed phase p (the CTA's threads are synchronised)
+__device__ __forceinline__ void nb_publish(const NbSync& s, const BG& g, int nbz, int b,
+                                           unsigned p) {
+#if DFM_NB_PUSH
+    if (threadIdx.x < 32) {
+        if (threadIdx.x == 0) fence_acq_rel_gpu();  // release: the CTA's phase outputs
+        __syncwarp();
+        const int n = nb_neighbour(g, nbz, b, threadIdx.x);
+        if (n >= 0)
+            asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(s.flags + 2 * n + (p & 1u))
+                         : "memory");
+    }
+#else
+    if (threadIdx.x == 0) {
+        fence_acq_rel_gpu();  // release: the CTA's phase outputs (ordered by the barrier)
+        st_relaxed_u32(s.flags + b, p);
+    }
+#endif
+}
+
+template <class T, int R, int CAPH>
+struct SmoothAdamNB : SmoothAdamB<T, R, CAPH> {
+    using Base = SmoothAdamB<T, R, CAPH>;
+    long long t;  // Adam step counter of this iteration (st->t after the commit)
+    int slot;     // record slot of this iteration
+    __device__ typename Base::Prol prologue() const {
+        typename Base::Prol p;
+        p.ic1 = static_cast<T>(1.0 / this->corr1[t]);
+        p.ic2 = static_cast<T>(1.0 / this->corr2[t]);
+        p.slot = slot;
+        return p;
+    }
+};
+
+template <class T, int R, int RG, int RW, int CAPH>
+struct PersistNbArgs {
+    LnccFwdB<T, R, true> fwd;  // partials: [iters][nb]
+    LnccBwdB<T, R> bwd;
+    SmoothAdamNB<T, RG, CAPH> sa;
+    ComposeSB<T, RW> co;
+    NbSync sync;
+    int iters;
+    LoopState* st;
+    double* loss;
+    unsigned long long* stamp;
+    int window;
+    double tol;
+};
+
+#ifndef DFM_NB_MINB
+#define DFM_NB_MINB 3
+#endif
+template <class T, int R, int RG, int RW, int CAPH>
+__global__ void __launch_bounds__(NTP, DFM_NB_MINB)
+    k_persist_nb(const __grid_constant__ PersistNbArgs<T, R, RG, RW, CAPH> a, const BG g,
+                 int nb) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ double s_red[32];
+    __shared__ int s_flag, s_done0, s_stop, s_bad;
+    __shared__ long long s_t0;
+    __shared__ int s_it0;
+    LoopState* st = a.st;
+    const NbSync& sy = a.sync;
+    if (threadIdx.x == 0) {  // read before this CTA's first publication (see header)
+        s_t0 = st->t;
+        s_it0 = st->it;
+        s_done0 = st->done;
+    }
+    __syncthreads();
+    if (s_done0) return;  // an earlier level failed
+    const long long t0 = s_t0;
+    const int it0 = s_it0;
+    const int nbz = (g.d.nz + BZ - 1) / BZ;
+    const int nbc = gridDim.x - 1;  // brick CTAs; the last CTA is the monitor
+    if (blockIdx.x == nbc) {
+        // monitor (pipeline.cpp:157-179): per iteration, once every brick's
+        // forward partial is in, the fixed-order sum and the record commit
+        const double nvox = static_cast<double>(g.d.nx) * g.d.ny * g.d.nz;
+        for (int it = 0; it < a.iters; ++it) {
+            if (threadIdx.x == 0) {
+                s_flag = nb_spin(sy, st, sy.fdone + it, static_cast<unsigned>(nb));
+                fence_acq_rel_gpu();
+            }
+            __syncthreads();
+            if (!s_flag) return;
+            const double* part = a.fwd.partials + static_cast<size_t>(it) * nb;
+            double acc = 0.0;
+            for (int k = threadIdx.x; k < nb; k += NTP) acc += __ldcg(part + k);
+            const double v = -bsum<NTP>(acc, s_red) / nvox;
+            if (threadIdx.x == 0) {
+                monitor_commit(st, v, 0.0, 0.0, a.loss, a.stamp, a.window, a.tol);
+                s_stop = st->done;
+                if (st->err) atomicExch(sy.abort_, 1u);  // non-finite loss
+                fence_acq_rel_gpu();
+                st_relaxed_u32(sy.mseq, static_cast<unsigned>(it + 1));
+            }
+            __syncthreads();
+            if (s_stop) return;  // converged (every brick stops before this update)
+        }
+        return;
+    }
+    int nupd = 0;
+    for (int it = 0; it < a.iters; ++it) {
+        const unsigned p0 = 4u * static_cast<unsigned>(it);
+        // F: loss forward; the partials go to the monitor CTA
+        {
+            auto fwd = a.fwd;
+            fwd.partials = a.fwd.partials + static_cast<size_t>(it) * nb;
+            for (int b = blockIdx.x; b < nb; b += nbc) {
+                auto pre = [&] { return nb_wait(sy, st, g, nbz, b, p0, &s_flag); };
+                if (!brick_body<decltype(fwd), NTP>(fwd, g, b, smem, s_red, pre)) return;
+                nb_publish(sy, g, nbz, b, p0 + 1);
+                if (threadIdx.x == 0)  // the partial is released by nb_publish's fence
+                    asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(sy.fdone + it)
+                                 : "memory");
+            }
+        }
+        // B: LNCC backward
+        for (int b = blockIdx.x; b < nb; b += nbc) {
+            auto pre = [&] { return nb_wait(sy, st, g, nbz, b, p0 + 1, &s_flag); };
+            if (!brick_body<decltype(a.bwd), NTP>(a.bwd, g, b, smem, s_red, pre)) return;
+            nb_publish(sy, g, nbz, b, p0 + 2);
+        }
+        // the level may stop at this iteration: wait for its record (every
+        // brick gets here: B(it) needs only F(it), which the commit follows)
+        if (it0 + it >= a.window) {
+            if (threadIdx.x == 0) {
+                const bool ok = nb_spin(sy, st, sy.mseq, static_cast<unsigned>(it + 1));
+                fence_acq_rel_gpu();
+                s_stop = !ok || *reinterpret_cast<volatile int*>(&st->done);
+            }
+            __syncthreads();
+            if (s_stop) break;
+        }
+        // A: smooth + Adam + pointwise compose into c
+        SmoothAdamNB<T, RG, CAPH> sa = a.sa;
+        ComposeSB<T, RW> co = a.co;
+        if (it & 1) {  // ping-pong of the field
+            sa.uin = a.co.uout;
+            co.uout = const_cast<T*>(a.sa.uin);
+        }
+        sa.t = t0 + it + 1;
+        sa.slot = it0 + it;
+        for (int b = blockIdx.x; b < nb; b += nbc) {
+            auto pre = [&] { return nb_wait(sy, st, g, nbz, b, p0 + 2, &s_flag); };
+            if (!brick_body<decltype(sa), NTP>(sa, g, b, smem, s_red, pre)) return;
+            nb_publish(sy, g, nbz, b, p0 + 3);
+        }
+        // C: sigma_warp smoothing of c, W/G; a non-finite step stops first
+        for (int b = blockIdx.x; b < nb; b += nbc) {
+            if (!nb_wait(sy, st, g, nbz, b, p0 + 3, &s_flag)) return;
+            if (threadIdx.x == 0) s_bad = *reinterpret_cast<volatile int*>(&st->bad_step);
+            __syncthreads();
+            if (s_bad) {  // diffeo.cpp:52-53
+                if (threadIdx.x == 0) {
+                    st->err = 2;
+                    st->done = 1;
+                    atomicExch(sy.abort_, 1u);
+                }
+                return;
+            }
+            brick_body<decltype(co), NTP>(co, g, b, smem, s_red);
+            nb_publish(sy, g, nbz, b, p0 + 4);
+        }
+        ++nupd;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&st->nupdates, nupd);
+}
+
+template <class T, int R, int RG, int RW, int CAPH>
+int run_persist_nb(const Launch& L, const PersistNbArgs<T, R, RG, RW, CAPH>& a, const Dims& d) {
+    using A = PersistNbArgs<T, R, RG, RW, CAPH>;
+    constexpr size_t b1 = BrickLayout<decltype(A::fwd)>::bytes;
+    constexpr size_t b2 = BrickLayout<decltype(A::bwd)>::bytes;
+    constexpr size_t b3 = BrickLayout<decltype(A::sa)>::bytes;
+    constexpr size_t b4 = BrickLayout<decltype(A::co)>::bytes;
+    constexpr size_t m12 = b1 > b2 ? b1 : b2, m34 = b3 > b4 ? b3 : b4;
+    constexpr size_t bytes = m12 > m34 ? m12 : m34;
+    if constexpr (bytes > kBrickSmemMax) {
+        return -2;
+    } else {
+        const void* fn = reinterpret_cast<const void*>(k_persist_nb<T, R, RG, RW, CAPH>);
+        const int per_sm = kernel_setup(fn, NTP, bytes);
+        if (per_sm < 1) return -3;
+        BG g;
+        g.d = d;
+        g.nbx = (d.nx + BX - 1) / BX;
+        g.nby = (d.ny + BY - 1) / BY;
+        int nb = g.nbx * g.nby * ((d.nz + BZ - 1) / BZ);
+        const int cap = per_sm * (L.num_sms > 0 ? L.num_sms : 148);
+        if (cap < 2) return -3;
+        const int grid = (nb < cap - 1 ? nb : cap - 1) + 1;  // + the monitor CTA
+        void* args[] = {const_cast<A*>(&a), &g, &nb};
+        // co-residency of every CTA is what makes the spin waits safe
+        const cudaError_t e =
+            cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(NTP), args, bytes, L.stream);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return -4;
+        }
+        L.bump();
+        return grid;
+    }
+}
+
 template <class T, int R, int RG, int RW>
 int run_persist(const Launch& L, const PersistArgs<T, R, RG, RW>& a, const Dims& d) {
     using A = PersistArgs<T, R, RG, RW>;
@@ -986,6 +1309,88 @@ int launch_persist_scale(const Launch& L, const PersistScale<T>& p) {
     return -2;
 }
 
+// words of the neighbour-synchronised solver's sync workspace for a level:
+// per-brick phase counters, per-iteration forward arrivals, commit sequence, abort
+int persist_nb_sync_words(Dims d, int iters) {
+    const int nb = ((d.nx + BX - 1) / BX) * ((d.ny + BY - 1) / BY) * ((d.nz + BZ - 1) / BZ);
+    return 2 * nb + iters + 2;
+}
+
+// the neighbour-synchronised solver: LNCC r 1..3 with the level's F
+// statistics, sigma_grad radius 3 (sigma 1.0), sigma_warp radius 2 (0.5),
+// step cap <= 1.5 (compose gather within 2 voxels)
+template <class T>
+int launch_persist_nb_scale(const Launch& L, const PersistScale<T>& p) {
+    if (!p.fstat || !p.sync || p.rg != 3 || p.rw != 2 || !(p.ap.cap <= 1.5)) return -2;
+    const int nbx = (p.d.nx + BX - 1) / BX, nby = (p.d.ny + BY - 1) / BY;
+    const int nb = nbx * nby * ((p.d.nz + BZ - 1) / BZ);
+    auto go = [&](auto rr, auto cc) -> int {
+        constexpr int R = decltype(rr)::value, CAPH = decltype(cc)::value;
+        PersistNbArgs<T, R, 3, 2, CAPH> a;
+        a.fwd.F = p.F;
+        a.fwd.W = p.W;
+        a.fwd.fstat = p.fstat;
+        a.fwd.coef = p.coef;
+        a.fwd.partials = p.partials;
+        a.fwd.st = p.st;
+        a.fwd.mon = MonitorArgs{nullptr, nullptr, nullptr, 0, 0.0};
+        a.fwd.d = p.d;
+        a.bwd.coef = p.coef;
+        a.bwd.F = p.F;
+        a.bwd.W = p.W;
+        a.bwd.G = p.G;
+        a.bwd.grad = p.grad;
+        a.bwd.m2n = -2.0 / static_cast<double>(p.d.n);
+        a.bwd.st = p.st;
+        a.bwd.d = p.d;
+        a.sa.grad = p.grad;
+        a.sa.w = p.wg;
+        a.sa.m = p.m;
+        a.sa.nu = p.nu;
+        a.sa.step = p.step;  // receives c
+        a.sa.uin = p.u0;
+        a.sa.ak = adam_k<T>(p.ap);
+        a.sa.corr1 = p.ap.corr1;
+        a.sa.corr2 = p.ap.corr2;
+        a.sa.st = p.st;
+        a.sa.maxstep = p.maxstep;
+        a.sa.d = p.d;
+        a.sa.t = 0;
+        a.sa.slot = 0;
+        a.co.c = p.step;
+        a.co.w = p.ww;
+        a.co.uout = p.u1;
+        a.co.M = p.M;
+        a.co.dm = p.d;
+        a.co.W = p.W;
+        a.co.G = p.G;
+        a.co.st = p.st;
+        a.co.count_update = 0;
+        a.co.d = p.d;
+        a.sync.flags = p.sync;
+        a.sync.fdone = p.sync + 2 * nb;
+        a.sync.mseq = p.sync + 2 * nb + p.iters;
+        a.sync.abort_ = p.sync + 2 * nb + p.iters + 1;
+        a.iters = p.iters;
+        a.st = p.st;
+        a.loss = p.loss;
+        a.stamp = p.stamp;
+        a.window = p.window;
+        a.tol = p.tol;
+        return run_persist_nb(L, a, p.d);
+    };
+    auto by_cap = [&](auto rr) -> int {
+        if (p.ap.cap <= 0.5) return go(rr, std::integral_constant<int, 1>{});
+        return go(rr, std::integral_constant<int, 2>{});
+    };
+    switch (p.lncc_r) {
+        case 1: return by_cap(std::integral_constant<int, 1>{});
+        case 2: return by_cap(std::integral_constant<int, 2>{});
+        case 3: return by_cap(std::integral_constant<int, 3>{});
+    }
+    return -2;
+}
+
 template <class T>
 int launch_smooth_adam_compose_brick(const Launch& L, int R, const GaussW<T>& w, const T* grad,
                                      T* m, T* nu, const T* uin, T* cout, double cap, Dims d,
@@ -1047,6 +1452,7 @@ int launch_compose_smooth_brick(const Launch& L, int R, const GaussW<T>& w, cons
                                          const T*, T*, const T*, Dims, Dims, T*, T*,           \
                                          LoopState*, bool);                                    \
     template int launch_persist_scale<T>(const Launch&, const PersistScale<T>&);              \
+    template int launch_persist_nb_scale<T>(const Launch&, const PersistScale<T>&);           \
     template int launch_smooth_adam_compose_brick<T>(const Launch&, int, const GaussW<T>&,      \
                                                      const T*, T*, T*, const T*, T*, double,   \
                                                      Dims, AdamParams, LoopState*,             \

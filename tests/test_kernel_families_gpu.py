@@ -17,7 +17,8 @@ from paper_2404_01249_b200.engine import (Context, OPT_BRICK_MAX, OPT_NARROW, OP
 
 pytestmark = pytest.mark.gpu
 
-FAMILIES = {"persist": (1 << 40, 1), "brick": (1 << 40, 0), "stream": (0, 0)}
+FAMILIES = {"persist": (1 << 40, 1), "persist_nb": (1 << 40, 2), "brick": (1 << 40, 0),
+            "stream": (0, 0)}
 
 
 def _ctx(prec, family):

@@ -1,7 +1,9 @@
 """Per-iteration device time of one pyramid level in the production (graph)
 path, for a list of volume sizes:  python tools/level_iter_time.py NXxNYxNZ ...
 (one registration at scale 1 with 64 iterations per size, early stop off;
-median IterationRecord.wall_ms, i.e. graph-chunk device time / iterations)."""
+median IterationRecord.wall_ms, i.e. graph-chunk device time / iterations).
+LIT_PERSIST=0/1/2 and LIT_BRICK_MAX select the brick solver (persistent
+levels stamp each iteration's record on the device)."""
 import os
 import sys
 
@@ -9,7 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 
 from paper_2404_01249_b200 import _abi as A, synth  # noqa: E402
-from paper_2404_01249_b200.engine import Context  # noqa: E402
+from paper_2404_01249_b200.engine import Context, OPT_BRICK_MAX, OPT_PERSIST  # noqa: E402
 
 iters = int(os.environ.get("LIT_ITERS", "64"))
 for spec in sys.argv[1:]:
@@ -20,6 +22,10 @@ for spec in sys.argv[1:]:
     best = None
     for rep in range(2):
         ctx = Context(0, "f32")
+        if "LIT_PERSIST" in os.environ:
+            ctx.set_option(OPT_PERSIST, int(os.environ["LIT_PERSIST"]))
+        if "LIT_BRICK_MAX" in os.environ:
+            ctx.set_option(OPT_BRICK_MAX, int(os.environ["LIT_BRICK_MAX"]))
         try:
             _, log = ctx.register_images(p.grid, p.fixed, p.moving, cfg,
                                          A.PyramidSchedule((1.0,), (iters,)))
