@@ -370,6 +370,7 @@ struct PersistScale {
     int iters;
     const double* fstat;  // neighbour-synchronised solver: the level's F statistics
     unsigned* sync;       // and its zeroed sync words (persist_nb_sync_words)
+    bool nb_any_size;     // also levels with more bricks than CTA slots
 };
 template <class T>
 int launch_persist_scale(const Launch& L, const PersistScale<T>& p);

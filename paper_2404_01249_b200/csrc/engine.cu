@@ -128,7 +128,8 @@ struct dfm_ctx {
     // pyramid levels up to this many voxels run the brick kernels
     int64_t brick_max = getenv("DFM_BRICK_MAX") ? atoll(getenv("DFM_BRICK_MAX")) : 200000;
     // brick levels of an LNCC registration run as one persistent launch per level
-    // (1: grid barriers between phases, 2: neighbour-synchronised bricks,
+    // (1: grid barriers between phases, 2: neighbour-synchronised bricks where
+    // every brick gets its own CTA, 3: also with several bricks per CTA;
     // measured 35.0 -> 34.0 us per 40x48x56 iteration, config-1 pair -0.4 ms)
     int persist = getenv("DFM_PERSIST") ? atoi(getenv("DFM_PERSIST")) : 2;
     double kt_ms[DFM_NUM_KCLASS] = {};
@@ -742,7 +743,7 @@ dfm_status dfm_ctx_set_option(dfm_ctx* ctx, int key, int64_t value) {
         } else if (key == DFM_OPT_FORCE_LEGACY) {
             ctx->force_legacy = value != 0;
         } else if (key == DFM_OPT_PERSIST) {
-            if (value < 0 || value > 2) fail(DFM_E_INVALID, "persist must be 0, 1 or 2");
+            if (value < 0 || value > 3) fail(DFM_E_INVALID, "persist must be 0..3");
             ctx->persist = static_cast<int>(value);
         } else if (key == DFM_OPT_PDL) {
             ctx->pdl = value != 0;
@@ -2514,7 +2515,8 @@ struct Registrar {
             ps.window = cfg->conv_window;
             ps.tol = cfg->conv_tol;
             ps.iters = T_si;
-            if (ctx->persist == 2 && fstat_ready) {
+            if (ctx->persist >= 2 && fstat_ready) {
+                ps.nb_any_size = ctx->persist == 3;
                 const int words = persist_nb_sync_words(d, T_si);
                 unsigned* sync = ctx->arr<unsigned>("nb_sync", words);
                 CK(cudaMemsetAsync(sync, 0, sizeof(unsigned) * words, ctx->stream));

@@ -27,6 +27,7 @@
 //   SmoothAdamB grad          -> m, nu, capped step, max |step|
 //   ComposeB    step, u       -> u' = smooth(step + u(x+step)), W, G
 #include <cstdint>
+#include <cstdio>
 #include <mutex>
 #include <type_traits>
 
@@ -709,7 +710,7 @@ struct PersistArgs {
     double tol;
 };
 
-constexpr int NTP = 256;  // persistent solver: 3 CTAs of 256 threads per SM (one brick each)
+constexpr int NTP = NTB;  // persistent solvers: 3 CTAs of 256 threads per SM (one brick each)
 
 template <class T, int R, int RG, int RW>
 __global__ void __launch_bounds__(NTP, 3)
@@ -821,6 +822,16 @@ __device__ bool nb_fail(const NbSync& s, LoopState* st, bool stalled) {
 #ifndef DFM_NB_PUSH
 #define DFM_NB_PUSH 1
 #endif
+// DFM_NB_TRACE=i (debug builds): every brick CTA printfs, for iteration i,
+// per phase the clock64 cycles spent waiting and in the body, and the
+// globaltimer at its publication
+#ifndef DFM_NB_TRACE
+#define DFM_NB_TRACE -1
+#endif
+#if DFM_NB_TRACE >= 0
+__device__ long long g_nb_tr_enter[1024][4], g_nb_tr_ready[1024][4], g_nb_tr_done[1024][4];
+__device__ unsigned long long g_nb_tr_pub[1024][4];
+#endif
 // existing neighbour l (0..26, 13 = self excluded) of brick b, or -1
 __device__ __forceinline__ int nb_neighbour(const BG& g, int nbz, int b, int l) {
     if (l >= 27 || l == 13) return -1;
@@ -849,6 +860,10 @@ __device__ bool nb_spin(const NbSync& s, LoopState* st, const unsigned* f, unsig
 // the 26 neighbours' own phase counters.
 __device__ bool nb_wait(const NbSync& s, LoopState* st, const BG& g, int nbz, int b,
                         unsigned target, int* s_flag) {
+#if DFM_NB_TRACE >= 0
+    if (threadIdx.x == 0 && target / 4 == DFM_NB_TRACE && blockIdx.x < 1024)
+        g_nb_tr_enter[blockIdx.x][target % 4] = clock64();
+#endif
     if (threadIdx.x < 32) {
         const int l = threadIdx.x;
         bool ok = true;
@@ -869,12 +884,22 @@ __device__ bool nb_wait(const NbSync& s, LoopState* st, const BG& g, int nbz, in
         }
     }
     __syncthreads();
+#if DFM_NB_TRACE >= 0
+    if (threadIdx.x == 0 && target / 4 == DFM_NB_TRACE && blockIdx.x < 1024)
+        g_nb_tr_ready[blockIdx.x][target % 4] = clock64();
+#endif
     return *s_flag != 0;
 }
 
 // publish: brick b completed phase p (the CTA's threads are synchronised)
 __device__ __forceinline__ void nb_publish(const NbSync& s, const BG& g, int nbz, int b,
                                            unsigned p) {
+#if DFM_NB_TRACE >= 0
+    if (threadIdx.x == 0 && (p - 1) / 4 == DFM_NB_TRACE && blockIdx.x < 1024) {
+        g_nb_tr_done[blockIdx.x][(p - 1) % 4] = clock64();
+        g_nb_tr_pub[blockIdx.x][(p - 1) % 4] = dfm_global_ns();
+    }
+#endif
 #if DFM_NB_PUSH
     if (threadIdx.x < 32) {
         if (threadIdx.x == 0) fence_acq_rel_gpu();  // release: the CTA's phase outputs
@@ -1037,12 +1062,27 @@ __global__ void __launch_bounds__(NTP, DFM_NB_MINB)
             nb_publish(sy, g, nbz, b, p0 + 4);
         }
         ++nupd;
+#if DFM_NB_TRACE >= 0
+        if (it == DFM_NB_TRACE && threadIdx.x == 0 && blockIdx.x < 1024) {
+            const int c = blockIdx.x;
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            printf("NBTR %d %d %lld %lld %lld %lld %lld %lld %lld %lld %llu %llu %llu %llu\n", c,
+                   (int)smid,
+                   g_nb_tr_ready[c][0] - g_nb_tr_enter[c][0], g_nb_tr_done[c][0] - g_nb_tr_ready[c][0],
+                   g_nb_tr_ready[c][1] - g_nb_tr_enter[c][1], g_nb_tr_done[c][1] - g_nb_tr_ready[c][1],
+                   g_nb_tr_ready[c][2] - g_nb_tr_enter[c][2], g_nb_tr_done[c][2] - g_nb_tr_ready[c][2],
+                   g_nb_tr_ready[c][3] - g_nb_tr_enter[c][3], g_nb_tr_done[c][3] - g_nb_tr_ready[c][3],
+                   g_nb_tr_pub[c][0], g_nb_tr_pub[c][1], g_nb_tr_pub[c][2], g_nb_tr_pub[c][3]);
+        }
+#endif
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&st->nupdates, nupd);
 }
 
 template <class T, int R, int RG, int RW, int CAPH>
-int run_persist_nb(const Launch& L, const PersistNbArgs<T, R, RG, RW, CAPH>& a, const Dims& d) {
+int run_persist_nb(const Launch& L, const PersistNbArgs<T, R, RG, RW, CAPH>& a, const Dims& d,
+                   bool any_size) {
     using A = PersistNbArgs<T, R, RG, RW, CAPH>;
     constexpr size_t b1 = BrickLayout<decltype(A::fwd)>::bytes;
     constexpr size_t b2 = BrickLayout<decltype(A::bwd)>::bytes;
@@ -1063,6 +1103,10 @@ int run_persist_nb(const Launch& L, const PersistNbArgs<T, R, RG, RW, CAPH>& a, 
         int nb = g.nbx * g.nby * ((d.nz + BZ - 1) / BZ);
         const int cap = per_sm * (L.num_sms > 0 ? L.num_sms : 148);
         if (cap < 2) return -3;
+        // several bricks per CTA serialise their phase latencies (48x48x52:
+        // 64 us per iteration vs 35 on the graph path): by default only levels
+        // whose bricks each get a CTA run here
+        if (nb > cap - 1 && !any_size) return -2;
         const int grid = (nb < cap - 1 ? nb : cap - 1) + 1;  // + the monitor CTA
         void* args[] = {const_cast<A*>(&a), &g, &nb};
         // co-residency of every CTA is what makes the spin waits safe
@@ -1377,7 +1421,7 @@ int launch_persist_nb_scale(const Launch& L, const PersistScale<T>& p) {
         a.stamp = p.stamp;
         a.window = p.window;
         a.tol = p.tol;
-        return run_persist_nb(L, a, p.d);
+        return run_persist_nb(L, a, p.d, p.nb_any_size);
     };
     auto by_cap = [&](auto rr) -> int {
         if (p.ap.cap <= 0.5) return go(rr, std::integral_constant<int, 1>{});
