@@ -506,11 +506,11 @@ DFM_API dfm_status dfm_ctx_kernel_times(const dfm_ctx* ctx, double* ms, int64_t*
 #define DFM_OPT_FORCE_LEGACY 2
 /* DFM_OPT_PERSIST: brick levels of an LNCC registration run as one
  * persistent cooperative launch per level: 2 = bricks synchronised with
- * their 26 neighbours only (default; levels whose bricks each get a CTA,
- * LNCC r 1..3, sigma_grad 1.0, sigma_warp 0.5, step cap <= 1.5 — others run
- * the graph path); 3 = as 2 for levels of any size (several bricks per
- * CTA); 1 = grid barriers between phases; 0 = one CUDA graph per 8
- * iterations.
+ * their 26 neighbours only (default; levels with at least two bricks per
+ * SM whose bricks each get a CTA, LNCC r 1..3, sigma_grad 1.0, sigma_warp
+ * 0.5, step cap <= 1.5 — others run the graph path); 3 = as 2 for brick
+ * levels of any size; 1 = grid barriers between phases; 0 = one CUDA graph
+ * per 8 iterations.
  * Env DFM_PERSIST. */
 #define DFM_OPT_PERSIST 3
 /* DFM_OPT_PDL: 1 = the loop kernels use programmatic dependent

@@ -1107,6 +1107,11 @@ int run_persist_nb(const Launch& L, const PersistNbArgs<T, R, RG, RW, CAPH>& a, 
         // 64 us per iteration vs 35 on the graph path): by default only levels
         // whose bricks each get a CTA run here
         if (nb > cap - 1 && !any_size) return -2;
+        // and few bricks: a kernel boundary inside the graph (0.6-0.9 us) is
+        // cheaper than a neighbour wait + release (16^3: 21.2 vs 26.0, 32^3:
+        // 24.4 vs 27.6 us per iteration; 40x48x56, 420 bricks: 36.3 vs 34.2)
+        const int sms = L.num_sms > 0 ? L.num_sms : 148;
+        if (nb < 2 * sms && !any_size) return -2;
         const int grid = (nb < cap - 1 ? nb : cap - 1) + 1;  // + the monitor CTA
         void* args[] = {const_cast<A*>(&a), &g, &nb};
         // co-residency of every CTA is what makes the spin waits safe

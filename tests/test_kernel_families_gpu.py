@@ -17,7 +17,7 @@ from paper_2404_01249_b200.engine import (Context, OPT_BRICK_MAX, OPT_NARROW, OP
 
 pytestmark = pytest.mark.gpu
 
-FAMILIES = {"persist": (1 << 40, 1), "persist_nb": (1 << 40, 2), "brick": (1 << 40, 0),
+FAMILIES = {"persist": (1 << 40, 1), "persist_nb": (1 << 40, 3), "brick": (1 << 40, 0),
             "stream": (0, 0)}
 
 

@@ -1,6 +1,8 @@
-"""The neighbour-synchronised persistent level solver (DFM_OPT_PERSIST = 2,
-kernels_brick.cu k_persist_nb): every brick level of an LNCC registration in
-one cooperative launch, bricks synchronised with their 26 neighbours only.
+"""The neighbour-synchronised persistent level solver (kernels_brick.cu
+k_persist_nb): every brick level of an LNCC registration in one cooperative
+launch, bricks synchronised with their 26 neighbours only.  DFM_OPT_PERSIST = 3
+forces it on every brick level (by default, 2, it runs where it is faster:
+at least two bricks per SM and at most one per CTA slot).
 
 It runs the brick kernels' per-voxel arithmetic in the same order, so it must
 reproduce the per-iteration CUDA-graph brick path (DFM_OPT_PERSIST = 0) bit for
@@ -47,7 +49,7 @@ def test_matches_graph_path_bitwise(prec):
     cfg = G.register_config("lncc", z, sched)
     dt = np.float64 if prec == "f64" else np.float32
     F, M = z["fixed"].astype(dt), z["moving"].astype(dt)
-    nb = _run(prec, 2, g, F, M, cfg, sched)
+    nb = _run(prec, 3, g, F, M, cfg, sched)
     _same(nb, _run(prec, 0, g, F, M, cfg, sched))
     if prec == "f64":  # and the reference golden (north_star criteria)
         losses = np.array([r.loss for r in nb[1].iterations])
@@ -71,7 +73,7 @@ def test_ragged_shapes_radii_caps(shape, r, cap):
     cfg.step_cap = cap
     for prec in ("f64", "f32"):
         dt = np.float64 if prec == "f64" else np.float32
-        _same(_run(prec, 2, g, fixed.astype(dt), moving.astype(dt), cfg, sched),
+        _same(_run(prec, 3, g, fixed.astype(dt), moving.astype(dt), cfg, sched),
               _run(prec, 0, g, fixed.astype(dt), moving.astype(dt), cfg, sched))
 
 
@@ -81,7 +83,7 @@ def test_early_stop_identical(window, tol):
     z, g, sched = G.register_inputs("lncc")
     cfg = G.register_config("lncc", z, sched)
     cfg.conv_window, cfg.conv_tol = window, tol
-    a = _run("f64", 2, g, z["fixed"], z["moving"], cfg, sched)
+    a = _run("f64", 3, g, z["fixed"], z["moving"], cfg, sched)
     b = _run("f64", 0, g, z["fixed"], z["moving"], cfg, sched)
     _same(a, b)
     assert len(a[1].iterations) < sum(sched.iterations)
@@ -92,7 +94,7 @@ def test_self_registration_stops():
     g = A.GridMeta.make_3d(16, 16, 16)
     cfg = A.RegistrationConfig()
     sched = A.PyramidSchedule()
-    _same(_run("f64", 2, g, z["fixed"], z["fixed"], cfg, sched),
+    _same(_run("f64", 3, g, z["fixed"], z["fixed"], cfg, sched),
           _run("f64", 0, g, z["fixed"], z["fixed"], cfg, sched))
 
 
@@ -104,7 +106,7 @@ def test_nonfinite_input_raises(prec):
     F[3, 2, 1] = np.nan
     sched = A.PyramidSchedule((1.0,), (5,))
     msgs = []
-    for persist in (2, 0):
+    for persist in (3, 0):
         with pytest.raises(A.NumericalError) as e:
             _run(prec, persist, g, F, M, A.RegistrationConfig(), sched)
         msgs.append(str(e.value))
@@ -120,3 +122,5 @@ def test_config1_coarse_levels():
     a = _run("f32", 3, p.grid, p.fixed, p.moving, p.config, sched)
     b = _run("f32", 0, p.grid, p.fixed, p.moving, p.config, sched)
     _same(a, b)
+    # the default (2) runs the 1/4 level (420 bricks) persistent, 1/2 on graphs
+    _same(_run("f32", 2, p.grid, p.fixed, p.moving, p.config, sched), b)
