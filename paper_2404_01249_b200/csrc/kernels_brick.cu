@@ -56,13 +56,25 @@ struct BG {
     int nbx, nby;
 };
 
+#ifndef DFM_BRICK_XQUAD
+#define DFM_BRICK_XQUAD 1
+#endif
+
 template <class Op>
 struct BrickLayout {
     using A = typename Op::Acc;
     using S = typename Op::Raw;
     static constexpr int R = Op::R, C = Op::C, NR = Op::NR;
     static constexpr int HX = BX + 2 * R, HY = BY + 2 * R, HZ = BZ + 2 * R;
-    static constexpr int nS = HX * HY * HZ;  // per staged channel
+    // quad x pass (DFM_BRICK_XQUAD): a thread filters 4 consecutive columns
+    // from one register window of 4 + 2R staged values per channel, read with
+    // 128-bit loads; staged rows are padded to HXP for the alignment
+    static constexpr int VEC = 16 / int(sizeof(S));  // staged values per 128-bit load
+    static constexpr int W4 = 4 + 2 * R;
+    static constexpr int NV4 = (W4 + VEC - 1) / VEC;  // vector loads per window
+    static constexpr int HXQ = (BX - 4) + NV4 * VEC > HX ? (BX - 4) + NV4 * VEC : HX;
+    static constexpr int HXP = DFM_BRICK_XQUAD ? (HXQ + VEC - 1) / VEC * VEC : HX;
+    static constexpr int nS = HXP * HY * HZ;  // per staged channel (padded rows)
     static constexpr int nX = HZ * HY * BX;  // per channel, x-pass output
     static constexpr int nY = HZ * BY * BX;  // per channel, y-pass output
     static constexpr size_t bX = (static_cast<size_t>(C) * nX * sizeof(A) + 15) / 16 * 16;
@@ -88,6 +100,22 @@ struct CenterOfB<Op, std::void_t<typename Op::Center>> {
 // One brick of one op: stage, x, y, z passes, per-voxel epilogue and the
 // CTA reduction; op.finish(b, ...) records brick b's partial.  Ends with the
 // CTA's threads synchronised (smem reusable).
+#ifndef DFM_NB_TRACE
+#define DFM_NB_TRACE -1
+#endif
+#if DFM_NB_TRACE >= 0
+__device__ long long g_nb_bt[1024][4][6];  // brick_body stage clocks (trace builds)
+#define DFM_BT(k)                                                               \
+    do {                                                                        \
+        if (trace >= 0 && threadIdx.x == 0 && blockIdx.x < 1024)                \
+            g_nb_bt[blockIdx.x][trace][k] = clock64();                          \
+    } while (0)
+#else
+#define DFM_BT(k) \
+    do {          \
+    } while (0)
+#endif
+
 struct NoPreStage {
     __device__ bool operator()() const { return true; }
 };
@@ -97,13 +125,16 @@ struct NoPreStage {
 // own-brick centre loads overlap the wait); false -> return false at once
 template <class Op, int NTB, class Pre = NoPreStage>
 __device__ __forceinline__ bool brick_body(const Op& op, const BG& g, int b, unsigned char* smem,
-                                           double* s_red, const Pre& pre = Pre{}) {
+                                           double* s_red, const Pre& pre = Pre{},
+                                           int trace = -1) {
+    (void)trace;
     using Lay = BrickLayout<Op>;
     using A = typename Op::Acc;
     using S = typename Op::Raw;
     constexpr int R = Op::R, C = Op::C, NR = Op::NR, K = 2 * R + 1;
-    constexpr int HX = Lay::HX, HY = Lay::HY;
+    constexpr int HX = Lay::HX, HY = Lay::HY, HXP = Lay::HXP;
     constexpr int nS = Lay::nS, nX = Lay::nX, nY = Lay::nY;
+    constexpr int nE = HX * HY * Lay::HZ;  // staged elements per channel
     A* sX = reinterpret_cast<A*>(smem);
     S* sS = reinterpret_cast<S*>(smem + Lay::bX);
     A* sY = reinterpret_cast<A*>(smem + Lay::bX);  // aliases sS after the x pass
@@ -131,11 +162,12 @@ __device__ __forceinline__ bool brick_body(const Op& op, const BG& g, int b, uns
         }
     }
     if (!pre()) return false;
+    DFM_BT(0);
     // 1. stage: the loads of a batch of elements are all issued before any is
     // stored (one L2 round trip per batch instead of one per element)
     const bool inner = x0 - R >= 0 && x0 + BX + R <= d.nx && y0 - R >= 0 &&
                        y0 + BY + R <= d.ny && z0 - R >= 0 && z0 + BZ + R <= d.nz;
-    constexpr int IS = (nS + NTB - 1) / NTB, SB = Op::kStageBatch;
+    constexpr int IS = (nE + NTB - 1) / NTB, SB = Op::kStageBatch;
     for (int b0 = 0; b0 < IS; b0 += SB) {
         S v[SB][NR];
 #pragma unroll
@@ -143,7 +175,7 @@ __device__ __forceinline__ bool brick_body(const Op& op, const BG& g, int b, uns
             const int e = tid + (b0 + k) * NTB;
             const int xl = e % HX, t = e / HX, yl = t % HY, zl = t / HY;
             const int gx = x0 - R + xl, gy = y0 - R + yl, gz = z0 - R + zl;
-            if (b0 + k < IS && e < nS &&
+            if (b0 + k < IS && e < nE &&
                 (inner || (gx >= 0 && gx < d.nx && gy >= 0 && gy < d.ny && gz >= 0 &&
                            gz < d.nz))) {
                 op.stage(gx, gy, gz, v[k]);
@@ -155,29 +187,75 @@ __device__ __forceinline__ bool brick_body(const Op& op, const BG& g, int b, uns
 #pragma unroll
         for (int k = 0; k < SB; ++k) {
             const int e = tid + (b0 + k) * NTB;
-            if (b0 + k < IS && e < nS) {
+            if (b0 + k < IS && e < nE) {
+                const int xl = e % HX, t = e / HX;
 #pragma unroll
-                for (int c = 0; c < NR; ++c) sS[c * nS + e] = v[k][c];
+                for (int c = 0; c < NR; ++c) sS[c * nS + t * HXP + xl] = v[k][c];
             }
         }
     }
     __syncthreads();
+    DFM_BT(1);
     // 2. x pass
-    constexpr int IX = (nX + NTB - 1) / NTB;
+    if constexpr (DFM_BRICK_XQUAD != 0) {
+        // the same op.xpass arithmetic per output, its operands from a
+        // register window instead of 2R+1 shared loads per output
+        constexpr int W4 = Lay::W4, NV4 = Lay::NV4, VEC = Lay::VEC, NQ = BX / 4;
+        static_assert(BX % 4 == 0, "quad x pass: whole quads per brick row");
+        constexpr int nQ = Lay::HZ * HY * NQ;
+        constexpr int IQ = (nQ + NTB - 1) / NTB;
 #pragma unroll
-    for (int k = 0; k < IX; ++k) {
-        const int e = tid + k * NTB;
-        if (e < nX) {
-            const int xl = e % BX, t = e / BX;  // t = zl*HY + yl
-            const int gx = x0 + xl;
-            A v[C];
-            op.xpass(sS + t * HX + xl, nS, v);
-            const A nxv = gx < d.nx ? op.nrm(0, gx) : A(0);
+        for (int k = 0; k < IQ; ++k) {
+            const int e = tid + k * NTB;
+            if (e < nQ) {
+                const int q = e % NQ, t = e / NQ;  // t = zl*HY + yl
+                S wv[NR * NV4 * VEC];
 #pragma unroll
-            for (int c = 0; c < C; ++c) sX[c * nX + e] = v[c] * nxv;
+                for (int c = 0; c < NR; ++c) {
+                    const S* src = sS + c * nS + t * HXP + 4 * q;
+#pragma unroll
+                    for (int j = 0; j < NV4; ++j) {
+                        if constexpr (sizeof(S) == 4) {
+                            const float4 f = reinterpret_cast<const float4*>(src)[j];
+                            S* o = wv + c * NV4 * VEC + 4 * j;
+                            o[0] = f.x, o[1] = f.y, o[2] = f.z, o[3] = f.w;
+                        } else {
+                            const double2 f = reinterpret_cast<const double2*>(src)[j];
+                            S* o = wv + c * NV4 * VEC + 2 * j;
+                            o[0] = f.x, o[1] = f.y;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int o = 0; o < 4; ++o) {
+                    const int xl = 4 * q + o, gx = x0 + xl;
+                    A v[C];
+                    op.xpass(wv + o, NV4 * VEC, v);
+                    const A nxv = gx < d.nx ? op.nrm(0, gx) : A(0);
+#pragma unroll
+                    for (int c = 0; c < C; ++c) sX[c * nX + t * BX + xl] = v[c] * nxv;
+                }
+            }
+        }
+        (void)W4;
+    } else {
+        constexpr int IX = (nX + NTB - 1) / NTB;
+#pragma unroll
+        for (int k = 0; k < IX; ++k) {
+            const int e = tid + k * NTB;
+            if (e < nX) {
+                const int xl = e % BX, t = e / BX;  // t = zl*HY + yl
+                const int gx = x0 + xl;
+                A v[C];
+                op.xpass(sS + t * HXP + xl, nS, v);
+                const A nxv = gx < d.nx ? op.nrm(0, gx) : A(0);
+#pragma unroll
+                for (int c = 0; c < C; ++c) sX[c * nX + e] = v[c] * nxv;
+            }
         }
     }
     __syncthreads();
+    DFM_BT(2);
     // 3. y pass (into the dead staging buffer)
     constexpr int IY = (nY + NTB - 1) / NTB;
 #pragma unroll
@@ -198,6 +276,7 @@ __device__ __forceinline__ bool brick_body(const Op& op, const BG& g, int b, uns
         }
     }
     __syncthreads();
+    DFM_BT(3);
     // 4. z pass + per-voxel epilogue (both voxels of a thread in flight together)
     const typename Op::Prol pr = op.prologue();
     double rsum = 0.0, rmax = 0.0;
@@ -226,6 +305,7 @@ __device__ __forceinline__ bool brick_body(const Op& op, const BG& g, int b, uns
             rmax = fmax(rmax, r.mx);
         }
     }
+    DFM_BT(4);
     if constexpr (Op::kSum || Op::kMax) {
         const double bs = Op::kSum ? bsum<NTB>(rsum, s_red) : 0.0;
         const double bm = Op::kMax ? bmax<NTB>(rmax, s_red) : 0.0;
@@ -234,6 +314,7 @@ __device__ __forceinline__ bool brick_body(const Op& op, const BG& g, int b, uns
         if (tid == 0 && bid == 0) op.finish(0, 0.0, 0.0, pr);
         __syncthreads();
     }
+    DFM_BT(5);
     return true;
 }
 
@@ -824,10 +905,7 @@ __device__ bool nb_fail(const NbSync& s, LoopState* st, bool stalled) {
 #endif
 // DFM_NB_TRACE=i (debug builds): every brick CTA printfs, for iteration i,
 // per phase the clock64 cycles spent waiting and in the body, and the
-// globaltimer at its publication
-#ifndef DFM_NB_TRACE
-#define DFM_NB_TRACE -1
-#endif
+// globaltimer at its publication (NBTR), and brick_body's stage clocks (NBBT)
 #if DFM_NB_TRACE >= 0
 __device__ long long g_nb_tr_enter[1024][4], g_nb_tr_ready[1024][4], g_nb_tr_done[1024][4];
 __device__ unsigned long long g_nb_tr_pub[1024][4];
@@ -1007,7 +1085,9 @@ __global__ void __launch_bounds__(NTP, DFM_NB_MINB)
             fwd.partials = a.fwd.partials + static_cast<size_t>(it) * nb;
             for (int b = blockIdx.x; b < nb; b += nbc) {
                 auto pre = [&] { return nb_wait(sy, st, g, nbz, b, p0, &s_flag); };
-                if (!brick_body<decltype(fwd), NTP>(fwd, g, b, smem, s_red, pre)) return;
+                if (!brick_body<decltype(fwd), NTP>(fwd, g, b, smem, s_red, pre,
+                                                    it == DFM_NB_TRACE ? 0 : -1))
+                    return;
                 nb_publish(sy, g, nbz, b, p0 + 1);
                 if (threadIdx.x == 0)  // the partial is released by nb_publish's fence
                     asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(sy.fdone + it)
@@ -1017,7 +1097,9 @@ __global__ void __launch_bounds__(NTP, DFM_NB_MINB)
         // B: LNCC backward
         for (int b = blockIdx.x; b < nb; b += nbc) {
             auto pre = [&] { return nb_wait(sy, st, g, nbz, b, p0 + 1, &s_flag); };
-            if (!brick_body<decltype(a.bwd), NTP>(a.bwd, g, b, smem, s_red, pre)) return;
+            if (!brick_body<decltype(a.bwd), NTP>(a.bwd, g, b, smem, s_red, pre,
+                                                  it == DFM_NB_TRACE ? 1 : -1))
+                return;
             nb_publish(sy, g, nbz, b, p0 + 2);
         }
         // the level may stop at this iteration: wait for its record (every
@@ -1042,7 +1124,9 @@ __global__ void __launch_bounds__(NTP, DFM_NB_MINB)
         sa.slot = it0 + it;
         for (int b = blockIdx.x; b < nb; b += nbc) {
             auto pre = [&] { return nb_wait(sy, st, g, nbz, b, p0 + 2, &s_flag); };
-            if (!brick_body<decltype(sa), NTP>(sa, g, b, smem, s_red, pre)) return;
+            if (!brick_body<decltype(sa), NTP>(sa, g, b, smem, s_red, pre,
+                                               it == DFM_NB_TRACE ? 2 : -1))
+                return;
             nb_publish(sy, g, nbz, b, p0 + 3);
         }
         // C: sigma_warp smoothing of c, W/G; a non-finite step stops first
@@ -1058,7 +1142,8 @@ __global__ void __launch_bounds__(NTP, DFM_NB_MINB)
                 }
                 return;
             }
-            brick_body<decltype(co), NTP>(co, g, b, smem, s_red);
+            brick_body<decltype(co), NTP>(co, g, b, smem, s_red, NoPreStage{},
+                                          it == DFM_NB_TRACE ? 3 : -1);
             nb_publish(sy, g, nbz, b, p0 + 4);
         }
         ++nupd;
@@ -1074,6 +1159,11 @@ __global__ void __launch_bounds__(NTP, DFM_NB_MINB)
                    g_nb_tr_ready[c][2] - g_nb_tr_enter[c][2], g_nb_tr_done[c][2] - g_nb_tr_ready[c][2],
                    g_nb_tr_ready[c][3] - g_nb_tr_enter[c][3], g_nb_tr_done[c][3] - g_nb_tr_ready[c][3],
                    g_nb_tr_pub[c][0], g_nb_tr_pub[c][1], g_nb_tr_pub[c][2], g_nb_tr_pub[c][3]);
+            for (int k = 0; k < 4; ++k)
+                printf("NBBT %d %d %lld %lld %lld %lld %lld\n", c, k,
+                       g_nb_bt[c][k][1] - g_nb_bt[c][k][0], g_nb_bt[c][k][2] - g_nb_bt[c][k][1],
+                       g_nb_bt[c][k][3] - g_nb_bt[c][k][2], g_nb_bt[c][k][4] - g_nb_bt[c][k][3],
+                       g_nb_bt[c][k][5] - g_nb_bt[c][k][4]);
         }
 #endif
     }
