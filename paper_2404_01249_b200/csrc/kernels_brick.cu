@@ -60,20 +60,54 @@ struct BG {
 #define DFM_BRICK_XQUAD 1
 #endif
 
+// ops whose stage is a plain load of NR planes of T (Op::vsrc(c), Op::vnc(c)
+// = read-only) stage whole rows with 128-bit loads when the level allows it
+template <class Op, class = void>
+struct VecStageB {
+    static constexpr bool value = false;
+    using Src = typename Op::Raw;
+};
+template <class Op>
+struct VecStageB<Op, std::void_t<decltype(&Op::vsrc)>> {
+    static constexpr bool value = true;
+    using Src = typename Op::Src;
+};
+
+constexpr int round_up_b(int v, int m) { return (v + m - 1) / m * m; }
+
 template <class Op>
 struct BrickLayout {
     using A = typename Op::Acc;
     using S = typename Op::Raw;
+    using G = typename VecStageB<Op>::Src;
     static constexpr int R = Op::R, C = Op::C, NR = Op::NR;
     static constexpr int HX = BX + 2 * R, HY = BY + 2 * R, HZ = BZ + 2 * R;
-    // quad x pass (DFM_BRICK_XQUAD): a thread filters 4 consecutive columns
-    // from one register window of 4 + 2R staged values per channel, read with
-    // 128-bit loads; staged rows are padded to HXP for the alignment
+    // Staged rows start PADL columns left of the brick (PADL >= R, a whole
+    // number of 128-bit chunks of the global rows, so rows stage as aligned
+    // vectors) and are padded to HXP.  Quad x pass (DFM_BRICK_XQUAD): a thread
+    // filters 4 consecutive columns from one register window of 4 + 2R
+    // staged values per channel, read with 128-bit loads from the aligned
+    // position MIS values left of the window.
+    static constexpr int VT = 16 / int(sizeof(G));  // global values per 128-bit load
     static constexpr int VEC = 16 / int(sizeof(S));  // staged values per 128-bit load
     static constexpr int W4 = 4 + 2 * R;
-    static constexpr int NV4 = (W4 + VEC - 1) / VEC;  // vector loads per window
-    static constexpr int HXQ = (BX - 4) + NV4 * VEC > HX ? (BX - 4) + NV4 * VEC : HX;
-    static constexpr int HXP = DFM_BRICK_XQUAD ? (HXQ + VEC - 1) / VEC * VEC : HX;
+    // padded row length for a left pad PL
+    static constexpr int hxp(int PL) {
+        const int mis = (PL - R) % VEC, nv = (W4 + mis + VEC - 1) / VEC, q0 = PL - R - mis;
+        const int n = PL + BX + R > q0 + (BX - 4) + nv * VEC ? PL + BX + R
+                                                             : q0 + (BX - 4) + nv * VEC;
+        return round_up_b(n, VT > VEC ? VT : VEC);
+    }
+    // the vector stage's aligned left pad only where it keeps the row length
+    // (longer rows move the x pass's bank pattern: measured slower for r = 2)
+    static constexpr bool kVec = DFM_BRICK_XQUAD != 0 && VecStageB<Op>::value &&
+                                 hxp(round_up_b(R, VT)) == hxp(R);
+    static constexpr int PADL = kVec ? round_up_b(R, VT) : R;
+    static constexpr int MIS = (PADL - R) % VEC;
+    static constexpr int NV4 = (W4 + MIS + VEC - 1) / VEC;  // vector loads per window
+    static constexpr int XQ0 = PADL - R - MIS;              // first quad's aligned start
+    static constexpr int HXP = DFM_BRICK_XQUAD ? hxp(PADL) : HX;
+    static constexpr int NCH = HXP / VT;      // 128-bit chunks per staged row (vector stage)
     static constexpr int nS = HXP * HY * HZ;  // per staged channel (padded rows)
     static constexpr int nX = HZ * HY * BX;  // per channel, x-pass output
     static constexpr int nY = HZ * BY * BX;  // per channel, y-pass output
@@ -82,6 +116,13 @@ struct BrickLayout {
     static constexpr size_t bY = static_cast<size_t>(C) * nY * sizeof(A);
     static constexpr size_t bytes = bX + (bS > bY ? bS : bY);
 };
+
+__device__ __forceinline__ float4 ld_vec4(const float* p, bool nc) {
+    return nc ? __ldg(reinterpret_cast<const float4*>(p)) : *reinterpret_cast<const float4*>(p);
+}
+__device__ __forceinline__ double2 ld_vec4(const double* p, bool nc) {
+    return nc ? __ldg(reinterpret_cast<const double2*>(p)) : *reinterpret_cast<const double2*>(p);
+}
 
 // ops with centre operands (Op::Center, Op::load_center) have them loaded
 // before the stage, so their latency hides behind the stage round trip
@@ -134,7 +175,7 @@ __device__ __forceinline__ bool brick_body(const Op& op, const BG& g, int b, uns
     constexpr int R = Op::R, C = Op::C, NR = Op::NR, K = 2 * R + 1;
     constexpr int HX = Lay::HX, HY = Lay::HY, HXP = Lay::HXP;
     constexpr int nS = Lay::nS, nX = Lay::nX, nY = Lay::nY;
-    constexpr int nE = HX * HY * Lay::HZ;  // staged elements per channel
+    constexpr int nE = HX * HY * Lay::HZ;  // staged elements per channel (scalar stage)
     A* sX = reinterpret_cast<A*>(smem);
     S* sS = reinterpret_cast<S*>(smem + Lay::bX);
     A* sY = reinterpret_cast<A*>(smem + Lay::bX);  // aliases sS after the x pass
@@ -165,32 +206,90 @@ __device__ __forceinline__ bool brick_body(const Op& op, const BG& g, int b, uns
     DFM_BT(0);
     // 1. stage: the loads of a batch of elements are all issued before any is
     // stored (one L2 round trip per batch instead of one per element)
-    const bool inner = x0 - R >= 0 && x0 + BX + R <= d.nx && y0 - R >= 0 &&
-                       y0 + BY + R <= d.ny && z0 - R >= 0 && z0 + BZ + R <= d.nz;
-    constexpr int IS = (nE + NTB - 1) / NTB, SB = Op::kStageBatch;
-    for (int b0 = 0; b0 < IS; b0 += SB) {
-        S v[SB][NR];
+    constexpr int PADL = Lay::PADL;
+    bool vec = false;
+    if constexpr (Lay::kVec) {
+        // rows as aligned 128-bit chunks: chunk starts are multiples of VT and
+        // so is nx, so a chunk is wholly inside or wholly outside the volume
+        vec = d.nx % Lay::VT == 0;
 #pragma unroll
-        for (int k = 0; k < SB; ++k) {
-            const int e = tid + (b0 + k) * NTB;
-            const int xl = e % HX, t = e / HX, yl = t % HY, zl = t / HY;
-            const int gx = x0 - R + xl, gy = y0 - R + yl, gz = z0 - R + zl;
-            if (b0 + k < IS && e < nE &&
-                (inner || (gx >= 0 && gx < d.nx && gy >= 0 && gy < d.ny && gz >= 0 &&
-                           gz < d.nz))) {
-                op.stage(gx, gy, gz, v[k]);
-            } else {
+        for (int c = 0; c < NR; ++c)
+            vec = vec && (reinterpret_cast<uintptr_t>(op.vsrc(c)) & 15) == 0;
+    }
+    if (vec) {
+        if constexpr (Lay::kVec) {
+            using G = typename Lay::G;
+            using GV = typename std::conditional<sizeof(G) == 4, float4, double2>::type;
+            constexpr int VT = Lay::VT, NCH = Lay::NCH, NRW = HY * Lay::HZ;
+            constexpr int NI = NR * NRW * NCH, II = (NI + NTB - 1) / NTB, SBV = 8;
+            for (int b0 = 0; b0 < II; b0 += SBV) {
+                GV v[SBV];
 #pragma unroll
-                for (int c = 0; c < NR; ++c) v[k][c] = S(0);
+                for (int k = 0; k < SBV; ++k) {
+                    const int e = tid + (b0 + k) * NTB;
+                    const int ch = e % NCH, t = (e / NCH) % NRW, c = e / (NCH * NRW);
+                    const int yl = t % HY, zl = t / HY;
+                    const int gx = x0 - PADL + VT * ch, gy = y0 - R + yl, gz = z0 - R + zl;
+                    if (b0 + k < II && e < NI && gx >= 0 && gx + VT <= d.nx && gy >= 0 &&
+                        gy < d.ny && gz >= 0 && gz < d.nz) {
+                        v[k] = ld_vec4(op.vsrc(c) + d.idx32(gx, gy, gz), Op::vnc(c));
+                    } else {
+                        v[k] = GV{};
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < SBV; ++k) {
+                    const int e = tid + (b0 + k) * NTB;
+                    if (b0 + k < II && e < NI) {
+                        const int ch = e % NCH, t = (e / NCH) % NRW, c = e / (NCH * NRW);
+                        S* o = sS + c * nS + t * HXP + VT * ch;
+                        if constexpr (sizeof(G) == 4) {
+                            const float4 f = v[k];
+                            if constexpr (sizeof(S) == 4) {
+                                *reinterpret_cast<float4*>(o) = f;
+                            } else {
+                                reinterpret_cast<double2*>(o)[0] =
+                                    make_double2(static_cast<double>(f.x), static_cast<double>(f.y));
+                                reinterpret_cast<double2*>(o)[1] =
+                                    make_double2(static_cast<double>(f.z), static_cast<double>(f.w));
+                            }
+                        } else {
+                            *reinterpret_cast<double2*>(o) = v[k];
+                        }
+                    }
+                }
             }
         }
+    } else {
+        constexpr int HW = BX + 2 * R;  // the columns the x pass reads
+        const bool inner = x0 - R >= 0 && x0 + BX + R <= d.nx && y0 - R >= 0 &&
+                           y0 + BY + R <= d.ny && z0 - R >= 0 && z0 + BZ + R <= d.nz;
+        constexpr int IS = (nE + NTB - 1) / NTB, SB = Op::kStageBatch;
+        for (int b0 = 0; b0 < IS; b0 += SB) {
+            S v[SB][NR];
 #pragma unroll
-        for (int k = 0; k < SB; ++k) {
-            const int e = tid + (b0 + k) * NTB;
-            if (b0 + k < IS && e < nE) {
-                const int xl = e % HX, t = e / HX;
+            for (int k = 0; k < SB; ++k) {
+                const int e = tid + (b0 + k) * NTB;
+                const int xl = e % HW, t = e / HW, yl = t % HY, zl = t / HY;
+                const int gx = x0 - R + xl, gy = y0 - R + yl, gz = z0 - R + zl;
+                if (b0 + k < IS && e < nE &&
+                    (inner || (gx >= 0 && gx < d.nx && gy >= 0 && gy < d.ny && gz >= 0 &&
+                               gz < d.nz))) {
+                    op.stage(gx, gy, gz, v[k]);
+                } else {
 #pragma unroll
-                for (int c = 0; c < NR; ++c) sS[c * nS + t * HXP + xl] = v[k][c];
+                    for (int c = 0; c < NR; ++c) v[k][c] = S(0);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < SB; ++k) {
+                const int e = tid + (b0 + k) * NTB;
+                if (b0 + k < IS && e < nE) {
+                    const int xl = e % HW, t = e / HW;
+#pragma unroll
+                    for (int c = 0; c < NR; ++c)
+                        sS[c * nS + t * HXP + (PADL - R) + xl] = v[k][c];
+                }
             }
         }
     }
@@ -212,7 +311,7 @@ __device__ __forceinline__ bool brick_body(const Op& op, const BG& g, int b, uns
                 S wv[NR * NV4 * VEC];
 #pragma unroll
                 for (int c = 0; c < NR; ++c) {
-                    const S* src = sS + c * nS + t * HXP + 4 * q;
+                    const S* src = sS + c * nS + t * HXP + Lay::XQ0 + 4 * q;
 #pragma unroll
                     for (int j = 0; j < NV4; ++j) {
                         if constexpr (sizeof(S) == 4) {
@@ -230,7 +329,7 @@ __device__ __forceinline__ bool brick_body(const Op& op, const BG& g, int b, uns
                 for (int o = 0; o < 4; ++o) {
                     const int xl = 4 * q + o, gx = x0 + xl;
                     A v[C];
-                    op.xpass(wv + o, NV4 * VEC, v);
+                    op.xpass(wv + Lay::MIS + o, NV4 * VEC, v);
                     const A nxv = gx < d.nx ? op.nrm(0, gx) : A(0);
 #pragma unroll
                     for (int c = 0; c < C; ++c) sX[c * nX + t * BX + xl] = v[c] * nxv;
@@ -247,7 +346,7 @@ __device__ __forceinline__ bool brick_body(const Op& op, const BG& g, int b, uns
                 const int xl = e % BX, t = e / BX;  // t = zl*HY + yl
                 const int gx = x0 + xl;
                 A v[C];
-                op.xpass(sS + t * HXP + xl, nS, v);
+                op.xpass(sS + t * HXP + (PADL - R) + xl, nS, v);
                 const A nxv = gx < d.nx ? op.nrm(0, gx) : A(0);
 #pragma unroll
                 for (int c = 0; c < C; ++c) sX[c * nX + e] = v[c] * nxv;
@@ -360,6 +459,9 @@ struct LnccFwdB {
         v[0] = static_cast<double>(__ldg(F + i));
         v[1] = static_cast<double>(W[i]);
     }
+    using Src = T;  // vector stage: the same loads as stage()
+    __device__ const T* vsrc(int c) const { return c == 0 ? F : W; }
+    __device__ static constexpr bool vnc(int c) { return c == 0; }
     __device__ void xpass(const double* p, int cs, double v[C]) const {
         if constexpr (FS) {
             double a0 = 0, a1 = 0, a2 = 0;
@@ -440,6 +542,9 @@ struct FStatsB {
     __device__ void stage(int x, int y, int z, double v[1]) const {
         v[0] = static_cast<double>(__ldg(F + d.idx32(x, y, z)));
     }
+    using Src = T;
+    __device__ const T* vsrc(int) const { return F; }
+    __device__ static constexpr bool vnc(int) { return true; }
     __device__ void xpass(const double* p, int, double v[2]) const {
         double a0 = 0, a1 = 0;
 #pragma unroll
@@ -490,6 +595,9 @@ struct LnccBwdB {
 #pragma unroll
         for (int k = 0; k < 4; ++k) v[k] = static_cast<Acc>(coef[k * d.n + i]);
     }
+    using Src = T;
+    __device__ const T* vsrc(int c) const { return coef + static_cast<size_t>(c) * d.n; }
+    __device__ static constexpr bool vnc(int) { return false; }
     __device__ void xpass(const Acc* p, int cs, Acc v[4]) const {
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -573,6 +681,9 @@ struct SmoothAdamB {
 #pragma unroll
         for (int k = 0; k < 3; ++k) v[k] = grad[k * d.n + i];
     }
+    using Src = T;
+    __device__ const T* vsrc(int c) const { return grad + static_cast<size_t>(c) * d.n; }
+    __device__ static constexpr bool vnc(int) { return false; }
     __device__ void xpass(const T* p, int cs, T v[3]) const { gauss_xpass<T, R>(w, p, cs, v); }
     __device__ T wgt(int a, int j) const { return w.taps[a][j]; }
     __device__ T nrm(int a, int i) const {
@@ -738,6 +849,9 @@ struct ComposeSB {
 #pragma unroll
         for (int k = 0; k < 3; ++k) v[k] = c[k * d.n + i];
     }
+    using Src = T;
+    __device__ const T* vsrc(int k) const { return c + static_cast<size_t>(k) * d.n; }
+    __device__ static constexpr bool vnc(int) { return false; }
     __device__ void xpass(const T* p, int cs, T v[3]) const { gauss_xpass<T, R>(w, p, cs, v); }
     __device__ T wgt(int a, int j) const { return w.taps[a][j]; }
     __device__ T nrm(int a, int i) const {
