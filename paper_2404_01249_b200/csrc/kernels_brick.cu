@@ -91,23 +91,37 @@ struct BrickLayout {
     static constexpr int VT = 16 / int(sizeof(G));  // global values per 128-bit load
     static constexpr int VEC = 16 / int(sizeof(S));  // staged values per 128-bit load
     static constexpr int W4 = 4 + 2 * R;
-    // padded row length for a left pad PL
+    // padded row length for a left pad PL: long enough for the stage and the
+    // quad windows, a whole number of 128-bit chunks, and a row stride of 8 or
+    // 24 words mod 32, so the 8 lanes of each 128-bit shared-load phase of the
+    // quad x pass (4 rows x 2 quads) hit distinct banks
     static constexpr int hxp(int PL) {
         const int mis = (PL - R) % VEC, nv = (W4 + mis + VEC - 1) / VEC, q0 = PL - R - mis;
         const int n = PL + BX + R > q0 + (BX - 4) + nv * VEC ? PL + BX + R
                                                              : q0 + (BX - 4) + nv * VEC;
-        return round_up_b(n, VT > VEC ? VT : VEC);
+        const int step = VT > VEC ? VT : VEC;
+        int h = round_up_b(n, step);
+        for (int k = 0; k < 8; ++k) {
+            const int w = (h * int(sizeof(S)) / 4) % 32;
+            if (w == 8 || w == 24) break;
+            h += step;
+        }
+        return h;
     }
-    // the vector stage's aligned left pad only where it keeps the row length
-    // (longer rows move the x pass's bank pattern: measured slower for r = 2)
-    static constexpr bool kVec = DFM_BRICK_XQUAD != 0 && VecStageB<Op>::value &&
-                                 hxp(round_up_b(R, VT)) == hxp(R);
+    // the vector stage's aligned left pad for radii >= 3 (the sigma_grad
+    // smooth+Adam: stage 3.3 -> 1.9 us per brick phase) where its staged rows
+    // fit 48 KB; at radius 2 (LNCC, sigma_warp) the scalar stage measured as
+    // fast or faster
+    static constexpr bool kVec =
+        DFM_BRICK_XQUAD != 0 && VecStageB<Op>::value && R >= 3 &&
+        size_t(NR) * HY * HZ * hxp(round_up_b(R, VT)) * sizeof(S) <= 48 * 1024;
     static constexpr int PADL = kVec ? round_up_b(R, VT) : R;
     static constexpr int MIS = (PADL - R) % VEC;
     static constexpr int NV4 = (W4 + MIS + VEC - 1) / VEC;  // vector loads per window
     static constexpr int XQ0 = PADL - R - MIS;              // first quad's aligned start
     static constexpr int HXP = DFM_BRICK_XQUAD ? hxp(PADL) : HX;
-    static constexpr int NCH = HXP / VT;      // 128-bit chunks per staged row (vector stage)
+    // 128-bit chunks per staged row (vector stage): the columns the x pass uses
+    static constexpr int NCH = (PADL + BX + R + VT - 1) / VT;
     static constexpr int nS = HXP * HY * HZ;  // per staged channel (padded rows)
     static constexpr int nX = HZ * HY * BX;  // per channel, x-pass output
     static constexpr int nY = HZ * BY * BX;  // per channel, y-pass output
