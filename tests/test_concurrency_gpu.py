@@ -58,3 +58,44 @@ def test_sweep_rows_independent_of_workers():
             for w in (1, 3)]
     assert [(r.failed, r.metric_mean) for r in rows[0]] == \
         [(r.failed, r.metric_mean) for r in rows[1]]
+
+
+@pytest.mark.parametrize("persist", [2, 3])
+def test_concurrent_persistent_levels(persist):
+    """The neighbour-synchronised persistent solver is one cooperative launch
+    per brick level whose CTAs spin on their neighbours: several contexts
+    launching it at once must neither deadlock (a stall would raise) nor
+    change any bit.  40x48x56 is the config-1 coarse level (420 bricks, the
+    default solver's size); persist 3 also forces it on the small level."""
+    from paper_2404_01249_b200.engine import OPT_PERSIST
+    pairs = [synth.make_pair(1, seed=50 + k, shape=(112, 96, 80)) for k in range(3)]
+    sched = A.PyramidSchedule((2.0, 1.0), (12, 2))
+    cfg = synth.baseline_config(A.LOSS_LNCC, 2, 1.0, max_iters=12)
+    cfg.eta = 0.3
+
+    def run(p):
+        ctx = Context(0, "f32")
+        ctx.set_option(OPT_PERSIST, persist)
+        f, log = ctx.register_images(p.grid, p.fixed, p.moving, cfg, sched)
+        ctx.close()
+        return f, [r.loss for r in log.iterations]
+
+    alone = [run(p) for p in pairs]
+    together = [None] * len(pairs)
+    errors = []
+
+    def worker(k):
+        try:
+            together[k] = run(pairs[k])
+        except Exception as e:  # noqa: BLE001 - reported below
+            errors.append(e)
+
+    th = [threading.Thread(target=worker, args=(k,)) for k in range(len(pairs))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+    for (fa, la), (fb, lb) in zip(alone, together):
+        assert np.array_equal(fa, fb)
+        assert la == lb
