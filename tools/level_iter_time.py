@@ -3,7 +3,8 @@ path, for a list of volume sizes:  python tools/level_iter_time.py NXxNYxNZ ...
 (one registration at scale 1 with 64 iterations per size, early stop off;
 median IterationRecord.wall_ms, i.e. graph-chunk device time / iterations).
 LIT_PERSIST=0/1/2 and LIT_BRICK_MAX select the brick solver (persistent
-levels stamp each iteration's record on the device)."""
+levels stamp each iteration's record on the device); LIT_OPTS="key=value,..."
+sets any further dfm_ctx_set_option keys (numbers, include/difform_gpu.h)."""
 import os
 import sys
 
@@ -26,6 +27,9 @@ for spec in sys.argv[1:]:
             ctx.set_option(OPT_PERSIST, int(os.environ["LIT_PERSIST"]))
         if "LIT_BRICK_MAX" in os.environ:
             ctx.set_option(OPT_BRICK_MAX, int(os.environ["LIT_BRICK_MAX"]))
+        for kv in filter(None, os.environ.get("LIT_OPTS", "").split(",")):
+            k, v = kv.split("=")
+            ctx.set_option(int(k), int(v))
         try:
             _, log = ctx.register_images(p.grid, p.fixed, p.moving, cfg,
                                          A.PyramidSchedule((1.0,), (iters,)))
