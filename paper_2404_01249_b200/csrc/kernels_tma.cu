@@ -797,11 +797,37 @@ struct FStats2 {
 
 // similarity.cpp:122-168 with the F statistics precomputed (FStats2): three
 // fp64 box moments of W per iteration instead of five
+#ifndef DFM_FWD_WCARRY
+#define DFM_FWD_WCARRY 1
+#endif
+// The clipped window's 1/n of a voxel column (x, y fixed per thread row): the
+// x*y window length and the interior-plane quotient 1/(nxy K) are formed on
+// the first plane and carried, so the per-voxel work is one uniform z test;
+// only the 2R border planes divide.  Same n, same correctly rounded 1/n as
+// window_inv (border tiles no longer divide on every voxel).
+struct WinCarry {
+    int nxy;     // 0: not yet formed
+    double inv;  // 1 / (nxy K)
+};
+template <int R>
+__device__ __forceinline__ double window_inv_carried(int x, int y, int z, const Dims& d,
+                                                     WinCarry& c) {
+    constexpr int K = 2 * R + 1;
+    const int gz = d.gz(), zg = z + d.zoff;
+    if (gz <= 1) return window_inv<R>(x, y, z, d);
+    if (c.nxy == 0) {
+        c.nxy = box_len(x, d.nx, R) * box_len(y, d.ny, R);
+        c.inv = 1.0 / static_cast<double>(c.nxy * K);
+    }
+    if (static_cast<unsigned>(zg - R) < static_cast<unsigned>(max(gz - 2 * R, 0))) return c.inv;
+    return 1.0 / static_cast<double>(c.nxy * box_len(zg, gz, R));
+}
+
 template <class T, int R_, int TY_ = DFM_TY_FWD>
 struct LnccFwd3 {
     using Acc = double;
     using Prol = NoProl;
-    using Carry = NoCarry;
+    using Carry = typename std::conditional<DFM_FWD_WCARRY != 0, WinCarry, NoCarry>::type;
     static constexpr int R = R_, C = 3, BACK = 0, AHEAD = 0, S = DFM_S_FWD, TYv = TY_;
     // radius >= 3 (LNCC window 7+) or fp64 needs more than the 80 registers of
     // 3 CTAs per SM: 2 CTAs, no spills
@@ -880,8 +906,12 @@ struct LnccFwd3 {
         c.vF = __ldg(fstat + d.n + i);
     }
     __device__ Red2 emit(int x, int y, int z, const double s[3], const Center& c, const Prol&,
-                         Carry&) const {
-        const double inv_n = window_inv<R>(x, y, z, d);
+                         Carry& cr) const {
+        double inv_n;
+        if constexpr (DFM_FWD_WCARRY != 0)
+            inv_n = window_inv_carried<R>(x, y, z, d, cr);
+        else
+            inv_n = window_inv<R>(x, y, z, d);
         const LnccCoef k = lncc_coef_f(c.muF, c.vF, s[0], s[1], s[2], inv_n);
         const int i = d.idx32(x, y, z);
         coef[0][i] = static_cast<T>(k.an);
