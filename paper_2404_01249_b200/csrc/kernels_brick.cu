@@ -5,8 +5,8 @@
 // z-chunk, which is the right shape for a 160x192x224 volume but latency-bound
 // on the 40x48x56 and 80x96x112 levels: there a CTA walks only a few planes,
 // each a serial chain of TMA wait -> x pass -> barrier -> y pass -> z ring.
-// Here a CTA owns an 8x8x8 brick instead and does every pass for the whole
-// brick in parallel:
+// Here a CTA owns an 8 x BY x 8 brick (BY = 4 by default) instead and does
+// every pass for the whole brick in parallel:
 //   1. stage the haloed brick (8+2R)^3 of the op's raw channels into shared
 //      memory (all loads independent: one L2 round trip; zero outside the
 //      volume, which together with the per-position renormalisation factors
@@ -18,8 +18,10 @@
 // is loop_ops.cuh, shared with the plane-streaming kernels.
 //
 // Buffers the loop rewrites (W, G, coefficients, grad, step, u) are read with
-// plain coherent loads, never ld.global.nc: the persistent solver below reads
-// them after grid barriers within one launch.
+// plain coherent loads, never ld.global.nc: the persistent solvers below read
+// them within one launch, after a grid barrier (k_persist) or after an
+// acquire on their neighbour bricks' phase counters (k_persist_nb, the
+// default for the config-1 coarse level).
 //
 // Ops (same roles as in kernels_tma.cu):
 //   LnccFwdB    F, W          -> 4 window coefficients, cc^2 partials (+ monitor)
