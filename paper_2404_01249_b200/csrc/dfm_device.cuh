@@ -129,6 +129,37 @@ struct Cell3 {
     bool three;
 };
 
+// The three axes of a 3-D gather cell at once.  fp32 fast path
+// (DFM_LOCATE_FAST): when all three lower corners are strictly inside
+// [0, n-2] nothing clamps and locate_axis would return (i, u - floor(u),
+// false) — the same values without its border selects; otherwise (borders,
+// flat axes, huge or NaN displacements) the general per-axis search.
+#ifndef DFM_LOCATE_FAST
+#define DFM_LOCATE_FAST 1
+#endif
+template <class T, bool kFlat = true>
+__device__ __forceinline__ void locate_cells3(int x, int y, int z, T ux, T uy, T uz, int nx,
+                                              int ny, int nz, AxisCell<T>& ax, AxisCell<T>& ay,
+                                              AxisCell<T>& az) {
+    if constexpr (DFM_LOCATE_FAST != 0 && sizeof(T) == 4) {
+        const float flx = floorf(ux), fly = floorf(uy), flz = floorf(uz);
+        const int ix = x + static_cast<int>(fminf(fmaxf(flx, -1.0e9f), 1.0e9f));
+        const int iy = y + static_cast<int>(fminf(fmaxf(fly, -1.0e9f), 1.0e9f));
+        const int iz = z + static_cast<int>(fminf(fmaxf(flz, -1.0e9f), 1.0e9f));
+        if (static_cast<unsigned>(ix) < static_cast<unsigned>(nx - 1) &&
+            static_cast<unsigned>(iy) < static_cast<unsigned>(ny - 1) &&
+            static_cast<unsigned>(iz) < static_cast<unsigned>(nz - 1)) {
+            ax.i0 = ix, ax.f = ux - flx, ax.clamped = false;
+            ay.i0 = iy, ay.f = uy - fly, ay.clamped = false;
+            az.i0 = iz, az.f = uz - flz, az.clamped = false;
+            return;
+        }
+    }
+    ax = locate_axis<kFlat>(x, ux, nx);
+    ay = locate_axis<kFlat>(y, uy, ny);
+    az = locate_axis<kFlat>(z, uz, nz);
+}
+
 template <class T>
 __device__ __forceinline__ Cell3<T> locate3(const Dims& m, int x, int y, int z, T ux, T uy,
                                             T uz) {
@@ -244,9 +275,8 @@ struct WG3 {
 template <class T, bool NC = true, bool kFlat = true>
 __device__ __forceinline__ void wg3_fetch(const T* __restrict__ M, const Dims& m, int x, int y,
                                           int z, T ux, T uy, T uz, WG3<T>& w) {
-    const AxisCell<T> ax = locate_axis<kFlat>(x, ux, m.nx);
-    const AxisCell<T> ay = locate_axis<kFlat>(y, uy, m.ny);
-    const AxisCell<T> az = locate_axis<kFlat>(z, uz, m.nz);
+    AxisCell<T> ax, ay, az;
+    locate_cells3<T, kFlat>(x, y, z, ux, uy, uz, m.nx, m.ny, m.nz, ax, ay, az);
     w.fx = ax.f;
     w.fy = ay.f;
     w.fz = az.f;
@@ -270,9 +300,8 @@ template <class T, bool kFlat = true>
 __device__ __forceinline__ void wg3_fetch_async(const T* __restrict__ M, const Dims& m, int x,
                                                 int y, int z, T ux, T uy, T uz, WG3<T>& w,
                                                 T* s, int ss) {
-    const AxisCell<T> ax = locate_axis<kFlat>(x, ux, m.nx);
-    const AxisCell<T> ay = locate_axis<kFlat>(y, uy, m.ny);
-    const AxisCell<T> az = locate_axis<kFlat>(z, uz, m.nz);
+    AxisCell<T> ax, ay, az;
+    locate_cells3<T, kFlat>(x, y, z, ux, uy, uz, m.nx, m.ny, m.nz, ax, ay, az);
     w.fx = ax.f;
     w.fy = ay.f;
     w.fz = az.f;

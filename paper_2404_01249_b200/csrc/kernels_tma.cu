@@ -1406,9 +1406,8 @@ struct Compose2 {
         const int gx = x0 + col, gy = y0 + row, zg = zi + d.zoff;
         const int so = row * BXS + col + (XAS - R);
         const T s0 = pc.step[so], s1 = pc.step[PS + so], s2 = pc.step[2 * PS + so];
-        const AxisCell<T> ax = locate_axis(gx, s0, d.nx);
-        const AxisCell<T> ay = locate_axis(gy, s1, d.ny);
-        const AxisCell<T> az = locate_axis(zg, s2, d.gz());
+        AxisCell<T> ax, ay, az;
+        locate_cells3<T>(gx, gy, zg, s0, s1, s2, d.nx, d.ny, d.gz(), ax, ay, az);
         const int o = (ay.i0 - (y0 - HU)) * BXU + (ax.i0 - (x0 - XAU));
         const T fx = ax.f, fy = ay.f, fz = az.f;
         const T wx0 = T(1) - fx, wy0 = T(1) - fy, wz0 = T(1) - fz;
