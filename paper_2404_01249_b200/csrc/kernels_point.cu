@@ -340,7 +340,12 @@ __device__ __forceinline__ void locate_point(double p, int n, int& i0, double& f
     f = p - static_cast<double>(i);
 }
 
-template <class T>
+// NC > 0: the component count fixed at compile time, every component's 8
+// corners loaded before the first blend (up to 72 independent loads in flight
+// per thread; the full-size 1/2 -> 1 upsample of field and moments is 9
+// components). NC == 0: runtime count, one component at a time. Same
+// arithmetic either way.
+template <class T, int NC>
 __global__ void k_resample(ResampleArgs<T> a, Dims ds, Dims dd, int ncomp) {
     const int x = blockIdx.x * kRX + threadIdx.x;
     if (x >= dd.nx) return;
@@ -365,10 +370,21 @@ __global__ void k_resample(ResampleArgs<T> a, Dims ds, Dims dd, int ncomp) {
         c.fz = static_cast<T>(fz);
         c.clx = c.cly = c.clz = false;
         const int64_t i = dd.idx(x, y, z);
+        if constexpr (NC > 0) {
+            Corners<T> k[NC];
+#pragma unroll
+            for (int q = 0; q < NC; ++q) k[q] = fetch_corners<T>(a.src[q], c);
+#pragma unroll
+            for (int q = 0; q < NC; ++q) {
+                const T v = lerp_value(c, k[q]);
+                a.dst[q][i] = a.mult[q] == 1.0 ? v : static_cast<T>(v * a.mult[q]);
+            }
+        } else {
 #pragma unroll 3
-        for (int k = 0; k < ncomp; ++k) {
-            const T v = lerp_value(c, fetch_corners<T>(a.src[k], c));
-            a.dst[k][i] = a.mult[k] == 1.0 ? v : static_cast<T>(v * a.mult[k]);
+            for (int k = 0; k < ncomp; ++k) {
+                const T v = lerp_value(c, fetch_corners<T>(a.src[k], c));
+                a.dst[k][i] = a.mult[k] == 1.0 ? v : static_cast<T>(v * a.mult[k]);
+            }
         }
     }
 }
@@ -385,8 +401,13 @@ void launch_resample(const Launch& L, const T* const* src, Dims ds, T* const* ds
     }
     for (int k = 0; k < 3; ++k)
         a.step[k] = nd[k] > 1 ? static_cast<double>(ns[k] - 1) / (nd[k] - 1) : 0.0;
-    k_resample<T><<<rows_grid(dd.nx, static_cast<int64_t>(dd.ny) * dd.nz), dim3(kRX, kRY), 0,
-                    L.stream>>>(a, ds, dd, ncomp);
+    const dim3 grid = rows_grid(dd.nx, static_cast<int64_t>(dd.ny) * dd.nz), block(kRX, kRY);
+    // fp64 keeps the runtime count: 9 fixed components take 182 registers there
+    switch (sizeof(T) == 4 ? ncomp : 0) {
+        case 3: k_resample<T, 3><<<grid, block, 0, L.stream>>>(a, ds, dd, ncomp); break;
+        case 9: k_resample<T, 9><<<grid, block, 0, L.stream>>>(a, ds, dd, ncomp); break;
+        default: k_resample<T, 0><<<grid, block, 0, L.stream>>>(a, ds, dd, ncomp); break;
+    }
     L.bump();
 }
 
