@@ -293,6 +293,8 @@ def run_reference_arm(args, rank, world):
     v = float(np.mean(vals))
     cb["value"] = v
     cb["s_per_pair"] = float(np.mean(pairs_s))
+    cb["sample"] = (f"mean of {len(pairs_s)} samples ({', '.join(f'{x:.1f}' for x in pairs_s)} "
+                    f"s per pair); last: " + cb["sample"])
     line = {"impl": "reference", "metric": "voxel-iterations/sec", "value": v,
             "unit": "voxel-iter/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": float(np.mean(secs)) * 1e3,
