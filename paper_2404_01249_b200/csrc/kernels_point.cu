@@ -371,9 +371,26 @@ __global__ void k_resample(ResampleArgs<T> a, Dims ds, Dims dd, int ncomp) {
         c.clx = c.cly = c.clz = false;
         const int64_t i = dd.idx(x, y, z);
         if constexpr (NC > 0) {
+            // 3-D source with every axis > 1 (launcher): the +x corner is the
+            // next element, so each component needs four row pointers (base,
+            // +y, +z, +y+z) and reads two neighbours from each
+            const int64_t sy = ds.nx, sz = static_cast<int64_t>(ds.nx) * ds.ny;
             Corners<T> k[NC];
 #pragma unroll
-            for (int q = 0; q < NC; ++q) k[q] = fetch_corners<T>(a.src[q], c);
+            for (int q = 0; q < NC; ++q) {
+                const T* p0 = a.src[q] + c.base;
+                const T* p1 = p0 + sy;
+                const T* p2 = p0 + sz;
+                const T* p3 = p2 + sy;
+                k[q].v[0] = __ldg(p0);
+                k[q].v[1] = __ldg(p0 + 1);
+                k[q].v[2] = __ldg(p1);
+                k[q].v[3] = __ldg(p1 + 1);
+                k[q].v[4] = __ldg(p2);
+                k[q].v[5] = __ldg(p2 + 1);
+                k[q].v[6] = __ldg(p3);
+                k[q].v[7] = __ldg(p3 + 1);
+            }
 #pragma unroll
             for (int q = 0; q < NC; ++q) {
                 const T v = lerp_value(c, k[q]);
@@ -403,7 +420,8 @@ void launch_resample(const Launch& L, const T* const* src, Dims ds, T* const* ds
         a.step[k] = nd[k] > 1 ? static_cast<double>(ns[k] - 1) / (nd[k] - 1) : 0.0;
     const dim3 grid = rows_grid(dd.nx, static_cast<int64_t>(dd.ny) * dd.nz), block(kRX, kRY);
     // fp64 keeps the runtime count: 9 fixed components take 182 registers there
-    switch (sizeof(T) == 4 ? ncomp : 0) {
+    const bool solid = ds.nx > 1 && ds.ny > 1 && ds.nz > 1;
+    switch (sizeof(T) == 4 && solid ? ncomp : 0) {
         case 3: k_resample<T, 3><<<grid, block, 0, L.stream>>>(a, ds, dd, ncomp); break;
         case 9: k_resample<T, 9><<<grid, block, 0, L.stream>>>(a, ds, dd, ncomp); break;
         default: k_resample<T, 0><<<grid, block, 0, L.stream>>>(a, ds, dd, ncomp); break;
